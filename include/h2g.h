@@ -1,0 +1,91 @@
+/*
+ * h2g — C ABI of the B200-native adaptive H^2 x H^2 product (arXiv 2309.09061).
+ *
+ * Drop-in boundary for the reference package h2mul's hot path:
+ *   h2g_multiply   replaces h2mul.multiply            (/root/reference/pkg/src/h2mul/induced.py:358-372)
+ *                  i.e. cluster_basis_product (h2.py:127-145), basis_weights / total_weights
+ *                  (weights.py:37-101), compress_induced_row/col_basis (induced.py:76-200),
+ *                  build_product_block_tree (trees.py:314-359) and assemble_product (induced.py:220-355)
+ *   h2g_coarsen    replaces h2mul.coarsen             (coarsening.py:408-422)
+ *                  i.e. build_coarse_row/col_basis (coarsening.py:187-339) and project_final (:354-405)
+ *   h2g_recompress replaces h2mul.recompress          (coarsening.py:437-445), the input preparation
+ *
+ * The reference has no FFI of its own (callers import the Python functions directly, bench.py:21-31);
+ * these entry points are what a ctypes / cffi binding of that path binds.
+ *
+ * Data model: plain host arrays in the packed layout of paper_2309_09061_b200/packed.py —
+ * cluster trees (start, stop, child CSR; preorder ids), block trees (row, col, child CSR, adm),
+ * bases (rank, leaf_off, xfer_off, data; leaf = size x k, transfer = k_child x k_parent, row-major),
+ * couplings / nearfield (per-block offsets into one float64 array, -1 where absent).
+ *
+ * Status codes: 0 ok, 1 invalid input (h2mul InvalidInputError), 2 structural invariant
+ * (h2mul StructureError), 3 CUDA failure.  h2g_last_error() returns the message of the last failure
+ * on the calling thread.  Calls on one context are serialised on its stream; contexts are independent.
+ */
+#ifndef H2G_H
+#define H2G_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct h2g_ctx h2g_ctx;
+typedef struct h2g_tree h2g_tree;
+typedef struct h2g_blocks h2g_blocks;
+typedef struct h2g_h2 h2g_h2;
+
+/* context: device + stream (NULL stream -> a private non-blocking stream) */
+int h2g_ctx_create(int device, void* stream, h2g_ctx** out);
+int h2g_ctx_destroy(h2g_ctx* ctx);
+int h2g_ctx_set_timing(h2g_ctx* ctx, int on);
+/* ms per stage of the last multiply / coarsen: setup, t1_row, t1_col, t1_mat, t2_row, t2_col, t2_mat
+   (the reference harness's stage split, bench.py:195-237) */
+int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);
+/* kernel launches and host synchronisations since the last reset: out2 = {launches, syncs} */
+int h2g_ctx_counters(h2g_ctx* ctx, long long* out2, int reset);
+int h2g_ctx_synchronize(h2g_ctx* ctx);
+
+/* cluster tree (reference ClusterTree, trees.py:34-97): n nodes in preorder */
+int h2g_tree_create(h2g_ctx* ctx, int n, const long long* start, const long long* stop,
+                    const long long* child_ptr, const long long* child_idx, h2g_tree** out);
+void h2g_tree_destroy(h2g_tree* t);
+
+/* block tree (reference BlockTree, trees.py:176-227): nb blocks in preorder */
+int h2g_blocks_create(h2g_ctx* ctx, h2g_tree* rows, h2g_tree* cols, int nb, const long long* row,
+                      const long long* col, const long long* child_ptr, const long long* child_idx,
+                      const unsigned char* adm, h2g_blocks** out);
+void h2g_blocks_destroy(h2g_blocks* b);
+
+/* H^2 matrix (reference H2Matrix, h2.py:148-194) uploaded from the packed host layout.
+   share_bases != 0: the column basis is the row basis object (cb_* ignored). */
+int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt,
+                  const long long* rb_rank, const long long* rb_leaf_off, const long long* rb_xfer_off,
+                  const double* rb_data, long long rb_len,
+                  const long long* cb_rank, const long long* cb_leaf_off, const long long* cb_xfer_off,
+                  const double* cb_data, long long cb_len, int share_bases,
+                  const long long* coup_off, const double* coup_data, long long coup_len,
+                  const long long* near_off, const double* near_data, long long near_len, h2g_h2** out);
+void h2g_h2_destroy(h2g_h2* h);
+/* out8 = {nblocks, row-tree nodes, col-tree nodes, rb_len, cb_len, coup_len, near_len, block child_idx len} */
+int h2g_h2_sizes(h2g_h2* h, long long* out8);
+int h2g_h2_structure(h2g_h2* h, long long* row, long long* col, long long* child_ptr, long long* child_idx,
+                     unsigned char* adm);
+int h2g_h2_download(h2g_ctx* ctx, h2g_h2* h, long long* rb_rank, long long* rb_leaf_off,
+                    long long* rb_xfer_off, double* rb_data, long long* cb_rank, long long* cb_leaf_off,
+                    long long* cb_xfer_off, double* cb_data, long long* coup_off, double* coup_data,
+                    long long* near_off, double* near_data);
+
+/* Z = X * Y over the refined product tree T^XY (phase 1).  max_rank < 0: no cap. */
+int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, int scaling, h2g_h2** g);
+/* re-compression of g onto `coarse` (phase 2) */
+int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
+                h2g_h2** z);
+/* orthogonalise + coarsen onto the own block tree */
+int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z);
+
+const char* h2g_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2G_H */

@@ -1,1 +1,25 @@
-"""B200-native adaptive H^2 x H^2 product (arXiv 2309.09061), drop-in for h2mul's multiply/coarsen path."""
+"""B200-native adaptive H^2 x H^2 product (arXiv 2309.09061).
+
+Drop-in for the hot path of the reference package h2mul: the same container names
+(ClusterTree, BlockTree, ClusterBasis, H2Matrix) and the same entry points (multiply, coarsen,
+recompress, build_product_block_tree), computed by hand-written FP64 CUDA kernels for sm_100a
+behind the C ABI in include/h2g.h.
+"""
+
+from .errors import CudaError, InvalidInputError, StructureError
+from .h2 import BasisProduct, ClusterBasis, H2Matrix, expand_basis, h2_matvec_host, storage_bytes, to_dense
+from .trees import (BlockTree, ClusterTree, ColumnTree, build_block_tree, build_cluster_tree,
+                    same_cluster_tree, sparsity_constant)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # GPU entry points import the native binding lazily (the CPU test tier imports this package)
+    if name in ("multiply", "coarsen", "recompress", "multiply_coarsen"):
+        from . import api
+        return getattr(api, name)
+    if name in ("Context", "DeviceH2", "default_context"):
+        from . import device
+        return getattr(device, name)
+    raise AttributeError(name)

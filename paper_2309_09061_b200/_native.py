@@ -1,0 +1,90 @@
+"""ctypes binding of libh2g.so (include/h2g.h).
+
+The library is built in-tree (paper_2309_09061_b200/libh2g.so) by __graft_entry__.build() /
+`make -C paper_2309_09061_b200/csrc`.  There is no CPU fallback: every product entry point
+raises if the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .errors import CudaError, InvalidInputError, StructureError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libh2g.so")
+
+_lib = None
+
+P = C.c_void_p
+I64P = C.POINTER(C.c_longlong)
+F64P = C.POINTER(C.c_double)
+U8P = C.POINTER(C.c_ubyte)
+
+SIGNATURES = {
+    "h2g_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
+    "h2g_ctx_destroy": (C.c_int, [P]),
+    "h2g_ctx_set_timing": (C.c_int, [P, C.c_int]),
+    "h2g_ctx_stage_times": (C.c_int, [P, F64P]),
+    "h2g_ctx_counters": (C.c_int, [P, I64P, C.c_int]),
+    "h2g_ctx_synchronize": (C.c_int, [P]),
+    "h2g_tree_create": (C.c_int, [P, C.c_int, I64P, I64P, I64P, I64P, C.POINTER(P)]),
+    "h2g_tree_destroy": (None, [P]),
+    "h2g_blocks_create": (C.c_int, [P, P, P, C.c_int, I64P, I64P, I64P, I64P, U8P, C.POINTER(P)]),
+    "h2g_blocks_destroy": (None, [P]),
+    "h2g_h2_upload": (C.c_int, [P, P, I64P, I64P, I64P, F64P, C.c_longlong, I64P, I64P, I64P, F64P,
+                                C.c_longlong, C.c_int, I64P, F64P, C.c_longlong, I64P, F64P, C.c_longlong,
+                                C.POINTER(P)]),
+    "h2g_h2_destroy": (None, [P]),
+    "h2g_h2_sizes": (C.c_int, [P, I64P]),
+    "h2g_h2_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, U8P]),
+    "h2g_h2_download": (C.c_int, [P, P, I64P, I64P, I64P, F64P, I64P, I64P, I64P, F64P, I64P, F64P, I64P, F64P]),
+    "h2g_multiply": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
+    "h2g_coarsen": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
+    "h2g_recompress": (C.c_int, [P, P, C.c_double, C.c_int, C.POINTER(P)]),
+    "h2g_last_error": (C.c_char_p, []),
+}
+
+
+def load(path: str = LIB_PATH):
+    """Load the native library and declare every exported symbol of include/h2g.h."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CudaError(f"native library {path} is missing; run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status == 0:
+        return
+    msg = load().h2g_last_error().decode()
+    if status == 1:
+        raise InvalidInputError(msg)
+    if status == 2:
+        raise StructureError(msg)
+    raise CudaError(msg)
+
+
+def i64(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, a.ctypes.data_as(I64P)
+
+
+def f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(F64P)
+
+
+def u8(a):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    return a, a.ctypes.data_as(U8P)

@@ -1,0 +1,334 @@
+// extern "C" boundary (include/h2g.h): handles, upload / download in the packed layout, status codes.
+#include <cstring>
+
+#include "../../include/h2g.h"
+#include "engine.h"
+
+using namespace h2g;
+
+struct h2g_ctx {
+  Ctx c;
+  h2g_ctx(int dev, cudaStream_t s) : c(dev, s) {}
+};
+struct h2g_tree {
+  std::shared_ptr<Tree> t;
+};
+struct h2g_blocks {
+  std::shared_ptr<Blocks> b;
+  std::shared_ptr<Tree> rows, cols;
+};
+struct h2g_h2 {
+  std::shared_ptr<H2> h;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const InvalidInput& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const StructureErr& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const CudaFailure& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+extern "C" {
+
+const char* h2g_last_error(void) { return g_err.c_str(); }
+
+int h2g_ctx_create(int device, void* stream, h2g_ctx** out) {
+  return guarded([&] { *out = new h2g_ctx(device, (cudaStream_t)stream); });
+}
+
+int h2g_ctx_destroy(h2g_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int h2g_ctx_set_timing(h2g_ctx* ctx, int on) {
+  ctx->c.timing = on != 0;
+  return 0;
+}
+
+int h2g_ctx_stage_times(h2g_ctx* ctx, double* o) {
+  const StageTimes& t = ctx->c.times;
+  o[0] = t.setup; o[1] = t.t1_row; o[2] = t.t1_col; o[3] = t.t1_mat;
+  o[4] = t.t2_row; o[5] = t.t2_col; o[6] = t.t2_mat;
+  return 0;
+}
+
+int h2g_ctx_counters(h2g_ctx* ctx, long long* o, int reset) {
+  o[0] = ctx->c.launches;
+  o[1] = ctx->c.syncs;
+  if (reset) ctx->c.launches = ctx->c.syncs = 0;
+  return 0;
+}
+
+int h2g_ctx_synchronize(h2g_ctx* ctx) {
+  return guarded([&] { ctx->c.sync(); });
+}
+
+int h2g_tree_create(h2g_ctx*, int n, const long long* start, const long long* stop, const long long* cptr,
+                    const long long* cidx, h2g_tree** out) {
+  return guarded([&] {
+    if (n <= 0) throw InvalidInput("cluster tree must be non-empty");
+    *out = new h2g_tree{make_tree(n, start, stop, cptr, cidx)};
+  });
+}
+
+void h2g_tree_destroy(h2g_tree* t) { delete t; }
+
+int h2g_blocks_create(h2g_ctx*, h2g_tree* rows, h2g_tree* cols, int nb, const long long* row,
+                      const long long* col, const long long* cptr, const long long* cidx,
+                      const unsigned char* adm, h2g_blocks** out) {
+  return guarded([&] {
+    if (nb <= 0) throw InvalidInput("block tree must be non-empty");
+    for (int b = 0; b < nb; ++b)
+      if (row[b] < 0 || row[b] >= rows->t->n || col[b] < 0 || col[b] >= cols->t->n)
+        throw InvalidInput("block references a cluster outside its tree");
+    auto bl = make_blocks(rows->t.get(), cols->t.get(), nb, row, col, cptr, cidx, adm);
+    *out = new h2g_blocks{bl, rows->t, cols->t};
+  });
+}
+
+void h2g_blocks_destroy(h2g_blocks* b) { delete b; }
+
+static std::shared_ptr<Basis> upload_basis(Ctx& C, Arena& ar, const Tree* tree, const long long* rank,
+                                           const long long* loff, const long long* xoff, const double* data,
+                                           long long len) {
+  auto B = std::make_shared<Basis>();
+  B->tree = tree;
+  B->rank.assign(rank, rank + tree->n);
+  B->leaf.assign(tree->n, nullptr);
+  B->xfer.assign(tree->n, nullptr);
+  double* d = ar.alloc(len > 0 ? len : 1);
+  if (len > 0) cuda_check(cudaMemcpyAsync(d, data, len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
+  for (int t = 0; t < tree->n; ++t) {
+    if (B->rank[t] < 0) throw InvalidInput("negative rank");
+    if (tree->leaf(t)) {
+      if (loff[t] < 0 || loff[t] + (long long)tree->size(t) * B->rank[t] > len) throw InvalidInput("leaf matrix out of range");
+      B->leaf[t] = d + loff[t];
+    }
+    if (tree->parent[t] >= 0) {
+      if (xoff[t] < 0 || xoff[t] + (long long)B->rank[t] * rank[tree->parent[t]] > len)
+        throw InvalidInput("transfer matrix out of range");
+      B->xfer[t] = d + xoff[t];
+    }
+  }
+  return B;
+}
+
+int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
+                  const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
+                  const long long* cb_loff, const long long* cb_xoff, const double* cb_data, long long cb_len,
+                  int share, const long long* coup_off, const double* coup_data, long long coup_len,
+                  const long long* near_off, const double* near_data, long long near_len, h2g_h2** out) {
+  return guarded([&] {
+    Ctx& C = ctx->c;
+    auto h = std::make_shared<H2>();
+    auto ar = std::make_shared<Arena>(C.st);
+    h->owned.push_back(ar);
+    h->bt = bt->b;
+    h->own_rows = bt->rows;
+    h->own_cols = bt->cols;
+    const Blocks& B = *bt->b;
+    h->rb = upload_basis(C, *ar, B.rows, rb_rank, rb_loff, rb_xoff, rb_data, rb_len);
+    if (share) {
+      if (!B.rows->same(*B.cols)) throw InvalidInput("shared bases need identical row and column trees");
+      h->cb = h->rb;
+    } else {
+      h->cb = upload_basis(C, *ar, B.cols, cb_rank, cb_loff, cb_xoff, cb_data, cb_len);
+    }
+    double* dc = ar->alloc(coup_len > 0 ? coup_len : 1);
+    double* dn = ar->alloc(near_len > 0 ? near_len : 1);
+    if (coup_len > 0)
+      cuda_check(cudaMemcpyAsync(dc, coup_data, coup_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
+    if (near_len > 0)
+      cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
+    h->coup.assign(B.nb, nullptr);
+    h->near.assign(B.nb, nullptr);
+    for (int b = 0; b < B.nb; ++b) {
+      if (!B.leaf(b)) continue;
+      const int t = B.row[b], s = B.col[b];
+      if (B.adm[b]) {
+        const long long n = (long long)h->rb->rank[t] * h->cb->rank[s];
+        if (coup_off[b] < 0 || coup_off[b] + n > coup_len) throw InvalidInput("coupling out of range");
+        h->coup[b] = dc + coup_off[b];
+      } else {
+        const long long n = (long long)B.rows->size(t) * B.cols->size(s);
+        if (near_off[b] < 0 || near_off[b] + n > near_len) throw InvalidInput("nearfield out of range");
+        h->near[b] = dn + near_off[b];
+      }
+    }
+    C.sync();  // host arrays may be released by the caller after return
+    *out = new h2g_h2{h};
+  });
+}
+
+void h2g_h2_destroy(h2g_h2* h) { delete h; }
+
+static long long basis_len(const Basis& B) {
+  const Tree& tr = *B.tree;
+  long long n = 0;
+  for (int t = 0; t < tr.n; ++t) {
+    if (tr.leaf(t)) n += (long long)tr.size(t) * B.rank[t];
+    if (tr.parent[t] >= 0) n += (long long)B.rank[t] * B.rank[tr.parent[t]];
+  }
+  return n;
+}
+
+int h2g_h2_sizes(h2g_h2* hh, long long* o) {
+  return guarded([&] {
+    const H2& h = *hh->h;
+    const Blocks& B = *h.bt;
+    long long cl = 0, nl = 0;
+    for (int b = 0; b < B.nb; ++b) {
+      if (!B.leaf(b)) continue;
+      const int t = B.row[b], s = B.col[b];
+      if (B.adm[b]) cl += (long long)h.rb->rank[t] * h.cb->rank[s];
+      else nl += (long long)B.rows->size(t) * B.cols->size(s);
+    }
+    o[0] = B.nb;
+    o[1] = B.rows->n;
+    o[2] = B.cols->n;
+    o[3] = basis_len(*h.rb);
+    o[4] = basis_len(*h.cb);
+    o[5] = cl;
+    o[6] = nl;
+    o[7] = (long long)B.cidx.size();
+  });
+}
+
+int h2g_h2_structure(h2g_h2* hh, long long* row, long long* col, long long* cptr, long long* cidx,
+                     unsigned char* adm) {
+  return guarded([&] {
+    const Blocks& B = *hh->h->bt;
+    for (int b = 0; b < B.nb; ++b) {
+      row[b] = B.row[b];
+      col[b] = B.col[b];
+      adm[b] = B.leaf(b) ? B.adm[b] : 0;
+      cptr[b] = B.cptr[b];
+    }
+    cptr[B.nb] = B.cptr[B.nb];
+    for (size_t i = 0; i < B.cidx.size(); ++i) cidx[i] = B.cidx[i];
+  });
+}
+
+struct Gather {
+  std::vector<long long> items;  // src, n, dst-offset (patched to absolute)
+  long long total = 0;
+  void add(const double* src, long long n) {
+    if (n <= 0) return;
+    items.push_back((long long)src);
+    items.push_back(n);
+    items.push_back(total);
+    total += n;
+  }
+  void run(Ctx& C, Arena& ar, double* host) {
+    if (total == 0) return;
+    double* d = ar.alloc(total);
+    for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(d + items[i]);
+    long long* di = C.push(items);
+    cuda_check(launch_gather(di, (int)(items.size() / 3), C.st), "gather");
+    cuda_check(cudaMemcpyAsync(host, d, total * sizeof(double), cudaMemcpyDeviceToHost, C.st), "download");
+  }
+};
+
+static void pack_basis(const Basis& B, long long* rank, long long* loff, long long* xoff, Gather& g) {
+  const Tree& tr = *B.tree;
+  for (int t = 0; t < tr.n; ++t) {
+    rank[t] = B.rank[t];
+    loff[t] = -1;
+    xoff[t] = -1;
+  }
+  for (int t = 0; t < tr.n; ++t)
+    if (tr.leaf(t)) {
+      loff[t] = g.total;
+      g.add(B.leaf[t], (long long)tr.size(t) * B.rank[t]);
+    }
+  for (int t = 0; t < tr.n; ++t)
+    if (tr.parent[t] >= 0) {
+      xoff[t] = g.total;
+      g.add(B.xfer[t], (long long)B.rank[t] * B.rank[tr.parent[t]]);
+    }
+}
+
+int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_loff, long long* rb_xoff,
+                    double* rb_data, long long* cb_rank, long long* cb_loff, long long* cb_xoff, double* cb_data,
+                    long long* coup_off, double* coup_data, long long* near_off, double* near_data) {
+  return guarded([&] {
+    Ctx& C = ctx->c;
+    const H2& h = *hh->h;
+    const Blocks& B = *h.bt;
+    Arena ar(C.st);
+    Gather gr, gc, gcp, gn;
+    pack_basis(*h.rb, rb_rank, rb_loff, rb_xoff, gr);
+    pack_basis(*h.cb, cb_rank, cb_loff, cb_xoff, gc);
+    for (int b = 0; b < B.nb; ++b) {
+      coup_off[b] = -1;
+      near_off[b] = -1;
+      if (!B.leaf(b)) continue;
+      const int t = B.row[b], s = B.col[b];
+      if (B.adm[b]) {
+        coup_off[b] = gcp.total;
+        gcp.add(h.coup[b], (long long)h.rb->rank[t] * h.cb->rank[s]);
+      } else {
+        near_off[b] = gn.total;
+        gn.add(h.near[b], (long long)B.rows->size(t) * B.cols->size(s));
+      }
+    }
+    gr.run(C, ar, rb_data);
+    gc.run(C, ar, cb_data);
+    gcp.run(C, ar, coup_data);
+    gn.run(C, ar, near_data);
+    C.sync();
+  });
+}
+
+int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, int scaling, h2g_h2** g) {
+  return guarded([&] {
+    auto G = multiply(ctx->c, *x->h, *y->h, tol, max_rank, scaling != 0);
+    G->keep.push_back(x->h->bt);
+    G->keep.push_back(y->h->bt);
+    G->keep.push_back(x->h->own_rows);
+    G->keep.push_back(y->h->own_cols);
+    *g = new h2g_h2{G};
+  });
+}
+
+int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
+                h2g_h2** z) {
+  return guarded([&] {
+    auto Z = coarsen(ctx->c, *g->h, coarse->b, tol, max_rank, scale_blocks != 0);
+    Z->keep.push_back(coarse->rows);
+    Z->keep.push_back(coarse->cols);
+    Z->keep.push_back(g->h->bt);
+    Z->keep.push_back(g->h->own_rows);
+    Z->keep.push_back(g->h->own_cols);
+    for (auto& k : g->h->keep) Z->keep.push_back(k);
+    *z = new h2g_h2{Z};
+  });
+}
+
+int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z) {
+  return guarded([&] {
+    if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+    auto Z = recompress(ctx->c, *x->h, tol, max_rank);
+    Z->keep.push_back(x->h->bt);
+    Z->keep.push_back(x->h->own_rows);
+    Z->keep.push_back(x->h->own_cols);
+    *z = new h2g_h2{Z};
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+// Host-side engine of the B200 H^2 product: structure, device arenas, batch planning.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "h2g_types.h"
+
+namespace h2g {
+
+// ------------------------------------------------------------------ errors (C-ABI status codes)
+struct InvalidInput : std::runtime_error { using std::runtime_error::runtime_error; };   // 1
+struct StructureErr : std::runtime_error { using std::runtime_error::runtime_error; };   // 2
+struct CudaFailure : std::runtime_error { using std::runtime_error::runtime_error; };    // 3
+
+void cuda_check(cudaError_t e, const char* what);
+
+// ------------------------------------------------------------------ kernels (kernels.cu)
+cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
+cudaError_t launch_qr(const QrItem*, const Seg*, int nitems, int nmax, bool ws, cudaStream_t);
+cudaError_t launch_svd(const SvdItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
+cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
+cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
+size_t qr_smem(int n, bool ws);
+size_t svd_smem(int m, int kx, bool ws);
+size_t norm_smem(int m, long long N);
+size_t gsum_smem(int k2max);
+
+// ------------------------------------------------------------------ structure
+struct Tree {
+  int n = 0, depth = 0;
+  std::vector<long long> start, stop;
+  std::vector<int> parent, level, cptr, cidx;
+  std::vector<std::vector<int>> by_level;
+  bool leaf(int t) const { return cptr[t + 1] == cptr[t]; }
+  int size(int t) const { return (int)(stop[t] - start[t]); }
+  int nkids(int t) const { return cptr[t + 1] - cptr[t]; }
+  int kid(int t, int i) const { return cidx[cptr[t] + i]; }
+  bool same(const Tree& o) const;
+  void finalize();
+};
+
+struct Blocks {
+  const Tree* rows = nullptr;
+  const Tree* cols = nullptr;
+  int nb = 0, depth = 0;
+  std::vector<int> row, col, cptr, cidx, parent, level;
+  std::vector<unsigned char> adm;
+  std::unordered_map<long long, int> index;
+  std::vector<std::vector<int>> by_level;
+  bool leaf(int b) const { return cptr[b + 1] == cptr[b]; }
+  bool adm_leaf(int b) const { return leaf(b) && adm[b]; }
+  bool near_leaf(int b) const { return leaf(b) && !adm[b]; }
+  int nkids(int b) const { return cptr[b + 1] - cptr[b]; }
+  int kid(int b, int i) const { return cidx[cptr[b] + i]; }
+  int find(int t, int s) const {
+    auto it = index.find((long long)t * cols->n + s);
+    return it == index.end() ? -1 : it->second;
+  }
+  void finalize();
+};
+
+// Row/column-swapped view of a block tree (reference BlockTree.transposed, trees.py:211-214).
+struct BView {
+  const Blocks* b;
+  bool T;
+  const Tree& rows() const { return T ? *b->cols : *b->rows; }
+  const Tree& cols() const { return T ? *b->rows : *b->cols; }
+  int row(int i) const { return T ? b->col[i] : b->row[i]; }
+  int col(int i) const { return T ? b->row[i] : b->col[i]; }
+  int find(int t, int s) const { return T ? b->find(s, t) : b->find(t, s); }
+  int nb() const { return b->nb; }
+};
+
+// ------------------------------------------------------------------ device memory
+struct Arena {  // bump allocator over cudaMalloc'd chunks, freed together
+  cudaStream_t st = nullptr;
+  std::vector<void*> chunks;
+  char* cur = nullptr;
+  size_t left = 0;
+  size_t bytes = 0;
+  explicit Arena(cudaStream_t s) : st(s) {}
+  ~Arena();
+  double* alloc(size_t ndoubles);
+  void* alloc_bytes(size_t nbytes);
+};
+using ArenaPtr = std::shared_ptr<Arena>;
+
+struct Mat {
+  double* p = nullptr;
+  int r = 0, c = 0;
+  MatRef ref() const { return MatRef{p, c, 1}; }
+  MatRef tref() const { return MatRef{p, 1, c}; }
+  Mat band(int r0, int nr) const { return Mat{p + (long long)r0 * c, nr, c}; }
+};
+inline MatRef trn(MatRef m) { return MatRef{m.p, m.cs, m.rs}; }
+
+struct Basis {  // leaf (size x k, ld k); xfer (k_c x k_parent, ld k_parent)
+  const Tree* tree = nullptr;
+  std::vector<int> rank;
+  std::vector<double*> leaf, xfer;
+  Mat leafm(int t) const { return Mat{leaf[t], tree->size(t), rank[t]}; }
+  Mat xferm(int c) const { return Mat{xfer[c], rank[c], rank[tree->parent[c]]}; }
+};
+
+struct H2 {
+  std::shared_ptr<const Blocks> bt;
+  std::shared_ptr<Basis> rb, cb;
+  std::vector<double*> coup, near;
+  std::vector<ArenaPtr> owned;
+  std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
+  std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
+};
+
+// Transposable view of an H^2 matrix (reference H2Matrix.transposed, h2.py:169-173).
+struct HView {
+  const H2* h;
+  bool T;
+  BView bv() const { return BView{h->bt.get(), T}; }
+  const Tree& rows() const { return T ? *h->bt->cols : *h->bt->rows; }
+  const Tree& cols() const { return T ? *h->bt->rows : *h->bt->cols; }
+  const Basis& rb() const { return T ? *h->cb : *h->rb; }
+  const Basis& cb() const { return T ? *h->rb : *h->cb; }
+  int row(int b) const { return T ? h->bt->col[b] : h->bt->row[b]; }
+  int col(int b) const { return T ? h->bt->row[b] : h->bt->col[b]; }
+  int find(int t, int s) const { return T ? h->bt->find(s, t) : h->bt->find(t, s); }
+  MatRef coup(int b) const {
+    const int ld = h->cb->rank[h->bt->col[b]];
+    return T ? MatRef{h->coup[b], 1, ld} : MatRef{h->coup[b], ld, 1};
+  }
+  MatRef near(int b) const {
+    const int ld = h->bt->cols->size(h->bt->col[b]);
+    return T ? MatRef{h->near[b], 1, ld} : MatRef{h->near[b], ld, 1};
+  }
+};
+
+// ------------------------------------------------------------------ context: stream + staging
+struct StageTimes {
+  float setup = 0, t1_row = 0, t1_col = 0, t1_mat = 0, t2_row = 0, t2_col = 0, t2_mat = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  // pinned host staging and device staging for descriptors (reset at every host sync)
+  char* hstage = nullptr;
+  char* dstage = nullptr;
+  size_t stage_cap = 0, stage_off = 0;
+  char* hread = nullptr;  // pinned read-back area
+  size_t read_cap = 0;
+  long long launches = 0;  // kernels launched since the last reset
+  long long syncs = 0;
+  StageTimes times;
+  bool timing = false;
+  std::vector<cudaEvent_t> evpool;
+
+  Ctx(int dev, cudaStream_t s);
+  ~Ctx();
+  void* stage(const void* src, size_t bytes);  // returns device pointer (async copy enqueued)
+  template <class T> T* push(const std::vector<T>& v) {
+    return v.empty() ? nullptr : (T*)stage(v.data(), v.size() * sizeof(T));
+  }
+  void sync();
+  template <class T> std::vector<T> read(const T* dptr, size_t n) {
+    std::vector<T> out(n);
+    if (n == 0) return out;
+    ensure_read(n * sizeof(T));
+    cuda_check(cudaMemcpyAsync(hread, dptr, n * sizeof(T), cudaMemcpyDeviceToHost, st), "read");
+    sync();
+    memcpy(out.data(), hread, n * sizeof(T));
+    return out;
+  }
+  void ensure_read(size_t bytes);
+  cudaEvent_t event();
+};
+
+// ------------------------------------------------------------------ batches
+struct GBatch {
+  std::vector<GOut> outs;
+  std::vector<GTerm> terms;
+  int k2max = 0;
+  void out(Mat c, bool beta) { outs.push_back(GOut{c.p, c.c, c.r, c.c, beta ? 1 : 0, (int)terms.size(), (int)terms.size()}); }
+  void t1(MatRef a, double al = 1.0);
+  void t2(MatRef a, MatRef b, int k, double al = 1.0);
+  void t3(MatRef a, MatRef b, MatRef d, int k, int k2, double al = 1.0);
+  void run(Ctx& C);
+  bool empty() const { return outs.empty(); }
+};
+
+struct SegList {
+  std::vector<Seg> segs;
+  int begin() const { return (int)segs.size(); }
+  void add(MatRef a, int w, double scale = 1.0) {
+    if (w > 0) segs.push_back(Seg{a, w, 0, scale});
+  }
+};
+
+struct QrBatch {
+  SegList sl;
+  std::vector<QrItem> items;
+  // returns Mat (min(M, n) x n) output allocated from `ar`
+  void run(Ctx& C, Arena& scratch);
+};
+
+struct NormBatch {
+  SegList sl;
+  std::vector<NormItem> items;
+  std::vector<double> run(Ctx& C, Arena& scratch);  // sync + values
+};
+
+struct SvdBatch {
+  SegList sl;
+  std::vector<SvdItem> items;
+  std::vector<int> run(Ctx& C, Arena& scratch);  // sync + ranks (k1 + k2)
+};
+
+using MatStore = std::vector<Mat>;
+struct PRef {  // basis product view (transposed for the column pass)
+  const MatStore* P;
+  bool T;
+  MatRef at(int s) const { return T ? (*P)[s].tref() : (*P)[s].ref(); }
+  int rows(int s) const { return T ? (*P)[s].c : (*P)[s].r; }
+  int cols(int s) const { return T ? (*P)[s].r : (*P)[s].c; }
+};
+
+struct PairMap {
+  std::unordered_map<long long, Mat> m;
+  static long long key(int a, int b) { return ((long long)a << 32) | (unsigned)b; }
+  Mat* get(int a, int b) {
+    auto it = m.find(key(a, b));
+    return it == m.end() ? nullptr : &it->second;
+  }
+  void put(int a, int b, Mat v) { m[key(a, b)] = v; }
+};
+
+struct Induced {
+  std::shared_ptr<Basis> q;
+  MatStore bc;
+  PairMap proj;
+  PairMap xv;               // memoised X|ts V_Y,s for leaf rows (induced.py:59-73)
+  std::vector<double> gap;  // min |sigma - thr| / thr per cluster (diagnostic)
+};
+
+struct PTree {  // product block tree with the classified triples per node
+  std::shared_ptr<Blocks> bt;
+  std::vector<int> tptr;  // per node: triples [tptr[b], tptr[b+1])
+  std::vector<int> ts;    // middle cluster
+  std::vector<char> tk;   // kind 'a' 'b' 'c'
+};
+
+// ------------------------------------------------------------------ stages
+std::shared_ptr<Tree> make_tree(int n, const long long* start, const long long* stop, const long long* cptr,
+                                const long long* cidx);
+std::shared_ptr<Blocks> make_blocks(const Tree* rows, const Tree* cols, int nb, const long long* row,
+                                    const long long* col, const long long* cptr, const long long* cidx,
+                                    const unsigned char* adm);
+
+void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<std::pair<int, int>>& want,
+                PairMap& memo);
+MatStore basis_product(Ctx& C, Arena& ar, const Basis& W, const Basis& V);
+MatStore basis_weights(Ctx& C, Arena& ar, const Basis& W);
+MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling);
+Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, PRef P, double tol,
+                     int max_rank, bool scale, double level_decay);
+PTree product_tree(BView bx, BView by);
+std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt);
+std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling);
+std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
+                            bool scale);
+std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank);
+
+}  // namespace h2g

@@ -1,0 +1,84 @@
+// Descriptor types shared by the host planner (engine.cu) and the batched kernels (kernels.cu).
+// All numerics are FP64, row-major unless a MatRef says otherwise (reference dense.py:3-4).
+#pragma once
+#include <cstdint>
+
+namespace h2g {
+
+// Strided view of a matrix: element (i, j) lives at p[i * rs + j * cs].
+// A transposed view is the same pointer with rs/cs swapped.
+struct MatRef {
+  const double* p;
+  int rs;
+  int cs;
+};
+
+// One product term accumulated into a GOut:  C += alpha * op
+//   nf = 1: A (m x n)
+//   nf = 2: A (m x k) * B (k x n)
+//   nf = 3: (A (m x k) * B (k x k2)) * D (k2 x n)
+struct GTerm {
+  MatRef a, b, d;
+  int k, k2, nf;
+  int pad_;
+  double alpha;
+};
+
+// One output matrix: C (m x n, row-major, ldc) = (beta ? C : 0) + sum_{t0 <= i < t1} term_i
+struct GOut {
+  double* c;
+  int ldc, m, n, beta;
+  int t0, t1;
+};
+
+// One 64 x 64 output tile of a GOut.
+struct GTile {
+  int out;
+  int tij;  // ti | (tj << 16)
+};
+
+// Segment of a stacked operand.  hstack: a is (m x w); vstack: a is (w x n).  Scaled by `scale`.
+struct Seg {
+  MatRef a;
+  int w;
+  int pad_;
+  double scale;
+};
+
+// R-only QR of vstack(segs[s0:s1]) (M x n); writes min(M, n) x n rows (ld n) to out.
+struct QrItem {
+  int s0, s1, n, pad_;
+  long long M;
+  double* out;
+  double* ws;  // optional global workspace (n x n) when R does not fit shared memory
+};
+
+// Truncated SVD of hstack(segs[s0:s1]) (m x N), optionally protecting range(V) (m x kx)
+// first (Fig. 3 of the paper, reference induced.py:127-137):
+//   k1 = min(m, kx); B = (Q_V^T A)[k1:]; U, k2 = trunc_svd(B, tol, cap)
+//   q_out  (m x (k1 + k2), ld k1 + k2) = Q_V [[I, 0], [0, U]]
+//   bc_out ((k1 + k2) x kx, ld kx)    = [R_V[:k1]; 0]
+// Without V (kx = 0): q_out = U (m x k2), the reference's truncated_svd(A).u (dense.py:77-101).
+// Rank rule: thr = max(tol, max(rows(B), N) * eps * sigma_1); k2 = #{sigma > thr}, min(k2, cap).
+struct SvdItem {
+  int s0, s1, m, kx;
+  long long N;
+  MatRef v;
+  double tol;
+  int cap;  // < 0: no cap
+  int pad_;
+  double* q_out;
+  double* bc_out;
+  int* rank_out;    // k1 + k2
+  double* sig_out;  // optional: sorted singular values of B (capacity m)
+  double* ws;       // optional global workspace for R ((m - k1)^2)
+};
+
+// sigma_1 of hstack(segs[s0:s1]) (m x N) (reference dense.py:104-142).
+struct NormItem {
+  int s0, s1, m, pad_;
+  long long N;
+  double* out;
+};
+
+}  // namespace h2g

@@ -1,0 +1,787 @@
+// Batched FP64 kernels for the adaptive H^2 product on sm_100a.
+//
+//   gsum_kernel  : grouped small-matrix chain products C (+)= sum alpha * A*B(*D)   (all GEMM work)
+//   qr_r_kernel  : R factor of a stacked tall matrix, streamed in 32-row panels    (dense.py:145-150)
+//   svd_kernel   : protected, QR-preconditioned one-sided Jacobi truncated SVD    (dense.py:77-101,
+//                  induced.py:115-146, coarsening.py:294-326)
+//   norm_kernel  : sigma_1 via a streamed Gram matrix, Householder tridiagonalisation
+//                  and Sturm bisection                                            (dense.py:104-142)
+//
+// FP64 has no tcgen05 kind; B200's FP64 pipe (DFMA and legacy DMMA measured at the same
+// ~37 TFLOP/s, profiles/r01_fp64_peak.json) is fed from shared-memory tiles.  One CTA per
+// output tile (gsum) or per matrix (factorisations); grids are sized by the batch.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "h2g_types.h"
+
+namespace h2g {
+
+static constexpr int kThreads = 256;
+static constexpr int kTile = 64;   // gsum output tile
+static constexpr int kKc = 16;     // gsum k-chunk
+static constexpr int kLdS = kTile + 2;
+static constexpr int kPanel = 32;  // TSQR / Gram panel rows (one per lane)
+static constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double mref(const MatRef& a, long long i, long long j) {
+  return a.p[i * a.rs + j * a.cs];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------------------------
+// gsum: 64x64 output tile per CTA, 4x4 per thread (rows ty+16r, cols tx+16c), k streamed in
+// 16-wide chunks through shared memory.
+// ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ void tile_mma(double (&acc)[4][4], const MatRef& A, int ai0, int mt,
+                                         const MatRef& B, int bj0, int nt, int k, double alpha,
+                                         double* As, double* Bs) {
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int kk = 0; kk < k; kk += kKc) {
+    const int kc = min(kKc, k - kk);
+    for (int e = tid; e < kTile * kKc; e += kThreads) {
+      const int l = e % kKc, i = e / kKc;
+      As[l * kLdS + i] = (i < mt && l < kc) ? alpha * mref(A, ai0 + i, kk + l) : 0.0;
+    }
+    for (int e = tid; e < kTile * kKc; e += kThreads) {
+      const int j = e % kTile, l = e / kTile;
+      Bs[l * kLdS + j] = (j < nt && l < kc) ? mref(B, kk + l, bj0 + j) : 0.0;
+    }
+    __syncthreads();
+    for (int l = 0; l < kc; ++l) {
+      double a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[l * kLdS + ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[l * kLdS + tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) gsum_kernel(const GOut* __restrict__ outs,
+                                                        const GTerm* __restrict__ terms,
+                                                        const GTile* __restrict__ tiles,
+                                                        int k2max) {
+  extern __shared__ double smem[];
+  double* As = smem;
+  double* Bs = As + kKc * kLdS;
+  double* Ts = Bs + kKc * kLdS;  // kTile x (k2max + 1)
+  const int ldT = k2max + 1;
+  const GTile tl = tiles[blockIdx.x];
+  const GOut o = outs[tl.out];
+  const int i0 = (tl.tij & 0xffff) * kTile, j0 = (tl.tij >> 16) * kTile;
+  const int mt = min(kTile, o.m - i0), nt = min(kTile, o.n - j0);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+
+  for (int ti = o.t0; ti < o.t1; ++ti) {
+    const GTerm t = terms[ti];
+    if (t.nf == 1) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = ty + 16 * r, j = tx + 16 * c;
+          if (i < mt && j < nt) acc[r][c] += t.alpha * mref(t.a, i0 + i, j0 + j);
+        }
+    } else if (t.nf == 2) {
+      tile_mma(acc, t.a, i0, mt, t.b, j0, nt, t.k, t.alpha, As, Bs);
+    } else {
+      // T = alpha * A[i0:i0+mt, :] * B  (mt x k2) into shared memory, 64 columns at a time
+      for (int js = 0; js < t.k2; js += kTile) {
+        double tacc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tacc[r][c] = 0.0;
+        const int ns = min(kTile, t.k2 - js);
+        tile_mma(tacc, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int i = ty + 16 * r, j = tx + 16 * c;
+            if (j < ns) Ts[i * ldT + js + j] = tacc[r][c];
+          }
+      }
+      __syncthreads();
+      MatRef T{Ts, ldT, 1};
+      tile_mma(acc, T, 0, mt, t.d, j0, nt, t.k2, 1.0, As, Bs);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = ty + 16 * r, j = tx + 16 * c;
+      if (i < mt && j < nt) {
+        double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+        *dst = (o.beta ? *dst : 0.0) + acc[r][c];
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Streamed structured Householder update (TSQR step): [R; P] -> R', R (n x n upper triangular),
+// P (32 x n) the next rows.  One column per iteration, one barrier per column: the warp owning
+// column j+1 applies reflector j to it and immediately builds reflector j+1.
+// ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int j, double* vb, double* tb) {
+  const int lane = threadIdx.x & 31;
+  const double x = P[lane * n + j];
+  const double s = warp_sum(x * x);
+  const double alpha = R[(long long)j * n + j];
+  double v = 0.0, tau = 0.0;
+  if (s != 0.0) {
+    const double nrm = sqrt(alpha * alpha + s);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = (beta - alpha) / beta;
+    v = x / (alpha - beta);
+    if (lane == 0) R[(long long)j * n + j] = beta;
+  }
+  vb[lane] = v;
+  if (lane == 0) *tb = tau;
+  P[lane * n + j] = 0.0;
+}
+
+__device__ __forceinline__ void tsqr_apply(double* R, int n, double* P, int j, int c, double v, double tau) {
+  const int lane = threadIdx.x & 31;
+  const double p = P[lane * n + c];
+  const double w = R[(long long)j * n + c] + warp_sum(v * p);
+  __syncwarp();
+  if (lane == 0) R[(long long)j * n + c] -= tau * w;
+  P[lane * n + c] = p - tau * w * v;
+}
+
+__device__ void tsqr_absorb(double* R, int n, double* P, double* vb /*64*/, double* tb /*2*/) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (warp == 0) tsqr_make(R, n, P, 0, vb, tb);
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const int cur = j & 1;
+    const double v = vb[cur * 32 + lane];
+    const double tau = tb[cur];
+    const bool active = tau != 0.0;
+    if (j + 1 < n && warp == (j + 1) % nw) {
+      if (active) tsqr_apply(R, n, P, j, j + 1, v, tau);
+      __syncwarp();
+      tsqr_make(R, n, P, j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
+    }
+    if (active) {
+      int c0 = j + 2 + ((warp - (j + 2)) % nw + nw) % nw;
+      for (int c = c0; c < n; c += nw) tsqr_apply(R, n, P, j, c, v, tau);
+    }
+    __syncthreads();
+  }
+}
+
+// Locate element col `c` of an hstack of segments: returns the segment index (linear scan cursor).
+struct SegCursor {
+  int s;          // current segment
+  long long off;  // first global column of segment s
+};
+
+// Fill P (32 x nrows) with P[p][i] = scale * A(i, col0 + p) for an hstack of segments (A: m x N).
+// With `raw` non-null, writes raw[i * 32 + p] instead (m x 32 panel, column p).
+__device__ void load_hpanel(const Seg* segs, int s0, int s1, int m, long long N, long long col0,
+                            double* dst, bool transpose_rows, int ldd) {
+  // each warp handles a set of panel columns; lanes run over rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int p = warp; p < kPanel; p += nw) {
+    const long long c = col0 + p;
+    if (c >= N) {
+      for (int i = lane; i < m; i += 32) {
+        if (transpose_rows) dst[p * ldd + i] = 0.0; else dst[i * ldd + p] = 0.0;
+      }
+      continue;
+    }
+    // find the segment containing column c
+    long long off = 0;
+    int s = s0;
+    for (; s < s1; ++s) {
+      if (c < off + segs[s].w) break;
+      off += segs[s].w;
+    }
+    const Seg sg = segs[s];
+    const long long lc = c - off;
+    for (int i = lane; i < m; i += 32) {
+      const double val = sg.scale * mref(sg.a, i, lc);
+      if (transpose_rows) dst[p * ldd + i] = val; else dst[i * ldd + p] = val;
+    }
+  }
+}
+
+// Fill P (32 x n) with rows row0.. of vstack(segs) (M x n), zero beyond M.
+__device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M, long long row0, double* P) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int p = warp; p < kPanel; p += nw) {
+    const long long r = row0 + p;
+    if (r >= M) {
+      for (int j = lane; j < n; j += 32) P[p * n + j] = 0.0;
+      continue;
+    }
+    long long off = 0;
+    int s = s0;
+    for (; s < s1; ++s) {
+      if (r < off + segs[s].w) break;
+      off += segs[s].w;
+    }
+    const Seg sg = segs[s];
+    const long long lr = r - off;
+    for (int j = lane; j < n; j += 32) P[p * n + j] = sg.scale * mref(sg.a, lr, j);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// qr_r: R factor of vstack(segs) (reference dense.py:145-150 / numpy qr mode="r").
+// ---------------------------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) qr_r_kernel(const QrItem* __restrict__ items,
+                                                        const Seg* __restrict__ segs) {
+  extern __shared__ double smem[];
+  const QrItem it = items[blockIdx.x];
+  const int n = it.n;
+  double* P = smem;                    // 32 x n
+  double* vb = P + kPanel * n;         // 64
+  double* tb = vb + 64;                // 2 (+pad)
+  double* R = it.ws ? it.ws : tb + 4;  // n x n
+  const long long nn = (long long)n * n;
+  for (long long e = threadIdx.x; e < nn; e += blockDim.x) R[e] = 0.0;
+  __syncthreads();
+  for (long long r0 = 0; r0 < it.M; r0 += kPanel) {
+    load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P);
+    __syncthreads();
+    tsqr_absorb(R, n, P, vb, tb);
+  }
+  const long long rows = it.M < n ? it.M : n;
+  for (long long e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    const long long i = e / n, j = e % n;
+    it.out[e] = j >= i ? R[i * n + j] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// One-sided Jacobi on the ROWS of W (n x n, row-major): afterwards the rows are mutually
+// orthogonal to working precision (relative cosine criterion), so normalised rows are
+// orthonormal regardless of the row norms.  Round-robin pairing, one pair per warp at a time.
+// ---------------------------------------------------------------------------------------------
+
+__device__ void jacobi_rows(double* W, int n, int* flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int np = (n + 1) & ~1;  // even number of players, player n (if odd) is a bye
+  const int npairs = np / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int step = 0; step < np - 1; ++step) {
+      for (int q = warp; q < npairs; q += nw) {
+        // circle method: player 0 fixed, players 1..np-1 rotate by `step`
+        const int a = (q == 0) ? 0 : 1 + (q + step) % (np - 1);
+        const int b = 1 + ((q == 0 ? 0 : np - 1 - q) + step) % (np - 1);
+        if (a >= n || b >= n) continue;
+        double* ra = W + (long long)a * n;
+        double* rb = W + (long long)b * n;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          const double x = ra[j], y = rb[j];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > kEps * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t);
+          const double s = c * t;
+          for (int j = lane; j < n; j += 32) {
+            const double x = ra[j], y = rb[j];
+            ra[j] = c * x - s * y;
+            rb[j] = s * x + c * y;
+          }
+          if (lane == 0) *flag = 1;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// svd_kernel: see SvdItem.  Shared memory carve-up (doubles):
+//   V  : m x kx           Householder factorisation of the protected basis
+//   tv : kx               reflector coefficients
+//   raw: m x 32           current column panel (protect case)
+//   P  : 32 x n'          transposed panel rows for TSQR
+//   R  : n' x n'          (shared or global workspace)
+//   sig: n'  ord: n'      singular values and order
+// ---------------------------------------------------------------------------------------------
+
+__device__ void householder_qr_cols(double* V, int m, int kx, int k1, double* tv, double* red) {
+  // In-place Householder QR of V (m x kx, row-major): reflector j stored below the diagonal
+  // (implicit 1 on the diagonal), R on and above.  LAPACK dgeqrf sign convention.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = 0; j < k1; ++j) {
+    // norm of V[j+1:, j]
+    double part = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) part += V[i * kx + j] * V[i * kx + j];
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w];
+      const double alpha = V[j * kx + j];
+      double tau = 0.0, scale = 0.0;
+      if (s != 0.0) {
+        const double nrm = sqrt(alpha * alpha + s);
+        const double beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+        V[j * kx + j] = beta;
+      }
+      tv[j] = tau;
+      red[nw] = scale;
+    }
+    __syncthreads();
+    const double scale = red[nw];
+    const double tau = tv[j];
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) V[i * kx + j] *= scale;
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < kx; c += nw) {
+        double w = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w += V[i * kx + j] * V[i * kx + c];
+        w = warp_sum(w) + V[j * kx + c];
+        __syncwarp();
+        if (lane == 0) V[j * kx + c] -= tau * w;
+        for (int i = j + 1 + lane; i < m; i += 32) V[i * kx + c] -= tau * w * V[i * kx + j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Apply H_j (j in [jb, je) in the given direction) to column c of X (rows m, ld ldx) by one warp.
+__device__ __forceinline__ void apply_reflector_col(const double* V, int kx, int m, int j, double tau,
+                                                    double* X, int ldx, int c) {
+  const int lane = threadIdx.x & 31;
+  double w = X[(long long)j * ldx + c];
+  double part = 0.0;
+  for (int i = j + 1 + lane; i < m; i += 32) part += V[i * kx + j] * X[(long long)i * ldx + c];
+  w += warp_sum(part);
+  __syncwarp();
+  if (lane == 0) X[(long long)j * ldx + c] -= tau * w;
+  for (int i = j + 1 + lane; i < m; i += 32) X[(long long)i * ldx + c] -= tau * w * V[i * kx + j];
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads) svd_kernel(const SvdItem* __restrict__ items,
+                                                       const Seg* __restrict__ segs) {
+  extern __shared__ double smem[];
+  __shared__ double red[40];
+  __shared__ int flag;
+  __shared__ int s_k2;
+  const SvdItem it = items[blockIdx.x];
+  const int m = it.m, kx = it.kx;
+  const int k1 = min(m, kx);
+  const int n = m - k1;  // rows of the matrix actually truncated
+  const long long N = it.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+  double* V = smem;                         // m x kx
+  double* tv = V + (long long)m * kx;       // kx (+1)
+  double* raw = tv + kx + 1;                // m x 32 (protect case only)
+  double* P = raw + (kx > 0 ? m * kPanel : 0);  // 32 x n
+  double* vb = P + kPanel * n;              // 64
+  double* tb = vb + 64;                     // 4
+  double* sig = tb + 4;                     // n
+  int* ord = (int*)(sig + n);               // n ints (n/2 + 1 doubles)
+  double* R = it.ws ? it.ws : sig + n + (n / 2 + 1);  // n x n
+
+  // 1. protect: Householder QR of V
+  if (kx > 0) {
+    for (int e = threadIdx.x; e < m * kx; e += blockDim.x) {
+      const int i = e / kx, j = e % kx;
+      V[e] = mref(it.v, i, j);
+    }
+    __syncthreads();
+    householder_qr_cols(V, m, kx, k1, tv, red);
+  }
+
+  // 2. TSQR of B^T, B = (Q^T A)[k1:]
+  int k2 = 0;
+  if (n > 0 && N > 0) {
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = 0.0;
+    __syncthreads();
+    for (long long c0 = 0; c0 < N; c0 += kPanel) {
+      if (kx > 0) {
+        load_hpanel(segs, it.s0, it.s1, m, N, c0, raw, false, kPanel);
+        __syncthreads();
+        // Q^T raw = H_{k1-1} ... H_0 raw: warp per panel column, reflectors in order 0..k1-1
+        for (int p = warp; p < kPanel; p += nw)
+          for (int j = 0; j < k1; ++j)
+            if (tv[j] != 0.0) apply_reflector_col(V, kx, m, j, tv[j], raw, kPanel, p);
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
+          const int p = e / n, i = e % n;
+          P[p * n + i] = raw[(k1 + i) * kPanel + p];
+        }
+      } else {
+        load_hpanel(segs, it.s0, it.s1, m, N, c0, P, true, n);
+      }
+      __syncthreads();
+      tsqr_absorb(R, n, P, vb, tb);
+    }
+    // 3. Jacobi on the rows of R: B = R^T Q_B^T, left singular vectors of B = normalised rows of R*
+    jacobi_rows(R, n, &flag);
+    // 4. singular values, order, rank
+    for (int i = warp; i < n; i += nw) {
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * n + j], R[(long long)i * n + j], s);
+      s = warp_sum(s);
+      if (lane == 0) sig[i] = sqrt(s);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int pos = 0;
+      const double si = sig[i];
+      for (int j = 0; j < n; ++j) {
+        const double sj = sig[j];
+        pos += (sj > si) || (sj == si && j < i);
+      }
+      ord[pos] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double s1 = sig[ord[0]];
+      const long long big = (long long)n > N ? (long long)n : N;
+      const double thr = fmax(it.tol, (double)big * kEps * s1);
+      int k = 0;
+      while (k < n && sig[ord[k]] > thr) ++k;
+      if (it.cap >= 0 && k > it.cap) k = it.cap;
+      s_k2 = k;
+    }
+    __syncthreads();
+    k2 = s_k2;
+    if (it.sig_out)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) it.sig_out[i] = sig[ord[i]];
+  }
+
+  // 5. outputs
+  const int kt = k1 + k2;
+  double* Q = it.q_out;  // m x kt
+  for (long long e = threadIdx.x; e < (long long)m * kt; e += blockDim.x) {
+    const int i = (int)(e / kt), j = (int)(e % kt);
+    double val;
+    if (j < k1) {
+      val = (i == j) ? 1.0 : 0.0;
+    } else {
+      const int src = ord[j - k1];
+      val = (i < k1) ? 0.0 : R[(long long)src * n + (i - k1)] / sig[src];
+    }
+    Q[e] = val;
+  }
+  __syncthreads();
+  if (k1 > 0) {
+    // Q = H_0 H_1 ... H_{k1-1} Y: apply the reflectors in reverse order, warp per column
+    for (int c = warp; c < kt; c += nw)
+      for (int j = k1 - 1; j >= 0; --j)
+        if (tv[j] != 0.0) apply_reflector_col(V, kx, m, j, tv[j], Q, kt, c);
+  }
+  if (it.bc_out) {
+    for (int e = threadIdx.x; e < kt * kx; e += blockDim.x) {
+      const int i = e / kx, j = e % kx;
+      it.bc_out[e] = (i < k1 && j >= i) ? V[i * kx + j] : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) *it.rank_out = kt;
+}
+
+// ---------------------------------------------------------------------------------------------
+// norm_kernel: sigma_1 of hstack(segs) (m x N).  Gram on the row side (m <= N or m <= 160),
+// else on the column side; tridiagonalise; Sturm multisection for lambda_max.
+// ---------------------------------------------------------------------------------------------
+
+__device__ double sturm_lambda_max(const double* d, const double* e, int g, double* red) {
+  // all threads call; warp 0 computes
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = lane; i < g; i += 32) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < g ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - r);
+      hi = fmax(hi, d[i] + r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const double span = fmax(fabs(lo), fabs(hi));
+    if (span == 0.0) {  // exactly zero Gram: sigma_1 == 0 exactly (zero-norm skips are exact tests)
+      if (lane == 0) red[0] = 0.0;
+      lo = hi = 0.0;
+    }
+    hi += 2.0 * kEps * span + 1e-300;
+    lo -= 2.0 * kEps * span + 1e-300;
+    for (int round = 0; round < 64 && span != 0.0; ++round) {
+      if (hi - lo <= 2.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
+      const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+      int cnt = 0;
+      double q = d[0] - x;
+      if (q < 0.0) ++cnt;
+      for (int i = 1; i < g; ++i) {
+        if (q == 0.0) q = -1e-300;
+        q = (d[i] - x) - e[i - 1] * e[i - 1] / q;
+        if (q < 0.0) ++cnt;
+      }
+      // first lane whose point has all g eigenvalues below it
+      const unsigned full = __ballot_sync(0xffffffffu, cnt >= g);
+      double nlo = lo, nhi = hi;
+      if (full) {
+        const int f = __ffs(full) - 1;
+        nhi = lo + (hi - lo) * (double)(f + 1) / 33.0;
+        nlo = f > 0 ? lo + (hi - lo) * (double)f / 33.0 : lo;
+      } else {
+        nlo = lo + (hi - lo) * 32.0 / 33.0;
+      }
+      lo = nlo;
+      hi = nhi;
+    }
+    if (lane == 0) red[0] = span == 0.0 ? 0.0 : 0.5 * (lo + hi);
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restrict__ items,
+                                                        const Seg* __restrict__ segs) {
+  extern __shared__ double smem[];
+  __shared__ double red[40];
+  const NormItem it = items[blockIdx.x];
+  const int m = it.m;
+  const long long N = it.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (m == 0 || N == 0) {
+    if (threadIdx.x == 0) *it.out = 0.0;
+    return;
+  }
+  const bool rowside = (m <= N) || (m <= 160);
+  const int g = rowside ? m : (int)N;
+  double* G = smem;                       // g x g
+  double* Pn = G + (long long)g * g;      // 32 x max(m, N) panel
+  double* d = Pn + kPanel * (rowside ? m : (int)N);
+  double* e = d + g;
+  double* v = e + g;
+  double* p = v + g;
+  for (int q = threadIdx.x; q < g * g; q += blockDim.x) G[q] = 0.0;
+  __syncthreads();
+  if (rowside) {
+    // G = sum over column panels of A_panel A_panel^T, panel stored transposed (32 x m)
+    for (long long c0 = 0; c0 < N; c0 += kPanel) {
+      load_hpanel(segs, it.s0, it.s1, m, N, c0, Pn, true, m);
+      __syncthreads();
+      for (int q = threadIdx.x; q < g * g; q += blockDim.x) {
+        const int i = q / g, j = q % g;
+        if (j < i) continue;
+        double s = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < kPanel; ++c) s = fma(Pn[c * m + i], Pn[c * m + j], s);
+        G[i * g + j] += s;
+      }
+      __syncthreads();
+    }
+  } else {
+    // G = sum over row panels of P^T P (P: 32 x N from an hstack of column segments)
+    for (long long r0 = 0; r0 < m; r0 += kPanel) {
+      for (int pr = warp; pr < kPanel; pr += nw) {
+        const long long r = r0 + pr;
+        long long off = 0;
+        for (int s = it.s0; s < it.s1; ++s) {
+          const Seg sg = segs[s];
+          for (int c = lane; c < sg.w; c += 32)
+            Pn[pr * N + off + c] = (r < m) ? sg.scale * mref(sg.a, r, c) : 0.0;
+          off += sg.w;
+        }
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < g * g; q += blockDim.x) {
+        const int i = q / g, j = q % g;
+        if (j < i) continue;
+        double s = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < kPanel; ++c) s = fma(Pn[c * N + i], Pn[c * N + j], s);
+        G[i * g + j] += s;
+      }
+      __syncthreads();
+    }
+  }
+  for (int q = threadIdx.x; q < g * g; q += blockDim.x) {
+    const int i = q / g, j = q % g;
+    if (j < i) G[q] = G[j * g + i];
+  }
+  __syncthreads();
+  // Householder tridiagonalisation (lower), trailing block updated in place
+  for (int j = 0; j + 2 < g; ++j) {
+    double part = 0.0;
+    for (int i = j + 2 + threadIdx.x; i < g; i += blockDim.x) part += G[i * g + j] * G[i * g + j];
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    const double alpha = G[(j + 1) * g + j];
+    __syncthreads();
+    if (s == 0.0) {
+      if (threadIdx.x == 0) { e[j] = alpha; d[j] = G[j * g + j]; }
+      __syncthreads();
+      continue;
+    }
+    const double nrm = sqrt(alpha * alpha + s);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    const double tau = (beta - alpha) / beta;
+    const double scale = 1.0 / (alpha - beta);
+    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) v[i] = (i == j + 1) ? 1.0 : G[i * g + j] * scale;
+    __syncthreads();
+    // p = tau * G' v
+    for (int i = j + 1 + warp; i < g; i += nw) {
+      double acc = 0.0;
+      for (int c = j + 1 + lane; c < g; c += 32) acc = fma(G[i * g + c], v[c], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) p[i] = tau * acc;
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) pv += p[i] * v[i];
+    pv = warp_sum(pv);
+    if (lane == 0) red[warp] = pv;
+    __syncthreads();
+    double kk = 0.0;
+    for (int w = 0; w < nw; ++w) kk += red[w];
+    kk *= 0.5 * tau;
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) p[i] -= kk * v[i];  // w
+    __syncthreads();
+    const int t = g - j - 1;
+    for (int q = threadIdx.x; q < t * t; q += blockDim.x) {
+      const int i = j + 1 + q / t, c = j + 1 + q % t;
+      G[i * g + c] -= v[i] * p[c] + p[i] * v[c];
+    }
+    if (threadIdx.x == 0) { e[j] = beta; d[j] = G[j * g + j]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (g >= 2) {
+      d[g - 2] = G[(g - 2) * g + (g - 2)];
+      e[g - 2] = G[(g - 1) * g + (g - 2)];
+    }
+    d[g - 1] = G[(g - 1) * g + (g - 1)];
+  }
+  __syncthreads();
+  const double lam = sturm_lambda_max(d, e, g, red);
+  if (threadIdx.x == 0) *it.out = sqrt(fmax(lam, 0.0));
+}
+
+// ---------------------------------------------------------------------------------------------
+// gather: items (src, count, dst) as int64 triples; one CTA per item (packing for download)
+// ---------------------------------------------------------------------------------------------
+
+__global__ void gather_kernel(const long long* __restrict__ items) {
+  const long long* it = items + 3 * blockIdx.x;
+  const double* src = (const double*)it[0];
+  const long long n = it[1];
+  double* dst = (double*)it[2];
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------------
+
+size_t gsum_smem(int k2max) {
+  return sizeof(double) * (2 * kKc * kLdS + (k2max > 0 ? (size_t)kTile * (k2max + 1) : 0));
+}
+
+cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
+                        cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  const size_t sm = gsum_smem(k2max);
+  cudaFuncSetAttribute(gsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  gsum_kernel<<<ntiles, kThreads, sm, st>>>(outs, terms, tiles, k2max);
+  return cudaGetLastError();
+}
+
+size_t qr_smem(int n, bool ws) {
+  return sizeof(double) * ((size_t)kPanel * n + 64 + 4 + (ws ? 0 : (size_t)n * n));
+}
+
+cudaError_t launch_qr(const QrItem* items, const Seg* segs, int nitems, int nmax, bool ws, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  const size_t sm = qr_smem(nmax, ws);
+  cudaFuncSetAttribute(qr_r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  qr_r_kernel<<<nitems, kThreads, sm, st>>>(items, segs);
+  return cudaGetLastError();
+}
+
+size_t svd_smem(int m, int kx, bool ws) {
+  const int k1 = m < kx ? m : kx;
+  const int n = m - k1;
+  size_t d = (size_t)m * kx + kx + 1 + (kx > 0 ? (size_t)m * kPanel : 0) + (size_t)kPanel * n + 64 + 4 + n +
+             (n / 2 + 1);
+  if (!ws) d += (size_t)n * n;
+  return d * sizeof(double);
+}
+
+cudaError_t launch_svd(const SvdItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  svd_kernel<<<nitems, kThreads, smem, st>>>(items, segs);
+  return cudaGetLastError();
+}
+
+size_t norm_smem(int m, long long N) {
+  const bool rowside = (m <= N) || (m <= 160);
+  const int g = rowside ? m : (int)N;
+  const int w = rowside ? m : (int)N;
+  return sizeof(double) * ((size_t)g * g + (size_t)kPanel * w + 4 * (size_t)g);
+}
+
+cudaError_t launch_norm(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  cudaFuncSetAttribute(norm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  norm_kernel<<<nitems, kThreads, smem, st>>>(items, segs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  gather_kernel<<<nitems, kThreads, 0, st>>>(items);
+  return cudaGetLastError();
+}
+
+}  // namespace h2g

@@ -1,0 +1,424 @@
+// Phase 1 of the product: compressed induced bases (Fig. 3) and exact-structure assembly over
+// the refined product tree (reference induced.py:49-372).
+#include <algorithm>
+#include <cmath>
+#include <functional>
+
+#include "engine.h"
+
+namespace h2g {
+
+// X|ts V_Y,s for leaf row clusters t by block descent (reference induced.py:59-73).
+// Each requested (t, s) pair and every block below it (same row t) is computed once, deepest first.
+void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<std::pair<int, int>>& want,
+                PairMap& memo) {
+  const Blocks& B = *x.h->bt;
+  std::vector<std::vector<int>> by_h;  // block ids by height
+  std::unordered_map<long long, int> height;  // pairs scheduled by this call
+  std::function<int(int)> visit = [&](int b) -> int {
+    const int t = x.row(b), s = x.col(b);
+    const long long key = PairMap::key(t, s);
+    auto hit = height.find(key);
+    if (hit != height.end()) return hit->second;
+    if (memo.get(t, s)) return -1;  // computed by an earlier call
+    int h = 0;
+    for (int i = 0; i < B.nkids(b); ++i) h = std::max(h, visit(B.kid(b, i)) + 1);
+    height[key] = h;
+    if ((int)by_h.size() <= h) by_h.resize(h + 1);
+    by_h[h].push_back(b);
+    return h;
+  };
+  for (auto& pr : want) {
+    const int b = x.find(pr.first, pr.second);
+    if (b < 0) throw StructureErr("xv: pair not in the block tree");
+    visit(b);
+  }
+  const Basis& VX = x.rb();
+  const Basis& VY = y.rb();
+  const Tree& rows = x.rows();
+  for (auto& lvl : by_h) {
+    GBatch g;
+    for (int b : lvl) {
+      const int t = x.row(b), s = x.col(b);
+      Mat m{ar.alloc((size_t)rows.size(t) * VY.rank[s]), rows.size(t), VY.rank[s]};
+      memo.put(t, s, m);
+      g.out(m, false);
+      if (B.adm_leaf(b)) {
+        g.t3(VX.leafm(t).ref(), x.coup(b), P.at(s), VX.rank[t], P.rows(s));
+      } else if (B.leaf(b)) {
+        g.t2(x.near(b), VY.leafm(s).ref(), VY.tree->size(s));
+      } else {
+        for (int i = 0; i < B.nkids(b); ++i) {
+          const int b2 = B.kid(b, i);
+          const int s2 = x.col(b2);
+          const Mat part = *memo.get(x.row(b2), s2);
+          if (s2 != s) g.t2(part.ref(), VY.xferm(s2).ref(), VY.rank[s2]);
+          else g.t1(part.ref());
+        }
+      }
+    }
+    g.run(C);
+  }
+}
+
+// Fig. 3: bottom-up compression of the induced row basis (reference induced.py:76-184).
+Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, PRef P, double tol,
+                     int max_rank, bool scale, double level_decay) {
+  if (!x.cols().same(y.rows())) throw InvalidInput("x and y do not share the middle cluster tree");
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  const Blocks& B = *x.h->bt;
+  const Tree& tr = x.rows();
+  const Basis& VX = x.rb();
+  const Basis& VY = y.rb();
+  Arena sc(C.st);
+  // middles: columns of the non-admissible-leaf blocks per row cluster, block preorder (induced.py:49-56)
+  std::vector<std::vector<int>> mids(tr.n);
+  for (int b = 0; b < B.nb; ++b)
+    if (!B.adm_leaf(b)) mids[x.row(b)].push_back(b);
+
+  Induced R;
+  R.q = std::make_shared<Basis>();
+  Basis& q = *R.q;
+  q.tree = &tr;
+  q.rank.assign(tr.n, 0);
+  q.leaf.assign(tr.n, nullptr);
+  q.xfer.assign(tr.n, nullptr);
+  R.bc.assign(tr.n, Mat{});
+
+  std::vector<std::pair<int, int>> leaf_pairs;
+  for (int t = 0; t < tr.n; ++t)
+    if (tr.leaf(t))
+      for (int b : mids[t]) leaf_pairs.emplace_back(t, x.col(b));
+  xv_compute(C, out, x, y, P, leaf_pairs, R.xv);
+
+  std::vector<Mat> blk(B.nb);
+  std::vector<Mat> vx(tr.n);
+  for (int lev = tr.depth; lev >= 0; --lev) {
+    const std::vector<int>& L = tr.by_level[lev];
+    GBatch g1, g2;
+    PairMap rf;
+    for (int t : L) {
+      if (tr.leaf(t)) {
+        vx[t] = VX.leafm(t);
+        for (int b : mids[t]) blk[b] = *R.xv.get(t, x.col(b));
+        continue;
+      }
+      const int kx = VX.rank[t];
+      int m = 0;
+      for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
+      Mat vh{sc.alloc((size_t)m * kx), m, kx};
+      int off = 0;
+      for (int i = 0; i < tr.nkids(t); ++i) {  // vhat = vstack(bc_c E_X,c) (induced.py:177-178)
+        const int c = tr.kid(t, i);
+        g1.out(vh.band(off, q.rank[c]), false);
+        g1.t2(R.bc[c].ref(), VX.xferm(c).ref(), R.bc[c].c);
+        off += q.rank[c];
+      }
+      vx[t] = vh;
+      for (int b : mids[t])
+        for (int i = 0; i < B.nkids(b); ++i) {  // projected_block for admissible children (induced.py:148-153)
+          const int b2 = B.kid(b, i);
+          if (!B.adm_leaf(b2)) continue;
+          const int t2 = x.row(b2), s2 = x.col(b2);
+          Mat m2{sc.alloc((size_t)q.rank[t2] * VY.rank[s2]), q.rank[t2], VY.rank[s2]};
+          g1.out(m2, false);
+          g1.t3(R.bc[t2].ref(), x.coup(b2), P.at(s2), R.bc[t2].c, P.rows(s2));
+          rf.put(b2, 0, m2);
+        }
+    }
+    g1.run(C);
+    for (int t : L) {  // ahat (induced.py:155-167), one output band per child row cluster
+      if (tr.leaf(t)) continue;
+      const int m = vx[t].r;
+      for (int b : mids[t]) {
+        const int s = x.col(b);
+        Mat A{sc.alloc((size_t)m * VY.rank[s]), m, VY.rank[s]};
+        blk[b] = A;
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {
+          const int c = tr.kid(t, i);
+          g2.out(A.band(off, q.rank[c]), false);
+          for (int j = 0; j < B.nkids(b); ++j) {
+            const int b2 = B.kid(b, j);
+            if (x.row(b2) != c) continue;
+            const int s2 = x.col(b2);
+            const Mat pb = B.adm_leaf(b2) ? *rf.get(b2, 0) : *R.proj.get(c, s2);
+            if (s2 != s) g2.t2(pb.ref(), VY.xferm(s2).ref(), VY.rank[s2]);
+            else g2.t1(pb.ref());
+          }
+          off += q.rank[c];
+        }
+      }
+    }
+    g2.run(C);
+
+    // block norms for block-relative scaling (induced.py:121-125); exact zero norms are skipped
+    std::vector<double> nrm(B.nb, 1.0);
+    if (scale) {
+      NormBatch nbat;
+      std::vector<int> ids;
+      for (int t : L)
+        for (int b : mids[t]) {
+          NormItem it{};
+          it.s0 = nbat.sl.begin();
+          nbat.sl.add(blk[b].ref(), blk[b].c);
+          it.s1 = nbat.sl.begin();
+          it.m = blk[b].r;
+          it.N = blk[b].c;
+          nbat.items.push_back(it);
+          ids.push_back(b);
+        }
+      auto v = nbat.run(C, sc);
+      for (size_t i = 0; i < ids.size(); ++i) nrm[ids[i]] = v[i];
+    }
+
+    // weighted stack w_i = blk_i Z_s^T / ||blk_i|| and the protected truncated SVD (induced.py:115-146)
+    GBatch g3;
+    SvdBatch sv;
+    std::vector<Mat> qbuf(L.size()), bcbuf(L.size());
+    for (size_t li = 0; li < L.size(); ++li) {
+      const int t = L[li];
+      const int m = vx[t].r, kx = vx[t].c, k1 = std::min(m, kx);
+      SvdItem it{};
+      it.s0 = sv.sl.begin();
+      long long N = 0;
+      for (int b : mids[t]) {
+        if (scale && nrm[b] == 0.0) continue;
+        const Mat& Z = zy[x.col(b)];
+        if (Z.r == 0 || m == 0) continue;
+        Mat w{sc.alloc((size_t)m * Z.r), m, Z.r};
+        g3.out(w, false);
+        g3.t2(blk[b].ref(), Z.tref(), Z.c, scale ? 1.0 / nrm[b] : 1.0);
+        sv.sl.add(w.ref(), Z.r);
+        N += Z.r;
+      }
+      it.s1 = sv.sl.begin();
+      it.m = m;
+      it.kx = kx;
+      it.N = N;
+      it.v = vx[t].ref();
+      it.tol = tol * std::pow(level_decay, (double)lev);
+      it.cap = max_rank < 0 ? -1 : std::max(0, max_rank - k1);
+      const long long kcap = std::min<long long>(m, k1 + N);
+      qbuf[li] = Mat{out.alloc((size_t)m * kcap), m, (int)kcap};
+      bcbuf[li] = Mat{out.alloc((size_t)kcap * kx), (int)kcap, kx};
+      it.q_out = qbuf[li].p;
+      it.bc_out = bcbuf[li].p;
+      sv.items.push_back(it);
+    }
+    g3.run(C);
+    std::vector<int> rk = sv.run(C, sc);
+
+    GBatch g4;
+    for (size_t li = 0; li < L.size(); ++li) {
+      const int t = L[li];
+      const int k = rk[li];
+      const int m = vx[t].r, kx = vx[t].c;
+      q.rank[t] = k;
+      Mat Q{qbuf[li].p, m, k};
+      R.bc[t] = Mat{bcbuf[li].p, k, kx};
+      if (tr.leaf(t)) {
+        q.leaf[t] = Q.p;
+      } else {
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {  // transfers = row split of Q_t (induced.py:143-146)
+          const int c = tr.kid(t, i);
+          q.xfer[c] = Q.p + (long long)off * k;
+          off += q.rank[c];
+        }
+      }
+      for (int b : mids[t]) {  // A_ts = Q_t^T blk for every middle (induced.py:138-139)
+        const int s = x.col(b);
+        Mat pm{out.alloc((size_t)k * VY.rank[s]), k, VY.rank[s]};
+        g4.out(pm, false);
+        g4.t2(Q.tref(), blk[b].ref(), m);
+        R.proj.put(t, s, pm);
+      }
+    }
+    g4.run(C);
+  }
+  return R;
+}
+
+static void emit_push(GBatch& g, const Mat* E, const Mat& S, const Mat* F) {
+  if (E && F) g.t3(E->ref(), S.ref(), F->tref(), E->c, S.c);
+  else if (E) g.t2(E->ref(), S.ref(), E->c);
+  else if (F) g.t2(S.ref(), F->tref(), S.c);
+  else g.t1(S.ref());
+}
+
+// Product over T^XY in the induced bases + push-down (reference induced.py:220-355).
+std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt) {
+  auto G = std::make_shared<H2>();
+  G->bt = pt.bt;
+  G->rb = qr.q;
+  G->cb = qc.q;
+  auto ar = std::make_shared<Arena>(C.st);
+  G->owned.push_back(ar);
+  Arena sc(C.st);
+  const Blocks& B = *pt.bt;
+  const Tree& rows = *B.rows;
+  const Tree& cols = *B.cols;
+  const BView bx = x.bv(), by = y.bv();
+  const Basis& Q = *qr.q;
+  const Basis& W = *qc.q;
+  G->coup.assign(B.nb, nullptr);
+  G->near.assign(B.nb, nullptr);
+  std::vector<Mat> cp(B.nb);
+  for (int b = 0; b < B.nb; ++b) {
+    const int t = B.row[b], r = B.col[b];
+    if (B.near_leaf(b)) {
+      G->near[b] = ar->alloc((size_t)rows.size(t) * cols.size(r));
+    } else {
+      Arena& a = B.adm_leaf(b) ? *ar : sc;
+      cp[b] = Mat{a.alloc((size_t)Q.rank[t] * W.rank[r]), Q.rank[t], W.rank[r]};
+      if (B.adm_leaf(b)) G->coup[b] = cp[b].p;
+    }
+  }
+  // memoised leaf products needed by dense targets, and row factors of admissible X blocks
+  std::vector<std::pair<int, int>> need_xv, need_wy;
+  for (int b = 0; b < B.nb; ++b) {
+    if (!B.near_leaf(b)) continue;
+    const int t = B.row[b], r = B.col[b];
+    for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+      const int s = pt.ts[i];
+      if (pt.tk[i] == 'a' && !qr.xv.get(t, s)) need_xv.emplace_back(t, s);
+      if (pt.tk[i] == 'b' && !qc.xv.get(r, s)) need_wy.emplace_back(r, s);
+    }
+  }
+  HView yT{y.h, !y.T}, xT{x.h, !x.T};
+  xv_compute(C, sc, x, y, P, need_xv, qr.xv);
+  xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, need_wy, qc.xv);
+  PairMap rf;
+  {
+    GBatch g;
+    for (int b = 0; b < B.nb; ++b) {
+      if (B.near_leaf(b)) continue;
+      const int t = B.row[b];
+      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+        if (pt.tk[i] != 'a') continue;
+        const int s = pt.ts[i];
+        const int bts = bx.find(t, s);
+        if (!bx.b->adm_leaf(bts) || rf.get(t, s)) continue;
+        // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
+        Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
+        g.out(m, false);
+        g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
+        rf.put(t, s, m);
+      }
+    }
+    g.run(C);
+  }
+  // all terminal triples (induced.py:286-307), one output per product block
+  {
+    GBatch g;
+    for (int b = 0; b < B.nb; ++b) {
+      const int t = B.row[b], r = B.col[b];
+      const bool dense = B.near_leaf(b);
+      const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
+      g.out(tgt, false);
+      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+        const int s = pt.ts[i];
+        const int bts = bx.find(t, s), bsr = by.find(s, r);
+        const char k = pt.tk[i];
+        if (k == 'a') {
+          const MatRef SY = y.coup(bsr);
+          const int ks = y.rb().rank[s], kr = y.cb().rank[r];
+          if (dense) {
+            g.t3(qr.xv.get(t, s)->ref(), SY, y.cb().leafm(r).tref(), ks, kr);
+          } else {
+            const Mat A = bx.b->adm_leaf(bts) ? *rf.get(t, s) : *qr.proj.get(t, s);
+            g.t3(A.ref(), SY, qc.bc[r].tref(), ks, kr);
+          }
+        } else if (k == 'b') {
+          const MatRef SX = x.coup(bts);
+          const int kt = x.rb().rank[t], ks = x.cb().rank[s];
+          if (dense) g.t3(x.rb().leafm(t).ref(), SX, qc.xv.get(r, s)->tref(), kt, ks);
+          else g.t3(qr.bc[t].ref(), SX, qc.proj.get(r, s)->tref(), kt, ks);
+        } else {
+          g.t2(x.near(bts), y.near(bsr), x.cols().size(s));
+        }
+      }
+    }
+    g.run(C);
+  }
+  // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
+  for (int lev = 0; lev < B.depth; ++lev) {
+    GBatch g1, g2;
+    for (int b : B.by_level[lev]) {
+      if (B.leaf(b)) continue;
+      const int t = B.row[b], r = B.col[b];
+      const Mat& S = cp[b];
+      for (int i = 0; i < B.nkids(b); ++i) {
+        const int ch = B.kid(b, i);
+        const int t2 = B.row[ch], r2 = B.col[ch];
+        Mat E, F;
+        if (t2 != t) E = Q.xferm(t2);
+        if (r2 != r) F = W.xferm(r2);
+        if (B.near_leaf(ch)) {
+          Mat part{sc.alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
+          g1.out(part, false);
+          emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
+          g2.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
+          g2.t3(Q.leafm(t2).ref(), part.ref(), W.leafm(r2).tref(), Q.rank[t2], W.rank[r2]);
+        } else {
+          g1.out(cp[ch], true);
+          emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
+        }
+      }
+    }
+    g1.run(C);
+    g2.run(C);
+  }
+  return G;  // scratch is released stream-ordered (cudaFreeAsync) after the queued work
+
+}
+
+static void record(Ctx& C, cudaEvent_t& e) {
+  if (!C.timing) return;
+  e = C.event();
+  cudaEventRecord(e, C.st);
+}
+
+static float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  if (a && b) cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Phase-1 driver (reference induced.py:358-372).
+std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling) {
+  if (!x.bt->cols->same(*y.bt->rows)) throw InvalidInput("x and y do not share the middle cluster tree");
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr, e4 = nullptr;
+  record(C, e0);
+  auto keep = std::make_shared<Arena>(C.st);
+  Arena sc(C.st);
+  HView X{&x, false}, Y{&y, false}, XT{&x, true}, YT{&y, true};
+  MatStore P = basis_product(C, sc, *x.cb, *y.rb);
+  MatStore rwy = basis_weights(C, sc, *y.cb);
+  MatStore zy = total_weights(C, sc, Y, rwy, scaling);
+  MatStore rwx = basis_weights(C, sc, *x.rb);
+  MatStore zxt = total_weights(C, sc, XT, rwx, scaling);
+  record(C, e1);
+  Induced qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+  record(C, e2);
+  Induced qc = induced_rows(C, *keep, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+  record(C, e3);
+  PTree pt = product_tree(X.bv(), Y.bv());
+  auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
+  record(C, e4);
+  G->owned.push_back(keep);
+  G->own_rows = x.own_rows;
+  G->own_cols = y.own_cols;
+  if (C.timing) {
+    C.sync();
+    C.times.setup = elapsed(e0, e1);
+    C.times.t1_row = elapsed(e1, e2);
+    C.times.t1_col = elapsed(e2, e3);
+    C.times.t1_mat = elapsed(e3, e4);
+  }
+  return G;
+}
+
+}  // namespace h2g

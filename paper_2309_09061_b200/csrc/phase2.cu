@@ -1,0 +1,758 @@
+// Phase 2 of the product: adaptive re-compression onto the prescribed block tree (Figs. 4-5) and
+// the final projection (reference coarsening.py:36-445), plus input recompression.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <map>
+
+#include "engine.h"
+
+namespace h2g {
+
+// ------------------------------------------------------------------ column trees (trees.py:362-406)
+struct CT {
+  std::vector<int> cl;
+  std::vector<char> adm;
+  std::vector<std::vector<int>> kids;
+  std::vector<Mat> mat;
+  int add(int c, bool a, Mat m = Mat{}) {
+    cl.push_back(c);
+    adm.push_back(a ? 1 : 0);
+    kids.emplace_back();
+    mat.push_back(m);
+    return (int)cl.size() - 1;
+  }
+  bool leaf(int u) const { return kids[u].empty(); }
+  void leaves(int u, std::vector<int>& out) const {
+    if (leaf(u)) { out.push_back(u); return; }
+    for (int k : kids[u]) leaves(k, out);
+  }
+};
+using CTP = std::shared_ptr<CT>;
+
+static int ct_copy(const CT& a, int u, CT& out, bool with_mats) {
+  const int v = out.add(a.cl[u], a.adm[u], with_mats ? a.mat[u] : Mat{});
+  for (int k : a.kids[u]) {
+    const int w = ct_copy(a, k, out, with_mats);
+    out.kids[v].push_back(w);
+  }
+  return v;
+}
+
+// Structure-only union (coarsening.py:89-105).
+static int ct_union(const CT* a, int ua, const CT* b, int ub, CT& out) {
+  if (!a) return ct_copy(*b, ub, out, false);
+  if (!b) return ct_copy(*a, ua, out, false);
+  if (a->cl[ua] != b->cl[ub]) throw StructureErr("column trees rooted at different clusters");
+  const bool ak = !a->leaf(ua), bk = !b->leaf(ub);
+  if (ak && bk) {
+    const int v = out.add(a->cl[ua], true);
+    const size_t n = std::min(a->kids[ua].size(), b->kids[ub].size());
+    for (size_t i = 0; i < n; ++i) {
+      const int w = ct_union(a, a->kids[ua][i], b, b->kids[ub][i], out);
+      out.kids[v].push_back(w);
+    }
+    return v;
+  }
+  if (ak) return ct_copy(*a, ua, out, false);
+  if (bk) return ct_copy(*b, ub, out, false);
+  return out.add(a->cl[ua], a->adm[ua] && b->adm[ub]);
+}
+
+// Deferred products  dst = src * F_{path[0]}^T * ... * F_{path[-1]}^T (* W_leaf^T)  (match_column,
+// coarsening.py:108-136), resolved with memoised prefix products in dependency waves.
+struct Jobs {
+  struct J {
+    Mat dst, src;
+    std::vector<int> path;
+    bool conv;
+    int leafcl;
+  };
+  std::vector<J> v;
+};
+
+static void ct_push_down(const Mat& src, std::vector<int>& path, const CT& T, int tu, int ro, Jobs& J) {
+  if (!T.leaf(tu)) {
+    for (int tc : T.kids[tu]) {
+      path.push_back(T.cl[tc]);
+      ct_push_down(src, path, T, tc, ro, J);
+      path.pop_back();
+    }
+    return;
+  }
+  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, path, !T.adm[tu], T.cl[tu]});
+}
+
+static void ct_match(const CT& P, int pu, const CT& T, int tu, int ro, Jobs& J) {
+  if (P.cl[pu] != T.cl[tu]) throw InvalidInput("representation and target roots differ");
+  if (!P.leaf(pu)) {
+    if (T.leaf(tu)) throw StructureErr("match_column: target coarser than representation");
+    for (size_t i = 0; i < P.kids[pu].size(); ++i) ct_match(P, P.kids[pu][i], T, T.kids[tu][i], ro, J);
+    return;
+  }
+  const Mat& src = P.mat[pu];
+  if (!T.leaf(tu)) {
+    std::vector<int> path;
+    for (int tc : T.kids[tu]) {
+      path.assign(1, T.cl[tc]);
+      ct_push_down(src, path, T, tc, ro, J);
+    }
+    return;
+  }
+  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, {}, P.adm[pu] && !T.adm[tu], T.cl[tu]});
+}
+
+static void resolve_jobs(Ctx& C, Arena& sc, Jobs& J, const Basis& w) {
+  std::map<std::pair<const double*, int>, Mat> inter;
+  std::vector<std::vector<std::pair<const Jobs::J*, int>>> waves;
+  for (const auto& j : J.v) {
+    const int nf = (int)j.path.size() + (j.conv ? 1 : 0);
+    const int L = nf - 2;
+    for (int i = 0; i < L; ++i) {
+      auto key = std::make_pair((const double*)j.src.p, j.path[i]);
+      if (inter.count(key)) continue;
+      inter[key] = Mat{sc.alloc((size_t)j.src.r * w.rank[j.path[i]]), j.src.r, w.rank[j.path[i]]};
+      if ((int)waves.size() <= i) waves.resize(i + 1);
+      waves[i].emplace_back(&j, i);
+    }
+  }
+  for (auto& wave : waves) {
+    GBatch g;
+    for (auto& pr : wave) {
+      const Jobs::J& j = *pr.first;
+      const int i = pr.second;
+      const Mat in = i == 0 ? j.src : inter[std::make_pair((const double*)j.src.p, j.path[i - 1])];
+      g.out(inter[std::make_pair((const double*)j.src.p, j.path[i])], false);
+      g.t2(in.ref(), w.xferm(j.path[i]).tref(), in.c);
+    }
+    g.run(C);
+  }
+  GBatch g;
+  for (const auto& j : J.v) {
+    const int nf = (int)j.path.size() + (j.conv ? 1 : 0);
+    const int L = std::max(0, nf - 2);
+    const Mat base = L > 0 ? inter[std::make_pair((const double*)j.src.p, j.path[L - 1])] : j.src;
+    std::vector<std::pair<MatRef, int>> f;  // remaining factors with their column counts
+    for (size_t i = L; i < j.path.size(); ++i) f.emplace_back(w.xferm(j.path[i]).tref(), w.rank[j.path[i]]);
+    if (j.conv) f.emplace_back(w.leafm(j.leafcl).tref(), w.tree->size(j.leafcl));
+    g.out(j.dst, false);
+    if (f.empty()) g.t1(base.ref());
+    else if (f.size() == 1) g.t2(base.ref(), f[0].first, base.c);
+    else g.t3(base.ref(), f[0].first, f[1].first, base.c, f[0].second);
+  }
+  g.run(C);
+  J.v.clear();
+}
+
+// ------------------------------------------------------------------ coverage (coarsening.py:160-184)
+static void validate_coarse(BView pt, BView coarse) {
+  if (!(pt.rows().same(coarse.rows()) && pt.cols().same(coarse.cols())))
+    throw InvalidInput("coarse tree lives on different cluster trees");
+  for (int b = 0; b < coarse.nb(); ++b)
+    if (pt.find(coarse.row(b), coarse.col(b)) < 0)
+      throw InvalidInput("coarse block is finer than the product block tree");
+}
+
+static std::vector<char> coverage(BView pt, BView coarse) {
+  std::vector<char> cov(pt.nb(), 0);
+  struct F { int pb, cb, state; };  // state: 0 none, 1 admissible, 2 inadmissible
+  std::vector<F> st{{0, 0, 0}};
+  while (!st.empty()) {
+    F f = st.back();
+    st.pop_back();
+    if (f.state == 0 && f.cb >= 0 && coarse.b->leaf(f.cb)) f.state = coarse.b->adm[f.cb] ? 1 : 2;
+    cov[f.pb] = f.state == 1;
+    for (int i = 0; i < pt.b->nkids(f.pb); ++i) {
+      const int ch = pt.b->kid(f.pb, i);
+      const int cb = f.state == 0 ? coarse.find(pt.row(ch), pt.col(ch)) : -1;
+      st.push_back(F{ch, cb, f.state});
+    }
+  }
+  return cov;
+}
+
+struct CState {
+  std::shared_ptr<Basis> q;
+  MatStore r, z;
+  std::vector<CTP> reps;
+};
+
+// Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
+static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
+                          const std::vector<double>& cn, const std::vector<double>& nn) {
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  const BView pv = g.bv();
+  const Blocks& pt = *g.h->bt;
+  validate_coarse(pv, coarse);
+  const std::vector<char> cov = coverage(pv, coarse);
+  const Tree& tr = pv.rows();
+  const Basis& v1 = g.rb();
+  const Basis& w1 = g.cb();
+  std::vector<std::vector<int>> row_adm(tr.n), near_cov(tr.n), sub_cov(tr.n);
+  for (int b = 0; b < pt.nb; ++b) {
+    const int t = pv.row(b);
+    if (pt.adm_leaf(b)) row_adm[t].push_back(b);
+    else if (pt.near_leaf(b)) { if (cov[b]) near_cov[t].push_back(b); }
+    else if (cov[b]) sub_cov[t].push_back(b);
+  }
+  CState S;
+  S.q = std::make_shared<Basis>();
+  Basis& q = *S.q;
+  q.tree = &tr;
+  q.rank.assign(tr.n, 0);
+  q.leaf.assign(tr.n, nullptr);
+  q.xfer.assign(tr.n, nullptr);
+  S.r.assign(tr.n, Mat{});
+  S.z.assign(tr.n, Mat{});
+  S.reps.assign(pt.nb, nullptr);
+  Arena sc(C.st);
+
+  // top-down condensation weights Z_t (coarsening.py:231-245)
+  for (int lev = 0; lev <= tr.depth; ++lev) {
+    GBatch ge;
+    QrBatch qb;
+    for (int t : tr.by_level[lev]) {
+      const int k = v1.rank[t];
+      QrItem it{};
+      it.s0 = qb.sl.begin();
+      it.n = k;
+      long long M = 0;
+      const int p = tr.parent[t];
+      if (p >= 0 && S.z[p].r > 0) {
+        Mat ze{sc.alloc((size_t)S.z[p].r * k), S.z[p].r, k};
+        ge.out(ze, false);
+        ge.t2(S.z[p].ref(), v1.xferm(t).tref(), S.z[p].c);
+        qb.sl.add(ze.ref(), ze.r);
+        M += ze.r;
+      }
+      for (int b : row_adm[t]) {
+        if (scale && cn[b] == 0.0) continue;
+        const int kc = w1.rank[pv.col(b)];
+        qb.sl.add(trn(g.coup(b)), kc, scale ? 1.0 / cn[b] : 1.0);
+        M += kc;
+      }
+      it.s1 = qb.sl.begin();
+      it.M = M;
+      const int rows = (int)std::min<long long>(M, k);
+      S.z[t] = Mat{sc.alloc((size_t)rows * k), rows, k};
+      it.out = S.z[t].p;
+      qb.items.push_back(it);
+    }
+    ge.run(C);
+    qb.run(C, sc);
+  }
+
+  std::vector<Mat> lm(pt.nb);  // R_t S_b for admissible leaves used inside representations
+  for (int lev = tr.depth; lev >= 0; --lev) {
+    const std::vector<int>& L = tr.by_level[lev];
+    const size_t nl = L.size();
+    GBatch g1, g2;
+    std::vector<Mat> V(nl), VZ(nl);
+    for (size_t li = 0; li < nl; ++li) {
+      const int t = L[li];
+      const Mat& Z = S.z[t];
+      if (tr.leaf(t)) {
+        V[li] = v1.leafm(t);
+      } else {
+        int m = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
+        V[li] = Mat{sc.alloc((size_t)m * v1.rank[t]), m, v1.rank[t]};
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {  // vhat = vstack(R_c E_c) (coarsening.py:313-314)
+          const int c = tr.kid(t, i);
+          g1.out(V[li].band(off, q.rank[c]), false);
+          g1.t2(S.r[c].ref(), v1.xferm(c).ref(), S.r[c].c);
+          off += q.rank[c];
+        }
+        for (int b : sub_cov[t])
+          for (int i = 0; i < pt.nkids(b); ++i) {  // child_rep of admissible children (coarsening.py:254-258)
+            const int b2 = pt.kid(b, i);
+            if (!pt.adm_leaf(b2) || lm[b2].p) continue;
+            const int t2 = pv.row(b2), r2 = pv.col(b2);
+            lm[b2] = Mat{sc.alloc((size_t)q.rank[t2] * w1.rank[r2]), q.rank[t2], w1.rank[r2]};
+            g1.out(lm[b2], false);
+            g1.t2(S.r[t2].ref(), g.coup(b2), S.r[t2].c);
+          }
+      }
+      VZ[li] = Mat{sc.alloc((size_t)V[li].r * Z.r), V[li].r, Z.r};
+      GBatch& gz = tr.leaf(t) ? g1 : g2;
+      gz.out(VZ[li], false);
+      gz.t2(V[li].ref(), Z.tref(), Z.c);
+    }
+    g1.run(C);
+    g2.run(C);
+
+    // merged representations of subdivided covered blocks (coarsening.py:260-279)
+    std::map<int, CTP> merged;
+    Jobs J;
+    for (size_t li = 0; li < nl; ++li) {
+      const int t = L[li];
+      if (tr.leaf(t)) continue;
+      for (int b : sub_cov[t]) {
+        std::vector<int> order;
+        std::map<int, std::vector<std::pair<CTP, int>>> groups;  // r2 -> (part, rows)
+        for (int i = 0; i < pt.nkids(b); ++i) {
+          const int b2 = pt.kid(b, i);
+          const int r2 = pv.col(b2);
+          CTP part;
+          if (pt.adm_leaf(b2)) {
+            part = std::make_shared<CT>();
+            part->add(r2, true, lm[b2]);
+          } else {
+            part = S.reps[b2];
+            if (!part) throw StructureErr("missing child representation");
+          }
+          if (!groups.count(r2)) order.push_back(r2);
+          groups[r2].emplace_back(part, q.rank[pv.row(b2)]);
+        }
+        std::map<int, CTP> per;
+        for (int r2 : order) {
+          auto& parts = groups[r2];
+          CTP tgt = std::make_shared<CT>();
+          {
+            CT acc;
+            ct_union(nullptr, 0, parts[0].first.get(), 0, acc);
+            for (size_t i = 1; i < parts.size(); ++i) {
+              CT nxt;
+              ct_union(&acc, 0, parts[i].first.get(), 0, nxt);
+              acc = std::move(nxt);
+            }
+            *tgt = std::move(acc);
+          }
+          int rows = 0;
+          for (auto& pr : parts) rows += pr.second;
+          std::vector<int> lv;
+          tgt->leaves(0, lv);
+          for (int u : lv) {
+            const int c = tgt->cl[u];
+            const int cols = tgt->adm[u] ? w1.rank[c] : w1.tree->size(c);
+            tgt->mat[u] = Mat{sc.alloc((size_t)rows * cols), rows, cols};
+          }
+          int ro = 0;
+          for (auto& pr : parts) {
+            ct_match(*pr.first, 0, *tgt, 0, ro, J);
+            ro += pr.second;
+          }
+          per[r2] = tgt;
+        }
+        const int r = pv.col(b);
+        if (order.size() == 1 && order[0] == r) {
+          merged[b] = per[r];
+        } else {
+          CTP w = std::make_shared<CT>();
+          const int root = w->add(r, true);
+          for (int r2 : order) {
+            const int k = ct_copy(*per[r2], 0, *w, true);
+            w->kids[root].push_back(k);
+          }
+          merged[b] = w;
+        }
+      }
+    }
+    resolve_jobs(C, sc, J, w1);
+
+    // scales of the flattened merged reps (coarsening.py:316-317)
+    std::map<int, double> msc;
+    if (scale && !merged.empty()) {
+      NormBatch nbat;
+      std::vector<int> ids;
+      for (auto& kv : merged) {
+        std::vector<int> lv;
+        kv.second->leaves(0, lv);
+        NormItem it{};
+        it.s0 = nbat.sl.begin();
+        long long N = 0;
+        for (int u : lv) {
+          nbat.sl.add(kv.second->mat[u].ref(), kv.second->mat[u].c);
+          N += kv.second->mat[u].c;
+        }
+        it.s1 = nbat.sl.begin();
+        it.m = lv.empty() ? 0 : kv.second->mat[lv[0]].r;
+        it.N = N;
+        nbat.items.push_back(it);
+        ids.push_back(kv.first);
+      }
+      auto v = nbat.run(C, sc);
+      for (size_t i = 0; i < ids.size(); ++i) msc[ids[i]] = v[i];
+    }
+
+    // truncated SVDs of C_t = [V Z^T | scaled columns] (coarsening.py:294-326)
+    SvdBatch sv;
+    std::vector<Mat> qbuf(nl);
+    for (size_t li = 0; li < nl; ++li) {
+      const int t = L[li];
+      const int m = V[li].r;
+      SvdItem it{};
+      it.s0 = sv.sl.begin();
+      sv.sl.add(VZ[li].ref(), VZ[li].c);
+      long long N = VZ[li].c;
+      if (tr.leaf(t)) {
+        for (int b : near_cov[t]) {
+          const int w = w1.tree->size(pv.col(b));
+          const double s = (scale && nn[b] > 0.0) ? 1.0 / nn[b] : 1.0;
+          sv.sl.add(g.near(b), w, s);
+          N += w;
+        }
+      } else {
+        for (int b : sub_cov[t]) {
+          const CT& M = *merged[b];
+          std::vector<int> lv;
+          M.leaves(0, lv);
+          const double nv = scale ? msc[b] : 0.0;
+          const double s = (scale && nv > 0.0) ? 1.0 / nv : 1.0;
+          for (int u : lv) {
+            sv.sl.add(M.mat[u].ref(), M.mat[u].c, s);
+            N += M.mat[u].c;
+          }
+        }
+      }
+      it.s1 = sv.sl.begin();
+      it.m = m;
+      it.kx = 0;
+      it.N = N;
+      it.tol = tol;
+      it.cap = max_rank;
+      const long long kcap = std::min<long long>(m, N);
+      qbuf[li] = Mat{out.alloc((size_t)m * std::max<long long>(kcap, 0)), m, (int)kcap};
+      it.q_out = qbuf[li].p;
+      sv.items.push_back(it);
+    }
+    std::vector<int> rk = sv.run(C, sc);
+
+    GBatch gp, gq;
+    for (size_t li = 0; li < nl; ++li) {
+      const int t = L[li];
+      const int k = rk[li];
+      const Mat Q{qbuf[li].p, V[li].r, k};
+      q.rank[t] = k;
+      S.r[t] = Mat{out.alloc((size_t)k * V[li].c), k, V[li].c};
+      gp.out(S.r[t], false);  // R_t = Q_t^T V_t
+      gp.t2(Q.tref(), V[li].ref(), Q.r);
+      if (tr.leaf(t)) {
+        q.leaf[t] = Q.p;
+        for (int b : near_cov[t]) {  // reps: Q_t^T N (coarsening.py:306-307)
+          const int r = pv.col(b);
+          Mat rep{out.alloc((size_t)k * w1.tree->size(r)), k, w1.tree->size(r)};
+          gp.out(rep, false);
+          gp.t2(Q.tref(), g.near(b), Q.r);
+          CTP c = std::make_shared<CT>();
+          c->add(r, false, rep);
+          S.reps[b] = c;
+        }
+      } else {
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {
+          const int c = tr.kid(t, i);
+          q.xfer[c] = Q.p + (long long)off * k;
+          off += q.rank[c];
+        }
+        for (int b : sub_cov[t]) {  // stored reps are Q^T (unscaled rep) (coarsening.py:327-328)
+          const CT& M = *merged[b];
+          CTP c = std::make_shared<CT>();
+          ct_copy(M, 0, *c, false);
+          std::vector<int> lv;
+          c->leaves(0, lv);
+          for (int u : lv) {
+            const Mat& src = M.mat[u];
+            c->mat[u] = Mat{out.alloc((size_t)k * src.c), k, src.c};
+            gp.out(c->mat[u], false);
+            gp.t2(Q.tref(), src.ref(), Q.r);
+          }
+          S.reps[b] = c;
+        }
+      }
+    }
+    gp.run(C);
+    // compose_leaf_rep for subdivided covered blocks at leaf row clusters (coarsening.py:281-290)
+    for (size_t li = 0; li < nl; ++li) {
+      const int t = L[li];
+      if (!tr.leaf(t)) continue;
+      std::function<int(CT&, int)> build = [&](CT& T, int b) -> int {
+        const int r = pv.col(b);
+        if (pt.adm_leaf(b)) {
+          if (!lm[b].p) {
+            lm[b] = Mat{out.alloc((size_t)q.rank[t] * w1.rank[r]), q.rank[t], w1.rank[r]};
+            gq.out(lm[b], false);
+            gq.t2(S.r[t].ref(), g.coup(b), S.r[t].c);
+          }
+          return T.add(r, true, lm[b]);
+        }
+        if (pt.near_leaf(b)) return T.add(r, false, S.reps[b]->mat[0]);
+        const int v = T.add(r, true);
+        for (int i = 0; i < pt.nkids(b); ++i) {
+          const int w = build(T, pt.kid(b, i));
+          T.kids[v].push_back(w);
+        }
+        return v;
+      };
+      std::function<void(int)> all = [&](int b) {
+        if (pt.leaf(b)) return;
+        CTP c = std::make_shared<CT>();
+        build(*c, b);
+        S.reps[b] = c;
+        for (int i = 0; i < pt.nkids(b); ++i) all(pt.kid(b, i));
+      };
+      for (int b : sub_cov[t]) all(b);
+    }
+    gq.run(C);
+  }
+  return S;
+}
+
+// Final projection (reference coarsening.py:354-405).
+static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs,
+                                         std::shared_ptr<const Blocks> coarse, ArenaPtr ar) {
+  const BView pv = g.bv();
+  const BView cv{coarse.get(), false};
+  validate_coarse(pv, cv);
+  auto Z = std::make_shared<H2>();
+  Z->bt = coarse;
+  Z->rb = rs.q;
+  Z->cb = cs.q;
+  Z->owned.push_back(ar);
+  const Blocks& cb = *coarse;
+  const Blocks& pt = *g.h->bt;
+  const Basis& qr = *rs.q;
+  const Basis& qc = *cs.q;
+  const Tree& ctree = *cb.cols;
+  Z->coup.assign(cb.nb, nullptr);
+  Z->near.assign(cb.nb, nullptr);
+  Arena sc(C.st);
+  // chain(r, c) = F'_c F'_parent ... (k'_c x k'_r), memoised, depth >= 2 materialised in waves
+  std::map<std::pair<int, int>, Mat> chain;
+  std::vector<std::vector<std::pair<int, int>>> waves;
+  std::function<void(int, int)> need = [&](int r, int c) {
+    if (ctree.parent[c] == r || c == r) return;
+    auto key = std::make_pair(r, c);
+    if (chain.count(key)) return;
+    need(r, ctree.parent[c]);
+    int d = 0;
+    for (int u = c; u != r; u = ctree.parent[u]) ++d;
+    chain[key] = Mat{sc.alloc((size_t)qc.rank[c] * qc.rank[r]), qc.rank[c], qc.rank[r]};
+    if ((int)waves.size() <= d) waves.resize(d + 1);
+    waves[d].push_back(key);
+  };
+  auto chain_ref = [&](int r, int c) -> Mat {
+    if (ctree.parent[c] == r) return qc.xferm(c);
+    return chain[std::make_pair(r, c)];
+  };
+  // collect the needed chains
+  for (int b = 0; b < cb.nb; ++b) {
+    if (!cb.adm_leaf(b)) continue;
+    const int pb = pt.find(cb.row[b], cb.col[b]);
+    if (pt.adm_leaf(pb)) continue;
+    const CT& rep = *rs.reps[pb];
+    std::vector<int> lv;
+    rep.leaves(0, lv);
+    for (int u : lv) need(cb.col[b], rep.cl[u]);
+  }
+  for (auto& wave : waves) {
+    GBatch gw;
+    for (auto& key : wave) {
+      const int r = key.first, c = key.second;
+      gw.out(chain[key], false);
+      const Mat up = chain_ref(r, ctree.parent[c]);
+      gw.t2(qc.xferm(c).ref(), up.ref(), qc.rank[ctree.parent[c]]);
+    }
+    gw.run(C);
+  }
+  GBatch g1;
+  for (int b = 0; b < cb.nb; ++b) {
+    if (!cb.leaf(b)) continue;
+    const int t = cb.row[b], r = cb.col[b];
+    const int pb = pt.find(t, r);
+    if (cb.adm[b]) {
+      Mat S{ar->alloc((size_t)qr.rank[t] * qc.rank[r]), qr.rank[t], qc.rank[r]};
+      Z->coup[b] = S.p;
+      g1.out(S, false);
+      if (pt.adm_leaf(pb)) {
+        g1.t3(rs.r[t].ref(), g.coup(pb), cs.r[r].tref(), rs.r[t].c, cs.r[r].c);
+      } else {
+        const CT& rep = *rs.reps[pb];
+        std::vector<int> lv;
+        rep.leaves(0, lv);
+        for (int u : lv) {  // lift (coarsening.py:374-382)
+          const int c = rep.cl[u];
+          const Mat& M = rep.mat[u];
+          const MatRef X = rep.adm[u] ? cs.r[c].tref() : qc.leafm(c).ref();
+          if (c == r) g1.t2(M.ref(), X, M.c);
+          else g1.t3(M.ref(), X, chain_ref(r, c).ref(), M.c, qc.rank[c]);
+        }
+      }
+    } else {
+      const int nr = cb.rows->size(t), nc = ctree.size(r);
+      Mat N{ar->alloc((size_t)nr * nc), nr, nc};
+      Z->near[b] = N.p;
+      g1.out(N, false);
+      if (pt.near_leaf(pb)) g1.t1(g.near(pb));
+      else if (pt.adm_leaf(pb)) g1.t3(g.rb().leafm(t).ref(), g.coup(pb), g.cb().leafm(r).tref(), g.rb().rank[t], g.cb().rank[r]);
+      else throw StructureErr("inadmissible coarse leaf is subdivided in the product tree");
+    }
+  }
+  g1.run(C);
+  return Z;
+}
+
+static std::vector<double> all_norms(Ctx& C, Arena& sc, const H2& g, bool coupling) {
+  const Blocks& B = *g.bt;
+  NormBatch nb;
+  std::vector<int> ids;
+  HView v{&g, false};
+  for (int b = 0; b < B.nb; ++b) {
+    if (coupling ? !B.adm_leaf(b) : !B.near_leaf(b)) continue;
+    const int t = B.row[b], s = B.col[b];
+    const int m = coupling ? g.rb->rank[t] : B.rows->size(t);
+    const int n = coupling ? g.cb->rank[s] : B.cols->size(s);
+    NormItem it{};
+    it.s0 = nb.sl.begin();
+    nb.sl.add(coupling ? v.coup(b) : v.near(b), n);
+    it.s1 = nb.sl.begin();
+    it.m = m;
+    it.N = n;
+    nb.items.push_back(it);
+    ids.push_back(b);
+  }
+  std::vector<double> out(B.nb, 0.0);
+  auto vals = nb.run(C, sc);
+  for (size_t i = 0; i < ids.size(); ++i) out[ids[i]] = vals[i];
+  return out;
+}
+
+// Phase-2 driver (reference coarsening.py:408-422).
+std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
+                            bool scale) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
+  Arena sc(C.st);
+  std::vector<double> cn, nn;
+  if (scale) {
+    cn = all_norms(C, sc, g, true);
+    nn = all_norms(C, sc, g, false);
+  }
+  auto ar = std::make_shared<Arena>(C.st);
+  CState rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, nn);
+  if (C.timing) { e1 = C.event(); cudaEventRecord(e1, C.st); }
+  CState cs = coarse_rows(C, *ar, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, nn);
+  if (C.timing) { e2 = C.event(); cudaEventRecord(e2, C.st); }
+  auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar);
+  Z->own_rows = g.own_rows;
+  Z->own_cols = g.own_cols;
+  if (C.timing) {
+    e3 = C.event();
+    cudaEventRecord(e3, C.st);
+    C.sync();
+    cudaEventElapsedTime(&C.times.t2_row, e0, e1);
+    cudaEventElapsedTime(&C.times.t2_col, e1, e2);
+    cudaEventElapsedTime(&C.times.t2_mat, e2, e3);
+  }
+  return Z;
+}
+
+// Isometric re-factorisation, exact-zero directions dropped (reference h2.py:79-113).
+static std::shared_ptr<Basis> orthogonalize(Ctx& C, Arena& out, const Basis& B, MatStore& rmap) {
+  const Tree& tr = *B.tree;
+  auto q = std::make_shared<Basis>();
+  q->tree = &tr;
+  q->rank.assign(tr.n, 0);
+  q->leaf.assign(tr.n, nullptr);
+  q->xfer.assign(tr.n, nullptr);
+  rmap.assign(tr.n, Mat{});
+  Arena sc(C.st);
+  for (int lev = tr.depth; lev >= 0; --lev) {
+    const auto& L = tr.by_level[lev];
+    GBatch g;
+    SvdBatch sv;
+    std::vector<Mat> st(L.size()), qb(L.size());
+    for (size_t li = 0; li < L.size(); ++li) {
+      const int t = L[li];
+      if (tr.leaf(t)) {
+        st[li] = B.leafm(t);
+      } else {
+        int m = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) m += rmap[tr.kid(t, i)].r;
+        st[li] = Mat{sc.alloc((size_t)m * B.rank[t]), m, B.rank[t]};
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {
+          const int c = tr.kid(t, i);
+          g.out(st[li].band(off, rmap[c].r), false);
+          g.t2(rmap[c].ref(), B.xferm(c).ref(), rmap[c].c);
+          off += rmap[c].r;
+        }
+      }
+      SvdItem it{};
+      it.s0 = sv.sl.begin();
+      sv.sl.add(st[li].ref(), st[li].c);
+      it.s1 = sv.sl.begin();
+      it.m = st[li].r;
+      it.N = st[li].c;
+      it.tol = 0.0;
+      it.cap = -1;
+      const int kc = std::min(st[li].r, st[li].c);
+      qb[li] = Mat{out.alloc((size_t)st[li].r * kc), st[li].r, kc};
+      it.q_out = qb[li].p;
+      sv.items.push_back(it);
+    }
+    g.run(C);
+    std::vector<int> rk = sv.run(C, sc);
+    GBatch g2;
+    for (size_t li = 0; li < L.size(); ++li) {
+      const int t = L[li];
+      const int k = rk[li];
+      const Mat Q{qb[li].p, st[li].r, k};
+      q->rank[t] = k;
+      rmap[t] = Mat{out.alloc((size_t)k * st[li].c), k, st[li].c};  // sigma V^T = U^T stacked
+      g2.out(rmap[t], false);
+      g2.t2(Q.tref(), st[li].ref(), Q.r);
+      if (tr.leaf(t)) {
+        q->leaf[t] = Q.p;
+      } else {
+        int off = 0;
+        for (int i = 0; i < tr.nkids(t); ++i) {
+          const int c = tr.kid(t, i);
+          q->xfer[c] = Q.p + (long long)off * k;
+          off += q->rank[c];
+        }
+      }
+    }
+    g2.run(C);
+  }
+  return q;
+}
+
+// Input preparation: orthogonalise, then coarsen onto the own block tree (coarsening.py:425-445).
+std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank) {
+  auto ar = std::make_shared<Arena>(C.st);
+  MatStore rr, rc;
+  auto qr = orthogonalize(C, *ar, *g.rb, rr);
+  std::shared_ptr<Basis> qc;
+  if (g.cb == g.rb) {
+    qc = qr;
+    rc = rr;
+  } else {
+    qc = orthogonalize(C, *ar, *g.cb, rc);
+  }
+  H2 o;
+  o.bt = g.bt;
+  o.rb = qr;
+  o.cb = qc;
+  o.near = g.near;
+  o.owned = g.owned;
+  o.owned.push_back(ar);
+  o.own_rows = g.own_rows;
+  o.own_cols = g.own_cols;
+  o.coup.assign(g.bt->nb, nullptr);
+  GBatch gb;
+  HView v{&g, false};
+  for (int b = 0; b < g.bt->nb; ++b) {
+    if (!g.bt->adm_leaf(b)) continue;
+    const int t = g.bt->row[b], s = g.bt->col[b];
+    Mat S{ar->alloc((size_t)rr[t].r * rc[s].r), rr[t].r, rc[s].r};
+    o.coup[b] = S.p;
+    gb.out(S, false);
+    gb.t3(rr[t].ref(), v.coup(b), rc[s].tref(), rr[t].c, rc[s].c);
+  }
+  gb.run(C);
+  return coarsen(C, o, g.bt, tol, max_rank, true);
+}
+
+}  // namespace h2g

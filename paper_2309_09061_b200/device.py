@@ -1,0 +1,205 @@
+"""Device-resident objects: context, cluster / block trees and H^2 matrices on the GPU.
+
+`DeviceH2` is the GPU counterpart of h2mul.H2Matrix (reference h2.py:148-194): the block tree
+and the bases / couplings / nearfield live in device arenas owned by the native library; the
+host keeps the structure (trees, block tree) needed to rebuild an `H2Matrix` on download.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .errors import CudaError, InvalidInputError
+from .h2 import H2Matrix
+from .packed import pack_h2, unpack_h2
+from .trees import BlockTree
+
+__all__ = ["Context", "DeviceH2", "default_context"]
+
+
+class Context:
+    """One native context per device: a CUDA stream plus pinned staging (h2g_ctx)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise CudaError("no CUDA device: the B200 product path has no CPU fallback")
+        self.lib = N.load()
+        self.device = device
+        h = N.P()
+        N.check(self.lib.h2g_ctx_create(device, stream, C.byref(h)))
+        self.h = h
+        self._trees = {}
+        self._blocks = {}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                for b in self._blocks.values():
+                    self.lib.h2g_blocks_destroy(b[0])
+                for t in self._trees.values():
+                    self.lib.h2g_tree_destroy(t[0])
+                self.lib.h2g_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+    def set_timing(self, on: bool):
+        N.check(self.lib.h2g_ctx_set_timing(self.h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        out = np.zeros(7)
+        N.check(self.lib.h2g_ctx_stage_times(self.h, out.ctypes.data_as(N.F64P)))
+        keys = ["t_setup", "t1_row", "t1_col", "t1_mat", "t2_row", "t2_col", "t2_mat"]
+        return {k: float(v) / 1e3 for k, v in zip(keys, out)}
+
+    def counters(self, reset: bool = False) -> dict:
+        out = np.zeros(2, np.int64)
+        N.check(self.lib.h2g_ctx_counters(self.h, out.ctypes.data_as(N.I64P), 1 if reset else 0))
+        return {"launches": int(out[0]), "syncs": int(out[1])}
+
+    def synchronize(self):
+        N.check(self.lib.h2g_ctx_synchronize(self.h))
+
+    # structure handles are cached per host object (trees and block trees are immutable)
+    def tree(self, tree):
+        key = id(tree)
+        if key in self._trees and self._trees[key][1] is tree:
+            return self._trees[key][0]
+        f = tree.flat()
+        arrs = [N.i64(tree.start), N.i64(tree.stop), N.i64(f["child_ptr"]), N.i64(f["child_idx"])]
+        h = N.P()
+        N.check(self.lib.h2g_tree_create(self.h, tree.nnodes, *[a[1] for a in arrs], C.byref(h)))
+        self._trees[key] = (h, tree)
+        return h
+
+    def blocks(self, bt: BlockTree):
+        key = id(bt)
+        if key in self._blocks and self._blocks[key][1] is bt:
+            return self._blocks[key][0]
+        f = bt.flat()
+        adm = np.asarray(bt.admissible, dtype=np.uint8)
+        arrs = [N.i64(f["row"]), N.i64(f["col"]), N.i64(f["child_ptr"]), N.i64(f["child_idx"])]
+        a8 = N.u8(adm)
+        h = N.P()
+        N.check(self.lib.h2g_blocks_create(self.h, self.tree(bt.rows), self.tree(bt.cols), bt.nblocks,
+                                           *[a[1] for a in arrs], a8[1], C.byref(h)))
+        self._blocks[key] = (h, bt)
+        return h
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+class DeviceH2:
+    """An H^2 matrix resident on the GPU (handle to a native h2g_h2)."""
+
+    def __init__(self, ctx: Context, handle, block_tree: BlockTree | None, rows, cols):
+        self.ctx = ctx
+        self.h = handle
+        self._bt = block_tree
+        self.rows, self.cols = rows, cols
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.h2g_h2_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @classmethod
+    def upload(cls, g: H2Matrix, ctx: Context | None = None) -> "DeviceH2":
+        ctx = ctx or default_context()
+        d = pack_h2(g)
+        share = g.row_basis is g.col_basis
+        a = {k: (N.f64(v) if k.endswith("data") else N.i64(v)) for k, v in d.items()
+             if not k.startswith(("rows.", "cols.", "bt."))}
+        h = N.P()
+        N.check(ctx.lib.h2g_h2_upload(
+            ctx.h, ctx.blocks(g.block_tree),
+            a["rb.rank"][1], a["rb.leaf_off"][1], a["rb.xfer_off"][1], a["rb.data"][1], len(a["rb.data"][0]),
+            a["cb.rank"][1], a["cb.leaf_off"][1], a["cb.xfer_off"][1], a["cb.data"][1], len(a["cb.data"][0]),
+            1 if share else 0,
+            a["coup_off"][1], a["coup_data"][1], len(a["coup_data"][0]),
+            a["near_off"][1], a["near_data"][1], len(a["near_data"][0]), C.byref(h)))
+        return cls(ctx, h, g.block_tree, g.block_tree.rows, g.block_tree.cols)
+
+    def sizes(self):
+        out = np.zeros(8, np.int64)
+        N.check(self.ctx.lib.h2g_h2_sizes(self.h, out.ctypes.data_as(N.I64P)))
+        return out
+
+    @property
+    def block_tree(self) -> BlockTree:
+        if self._bt is None:
+            s = self.sizes()
+            nb = int(s[0])
+            row, col = np.zeros(nb, np.int64), np.zeros(nb, np.int64)
+            ptr, idx = np.zeros(nb + 1, np.int64), np.zeros(int(s[7]), np.int64)
+            adm = np.zeros(nb, np.uint8)
+            N.check(self.ctx.lib.h2g_h2_structure(self.h, row.ctypes.data_as(N.I64P), col.ctypes.data_as(N.I64P),
+                                                  ptr.ctypes.data_as(N.I64P), idx.ctypes.data_as(N.I64P),
+                                                  adm.ctypes.data_as(N.U8P)))
+            kids = [tuple(int(c) for c in idx[ptr[b]:ptr[b + 1]]) for b in range(nb)]
+            self._bt = BlockTree(self.rows, self.cols, row, col, kids, adm.astype(bool))
+        return self._bt
+
+    def to_packed(self) -> dict:
+        s = self.sizes()
+        nb, nr, nc = int(s[0]), int(s[1]), int(s[2])
+        d = {}
+        for p, n, ln in (("rb.", nr, s[3]), ("cb.", nc, s[4])):
+            d[p + "rank"] = np.zeros(n, np.int64)
+            d[p + "leaf_off"] = np.zeros(n, np.int64)
+            d[p + "xfer_off"] = np.zeros(n, np.int64)
+            d[p + "data"] = np.zeros(int(ln))
+        d["coup_off"], d["coup_data"] = np.zeros(nb, np.int64), np.zeros(int(s[5]))
+        d["near_off"], d["near_data"] = np.zeros(nb, np.int64), np.zeros(int(s[6]))
+
+        def ip(k):
+            return d[k].ctypes.data_as(N.I64P)
+
+        def fp(k):
+            return d[k].ctypes.data_as(N.F64P)
+
+        N.check(self.ctx.lib.h2g_h2_download(
+            self.ctx.h, self.h, ip("rb.rank"), ip("rb.leaf_off"), ip("rb.xfer_off"), fp("rb.data"),
+            ip("cb.rank"), ip("cb.leaf_off"), ip("cb.xfer_off"), fp("cb.data"),
+            ip("coup_off"), fp("coup_data"), ip("near_off"), fp("near_data")))
+        bt = self.block_tree
+        f = bt.flat()
+        d["bt.row"], d["bt.col"] = f["row"], f["col"]
+        d["bt.child_ptr"], d["bt.child_idx"] = f["child_ptr"], f["child_idx"]
+        d["bt.adm"] = np.asarray(bt.admissible, dtype=np.uint8)
+        return d
+
+    def download(self) -> H2Matrix:
+        """Host H2Matrix with the reference's container interface."""
+        return unpack_h2(self.to_packed(), rows=self.rows, cols=self.cols)
+
+    @property
+    def ranks(self):
+        d = self.to_packed_ranks()
+        return d
+
+    def to_packed_ranks(self):
+        """(row ranks, column ranks) without moving matrix data (downloads sizes only)."""
+        return self.download_ranks()
+
+    def download_ranks(self):
+        d = self.to_packed()
+        return list(d["rb.rank"]), list(d["cb.rank"])
+
+
+def check_same_trees(a, b):
+    if not (a.nnodes == b.nnodes and np.array_equal(a.start, b.start) and np.array_equal(a.stop, b.stop)):
+        raise InvalidInputError("cluster trees differ")
