@@ -1,0 +1,344 @@
+"""Benchmark: the adaptive H^2 x H^2 product (multiply + coarsen) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--n N] [--impl ours|reference]
+
+One step = one full product Z = X*Y on the BASELINE config (default configs[1] = c2: n=16384 2-D
+uniform points, -log kernel, leaf 64, eta 1, Chebyshev order 4, eps 1e-6), i.e. phase 1
+(basis products + weights + induced bases + assembly over T^XY) followed by phase 2
+(re-compression onto X's block tree) -- the stages the reference harness times
+(bench.py:195-237 of h2mul; its t_total excludes only the weights, which we include).
+Inputs are built by the reference's interpolation recipe (synthetic seeded points) and
+recompressed at eps on the GPU before timing.  Metric: DOF/s = n / product time.
+
+--impl reference times the CPU oracle (a NumPy restatement of h2mul, oracle/) with all host
+threads on a bounded sample (the same generator at a reduced n) -- the reference arm.
+Multi-GPU (N > 1): independent replicas, one product per rank (weak scaling); the sharded
+product is future work.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=8192)
+    ap.add_argument("--profile-json", default=None, help="write per-stage / per-kernel detail here")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def reduce_max(value: float, device) -> float:
+    """Max over ranks (device timings are reported as the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def fp64_peak_tflops():
+    """cuBLAS DGEMM 8192^3 on this GPU (MEASURED_PEAKS.json has no FP64 entry)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn_like(a)
+    a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * n ** 3 / best / 1e9
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def build_inputs(cfg, n):
+    from paper_2309_09061_b200.problems import build_config
+    xr, yr, spec = build_config(cfg, n=n)
+    return xr, yr, spec
+
+
+def cpu_oracle_run(cfg, n, threads):
+    """Time the CPU oracle on the config's generator at size n; returns (seconds, detail)."""
+    os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    import oracle as O
+    from paper_2309_09061_b200.packed import pack_h2
+    xr, yr, spec = build_inputs(cfg, n)
+    ctxm = threadpool_limits(limits=threads) if threadpool_limits else None
+    try:
+        x = O.o_recompress(O.o_from_packed(pack_h2(xr)), spec["eps"])
+        y = x if yr is xr else O.o_recompress(O.o_from_packed(pack_h2(yr)), spec["eps"])
+        t0 = time.perf_counter()
+        final, induced, tm, _ = O.o_run_stages(x, y, x.bt, spec["eps"])
+        wall = time.perf_counter() - t0   # includes the weights (t_setup), like our timed step
+    finally:
+        if ctxm is not None:
+            ctxm.__exit__(None, None, None)
+    return wall, tm
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle with all host threads, bounded sample per step."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = args.cpu_sample_n
+    for _ in range(args.warmup):
+        cpu_oracle_run(args.config, n, threads)
+    times = []
+    for _ in range(args.steps):
+        t, _ = cpu_oracle_run(args.config, n, threads)
+        times.append(t)
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms / 1e3)
+    from paper_2309_09061_b200.problems import CONFIGS
+    spec = CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": "h2_product_dof_per_s", "value": value, "unit": "DOF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded points, BASELINE generator)",
+        "config": {"workload": f"{args.config} product X*Y -> Z (multiply + coarsen), sample n={n}",
+                   "n": n, "leaf": spec["leaf"], "eta": spec["eta"], "order": spec["order"], "eps": spec["eps"]},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.config} generator at n={n} (full product incl. weights), "
+                                   f"oracle/h2_oracle.py NumPy restatement, BLAS threads={threads}"},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2309_09061_b200 as P
+    from paper_2309_09061_b200.device import Context, DeviceH2
+    from paper_2309_09061_b200.problems import CONFIGS
+
+    spec = dict(CONFIGS[args.config])
+    n = args.n or spec["n"]
+    eps = spec["eps"]
+    ctx = Context(local)
+    t0 = time.perf_counter()
+    xr, yr, spec = build_inputs(args.config, n)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    dxr = DeviceH2.upload(xr, ctx)
+    dx = P.recompress(dxr, eps, ctx=ctx)
+    dy = dx if yr is xr else P.recompress(DeviceH2.upload(yr, ctx), eps, ctx=ctx)
+    del dxr
+    ctx.synchronize()
+    t_prep = time.perf_counter() - t0
+    coarse = dx.block_tree
+    stream = ctx.stream
+
+    def step():
+        g = P.multiply(dx, dy, eps, ctx=ctx)
+        return P.coarsen(g, coarse, eps, ctx=ctx)
+
+    for _ in range(max(3, args.warmup)):
+        z = step()
+    ctx.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.counters(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        z = step()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    cnt = ctx.counters(reset=True)
+    ms = reduce_max(e0.elapsed_time(e1) / args.steps, torch.device("cuda", local))
+    value = world * n / (ms / 1e3)
+
+    # stage split (reference harness stage names) and per-kernel-class accounting, untimed step
+    ctx.set_timing(True)
+    ctx.set_profile(True)
+    ctx.kernel_stats(reset=True)
+    g = P.multiply(dx, dy, eps, ctx=ctx)
+    st1 = ctx.stage_times()
+    z = P.coarsen(g, coarse, eps, ctx=ctx)
+    st2 = ctx.stage_times()
+    ks = ctx.kernel_stats(reset=True)
+    hts = ctx.host_times(reset=True)
+    ctx.set_profile(False)
+    ctx.set_timing(False)
+    stages = {k: st1[k] for k in ("t_setup", "t1_row", "t1_col", "t1_mat")}
+    stages.update({k: st2[k] for k in ("t2_row", "t2_col", "t2_mat")})
+    zr, zc = z.download().row_basis.rank, None
+
+    # end to end through the public API: host H2Matrix in, host H2Matrix out
+    xh = dx.download()
+    yh = xh if dy is dx else dy.download()
+    h2d = dx.packed_bytes() + (0 if dy is dx else dy.packed_bytes())
+    P.multiply_coarsen(xh, yh, eps, ctx=ctx)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        zh = P.multiply_coarsen(xh, yh, eps, ctx=ctx)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = reduce_max(sum(e2e_t) / len(e2e_t), torch.device("cuda", local))
+    from paper_2309_09061_b200.h2 import storage_bytes
+    d2h = storage_bytes(zh)
+
+    # roofline: dominant kernel class by device time in the profiled step
+    peak_fp64 = fp64_peak_tflops()
+    hbm, hbm_src = hbm_peak()
+    dom = max(ks, key=lambda k: ks[k]["ms"])
+    d = ks[dom]
+    achieved = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
+    total_flops = sum(v["flops"] for v in ks.values())
+    roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+                "frac": achieved / peak_fp64, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in MEASURED_PEAKS.json)",
+                "launches": d["launches"], "kernel_ms": d["ms"], "kernel_flops": d["flops"],
+                "phase_mix": {"ledger_flops": total_flops, "t_roof_ms": 1e3 * total_flops / (peak_fp64 * 1e12),
+                              "frac_of_step": (1e3 * total_flops / (peak_fp64 * 1e12)) / ms},
+                "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_n = args.cpu_sample_n
+        wall, tm = cpu_oracle_run(args.config, cpu_n, 1)
+        cpu = {"value": cpu_n / wall, "unit": "DOF/s", "cores": 1, "kind": "port",
+               "sample": f"{args.config} generator at n={cpu_n}, full product incl. weights "
+                         f"({wall:.1f} s), oracle/h2_oracle.py (NumPy restatement of h2mul), 1 BLAS thread",
+               "stages_s": tm}
+
+    if rank == 0:
+        line = {
+            "metric": "h2_product_dof_per_s", "value": value, "unit": "DOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded points per BASELINE generator; interpolation inputs recompressed on GPU)",
+            "config": {"workload": f"{args.config} product X*Y -> Z (multiply + coarsen onto X's tree)",
+                       "n": n, "geometry": spec["geometry"], "kernel_x": spec["kernel_x"],
+                       "kernel_y": spec["kernel_y"], "leaf": spec["leaf"], "eta": spec["eta"],
+                       "order": spec["order"], "eps": eps, "parallelism": f"replicas x{world}",
+                       "l2": f"inputs larger than L2 (X packed {dx.packed_bytes() / 1e6:.0f} MB)"},
+            "e2e": {"value": world * n / e2e_s, "unit": "DOF/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "seconds": e2e_s},
+            "gpu_launches": cnt["launches"] // args.steps * args.steps,
+            "host_syncs_per_step": cnt["syncs"] / args.steps,
+            "clocks": clk,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "stages_s": stages,
+            "ranks": {"final_max": int(max(zr)), "final_mean": float(sum(zr) / len(zr))},
+            "setup_s": {"build_inputs": t_build, "upload_recompress": t_prep},
+        }
+        if args.profile_json:
+            with open(args.profile_json, "w") as fh:
+                json.dump({"kernel_stats": ks, "host_ms": hts, "stages_s": stages, "line": line}, fh, indent=1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,6 +44,12 @@ int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);
 /* kernel launches and host synchronisations since the last reset: out2 = {launches, syncs} */
 int h2g_ctx_counters(h2g_ctx* ctx, long long* out2, int reset);
 int h2g_ctx_synchronize(h2g_ctx* ctx);
+/* host-side time per named section in timing mode, as "name=ms;..." (returns the full length) */
+int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset);
+/* profile mode: CUDA events around every batched launch, accumulated per kernel class
+   (0 gsum, 1 qr_r, 2 svd, 3 norm, 4 gather); out20 = per class {launches, ms, algorithmic flops, bytes} */
+int h2g_ctx_set_profile(h2g_ctx* ctx, int on);
+int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* out20, int reset);
 
 /* cluster tree (reference ClusterTree, trees.py:34-97): n nodes in preorder */
 int h2g_tree_create(h2g_ctx* ctx, int n, const long long* start, const long long* stop,
@@ -74,6 +80,13 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* h, long long* rb_rank, long long* rb_l
                     long long* rb_xfer_off, double* rb_data, long long* cb_rank, long long* cb_leaf_off,
                     long long* cb_xfer_off, double* cb_data, long long* coup_off, double* coup_data,
                     long long* near_off, double* near_data);
+
+/* Host-only structure: the refined product block tree T^XY of two block trees (trees.py:314-359),
+   with counts of terminal triples {a, b, c}; no device work, usable without a GPU. */
+int h2g_product_tree(h2g_blocks* bx, h2g_blocks* by, h2g_blocks** out, long long* ntriples3);
+/* sizes2 = {nblocks, child_idx length}; arrays may be NULL to query sizes only */
+int h2g_blocks_structure(h2g_blocks* b, long long* sizes2, long long* row, long long* col, long long* child_ptr,
+                         long long* child_idx, unsigned char* adm);
 
 /* Z = X * Y over the refined product tree T^XY (phase 1).  max_rank < 0: no cap. */
 int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, int scaling, h2g_h2** g);

@@ -30,6 +30,9 @@ SIGNATURES = {
     "h2g_ctx_stage_times": (C.c_int, [P, F64P]),
     "h2g_ctx_counters": (C.c_int, [P, I64P, C.c_int]),
     "h2g_ctx_synchronize": (C.c_int, [P]),
+    "h2g_ctx_host_times": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int]),
+    "h2g_ctx_set_profile": (C.c_int, [P, C.c_int]),
+    "h2g_ctx_kernel_stats": (C.c_int, [P, F64P, C.c_int]),
     "h2g_tree_create": (C.c_int, [P, C.c_int, I64P, I64P, I64P, I64P, C.POINTER(P)]),
     "h2g_tree_destroy": (None, [P]),
     "h2g_blocks_create": (C.c_int, [P, P, P, C.c_int, I64P, I64P, I64P, I64P, U8P, C.POINTER(P)]),
@@ -41,6 +44,8 @@ SIGNATURES = {
     "h2g_h2_sizes": (C.c_int, [P, I64P]),
     "h2g_h2_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, U8P]),
     "h2g_h2_download": (C.c_int, [P, P, I64P, I64P, I64P, F64P, I64P, I64P, I64P, F64P, I64P, F64P, I64P, F64P]),
+    "h2g_product_tree": (C.c_int, [P, P, C.POINTER(P), I64P]),
+    "h2g_blocks_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, I64P, U8P]),
     "h2g_multiply": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
     "h2g_coarsen": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
     "h2g_recompress": (C.c_int, [P, P, C.c_double, C.c_int, C.POINTER(P)]),

@@ -74,6 +74,36 @@ int h2g_ctx_counters(h2g_ctx* ctx, long long* o, int reset) {
   return 0;
 }
 
+int h2g_ctx_set_profile(h2g_ctx* ctx, int on) {
+  ctx->c.prof = on != 0;
+  return 0;
+}
+
+int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* o, int reset) {
+  return guarded([&] {
+    ctx->c.sync();
+    for (int k = 0; k < K_NCLASS; ++k) {
+      KStat& s = ctx->c.kstat[k];
+      o[4 * k + 0] = (double)s.launches;
+      o[4 * k + 1] = s.ms;
+      o[4 * k + 2] = s.flops;
+      o[4 * k + 3] = s.bytes;
+      if (reset) s = KStat{};
+    }
+  });
+}
+
+int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset) {
+  std::string out;
+  for (auto& kv : ctx->c.htime) out += kv.first + "=" + std::to_string(kv.second) + ";";
+  if (reset) ctx->c.htime.clear();
+  if (buf && len > 0) {
+    strncpy(buf, out.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)out.size();
+}
+
 int h2g_ctx_synchronize(h2g_ctx* ctx) {
   return guarded([&] { ctx->c.sync(); });
 }
@@ -216,7 +246,7 @@ int h2g_h2_structure(h2g_h2* hh, long long* row, long long* col, long long* cptr
     for (int b = 0; b < B.nb; ++b) {
       row[b] = B.row[b];
       col[b] = B.col[b];
-      adm[b] = B.leaf(b) ? B.adm[b] : 0;
+      adm[b] = B.adm[b];
       cptr[b] = B.cptr[b];
     }
     cptr[B.nb] = B.cptr[B.nb];
@@ -292,6 +322,36 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_
     gcp.run(C, ar, coup_data);
     gn.run(C, ar, near_data);
     C.sync();
+  });
+}
+
+int h2g_product_tree(h2g_blocks* bx, h2g_blocks* by, h2g_blocks** out, long long* ntriples) {
+  return guarded([&] {
+    PTree pt = product_tree(BView{bx->b.get(), false}, BView{by->b.get(), false});
+    *out = new h2g_blocks{pt.bt, bx->rows, by->cols};
+    if (ntriples) {
+      long long na = 0, nb = 0, nc = 0;
+      for (char k : pt.tk) { na += k == 'a'; nb += k == 'b'; nc += k == 'c'; }
+      ntriples[0] = na; ntriples[1] = nb; ntriples[2] = nc;
+    }
+  });
+}
+
+int h2g_blocks_structure(h2g_blocks* bb, long long* sizes2, long long* row, long long* col, long long* cptr,
+                         long long* cidx, unsigned char* adm) {
+  return guarded([&] {
+    const Blocks& B = *bb->b;
+    sizes2[0] = B.nb;
+    sizes2[1] = (long long)B.cidx.size();
+    if (!row) return;
+    for (int b = 0; b < B.nb; ++b) {
+      row[b] = B.row[b];
+      col[b] = B.col[b];
+      adm[b] = B.adm[b];
+      cptr[b] = B.cptr[b];
+    }
+    cptr[B.nb] = B.cptr[B.nb];
+    for (size_t i = 0; i < B.cidx.size(); ++i) cidx[i] = B.cidx[i];
   });
 }
 

@@ -49,6 +49,13 @@ Ctx::Ctx(int dev, cudaStream_t s) : device(dev), st(s) {
     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
     own_stream = true;
   }
+  // keep freed stream-ordered allocations in the pool between products (the default threshold of 0
+  // hands every arena back to the driver at each synchronisation)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   stage_cap = size_t(64) << 20;
   cuda_check(cudaMallocHost(&hstage, stage_cap), "cudaMallocHost");
   cuda_check(cudaMalloc(&dstage, stage_cap), "cudaMalloc stage");
@@ -72,9 +79,52 @@ void Ctx::ensure_read(size_t bytes) {
 }
 
 void Ctx::sync() {
+  HostTimer ht(*this, "sync_wait");
   cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   stage_off = 0;
   ++syncs;
+  if (!pending.empty()) drain_prof();
+}
+
+cudaEvent_t Ctx::prof_begin() {
+  if (!prof) return nullptr;
+  cudaEvent_t e;
+  if (free_ev.empty()) {
+    cuda_check(cudaEventCreate(&e), "event");
+  } else {
+    e = free_ev.back();
+    free_ev.pop_back();
+  }
+  cudaEventRecord(e, st);
+  return e;
+}
+
+void Ctx::prof_end(int cls, cudaEvent_t a, double flops, double bytes) {
+  if (!prof || !a) return;
+  cudaEvent_t b;
+  if (free_ev.empty()) {
+    cuda_check(cudaEventCreate(&b), "event");
+  } else {
+    b = free_ev.back();
+    free_ev.pop_back();
+  }
+  cudaEventRecord(b, st);
+  pending.push_back(Pending{cls, a, b, flops, bytes});
+}
+
+void Ctx::drain_prof() {
+  for (auto& p : pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    KStat& k = kstat[p.cls];
+    k.launches += 1;
+    k.ms += ms;
+    k.flops += p.flops;
+    k.bytes += p.bytes;
+    free_ev.push_back(p.a);
+    free_ev.push_back(p.b);
+  }
+  pending.clear();
 }
 
 void* Ctx::stage(const void* src, size_t bytes) {
@@ -91,6 +141,7 @@ void* Ctx::stage(const void* src, size_t bytes) {
   }
   char* h = hstage + stage_off;
   char* d = dstage + stage_off;
+  HostTimer ht(*this, "stage_memcpy");
   memcpy(h, src, bytes);
   cuda_check(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st), "stage copy");
   stage_off += need;
@@ -124,6 +175,7 @@ void GBatch::t3(MatRef a, MatRef b, MatRef d, int k, int k2, double al) {
 }
 
 void GBatch::run(Ctx& C) {
+  HostTimer ht(C, "gbatch_run");
   std::vector<GTile> tiles;
   for (int i = 0; i < (int)outs.size(); ++i) {
     const GOut& o = outs[i];
@@ -136,7 +188,25 @@ void GBatch::run(Ctx& C) {
   GOut* d_o = C.push(outs);
   GTerm* d_t = C.push(terms);
   GTile* d_l = C.push(tiles);
+  double fl = 0, by = 0;
+  if (C.prof) {  // algorithmic work: each product once at its own shape
+    for (const GOut& o : outs) {
+      if (o.m <= 0 || o.n <= 0) continue;
+      by += 8.0 * o.m * o.n * (1 + o.beta);
+      for (int i = o.t0; i < o.t1; ++i) {
+        const GTerm& t = terms[i];
+        if (t.nf == 1) { fl += (double)o.m * o.n; by += 8.0 * o.m * o.n; }
+        else if (t.nf == 2) { fl += 2.0 * o.m * o.n * t.k; by += 8.0 * ((double)o.m * t.k + (double)t.k * o.n); }
+        else {
+          fl += 2.0 * o.m * t.k * t.k2 + 2.0 * o.m * t.k2 * o.n;
+          by += 8.0 * ((double)o.m * t.k + (double)t.k * t.k2 + (double)t.k2 * o.n);
+        }
+      }
+    }
+  }
+  cudaEvent_t ev = C.prof_begin();
   cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+  C.prof_end(K_GSUM, ev, fl, by);
   ++C.launches;
   outs.clear();
   terms.clear();
@@ -161,14 +231,26 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   }
   if (small.empty() && big.empty()) { items.clear(); sl.segs.clear(); return; }
   Seg* d_s = C.push(sl.segs);
+  double fl = 0, by = 0;
+  if (C.prof)
+    for (auto* v : {&small, &big})
+      for (auto& it : *v) {  // Householder R-only: 2 M n^2 - 2/3 n^3 (M >= n)
+        const double M = (double)it.M, n = it.n;
+        fl += M >= n ? 2 * M * n * n - 2.0 / 3 * n * n * n : 2 * n * M * M - 2.0 / 3 * M * M * M;
+        by += 8 * (M * n + std::min(M, n) * n);
+      }
+  QrItem* d_small = C.push(small);
+  QrItem* d_big = C.push(big);
+  cudaEvent_t ev = C.prof_begin();
   if (!small.empty()) {
-    cuda_check(launch_qr(C.push(small), d_s, (int)small.size(), nsmall, false, C.st), "qr_r");
+    cuda_check(launch_qr(d_small, d_s, (int)small.size(), nsmall, false, C.st), "qr_r");
     ++C.launches;
   }
   if (!big.empty()) {
-    cuda_check(launch_qr(C.push(big), d_s, (int)big.size(), nbig, true, C.st), "qr_r ws");
+    cuda_check(launch_qr(d_big, d_s, (int)big.size(), nbig, true, C.st), "qr_r ws");
     ++C.launches;
   }
+  C.prof_end(K_QR, ev, fl, by);
   items.clear();
   sl.segs.clear();
 }
@@ -191,7 +273,18 @@ std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {
     where.push_back((int)i);
   }
   if (!live.empty()) {
-    cuda_check(launch_norm(C.push(live), C.push(sl.segs), (int)live.size(), smem, C.st), "norm");
+    double fl = 0, by = 0;
+    if (C.prof)
+      for (auto& it : live) {  // Gram on the short side + tridiagonalisation
+        const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
+        fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
+        by += 8 * mn * mx;
+      }
+    NormItem* d_i = C.push(live);
+    Seg* d_s = C.push(sl.segs);
+    cudaEvent_t ev = C.prof_begin();
+    cuda_check(launch_norm(d_i, d_s, (int)live.size(), smem, C.st), "norm");
+    C.prof_end(K_NORM, ev, fl, by);
     ++C.launches;
     std::vector<double> vals = C.read(d_out, items.size());
     for (int w : where) res[w] = vals[w];
@@ -206,35 +299,71 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   if (items.empty()) return ranks;
   int* d_rank = (int*)scratch.alloc_bytes(items.size() * sizeof(int));
   cuda_check(cudaMemsetAsync(d_rank, 0, items.size() * sizeof(int), C.st), "memset");
-  std::vector<SvdItem> small, big;
-  size_t sm_small = 0, sm_big = 0;
+  static constexpr long long kChunkCols = 256;  // columns per stage-1 CTA (8 panels of 32)
+  std::vector<SvdItem> live;
+  bool rsmem = true;
+  size_t sm_tsqr = 0, sm_merge = 0, sm_fin = 0;
   for (size_t i = 0; i < items.size(); ++i) {
     SvdItem& it = items[i];
     it.rank_out = d_rank + i;
     if (it.m == 0) continue;
     const int k1 = std::min(it.m, it.kx);
-    const size_t s1 = svd_smem(it.m, it.kx, false);
-    if (s1 <= kSmemLimit) {
-      small.push_back(it);
-      sm_small = std::max(sm_small, s1);
-    } else {
-      const size_t s2 = svd_smem(it.m, it.kx, true);
-      if (s2 > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
-      const int n = it.m - k1;
-      it.ws = scratch.alloc((size_t)n * n);
-      big.push_back(it);
-      sm_big = std::max(sm_big, s2);
+    const int n = it.m - k1;
+    it.nchunk = (int)std::max<long long>(1, (it.N + kChunkCols - 1) / kChunkCols);
+    it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
+    it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
+    if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || svd_merge_smem(n, true) > kSmemLimit ||
+        svd_finish_smem(it.m, it.kx, true) > kSmemLimit)
+      rsmem = false;
+    live.push_back(it);
+  }
+  if (live.empty()) return ranks;
+  std::vector<SvdWork> work;
+  std::vector<std::vector<SvdWork>> merges;
+  int maxchunk = 1;
+  for (size_t i = 0; i < live.size(); ++i) {
+    const SvdItem& it = live[i];
+    const int n = it.m - std::min(it.m, it.kx);
+    sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
+    sm_merge = std::max(sm_merge, svd_merge_smem(n, rsmem));
+    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, rsmem));
+    if (sm_tsqr > kSmemLimit || sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
+    for (int c = 0; c < it.nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
+    maxchunk = std::max(maxchunk, it.nchunk);
+  }
+  for (int stride = 1; stride < maxchunk; stride *= 2) {  // pairwise tree of R merges
+    std::vector<SvdWork> lvl;
+    for (size_t i = 0; i < live.size(); ++i) {
+      if (live[i].m - std::min(live[i].m, live[i].kx) == 0) continue;
+      for (int a = 0; a + stride < live[i].nchunk; a += 2 * stride) lvl.push_back(SvdWork{(int)i, a, a + stride, 0});
     }
+    merges.push_back(std::move(lvl));
   }
   Seg* d_s = C.push(sl.segs);
-  if (!small.empty()) {
-    cuda_check(launch_svd(C.push(small), d_s, (int)small.size(), sm_small, C.st), "svd");
+  SvdItem* d_items = C.push(live);
+  SvdWork* d_work = C.push(work);
+  std::vector<SvdWork*> d_merge;
+  for (auto& l : merges) d_merge.push_back(C.push(l));
+  double fl = 0, by = 0;
+  if (C.prof)
+    for (auto& it : live) {  // reference ops: full QR of V, Q^T A, gesdd of the remainder
+      const double m = it.m, kx = it.kx, N = (double)it.N, k1 = std::min(m, kx), r = m - k1;
+      if (kx > 0) fl += 2 * m * kx * kx - 2.0 / 3 * kx * kx * kx + 4.0 / 3 * m * m * m + 2 * r * m * N;
+      const double mn = std::min(r, N), mx = std::max(r, N);
+      fl += 4 * mx * mn * mn + 8 * mn * mn * mn;
+      by += 8 * (m * N + m * kx + m * m);
+    }
+  cudaEvent_t ev = C.prof_begin();
+  cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
+  ++C.launches;
+  for (size_t l = 0; l < merges.size(); ++l) {
+    if (merges[l].empty()) continue;
+    cuda_check(launch_svd_merge(d_items, d_merge[l], (int)merges[l].size(), sm_merge, rsmem, C.st), "svd_merge");
     ++C.launches;
   }
-  if (!big.empty()) {
-    cuda_check(launch_svd(C.push(big), d_s, (int)big.size(), sm_big, C.st), "svd ws");
-    ++C.launches;
-  }
+  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, rsmem, C.st), "svd_finish");
+  ++C.launches;
+  C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());
   items.clear();
   sl.segs.clear();
@@ -267,10 +396,32 @@ void Blocks::finalize() {
   parent.assign(nb, -1);
   level.assign(nb, 0);
   depth = 0;
-  index.clear();
-  index.reserve(nb * 2);
+  rptr.assign(rows->n + 1, 0);
   for (int b = 0; b < nb; ++b) {
-    index[(long long)row[b] * cols->n + col[b]] = b;
+    if (row[b] < 0 || row[b] >= rows->n || col[b] < 0 || col[b] >= cols->n)
+      throw InvalidInput("block references a cluster outside its tree");
+    ++rptr[row[b] + 1];
+  }
+  for (int t = 0; t < rows->n; ++t) rptr[t + 1] += rptr[t];
+  rcol.assign(nb, 0);
+  rblk.assign(nb, 0);
+  {
+    std::vector<int> fill(rptr.begin(), rptr.end() - 1);
+    for (int b = 0; b < nb; ++b) {
+      rcol[fill[row[b]]] = col[b];
+      rblk[fill[row[b]]++] = b;
+    }
+    for (int t = 0; t < rows->n; ++t) {
+      std::vector<std::pair<int, int>> v;
+      for (int i = rptr[t]; i < rptr[t + 1]; ++i) v.emplace_back(rcol[i], rblk[i]);
+      std::sort(v.begin(), v.end());
+      for (int i = rptr[t]; i < rptr[t + 1]; ++i) {
+        rcol[i] = v[i - rptr[t]].first;
+        rblk[i] = v[i - rptr[t]].second;
+      }
+    }
+  }
+  for (int b = 0; b < nb; ++b) {
     for (int i = cptr[b]; i < cptr[b + 1]; ++i) {
       const int c = cidx[i];
       if (c <= b || c >= nb) throw InvalidInput("block tree is not in preorder");
@@ -311,12 +462,24 @@ std::shared_ptr<Blocks> make_blocks(const Tree* rows, const Tree* cols, int nb, 
   return b;
 }
 
+// Locate block (row, col) of a block tree starting from a hint block: the hint itself, one of its
+// children, or (fallback) a binary search.  The product recursion always has the parent blocks of
+// X|ts and Y|sr at hand, so this replaces the reference's dict lookups (trees.py:187, :289-290).
+static inline int locate(BView v, int hint, int row, int col) {
+  if (hint >= 0) {
+    if (v.row(hint) == row && v.col(hint) == col) return hint;
+    const Blocks& B = *v.b;
+    for (int i = B.cptr[hint]; i < B.cptr[hint + 1]; ++i) {
+      const int c = B.cidx[i];
+      if (v.row(c) == row && v.col(c) == col) return c;
+    }
+  }
+  return v.find(row, col);
+}
+
 // Triple kind (reference trees.py:288-300): 'a' > 'b' > 'c' > 'n'.
-static char classify(BView bx, BView by, int t, int s, int r, int* pts, int* psr) {
-  const int bts = bx.find(t, s), bsr = by.find(s, r);
+static inline char classify(BView bx, BView by, int bts, int bsr) {
   if (bts < 0 || bsr < 0) throw StructureErr("triple not covered by the factor block trees");
-  *pts = bts;
-  *psr = bsr;
   if (by.b->adm_leaf(bsr)) return 'a';
   if (bx.b->adm_leaf(bts)) return 'b';
   if (by.b->leaf(bsr) && bx.b->leaf(bts)) return 'c';
@@ -334,15 +497,21 @@ PTree product_tree(BView bx, BView by) {
   bt->rows = &rows;
   bt->cols = &cols;
   std::vector<std::vector<int>> kids;
-  struct Frame {
-    int t, r, parent, slot;
-    std::vector<int> mids;
+  struct Mid {
+    int s, hx, hy;  // middle cluster and hint blocks (parents of X|ts, Y|sr)
   };
-  std::vector<Frame> stack;
-  stack.push_back(Frame{0, 0, -1, 0, {0}});
-  std::vector<int> pend, open;
+  struct Frame {
+    int t, r, parent, slot, m0, m1;  // middles in `pool[m0:m1]`
+  };
+  std::vector<Mid> pool{Mid{0, 0, 0}};
+  std::vector<Frame> stack{Frame{0, 0, -1, 0, 0, 1}};
+  struct Live {
+    int s, bts, bsr;
+  };
+  std::vector<Live> pend, open;
+  P.tptr.reserve(1 << 16);
   while (!stack.empty()) {
-    Frame f = std::move(stack.back());
+    const Frame f = stack.back();
     stack.pop_back();
     const int b = (int)bt->row.size();
     if (f.parent >= 0) kids[f.parent][f.slot] = b;
@@ -352,44 +521,51 @@ PTree product_tree(BView bx, BView by) {
     kids.emplace_back();
     P.tptr.push_back((int)P.ts.size());
     const bool both_leaf = rows.leaf(f.t) && cols.leaf(f.r);
-    pend = f.mids;
+    pend.clear();
+    for (int i = f.m0; i < f.m1; ++i) {
+      const Mid& m = pool[i];
+      pend.push_back(Live{m.s, locate(bx, m.hx, f.t, m.s), locate(by, m.hy, m.s, f.r)});
+    }
     open.clear();
     bool dense = false;
     while (!pend.empty()) {
-      const int s = pend.back();
+      const Live l = pend.back();
       pend.pop_back();
-      int bts, bsr;
-      const char k = classify(bx, by, f.t, s, f.r, &bts, &bsr);
+      const char k = classify(bx, by, l.bts, l.bsr);
       if (k == 'n') {
-        if (both_leaf) {
-          for (int i = 0; i < mid.nkids(s); ++i) pend.push_back(mid.kid(s, i));
+        if (both_leaf) {  // both clusters exhausted: chase the middle only (trees.py:343-345)
+          for (int i = 0; i < mid.nkids(l.s); ++i) {
+            const int s2 = mid.kid(l.s, i);
+            pend.push_back(Live{s2, locate(bx, l.bts, f.t, s2), locate(by, l.bsr, s2, f.r)});
+          }
         } else {
-          open.push_back(s);
+          open.push_back(l);
         }
         continue;
       }
       if (k == 'c') dense = true;
-      P.ts.push_back(s);
+      P.ts.push_back(l.s);
       P.tk.push_back(k);
+      P.tbx.push_back(l.bts);
+      P.tby.push_back(l.bsr);
     }
     if (!open.empty()) {
-      std::vector<int> subs;
-      for (int s : open) {  // _sub_middles (trees.py:303-311)
-        const int bts = bx.find(f.t, s), bsr = by.find(s, f.r);
-        if (!bx.b->leaf(bts) && !by.b->leaf(bsr) && mid.nkids(s) > 0) {
-          for (int i = 0; i < mid.nkids(s); ++i) subs.push_back(mid.kid(s, i));
+      const int m0 = (int)pool.size();
+      for (const Live& l : open) {  // _sub_middles (trees.py:303-311)
+        if (!bx.b->leaf(l.bts) && !by.b->leaf(l.bsr) && mid.nkids(l.s) > 0) {
+          for (int i = 0; i < mid.nkids(l.s); ++i) pool.push_back(Mid{mid.kid(l.s, i), l.bts, l.bsr});
         } else {
-          subs.push_back(s);
+          pool.push_back(Mid{l.s, l.bts, l.bsr});
         }
       }
-      std::vector<std::pair<int, int>> pairs;
+      const int m1 = (int)pool.size();
       const int nt = std::max(1, rows.nkids(f.t)), nr = std::max(1, cols.nkids(f.r));
-      for (int i = 0; i < nt; ++i)
-        for (int j = 0; j < nr; ++j)
-          pairs.emplace_back(rows.nkids(f.t) ? rows.kid(f.t, i) : f.t, cols.nkids(f.r) ? cols.kid(f.r, j) : f.r);
-      kids[b].assign(pairs.size(), -1);
-      for (int i = (int)pairs.size() - 1; i >= 0; --i)
-        stack.push_back(Frame{pairs[i].first, pairs[i].second, b, i, subs});
+      kids[b].assign(nt * nr, -1);
+      for (int i = nt * nr - 1; i >= 0; --i) {
+        const int t2 = rows.nkids(f.t) ? rows.kid(f.t, i / nr) : f.t;
+        const int r2 = cols.nkids(f.r) ? cols.kid(f.r, i % nr) : f.r;
+        stack.push_back(Frame{t2, r2, b, i, m0, m1});
+      }
     } else if (dense) {
       bt->adm[b] = 0;
     }
@@ -398,6 +574,7 @@ PTree product_tree(BView bx, BView by) {
   bt->nb = (int)bt->row.size();
   bt->cptr.assign(bt->nb + 1, 0);
   for (int b = 0; b < bt->nb; ++b) bt->cptr[b + 1] = bt->cptr[b] + (int)kids[b].size();
+  bt->cidx.reserve(bt->cptr[bt->nb]);
   for (int b = 0; b < bt->nb; ++b)
     for (int c : kids[b]) bt->cidx.push_back(c);
   bt->finalize();

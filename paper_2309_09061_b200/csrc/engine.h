@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -22,11 +24,16 @@ void cuda_check(cudaError_t e, const char* what);
 // ------------------------------------------------------------------ kernels (kernels.cu)
 cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
 cudaError_t launch_qr(const QrItem*, const Seg*, int nitems, int nmax, bool ws, cudaStream_t);
-cudaError_t launch_svd(const SvdItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
+cudaError_t launch_svd_tsqr(const SvdItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
+                            cudaStream_t);
+cudaError_t launch_svd_merge(const SvdItem*, const SvdWork*, int nwork, size_t smem, bool rsmem, cudaStream_t);
+cudaError_t launch_svd_finish(const SvdItem*, int nitems, size_t smem, bool rsmem, cudaStream_t);
 cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 size_t qr_smem(int n, bool ws);
-size_t svd_smem(int m, int kx, bool ws);
+size_t svd_tsqr_smem(int m, int kx, bool rsmem);
+size_t svd_merge_smem(int n, bool rsmem);
+size_t svd_finish_smem(int m, int kx, bool rsmem);
 size_t norm_smem(int m, long long N);
 size_t gsum_smem(int k2max);
 
@@ -50,16 +57,20 @@ struct Blocks {
   int nb = 0, depth = 0;
   std::vector<int> row, col, cptr, cidx, parent, level;
   std::vector<unsigned char> adm;
-  std::unordered_map<long long, int> index;
+  std::vector<int> rptr, rcol, rblk;  // per row cluster: blocks sorted by column (lookup table)
   std::vector<std::vector<int>> by_level;
   bool leaf(int b) const { return cptr[b + 1] == cptr[b]; }
   bool adm_leaf(int b) const { return leaf(b) && adm[b]; }
   bool near_leaf(int b) const { return leaf(b) && !adm[b]; }
   int nkids(int b) const { return cptr[b + 1] - cptr[b]; }
   int kid(int b, int i) const { return cidx[cptr[b] + i]; }
-  int find(int t, int s) const {
-    auto it = index.find((long long)t * cols->n + s);
-    return it == index.end() ? -1 : it->second;
+  int find(int t, int s) const {  // binary search in row t's blocks (replaces the reference's dict)
+    int lo = rptr[t], hi = rptr[t + 1];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (rcol[mid] < s) lo = mid + 1; else hi = mid;
+    }
+    return (lo < rptr[t + 1] && rcol[lo] == s) ? rblk[lo] : -1;
   }
   void finalize();
 };
@@ -143,6 +154,13 @@ struct StageTimes {
   float setup = 0, t1_row = 0, t1_col = 0, t1_mat = 0, t2_row = 0, t2_col = 0, t2_mat = 0;
 };
 
+// Per-kernel-class accounting for the roofline (profile mode only; never inside a timed step).
+enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_NCLASS = 5 };
+struct KStat {
+  long long launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -158,6 +176,19 @@ struct Ctx {
   StageTimes times;
   bool timing = false;
   std::vector<cudaEvent_t> evpool;
+  bool prof = false;
+  KStat kstat[K_NCLASS];
+  struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_ev;
+  std::map<std::string, double> htime;  // host-side ms per named section (timing mode)
+  cudaEvent_t prof_begin();
+  void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
+  void drain_prof();
 
   Ctx(int dev, cudaStream_t s);
   ~Ctx();
@@ -177,6 +208,18 @@ struct Ctx {
   }
   void ensure_read(size_t bytes);
   cudaEvent_t event();
+};
+
+// Scoped host timer, active when the context is in timing mode.
+struct HostTimer {
+  Ctx& C;
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  HostTimer(Ctx& c, const char* n) : C(c), name(n), t0(std::chrono::steady_clock::now()) {}
+  ~HostTimer() {
+    if (C.timing)
+      C.htime[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
 };
 
 // ------------------------------------------------------------------ batches
@@ -241,8 +284,8 @@ struct PairMap {
 struct Induced {
   std::shared_ptr<Basis> q;
   MatStore bc;
-  PairMap proj;
-  PairMap xv;               // memoised X|ts V_Y,s for leaf rows (induced.py:59-73)
+  std::vector<Mat> proj;    // per block of X (view): Q_t^T X|ts V_Y,s for non-admissible-leaf blocks
+  std::vector<Mat> xv;      // per block of X (view), leaf rows: X|ts V_Y,s (induced.py:59-73)
   std::vector<double> gap;  // min |sigma - thr| / thr per cluster (diagnostic)
 };
 
@@ -251,6 +294,7 @@ struct PTree {  // product block tree with the classified triples per node
   std::vector<int> tptr;  // per node: triples [tptr[b], tptr[b+1])
   std::vector<int> ts;    // middle cluster
   std::vector<char> tk;   // kind 'a' 'b' 'c'
+  std::vector<int> tbx, tby;  // block ids of X|ts and Y|sr
 };
 
 // ------------------------------------------------------------------ stages
@@ -260,8 +304,8 @@ std::shared_ptr<Blocks> make_blocks(const Tree* rows, const Tree* cols, int nb, 
                                     const long long* col, const long long* cptr, const long long* cidx,
                                     const unsigned char* adm);
 
-void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<std::pair<int, int>>& want,
-                PairMap& memo);
+void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<int>& want,
+                std::vector<Mat>& memo);
 MatStore basis_product(Ctx& C, Arena& ar, const Basis& W, const Basis& V);
 MatStore basis_weights(Ctx& C, Arena& ar, const Basis& W);
 MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling);

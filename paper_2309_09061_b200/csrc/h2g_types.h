@@ -66,12 +66,18 @@ struct SvdItem {
   MatRef v;
   double tol;
   int cap;  // < 0: no cap
-  int pad_;
+  int nchunk;  // column chunks of the streamed TSQR (>= 1)
   double* q_out;
   double* bc_out;
   int* rank_out;    // k1 + k2
   double* sig_out;  // optional: sorted singular values of B (capacity m)
-  double* ws;       // optional global workspace for R ((m - k1)^2)
+  double* rbuf;     // nchunk x (n x n) partial R factors, n = m - min(m, kx)
+  double* vws;      // m x kx Householder vectors of V + kx coefficients
+};
+
+// Work units of the SVD pipeline: stage-1 chunk (item, chunk) and tree merges R_a <- [R_a; R_b].
+struct SvdWork {
+  int item, a, b, pad_;
 };
 
 // sigma_1 of hstack(segs[s0:s1]) (m x N) (reference dense.py:104-142).

@@ -2,7 +2,7 @@
 //
 //   gsum_kernel  : grouped small-matrix chain products C (+)= sum alpha * A*B(*D)   (all GEMM work)
 //   qr_r_kernel  : R factor of a stacked tall matrix, streamed in 32-row panels    (dense.py:145-150)
-//   svd_kernel   : protected, QR-preconditioned one-sided Jacobi truncated SVD    (dense.py:77-101,
+//   svd_*_kernel : protected, QR-preconditioned one-sided Jacobi truncated SVD    (dense.py:77-101,
 //                  induced.py:115-146, coarsening.py:294-326)
 //   norm_kernel  : sigma_1 via a streamed Gram matrix, Householder tridiagonalisation
 //                  and Sturm bisection                                            (dense.py:104-142)
@@ -22,6 +22,7 @@ static constexpr int kTile = 64;   // gsum output tile
 static constexpr int kKc = 16;     // gsum k-chunk
 static constexpr int kLdS = kTile + 2;
 static constexpr int kPanel = 32;  // TSQR / Gram panel rows (one per lane)
+static constexpr int kRawLd = kPanel + 1;  // odd stride of the m x 32 protect panel
 static constexpr double kEps = 2.220446049250313e-16;
 
 __device__ __forceinline__ double mref(const MatRef& a, long long i, long long j) {
@@ -142,9 +143,9 @@ __global__ void __launch_bounds__(kThreads) gsum_kernel(const GOut* __restrict__
 // column j+1 applies reflector j to it and immediately builds reflector j+1.
 // ---------------------------------------------------------------------------------------------
 
-__device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int j, double* vb, double* tb) {
+__device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int ldp, int j, double* vb, double* tb) {
   const int lane = threadIdx.x & 31;
-  const double x = P[lane * n + j];
+  const double x = P[lane * ldp + j];
   const double s = warp_sum(x * x);
   const double alpha = R[(long long)j * n + j];
   double v = 0.0, tau = 0.0;
@@ -157,35 +158,39 @@ __device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int j, do
   }
   vb[lane] = v;
   if (lane == 0) *tb = tau;
-  P[lane * n + j] = 0.0;
+  P[lane * ldp + j] = 0.0;
 }
 
-__device__ __forceinline__ void tsqr_apply(double* R, int n, double* P, int j, int c, double v, double tau) {
+__device__ __forceinline__ void tsqr_apply(double* R, int n, double* P, int ldp, int j, int c, double v,
+                                           double tau) {
   const int lane = threadIdx.x & 31;
-  const double p = P[lane * n + c];
+  const double p = P[lane * ldp + c];
   const double w = R[(long long)j * n + c] + warp_sum(v * p);
   __syncwarp();
   if (lane == 0) R[(long long)j * n + c] -= tau * w;
-  P[lane * n + c] = p - tau * w * v;
+  P[lane * ldp + c] = p - tau * w * v;
 }
 
-__device__ void tsqr_absorb(double* R, int n, double* P, double* vb /*64*/, double* tb /*2*/) {
+__device__ void tsqr_absorb(double* R, int n, double* P, int ldp, double* vb /*64*/, double* tb /*2*/,
+                            int jstart = 0) {
+  // columns < jstart of P are known to be zero (triangular panels in merges): no reflector there
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (warp == 0) tsqr_make(R, n, P, 0, vb, tb);
+  if (jstart >= n) return;
+  if (warp == 0) tsqr_make(R, n, P, ldp, jstart, vb + (jstart & 1) * 32, tb + (jstart & 1));
   __syncthreads();
-  for (int j = 0; j < n; ++j) {
+  for (int j = jstart; j < n; ++j) {
     const int cur = j & 1;
     const double v = vb[cur * 32 + lane];
     const double tau = tb[cur];
     const bool active = tau != 0.0;
     if (j + 1 < n && warp == (j + 1) % nw) {
-      if (active) tsqr_apply(R, n, P, j, j + 1, v, tau);
+      if (active) tsqr_apply(R, n, P, ldp, j, j + 1, v, tau);
       __syncwarp();
-      tsqr_make(R, n, P, j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
+      tsqr_make(R, n, P, ldp, j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
     }
     if (active) {
       int c0 = j + 2 + ((warp - (j + 2)) % nw + nw) % nw;
-      for (int c = c0; c < n; c += nw) tsqr_apply(R, n, P, j, c, v, tau);
+      for (int c = c0; c < n; c += nw) tsqr_apply(R, n, P, ldp, j, c, v, tau);
     }
     __syncthreads();
   }
@@ -228,12 +233,13 @@ __device__ void load_hpanel(const Seg* segs, int s0, int s1, int m, long long N,
 }
 
 // Fill P (32 x n) with rows row0.. of vstack(segs) (M x n), zero beyond M.
-__device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M, long long row0, double* P) {
+__device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M, long long row0, double* P,
+                            int ldp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int p = warp; p < kPanel; p += nw) {
     const long long r = row0 + p;
     if (r >= M) {
-      for (int j = lane; j < n; j += 32) P[p * n + j] = 0.0;
+      for (int j = lane; j < n; j += 32) P[p * ldp + j] = 0.0;
       continue;
     }
     long long off = 0;
@@ -244,7 +250,7 @@ __device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M,
     }
     const Seg sg = segs[s];
     const long long lr = r - off;
-    for (int j = lane; j < n; j += 32) P[p * n + j] = sg.scale * mref(sg.a, lr, j);
+    for (int j = lane; j < n; j += 32) P[p * ldp + j] = sg.scale * mref(sg.a, lr, j);
   }
 }
 
@@ -257,17 +263,18 @@ __global__ void __launch_bounds__(kThreads) qr_r_kernel(const QrItem* __restrict
   extern __shared__ double smem[];
   const QrItem it = items[blockIdx.x];
   const int n = it.n;
-  double* P = smem;                    // 32 x n
-  double* vb = P + kPanel * n;         // 64
+  const int ldp = n | 1;               // odd row stride: lanes walk P's rows without bank conflicts
+  double* P = smem;                    // 32 x ldp
+  double* vb = P + kPanel * ldp;       // 64
   double* tb = vb + 64;                // 2 (+pad)
   double* R = it.ws ? it.ws : tb + 4;  // n x n
   const long long nn = (long long)n * n;
   for (long long e = threadIdx.x; e < nn; e += blockDim.x) R[e] = 0.0;
   __syncthreads();
   for (long long r0 = 0; r0 < it.M; r0 += kPanel) {
-    load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P);
+    load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P, ldp);
     __syncthreads();
-    tsqr_absorb(R, n, P, vb, tb);
+    tsqr_absorb(R, n, P, ldp, vb, tb);
   }
   const long long rows = it.M < n ? it.M : n;
   for (long long e = threadIdx.x; e < rows * n; e += blockDim.x) {
@@ -282,10 +289,35 @@ __global__ void __launch_bounds__(kThreads) qr_r_kernel(const QrItem* __restrict
 // orthonormal regardless of the row norms.  Round-robin pairing, one pair per warp at a time.
 // ---------------------------------------------------------------------------------------------
 
-__device__ void jacobi_rows(double* W, int n, int* flag) {
+__device__ void jacobi_rows(double* W, int n, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // Rows whose norm is below eps * (largest row norm) can never pass the truncation threshold
+  // (thr >= max(rows, cols) eps sigma_1); rotating against them moves the other row by less than
+  // eps relative, so they are frozen.  Without this the numerically-null rows of rank-deficient
+  // inputs keep the sweep loop busy orthogonalising rounding noise.
+  {
+    double mx = 0.0;
+    for (int i = warp; i < n; i += nw) {
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * n + j], W[(long long)i * n + j], s);
+      s = warp_sum(s);
+      mx = fmax(mx, s);
+    }
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < nw; ++w) m = fmax(m, red[w]);
+      red[nw] = m * kEps * kEps;
+    }
+    __syncthreads();
+  }
+  const double frozen = red[nw];
   const int np = (n + 1) & ~1;  // even number of players, player n (if odd) is a bye
   const int npairs = np / 2;
+  // convergence threshold sqrt(n) eps (LAPACK dgesvj): rounding noise of an n-term dot product
+  // never falls below eps, so a pure-eps test can keep rotating to the sweep limit
+  const double tol = kEps * sqrt((double)n);
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
@@ -304,10 +336,13 @@ __device__ void jacobi_rows(double* W, int n, int* flag) {
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > kEps * sqrt(al) * sqrt(be)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // three independent butterflies, interleaved
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga != 0.0 && al > frozen && be > frozen && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t);
@@ -330,37 +365,36 @@ __device__ void jacobi_rows(double* W, int n, int* flag) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// svd_kernel: see SvdItem.  Shared memory carve-up (doubles):
-//   V  : m x kx           Householder factorisation of the protected basis
-//   tv : kx               reflector coefficients
-//   raw: m x 32           current column panel (protect case)
-//   P  : 32 x n'          transposed panel rows for TSQR
-//   R  : n' x n'          (shared or global workspace)
-//   sig: n'  ord: n'      singular values and order
+// Truncated SVD pipeline (see SvdItem), split so one wide matrix spreads over many CTAs:
+//   svd_tsqr_kernel   one CTA per (item, column chunk): Householder QR of the protected V,
+//                     Q^T applied to each 32-column panel, structured TSQR into R_chunk
+//   svd_merge_kernel  one CTA per tree merge: R_a <- R([R_a; R_b]) (triangular panels skip
+//                     their known-zero columns)
+//   svd_finish_kernel one CTA per item: one-sided Jacobi on the rows of R, rank rule, outputs
 // ---------------------------------------------------------------------------------------------
 
-__device__ void householder_qr_cols(double* V, int m, int kx, int k1, double* tv, double* red) {
+__device__ void householder_qr_cols(double* V, int m, int kx, int ldv, int k1, double* tv, double* red) {
   // In-place Householder QR of V (m x kx, row-major): reflector j stored below the diagonal
   // (implicit 1 on the diagonal), R on and above.  LAPACK dgeqrf sign convention.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = 0; j < k1; ++j) {
     // norm of V[j+1:, j]
     double part = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) part += V[i * kx + j] * V[i * kx + j];
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) part += V[i * ldv + j] * V[i * ldv + j];
     part = warp_sum(part);
     if (lane == 0) red[warp] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0;
       for (int w = 0; w < nw; ++w) s += red[w];
-      const double alpha = V[j * kx + j];
+      const double alpha = V[j * ldv + j];
       double tau = 0.0, scale = 0.0;
       if (s != 0.0) {
         const double nrm = sqrt(alpha * alpha + s);
         const double beta = alpha >= 0.0 ? -nrm : nrm;
         tau = (beta - alpha) / beta;
         scale = 1.0 / (alpha - beta);
-        V[j * kx + j] = beta;
+        V[j * ldv + j] = beta;
       }
       tv[j] = tau;
       red[nw] = scale;
@@ -368,16 +402,16 @@ __device__ void householder_qr_cols(double* V, int m, int kx, int k1, double* tv
     __syncthreads();
     const double scale = red[nw];
     const double tau = tv[j];
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) V[i * kx + j] *= scale;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) V[i * ldv + j] *= scale;
     __syncthreads();
     if (tau != 0.0) {
       for (int c = j + 1 + warp; c < kx; c += nw) {
         double w = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) w += V[i * kx + j] * V[i * kx + c];
-        w = warp_sum(w) + V[j * kx + c];
+        for (int i = j + 1 + lane; i < m; i += 32) w += V[i * ldv + j] * V[i * ldv + c];
+        w = warp_sum(w) + V[j * ldv + c];
         __syncwarp();
-        if (lane == 0) V[j * kx + c] -= tau * w;
-        for (int i = j + 1 + lane; i < m; i += 32) V[i * kx + c] -= tau * w * V[i * kx + j];
+        if (lane == 0) V[j * ldv + c] -= tau * w;
+        for (int i = j + 1 + lane; i < m; i += 32) V[i * ldv + c] -= tau * w * V[i * ldv + j];
       }
     }
     __syncthreads();
@@ -385,79 +419,142 @@ __device__ void householder_qr_cols(double* V, int m, int kx, int k1, double* tv
 }
 
 // Apply H_j (j in [jb, je) in the given direction) to column c of X (rows m, ld ldx) by one warp.
-__device__ __forceinline__ void apply_reflector_col(const double* V, int kx, int m, int j, double tau,
+__device__ __forceinline__ void apply_reflector_col(const double* V, int ldv, int m, int j, double tau,
                                                     double* X, int ldx, int c) {
   const int lane = threadIdx.x & 31;
   double w = X[(long long)j * ldx + c];
   double part = 0.0;
-  for (int i = j + 1 + lane; i < m; i += 32) part += V[i * kx + j] * X[(long long)i * ldx + c];
+  for (int i = j + 1 + lane; i < m; i += 32) part += V[i * ldv + j] * X[(long long)i * ldx + c];
   w += warp_sum(part);
   __syncwarp();
   if (lane == 0) X[(long long)j * ldx + c] -= tau * w;
-  for (int i = j + 1 + lane; i < m; i += 32) X[(long long)i * ldx + c] -= tau * w * V[i * kx + j];
+  for (int i = j + 1 + lane; i < m; i += 32) X[(long long)i * ldx + c] -= tau * w * V[i * ldv + j];
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads) svd_kernel(const SvdItem* __restrict__ items,
-                                                       const Seg* __restrict__ segs) {
+
+__device__ __forceinline__ int svd_n(const SvdItem& it) { return it.m - min(it.m, it.kx); }
+
+__device__ void load_v_factor(const SvdItem& it, double* V, int ldv, double* tv, double* red) {
+  const int m = it.m, kx = it.kx, k1 = min(m, kx);
+  for (int e = threadIdx.x; e < m * kx; e += blockDim.x) V[(e / kx) * ldv + e % kx] = mref(it.v, e / kx, e % kx);
+  __syncthreads();
+  householder_qr_cols(V, m, kx, ldv, k1, tv, red);
+}
+
+__global__ void __launch_bounds__(kThreads) svd_tsqr_kernel(const SvdItem* __restrict__ items,
+                                                            const Seg* __restrict__ segs,
+                                                            const SvdWork* __restrict__ work, int rsmem) {
   extern __shared__ double smem[];
   __shared__ double red[40];
+  const SvdWork w = work[blockIdx.x];
+  const SvdItem it = items[w.item];
+  const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
+  const long long N = it.N;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ldv = kx | 1, ldp = n | 1;            // odd strides: conflict-free lane-per-row access
+  double* V = smem;                                // m x ldv
+  double* tv = V + (long long)m * ldv;             // kx + 1
+  double* raw = tv + kx + 1;                       // m x kRawLd (protect case)
+  double* P = raw + (kx > 0 ? m * kRawLd : 0);     // 32 x ldp
+  double* vb = P + kPanel * ldp;                   // 64
+  double* tb = vb + 64;                            // 4
+  double* R = rsmem ? tb + 4 : it.rbuf + (long long)w.a * n * n;
+  if (kx > 0) {
+    load_v_factor(it, V, ldv, tv, red);
+    if (w.a == 0) {
+      for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) it.vws[e] = V[e];
+      for (int e = threadIdx.x; e < kx; e += blockDim.x) it.vws[m * ldv + e] = tv[e];
+    }
+  }
+  if (n == 0) return;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = 0.0;
+  __syncthreads();
+  const long long per = (N + it.nchunk - 1) / it.nchunk;
+  const long long cbeg = w.a * per, cend = min(N, cbeg + per);
+  for (long long c0 = cbeg; c0 < cend; c0 += kPanel) {
+    const long long lim = min(cend, c0 + kPanel);  // columns beyond this chunk load as zero
+    if (kx > 0) {
+      load_hpanel(segs, it.s0, it.s1, m, lim, c0, raw, false, kRawLd);
+      __syncthreads();
+      for (int p = warp; p < kPanel; p += nw)
+        for (int j = 0; j < k1; ++j)
+          if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], raw, kRawLd, p);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
+        const int p = e / n, i = e % n;
+        P[p * ldp + i] = raw[(k1 + i) * kRawLd + p];
+      }
+    } else {
+      load_hpanel(segs, it.s0, it.s1, m, lim, c0, P, true, ldp);
+    }
+    __syncthreads();
+    tsqr_absorb(R, n, P, ldp, vb, tb);
+  }
+  if (rsmem) {
+    double* dst = it.rbuf + (long long)w.a * n * n;
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) dst[e] = R[e];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) svd_merge_kernel(const SvdItem* __restrict__ items,
+                                                             const SvdWork* __restrict__ work, int rsmem) {
+  extern __shared__ double smem[];
+  const SvdWork w = work[blockIdx.x];
+  const SvdItem it = items[w.item];
+  const int n = svd_n(it);
+  const int ldp = n | 1;
+  double* P = smem;               // 32 x ldp
+  double* vb = P + kPanel * ldp;  // 64
+  double* tb = vb + 64;         // 4
+  double* Ra = it.rbuf + (long long)w.a * n * n;
+  const double* Rb = it.rbuf + (long long)w.b * n * n;
+  double* R = rsmem ? tb + 4 : Ra;
+  if (rsmem) {
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = Ra[e];
+  }
+  for (int r0 = 0; r0 < n; r0 += kPanel) {
+    for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
+      const int p = e / n, j = e % n;
+      P[p * ldp + j] = (r0 + p < n) ? Rb[(long long)(r0 + p) * n + j] : 0.0;
+    }
+    __syncthreads();
+    tsqr_absorb(R, n, P, ldp, vb, tb, r0);
+  }
+  if (rsmem) {
+    __syncthreads();
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) Ra[e] = R[e];
+  }
+}
+
+static constexpr int kFinishThreads = 512;  // Jacobi: more warps = fewer row pairs per warp per step
+
+__global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
+  extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
+  __shared__ double jred[kFinishThreads / 32 + 1];
   const SvdItem it = items[blockIdx.x];
-  const int m = it.m, kx = it.kx;
-  const int k1 = min(m, kx);
-  const int n = m - k1;  // rows of the matrix actually truncated
+  const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
   const long long N = it.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-
-  double* V = smem;                         // m x kx
-  double* tv = V + (long long)m * kx;       // kx (+1)
-  double* raw = tv + kx + 1;                // m x 32 (protect case only)
-  double* P = raw + (kx > 0 ? m * kPanel : 0);  // 32 x n
-  double* vb = P + kPanel * n;              // 64
-  double* tb = vb + 64;                     // 4
-  double* sig = tb + 4;                     // n
-  int* ord = (int*)(sig + n);               // n ints (n/2 + 1 doubles)
-  double* R = it.ws ? it.ws : sig + n + (n / 2 + 1);  // n x n
-
-  // 1. protect: Householder QR of V
+  const int ldv = kx | 1;
+  double* V = smem;                          // m x ldv (reflectors from the tsqr stage)
+  double* tv = V + (long long)m * ldv;       // kx + 1
+  double* sig = tv + kx + 1;                 // n
+  int* ord = (int*)(sig + n);                // n ints
+  double* R = rsmem ? sig + n + (n / 2 + 1) : it.rbuf;
   if (kx > 0) {
-    for (int e = threadIdx.x; e < m * kx; e += blockDim.x) {
-      const int i = e / kx, j = e % kx;
-      V[e] = mref(it.v, i, j);
-    }
-    __syncthreads();
-    householder_qr_cols(V, m, kx, k1, tv, red);
+    for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
+    for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
   }
-
-  // 2. TSQR of B^T, B = (Q^T A)[k1:]
   int k2 = 0;
   if (n > 0 && N > 0) {
-    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = 0.0;
+    if (rsmem)
+      for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
     __syncthreads();
-    for (long long c0 = 0; c0 < N; c0 += kPanel) {
-      if (kx > 0) {
-        load_hpanel(segs, it.s0, it.s1, m, N, c0, raw, false, kPanel);
-        __syncthreads();
-        // Q^T raw = H_{k1-1} ... H_0 raw: warp per panel column, reflectors in order 0..k1-1
-        for (int p = warp; p < kPanel; p += nw)
-          for (int j = 0; j < k1; ++j)
-            if (tv[j] != 0.0) apply_reflector_col(V, kx, m, j, tv[j], raw, kPanel, p);
-        __syncthreads();
-        for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
-          const int p = e / n, i = e % n;
-          P[p * n + i] = raw[(k1 + i) * kPanel + p];
-        }
-      } else {
-        load_hpanel(segs, it.s0, it.s1, m, N, c0, P, true, n);
-      }
-      __syncthreads();
-      tsqr_absorb(R, n, P, vb, tb);
-    }
-    // 3. Jacobi on the rows of R: B = R^T Q_B^T, left singular vectors of B = normalised rows of R*
-    jacobi_rows(R, n, &flag);
-    // 4. singular values, order, rank
+    // B = R^T Q_B^T: left singular vectors of B are the normalised rows of R after Jacobi
+    jacobi_rows(R, n, &flag, jred);
     for (int i = warp; i < n; i += nw) {
       double s = 0.0;
       for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * n + j], R[(long long)i * n + j], s);
@@ -489,8 +586,7 @@ __global__ void __launch_bounds__(kThreads) svd_kernel(const SvdItem* __restrict
     if (it.sig_out)
       for (int i = threadIdx.x; i < n; i += blockDim.x) it.sig_out[i] = sig[ord[i]];
   }
-
-  // 5. outputs
+  __syncthreads();
   const int kt = k1 + k2;
   double* Q = it.q_out;  // m x kt
   for (long long e = threadIdx.x; e < (long long)m * kt; e += blockDim.x) {
@@ -506,15 +602,15 @@ __global__ void __launch_bounds__(kThreads) svd_kernel(const SvdItem* __restrict
   }
   __syncthreads();
   if (k1 > 0) {
-    // Q = H_0 H_1 ... H_{k1-1} Y: apply the reflectors in reverse order, warp per column
+    // Q = H_0 H_1 ... H_{k1-1} Y: reflectors in reverse order, one warp per column
     for (int c = warp; c < kt; c += nw)
       for (int j = k1 - 1; j >= 0; --j)
-        if (tv[j] != 0.0) apply_reflector_col(V, kx, m, j, tv[j], Q, kt, c);
+        if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], Q, kt, c);
   }
   if (it.bc_out) {
     for (int e = threadIdx.x; e < kt * kx; e += blockDim.x) {
       const int i = e / kx, j = e % kx;
-      it.bc_out[e] = (i < k1 && j >= i) ? V[i * kx + j] : 0.0;
+      it.bc_out[e] = (i < k1 && j >= i) ? V[i * ldv + j] : 0.0;
     }
   }
   if (threadIdx.x == 0) *it.rank_out = kt;
@@ -737,7 +833,7 @@ cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles
 }
 
 size_t qr_smem(int n, bool ws) {
-  return sizeof(double) * ((size_t)kPanel * n + 64 + 4 + (ws ? 0 : (size_t)n * n));
+  return sizeof(double) * ((size_t)kPanel * (n | 1) + 64 + 4 + (ws ? 0 : (size_t)n * n));
 }
 
 cudaError_t launch_qr(const QrItem* items, const Seg* segs, int nitems, int nmax, bool ws, cudaStream_t st) {
@@ -748,19 +844,44 @@ cudaError_t launch_qr(const QrItem* items, const Seg* segs, int nitems, int nmax
   return cudaGetLastError();
 }
 
-size_t svd_smem(int m, int kx, bool ws) {
+size_t svd_tsqr_smem(int m, int kx, bool rsmem) {
   const int k1 = m < kx ? m : kx;
   const int n = m - k1;
-  size_t d = (size_t)m * kx + kx + 1 + (kx > 0 ? (size_t)m * kPanel : 0) + (size_t)kPanel * n + 64 + 4 + n +
-             (n / 2 + 1);
-  if (!ws) d += (size_t)n * n;
+  size_t d = (size_t)m * (kx | 1) + kx + 1 + (kx > 0 ? (size_t)m * kRawLd : 0) + (size_t)kPanel * (n | 1) + 64 + 4;
+  if (rsmem) d += (size_t)n * n;
   return d * sizeof(double);
 }
 
-cudaError_t launch_svd(const SvdItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
+size_t svd_merge_smem(int n, bool rsmem) {
+  return sizeof(double) * ((size_t)kPanel * (n | 1) + 68 + (rsmem ? (size_t)n * n : 0));
+}
+
+size_t svd_finish_smem(int m, int kx, bool rsmem) {
+  const int k1 = m < kx ? m : kx;
+  const int n = m - k1;
+  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + n + (n / 2 + 1) + (rsmem ? (size_t)n * n : 0));
+}
+
+cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork* work, int nwork, size_t smem,
+                            bool rsmem, cudaStream_t st) {
+  if (nwork == 0) return cudaSuccess;
+  cudaFuncSetAttribute(svd_tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  svd_tsqr_kernel<<<nwork, kThreads, smem, st>>>(items, segs, work, rsmem ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_svd_merge(const SvdItem* items, const SvdWork* work, int nwork, size_t smem, bool rsmem,
+                             cudaStream_t st) {
+  if (nwork == 0) return cudaSuccess;
+  cudaFuncSetAttribute(svd_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  svd_merge_kernel<<<nwork, kThreads, smem, st>>>(items, work, rsmem ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, cudaStream_t st) {
   if (nitems == 0) return cudaSuccess;
-  cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  svd_kernel<<<nitems, kThreads, smem, st>>>(items, segs);
+  cudaFuncSetAttribute(svd_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  svd_finish_kernel<<<nitems, kFinishThreads, smem, st>>>(items, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -9,27 +9,25 @@
 namespace h2g {
 
 // X|ts V_Y,s for leaf row clusters t by block descent (reference induced.py:59-73).
-// Each requested (t, s) pair and every block below it (same row t) is computed once, deepest first.
-void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<std::pair<int, int>>& want,
-                PairMap& memo) {
+// Each requested block and every block below it (same row t) is computed once, deepest first;
+// `memo` is indexed by block id of the view x.
+void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<int>& want,
+                std::vector<Mat>& memo) {
   const Blocks& B = *x.h->bt;
-  std::vector<std::vector<int>> by_h;  // block ids by height
-  std::unordered_map<long long, int> height;  // pairs scheduled by this call
+  if ((int)memo.size() < B.nb) memo.resize(B.nb);
+  std::vector<std::vector<int>> by_h;   // block ids by height
+  std::vector<int> height(B.nb, -2);   // -2: not scheduled by this call
   std::function<int(int)> visit = [&](int b) -> int {
-    const int t = x.row(b), s = x.col(b);
-    const long long key = PairMap::key(t, s);
-    auto hit = height.find(key);
-    if (hit != height.end()) return hit->second;
-    if (memo.get(t, s)) return -1;  // computed by an earlier call
+    if (height[b] != -2) return height[b];
+    if (memo[b].p || (memo[b].r > 0 && memo[b].c == 0)) return -1;  // computed by an earlier call
     int h = 0;
     for (int i = 0; i < B.nkids(b); ++i) h = std::max(h, visit(B.kid(b, i)) + 1);
-    height[key] = h;
+    height[b] = h;
     if ((int)by_h.size() <= h) by_h.resize(h + 1);
     by_h[h].push_back(b);
     return h;
   };
-  for (auto& pr : want) {
-    const int b = x.find(pr.first, pr.second);
+  for (int b : want) {
     if (b < 0) throw StructureErr("xv: pair not in the block tree");
     visit(b);
   }
@@ -41,7 +39,7 @@ void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<s
     for (int b : lvl) {
       const int t = x.row(b), s = x.col(b);
       Mat m{ar.alloc((size_t)rows.size(t) * VY.rank[s]), rows.size(t), VY.rank[s]};
-      memo.put(t, s, m);
+      memo[b] = m;
       g.out(m, false);
       if (B.adm_leaf(b)) {
         g.t3(VX.leafm(t).ref(), x.coup(b), P.at(s), VX.rank[t], P.rows(s));
@@ -51,7 +49,7 @@ void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<s
         for (int i = 0; i < B.nkids(b); ++i) {
           const int b2 = B.kid(b, i);
           const int s2 = x.col(b2);
-          const Mat part = *memo.get(x.row(b2), s2);
+          const Mat part = memo[b2];
           if (s2 != s) g.t2(part.ref(), VY.xferm(s2).ref(), VY.rank[s2]);
           else g.t1(part.ref());
         }
@@ -85,22 +83,24 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
   q.xfer.assign(tr.n, nullptr);
   R.bc.assign(tr.n, Mat{});
 
-  std::vector<std::pair<int, int>> leaf_pairs;
+  std::vector<int> leaf_blocks;
   for (int t = 0; t < tr.n; ++t)
     if (tr.leaf(t))
-      for (int b : mids[t]) leaf_pairs.emplace_back(t, x.col(b));
-  xv_compute(C, out, x, y, P, leaf_pairs, R.xv);
+      for (int b : mids[t]) leaf_blocks.push_back(b);
+  R.proj.assign(B.nb, Mat{});
+  xv_compute(C, out, x, y, P, leaf_blocks, R.xv);
 
   std::vector<Mat> blk(B.nb);
   std::vector<Mat> vx(tr.n);
+  std::vector<Mat> rfb(B.nb);
   for (int lev = tr.depth; lev >= 0; --lev) {
     const std::vector<int>& L = tr.by_level[lev];
     GBatch g1, g2;
-    PairMap rf;
+    std::vector<Mat>& rf = rfb;
     for (int t : L) {
       if (tr.leaf(t)) {
         vx[t] = VX.leafm(t);
-        for (int b : mids[t]) blk[b] = *R.xv.get(t, x.col(b));
+        for (int b : mids[t]) blk[b] = R.xv[b];
         continue;
       }
       const int kx = VX.rank[t];
@@ -123,7 +123,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
           Mat m2{sc.alloc((size_t)q.rank[t2] * VY.rank[s2]), q.rank[t2], VY.rank[s2]};
           g1.out(m2, false);
           g1.t3(R.bc[t2].ref(), x.coup(b2), P.at(s2), R.bc[t2].c, P.rows(s2));
-          rf.put(b2, 0, m2);
+          rf[b2] = m2;
         }
     }
     g1.run(C);
@@ -142,7 +142,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
             const int b2 = B.kid(b, j);
             if (x.row(b2) != c) continue;
             const int s2 = x.col(b2);
-            const Mat pb = B.adm_leaf(b2) ? *rf.get(b2, 0) : *R.proj.get(c, s2);
+            const Mat pb = B.adm_leaf(b2) ? rf[b2] : R.proj[b2];
             if (s2 != s) g2.t2(pb.ref(), VY.xferm(s2).ref(), VY.rank[s2]);
             else g2.t1(pb.ref());
           }
@@ -232,7 +232,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
         Mat pm{out.alloc((size_t)k * VY.rank[s]), k, VY.rank[s]};
         g4.out(pm, false);
         g4.t2(Q.tref(), blk[b].ref(), m);
-        R.proj.put(t, s, pm);
+        R.proj[b] = pm;
       }
     }
     g4.run(C);
@@ -249,6 +249,7 @@ static void emit_push(GBatch& g, const Mat* E, const Mat& S, const Mat* F) {
 
 // Product over T^XY in the induced bases + push-down (reference induced.py:220-355).
 std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt) {
+  HostTimer ht(C, "assemble_total");
   auto G = std::make_shared<H2>();
   G->bt = pt.bt;
   G->rb = qr.q;
@@ -276,20 +277,19 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
   }
   // memoised leaf products needed by dense targets, and row factors of admissible X blocks
-  std::vector<std::pair<int, int>> need_xv, need_wy;
+  HostTimer ht1(C, "assemble_xv_rf");
+  std::vector<int> need_xv, need_wy;
   for (int b = 0; b < B.nb; ++b) {
     if (!B.near_leaf(b)) continue;
-    const int t = B.row[b], r = B.col[b];
     for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
-      const int s = pt.ts[i];
-      if (pt.tk[i] == 'a' && !qr.xv.get(t, s)) need_xv.emplace_back(t, s);
-      if (pt.tk[i] == 'b' && !qc.xv.get(r, s)) need_wy.emplace_back(r, s);
+      if (pt.tk[i] == 'a') need_xv.push_back(pt.tbx[i]);
+      if (pt.tk[i] == 'b') need_wy.push_back(pt.tby[i]);
     }
   }
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
   xv_compute(C, sc, x, y, P, need_xv, qr.xv);
   xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, need_wy, qc.xv);
-  PairMap rf;
+  std::vector<Mat> rf(x.h->bt->nb);
   {
     GBatch g;
     for (int b = 0; b < B.nb; ++b) {
@@ -298,19 +298,20 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
         if (pt.tk[i] != 'a') continue;
         const int s = pt.ts[i];
-        const int bts = bx.find(t, s);
-        if (!bx.b->adm_leaf(bts) || rf.get(t, s)) continue;
+        const int bts = pt.tbx[i];
+        if (!bx.b->adm_leaf(bts) || rf[bts].p) continue;
         // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
         Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
         g.out(m, false);
         g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
-        rf.put(t, s, m);
+        rf[bts] = m;
       }
     }
     g.run(C);
   }
   // all terminal triples (induced.py:286-307), one output per product block
   {
+    HostTimer ht2(C, "assemble_triples");
     GBatch g;
     for (int b = 0; b < B.nb; ++b) {
       const int t = B.row[b], r = B.col[b];
@@ -319,22 +320,22 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       g.out(tgt, false);
       for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
         const int s = pt.ts[i];
-        const int bts = bx.find(t, s), bsr = by.find(s, r);
+        const int bts = pt.tbx[i], bsr = pt.tby[i];
         const char k = pt.tk[i];
         if (k == 'a') {
           const MatRef SY = y.coup(bsr);
           const int ks = y.rb().rank[s], kr = y.cb().rank[r];
           if (dense) {
-            g.t3(qr.xv.get(t, s)->ref(), SY, y.cb().leafm(r).tref(), ks, kr);
+            g.t3(qr.xv[bts].ref(), SY, y.cb().leafm(r).tref(), ks, kr);
           } else {
-            const Mat A = bx.b->adm_leaf(bts) ? *rf.get(t, s) : *qr.proj.get(t, s);
+            const Mat A = bx.b->adm_leaf(bts) ? rf[bts] : qr.proj[bts];
             g.t3(A.ref(), SY, qc.bc[r].tref(), ks, kr);
           }
         } else if (k == 'b') {
           const MatRef SX = x.coup(bts);
           const int kt = x.rb().rank[t], ks = x.cb().rank[s];
-          if (dense) g.t3(x.rb().leafm(t).ref(), SX, qc.xv.get(r, s)->tref(), kt, ks);
-          else g.t3(qr.bc[t].ref(), SX, qc.proj.get(r, s)->tref(), kt, ks);
+          if (dense) g.t3(x.rb().leafm(t).ref(), SX, qc.xv[bsr].tref(), kt, ks);
+          else g.t3(qr.bc[t].ref(), SX, qc.proj[bsr].tref(), kt, ks);
         } else {
           g.t2(x.near(bts), y.near(bsr), x.cols().size(s));
         }
@@ -343,6 +344,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     g.run(C);
   }
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
+  HostTimer ht3(C, "assemble_pushdown");
   for (int lev = 0; lev < B.depth; ++lev) {
     GBatch g1, g2;
     for (int b : B.by_level[lev]) {
@@ -405,7 +407,11 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   record(C, e2);
   Induced qc = induced_rows(C, *keep, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
   record(C, e3);
-  PTree pt = product_tree(X.bv(), Y.bv());
+  PTree pt;
+  {
+    HostTimer ht(C, "product_tree");
+    pt = product_tree(X.bv(), Y.bv());
+  }
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
   record(C, e4);
   G->owned.push_back(keep);

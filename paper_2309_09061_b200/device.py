@@ -29,8 +29,10 @@ class Context:
             raise CudaError("no CUDA device: the B200 product path has no CPU fallback")
         self.lib = N.load()
         self.device = device
+        # the native context runs on a torch-owned stream so torch CUDA events can time it
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
         h = N.P()
-        N.check(self.lib.h2g_ctx_create(device, stream, C.byref(h)))
+        N.check(self.lib.h2g_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
         self.h = h
         self._trees = {}
         self._blocks = {}
@@ -59,6 +61,27 @@ class Context:
         out = np.zeros(2, np.int64)
         N.check(self.lib.h2g_ctx_counters(self.h, out.ctypes.data_as(N.I64P), 1 if reset else 0))
         return {"launches": int(out[0]), "syncs": int(out[1])}
+
+    KCLASSES = ("gsum", "qr_r", "svd", "norm", "gather")
+
+    def set_profile(self, on: bool):
+        N.check(self.lib.h2g_ctx_set_profile(self.h, 1 if on else 0))
+
+    def kernel_stats(self, reset: bool = True) -> dict:
+        out = np.zeros(20)
+        N.check(self.lib.h2g_ctx_kernel_stats(self.h, out.ctypes.data_as(N.F64P), 1 if reset else 0))
+        return {k: {"launches": int(out[4 * i]), "ms": float(out[4 * i + 1]), "flops": float(out[4 * i + 2]),
+                    "bytes": float(out[4 * i + 3])} for i, k in enumerate(self.KCLASSES)}
+
+    def host_times(self, reset: bool = True) -> dict:
+        buf = C.create_string_buffer(1 << 14)
+        self.lib.h2g_ctx_host_times(self.h, buf, len(buf), 1 if reset else 0)
+        out = {}
+        for part in buf.value.decode().split(";"):
+            if "=" in part:
+                k, v = part.split("=")
+                out[k] = float(v)
+        return out
 
     def synchronize(self):
         N.check(self.lib.h2g_ctx_synchronize(self.h))
@@ -186,18 +209,10 @@ class DeviceH2:
         """Host H2Matrix with the reference's container interface."""
         return unpack_h2(self.to_packed(), rows=self.rows, cols=self.cols)
 
-    @property
-    def ranks(self):
-        d = self.to_packed_ranks()
-        return d
-
-    def to_packed_ranks(self):
-        """(row ranks, column ranks) without moving matrix data (downloads sizes only)."""
-        return self.download_ranks()
-
-    def download_ranks(self):
-        d = self.to_packed()
-        return list(d["rb.rank"]), list(d["cb.rank"])
+    def packed_bytes(self) -> int:
+        """Bytes of the packed float64 payload (bases + couplings + nearfield)."""
+        s = self.sizes()
+        return int(8 * (s[3] + s[4] + s[5] + s[6]))
 
 
 def check_same_trees(a, b):

@@ -3,8 +3,8 @@
 Mirrors the reference interface in h2mul/trees.py (same class names, attribute
 names and preorder id conventions, trees.py:1-6) so callers can switch.  The
 product block tree -- the only structure built inside the timed product -- is
-built by the native planner (csrc/planner.cpp, `h2p_product_tree`) when the
-library is available; `build_product_block_tree` below wraps it.
+built by the native planner (csrc/engine.cu `product_tree`, exported as
+h2g_product_tree); `build_product_block_tree` below wraps it.
 """
 
 from __future__ import annotations
@@ -293,5 +293,4 @@ def build_product_block_tree(bx: BlockTree, by: BlockTree) -> BlockTree:
     from . import planner
     if not same_cluster_tree(bx.cols, by.rows):
         raise InvalidInputError("factors do not share the middle cluster tree")
-    pt = planner.product_tree(bx, by)
-    return pt.block_tree()
+    return planner.product_tree(bx, by)

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA product path (through the C ABI) against the reference's golden vectors
+and the live CPU oracle.
+
+Bars (BASELINE.json north_star): identical block structure; per-cluster ranks equal; relative
+error ||(Z_gpu - Z_ref) v|| / ||Z_ref v|| <= 10 eps on probe vectors (tol = 0 cases: <= 1e-10);
+||Z_gpu v - X(Y v)|| / ||X(Y v)|| within the reference's own value x 1.1 (or eps).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from helpers import CONFIG_CASES, RANDOM_CASES, load, rebuild_raw, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2309_09061_b200 as P
+    return P
+
+
+def _probe_tol(eps):
+    return 1e-10 if eps == 0 else 10 * eps
+
+
+def _inputs(d):
+    P = _P()
+    from paper_2309_09061_b200.packed import unpack_h2
+    eps = float(d["eps"][0])
+    if "x/bt.row" in d:
+        x = unpack_h2(d, "x/")
+        y = unpack_h2(d, "y/", rows=x.block_tree.cols)
+        return x, y, eps
+    xr, yr = rebuild_raw(d)
+    x = P.recompress(xr, eps)
+    y = x if yr is xr else P.recompress(yr, eps)
+    assert list(x.row_basis.rank) == list(d["rank.x_row"])   # GPU recompress = reference recompress
+    assert list(y.col_basis.rank) == list(d["rank.y_col"])
+    return x, y, eps
+
+
+@pytest.mark.parametrize("name", RANDOM_CASES + CONFIG_CASES)
+def test_golden_parity(name):
+    P = _P()
+    from paper_2309_09061_b200.h2 import h2_matvec_host
+    d = load(name)
+    x, y, eps = _inputs(d)
+    g = P.multiply(x, y, eps)
+    bt = g.block_tree
+    assert bt.row == list(d["pt.row"]) and bt.col == list(d["pt.col"])
+    assert [int(a) for a in bt.admissible] == list(d["pt.adm"])
+    assert list(g.row_basis.rank) == list(d["rank.induced_row"])
+    assert list(g.col_basis.rank) == list(d["rank.induced_col"])
+    z = P.coarsen(g, x.block_tree, eps)
+    assert list(z.row_basis.rank) == list(d["rank.final_row"])
+    assert list(z.col_basis.rank) == list(d["rank.final_col"])
+    tol = _probe_tol(eps)
+    for i, v in enumerate(d["probe.v"]):
+        assert rel(h2_matvec_host(g, v), d["probe.gv"][i]) <= tol
+        assert rel(h2_matvec_host(z, v), d["probe.zv"][i]) <= tol
+        ref_xy = rel(d["probe.zv"][i], d["probe.xyv"][i])
+        assert rel(h2_matvec_host(z, v), d["probe.xyv"][i]) <= max(eps, 1.1 * ref_xy, 1e-12)
+
+
+def _oracle_pair(seed, n=64, leaf=4, dim=2, rank=3, zero=False):
+    """Random unbalanced pair on three trees (reference tests/util.py:9-48), in package containers."""
+    from paper_2309_09061_b200.h2 import ClusterBasis, H2Matrix
+    from paper_2309_09061_b200.trees import build_block_tree, build_cluster_tree
+    rng = np.random.default_rng(seed)
+    trees = [build_cluster_tree(rng.uniform(size=(n, dim)), leaf) for _ in range(3)]
+
+    def basis(tree):
+        lm = {t: rng.standard_normal((tree.size(t), rank)) for t in range(tree.nnodes) if tree.is_leaf(t)}
+        xf = {c: rng.standard_normal((rank, rank)) for t in range(tree.nnodes) for c in tree.children[t]}
+        return ClusterBasis(tree, [rank] * tree.nnodes, lm, xf)
+
+    def h2(r, c):
+        bt = build_block_tree(r, c, 1.0)
+        s = 0.0 if zero else 1.0
+        cp = {b: s * rng.standard_normal((rank, rank)) for b in bt.admissible_leaves()}
+        nf = {b: s * rng.standard_normal((r.size(bt.row[b]), c.size(bt.col[b]))) for b in bt.inadmissible_leaves()}
+        return H2Matrix(bt, basis(r), basis(c), cp, nf)
+
+    return h2(trees[0], trees[1]), h2(trees[1], trees[2])
+
+
+@pytest.mark.parametrize("seed,tol", [(11, 1e-3), (12, 0.0), (13, 1e-6)])
+def test_live_oracle_random(seed, tol):
+    import oracle as O
+    from helpers import to_oracle
+    P = _P()
+    from paper_2309_09061_b200.h2 import h2_matvec_host
+    x, y = _oracle_pair(seed)
+    ox, oy = to_oracle(x), to_oracle(y)
+    og = O.o_multiply(ox, oy, tol)
+    oz = O.o_coarsen(og, ox.bt, tol)
+    z = P.multiply_coarsen(x, y, tol)
+    assert list(z.row_basis.rank) == oz.rb.rank and list(z.col_basis.rank) == oz.cb.rank
+    rng = np.random.default_rng(seed)
+    for _ in range(3):
+        v = rng.standard_normal(x.shape[1])
+        assert rel(h2_matvec_host(z, v), O.o_matvec(oz, v)) <= _probe_tol(tol)
+
+
+def test_exact_at_zero_tolerance_dense():
+    """tol = 0 reproduces the dense product (reference test_acceptance.py:35-49)."""
+    P = _P()
+    from paper_2309_09061_b200.h2 import to_dense
+    from paper_2309_09061_b200.problems import build_config
+    x, _, _ = build_config("c1", n=512)
+    dx = to_dense(x)
+    ref = dx @ dx
+    g = P.multiply(x, x, 0.0)
+    z = P.coarsen(g, x.block_tree, 0.0)
+    nref = np.linalg.norm(ref, 2)
+    assert np.linalg.norm(to_dense(g) - ref, 2) / nref <= 1e-10
+    assert np.linalg.norm(to_dense(z) - ref, 2) / nref <= 1e-10
+
+
+def test_zero_inputs_give_zero_product():
+    """Exact zero-norm skips (weights.py:88, induced.py:123, coarsening.py:239)."""
+    P = _P()
+    from paper_2309_09061_b200.h2 import to_dense
+    x, y = _oracle_pair(21, zero=True)
+    z = P.multiply_coarsen(x, y, 1e-4)
+    assert np.abs(to_dense(z)).max() == 0.0
+
+
+def test_max_rank_cap():
+    """max_rank caps every induced and final rank (dense.py:99-100, induced.py:131)."""
+    P = _P()
+    import oracle as O
+    from helpers import to_oracle
+    x, y = _oracle_pair(31)
+    g = P.multiply(x, y, 1e-8, max_rank=5)
+    assert max(g.row_basis.rank) <= max(5, 3) and max(g.col_basis.rank) <= max(5, 3)
+    og = O.o_multiply(to_oracle(x), to_oracle(y), 1e-8, max_rank=5)
+    assert list(g.row_basis.rank) == og.rb.rank
+    z = P.coarsen(g, x.block_tree, 1e-8, max_rank=4)
+    assert max(z.row_basis.rank) <= 4 and max(z.col_basis.rank) <= 4
+
+
+def test_error_behaviour():
+    P = _P()
+    from paper_2309_09061_b200 import InvalidInputError
+    from paper_2309_09061_b200.trees import build_block_tree, build_cluster_tree
+    x, y = _oracle_pair(41)
+    with pytest.raises(InvalidInputError):
+        P.multiply(x, y, -1.0)
+    with pytest.raises(InvalidInputError):
+        P.multiply(y, _oracle_pair(42, n=70)[0], 1e-3)   # middle trees differ
+    g = P.multiply(x, y, 1e-3)
+    other = build_cluster_tree(np.random.default_rng(1).uniform(size=(70, 2)), 4)
+    with pytest.raises(InvalidInputError):
+        P.coarsen(g, build_block_tree(other, other, 1.0), 1e-3)
+
+
+def test_native_library_loaded_from_repo():
+    P = _P()
+    from paper_2309_09061_b200 import _native
+    x, y = _oracle_pair(51)
+    P.multiply_coarsen(x, y, 1e-3)
+    maps = open("/proc/self/maps").read()
+    assert os.path.realpath(_native.LIB_PATH) in maps
