@@ -20,6 +20,11 @@ void cuda_check(cudaError_t e, const char* what) {
 // ============================================================================ infrastructure
 
 Arena::~Arena() {
+  if (cross_stream) {
+    cudaDeviceSynchronize();
+    for (void* p : chunks) cudaFree(p);
+    return;
+  }
   for (void* p : chunks) cudaFreeAsync(p, st);
 }
 
@@ -148,6 +153,40 @@ void* Ctx::stage(const void* src, size_t bytes) {
   return d;
 }
 
+Ctx& Ctx::side() {
+  if (!side_) side_.reset(new Ctx(device, nullptr));
+  side_->timing = timing;
+  side_->prof = prof;
+  // the side stream starts after everything queued so far on the main stream
+  cudaEvent_t e;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cudaEventRecord(e, st);
+  cudaStreamWaitEvent(side_->st, e, 0);
+  cudaEventDestroy(e);
+  return *side_;
+}
+
+void Ctx::join_side(Ctx& S) {
+  cudaEvent_t e;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cudaEventRecord(e, S.st);
+  cudaStreamWaitEvent(st, e, 0);
+  cudaEventDestroy(e);
+  launches += S.launches;
+  syncs += S.syncs;
+  S.launches = S.syncs = 0;
+  S.sync();  // drains the side's profile events (already complete once the join is waited on)
+  for (int k = 0; k < K_NCLASS; ++k) {
+    kstat[k].launches += S.kstat[k].launches;
+    kstat[k].ms += S.kstat[k].ms;
+    kstat[k].flops += S.kstat[k].flops;
+    kstat[k].bytes += S.kstat[k].bytes;
+    S.kstat[k] = KStat{};
+  }
+  for (auto& kv : S.htime) htime["side." + kv.first] += kv.second;
+  S.htime.clear();
+}
+
 cudaEvent_t Ctx::event() {
   cudaEvent_t e;
   cuda_check(cudaEventCreate(&e), "event");
@@ -213,7 +252,30 @@ void GBatch::run(Ctx& C) {
   k2max = 0;
 }
 
-static constexpr size_t kSmemLimit = 227 * 1024;
+void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
+  HostTimer ht(C, "gbatch_run");
+  std::vector<GTile> tiles;
+  for (int i = 0; i < (int)outs.size(); ++i) {
+    const GOut& o = outs[i];
+    if (o.m <= 0 || o.n <= 0) continue;
+    const int tm = (o.m + 63) / 64, tn = (o.n + 63) / 64;
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
+  }
+  if (!tiles.empty()) {
+    GOut* d_o = C.push(outs);
+    GTile* d_l = C.push(tiles);
+    cudaEvent_t ev = C.prof_begin();
+    cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+    C.prof_end(K_GSUM, ev, flops_hint, 0.0);
+    ++C.launches;
+  }
+  outs.clear();
+  terms.clear();
+  k2max = 0;
+}
+
+static constexpr size_t kSmemLimit = 227 * 1024 - 1024;  // minus the kernels' static shared memory
 
 void QrBatch::run(Ctx& C, Arena& scratch) {
   std::vector<QrItem> small, big;
@@ -259,35 +321,47 @@ std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {
   std::vector<double> res(items.size(), 0.0);
   if (items.empty()) return res;
   double* d_out = scratch.alloc(items.size());
+  cuda_check(cudaMemsetAsync(d_out, 0, items.size() * sizeof(double), C.st), "memset");
   size_t smem = 0;
-  std::vector<NormItem> live;
-  std::vector<int> where;
+  std::vector<NormItem> big, small;  // small: single segment, both sides <= 64 (warp Lanczos)
   for (size_t i = 0; i < items.size(); ++i) {
     items[i].out = d_out + i;
     if (items[i].m == 0 || items[i].N == 0) continue;
+    const long long mn = std::min<long long>(items[i].m, items[i].N), mx = std::max<long long>(items[i].m, items[i].N);
+    if (items[i].s1 - items[i].s0 == 1 && mn <= 64 && mx <= 128 && items[i].m * (items[i].N | 1) <= 64 * 65) {
+      small.push_back(items[i]);
+      continue;
+    }
     const bool rowside = (items[i].m <= items[i].N) || (items[i].m <= 160);
     const long long g = rowside ? items[i].m : items[i].N;
     if (g > 180) throw StructureErr("spectral norm: both sides above 180");
     smem = std::max(smem, norm_smem(items[i].m, items[i].N));
-    live.push_back(items[i]);
-    where.push_back((int)i);
+    big.push_back(items[i]);
   }
-  if (!live.empty()) {
+  if (!big.empty() || !small.empty()) {
     double fl = 0, by = 0;
     if (C.prof)
-      for (auto& it : live) {  // Gram on the short side + tridiagonalisation
-        const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
-        fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
-        by += 8 * mn * mx;
-      }
-    NormItem* d_i = C.push(live);
+      for (auto* v : {&big, &small})
+        for (auto& it : *v) {  // Gram on the short side + tridiagonalisation (reference's work)
+          const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
+          fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
+          by += 8 * mn * mx;
+        }
     Seg* d_s = C.push(sl.segs);
+    NormItem* d_big = C.push(big);
+    NormItem* d_small = C.push(small);
     cudaEvent_t ev = C.prof_begin();
-    cuda_check(launch_norm(d_i, d_s, (int)live.size(), smem, C.st), "norm");
+    if (!big.empty()) {
+      cuda_check(launch_norm(d_big, d_s, (int)big.size(), smem, C.st), "norm");
+      ++C.launches;
+    }
+    if (!small.empty()) {
+      cuda_check(launch_norm_warp(d_small, d_s, (int)small.size(), C.st), "norm_warp");
+      ++C.launches;
+    }
     C.prof_end(K_NORM, ev, fl, by);
-    ++C.launches;
     std::vector<double> vals = C.read(d_out, items.size());
-    for (int w : where) res[w] = vals[w];
+    for (size_t i = 0; i < items.size(); ++i) res[i] = vals[i];
   }
   items.clear();
   sl.segs.clear();

@@ -30,6 +30,8 @@ cudaError_t launch_svd_merge(const SvdItem*, const SvdWork*, int nwork, size_t s
 cudaError_t launch_svd_finish(const SvdItem*, int nitems, size_t smem, bool rsmem, cudaStream_t);
 cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
+cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
+cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t);
 size_t qr_smem(int n, bool ws);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t svd_merge_smem(int n, bool rsmem);
@@ -90,6 +92,7 @@ struct BView {
 // ------------------------------------------------------------------ device memory
 struct Arena {  // bump allocator over cudaMalloc'd chunks, freed together
   cudaStream_t st = nullptr;
+  bool cross_stream = false;  // used by other streams too: free after a device-wide sync
   std::vector<void*> chunks;
   char* cur = nullptr;
   size_t left = 0;
@@ -190,8 +193,11 @@ struct Ctx {
   void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
   void drain_prof();
 
+  std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
   Ctx(int dev, cudaStream_t s);
   ~Ctx();
+  Ctx& side();
+  void join_side(Ctx& S);  // main stream waits for the side stream's queued work
   void* stage(const void* src, size_t bytes);  // returns device pointer (async copy enqueued)
   template <class T> T* push(const std::vector<T>& v) {
     return v.empty() ? nullptr : (T*)stage(v.data(), v.size() * sizeof(T));
@@ -232,14 +238,23 @@ struct GBatch {
   void t2(MatRef a, MatRef b, int k, double al = 1.0);
   void t3(MatRef a, MatRef b, MatRef d, int k, int k2, double al = 1.0);
   void run(Ctx& C);
+  // launch with a device-resident term array (terms generated on the GPU); `outs` index into it
+  void run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint);
   bool empty() const { return outs.empty(); }
 };
 
-struct SegList {
+struct SegList {  // segments of the batch's items; begin() opens (and closes) an item
   std::vector<Seg> segs;
-  int begin() const { return (int)segs.size(); }
+  long long cur = 0;
+  int begin() {
+    cur = 0;
+    return (int)segs.size();
+  }
   void add(MatRef a, int w, double scale = 1.0) {
-    if (w > 0) segs.push_back(Seg{a, w, 0, scale});
+    if (w > 0) {
+      segs.push_back(Seg{a, w, 0, scale, cur});
+      cur += w;
+    }
   }
 };
 

@@ -43,6 +43,7 @@ struct Seg {
   int w;
   int pad_;
   double scale;
+  long long off;  // first stacked line of this segment within its item
 };
 
 // R-only QR of vstack(segs[s0:s1]) (M x n); writes min(M, n) x n rows (ld n) to out.
@@ -85,6 +86,43 @@ struct NormItem {
   int s0, s1, m, pad_;
   long long N;
   double* out;
+};
+
+// Device-side expansion of the product assembly (reference induced.py:286-307): one GTerm per
+// terminal triple (node, middle s, kind), operands looked up in per-block / per-cluster tables.
+struct AsmTables {
+  // per triple
+  const int* tnode;
+  const int* ts;
+  const char* tk;
+  const int* tbx;
+  const int* tby;
+  // per product node
+  const int* node_row;
+  const int* node_col;
+  const unsigned char* node_dense;
+  // per X block (row view): coupling, nearfield, admissible-leaf flag, row factor, projection, X|ts V_Y,s
+  const MatRef* xcoup;
+  const MatRef* xnear;
+  const unsigned char* xadm;
+  const MatRef* rf;
+  const MatRef* rproj;
+  const MatRef* xv;
+  // per Y block: coupling, nearfield, column projection, Y|sr^T W_X,s
+  const MatRef* ycoup;
+  const MatRef* ynear;
+  const MatRef* cproj;
+  const MatRef* wyl;
+  // per cluster
+  const MatRef* vxleaf;  // row tree: V_X leaf
+  const MatRef* bcr;     // row tree: induced basis change
+  const MatRef* wyleaf;  // column tree: W_Y leaf
+  const MatRef* bcc;     // column tree: induced basis change
+  const int* kx_row;     // rank of V_X per row cluster
+  const int* kwx_mid;    // rank of W_X per middle cluster
+  const int* ky_mid;     // rank of V_Y per middle cluster
+  const int* kwy_col;    // rank of W_Y per column cluster
+  const int* size_mid;   // middle cluster sizes
 };
 
 }  // namespace h2g

@@ -13,9 +13,13 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <mutex>
+
 #include "h2g_types.h"
 
 namespace h2g {
+
+static void init_attributes();
 
 static constexpr int kThreads = 256;
 static constexpr int kTile = 64;   // gsum output tile
@@ -139,10 +143,10 @@ __global__ void __launch_bounds__(kThreads) gsum_kernel(const GOut* __restrict__
 
 // ---------------------------------------------------------------------------------------------
 // Streamed structured Householder update (TSQR step): [R; P] -> R', R (n x n upper triangular),
-// P (32 x n) the next rows.  One column per iteration, one barrier per column: the warp owning
-// column j+1 applies reflector j to it and immediately builds reflector j+1.
+// P (32 x n) the next rows.
 // ---------------------------------------------------------------------------------------------
 
+// Reflector j from column j of P (one lane per panel row) and R[j][j]; run by one whole warp.
 __device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int ldp, int j, double* vb, double* tb) {
   const int lane = threadIdx.x & 31;
   const double x = P[lane * ldp + j];
@@ -158,39 +162,40 @@ __device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int ldp, 
   }
   vb[lane] = v;
   if (lane == 0) *tb = tau;
-  P[lane * ldp + j] = 0.0;
 }
 
-__device__ __forceinline__ void tsqr_apply(double* R, int n, double* P, int ldp, int j, int c, double v,
-                                           double tau) {
-  const int lane = threadIdx.x & 31;
-  const double p = P[lane * ldp + c];
-  const double w = R[(long long)j * n + c] + warp_sum(v * p);
-  __syncwarp();
-  if (lane == 0) R[(long long)j * n + c] -= tau * w;
-  P[lane * ldp + c] = p - tau * w * v;
-}
-
+// [R; P] -> R' (structured TSQR step).  One thread per trailing column applies reflector j with a
+// 32-term dot product and a 32-term update (no shuffles); the warp holding the owner of column j+1
+// then builds reflector j+1 cooperatively (lane per panel row).  One barrier per column; needs
+// n - 1 <= kThreads.  Columns < jstart of P are known to be zero (triangular panels in merges).
 __device__ void tsqr_absorb(double* R, int n, double* P, int ldp, double* vb /*64*/, double* tb /*2*/,
                             int jstart = 0) {
-  // columns < jstart of P are known to be zero (triangular panels in merges): no reflector there
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
   if (jstart >= n) return;
-  if (warp == 0) tsqr_make(R, n, P, ldp, jstart, vb + (jstart & 1) * 32, tb + (jstart & 1));
+  if (warp == ((jstart & (kThreads - 1)) >> 5)) tsqr_make(R, n, P, ldp, jstart, vb + (jstart & 1) * 32, tb + (jstart & 1));
   __syncthreads();
   for (int j = jstart; j < n; ++j) {
     const int cur = j & 1;
-    const double v = vb[cur * 32 + lane];
     const double tau = tb[cur];
-    const bool active = tau != 0.0;
-    if (j + 1 < n && warp == (j + 1) % nw) {
-      if (active) tsqr_apply(R, n, P, ldp, j, j + 1, v, tau);
+    const double* v = vb + cur * 32;
+    const int c = j + 1 + ((tid - (j + 1)) & (kThreads - 1));  // this thread's column (at most one)
+    if (tau != 0.0 && c < n) {
+      double w0 = R[(long long)j * n + c], w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < kPanel; i += 4) {
+        w0 = fma(v[i], P[i * ldp + c], w0);
+        w1 = fma(v[i + 1], P[(i + 1) * ldp + c], w1);
+        w2 = fma(v[i + 2], P[(i + 2) * ldp + c], w2);
+        w3 = fma(v[i + 3], P[(i + 3) * ldp + c], w3);
+      }
+      const double tw = tau * ((w0 + w1) + (w2 + w3));
+      R[(long long)j * n + c] -= tw;
+#pragma unroll 8
+      for (int i = 0; i < kPanel; ++i) P[i * ldp + c] -= tw * v[i];
+    }
+    if (j + 1 < n && warp == (((j + 1) & (kThreads - 1)) >> 5)) {
       __syncwarp();
       tsqr_make(R, n, P, ldp, j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
-    }
-    if (active) {
-      int c0 = j + 2 + ((warp - (j + 2)) % nw + nw) % nw;
-      for (int c = c0; c < n; c += nw) tsqr_apply(R, n, P, ldp, j, c, v, tau);
     }
     __syncthreads();
   }
@@ -254,11 +259,108 @@ __device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M,
   }
 }
 
+// Register-staged panel fetch: every thread holds up to kFetch elements of the NEXT 32-line panel,
+// so its global loads are in flight while the current panel is absorbed (the absorb loop is
+// latency bound; without the prefetch each panel waited on a chain of dependent HBM loads).
+static constexpr int kFetch = 16;  // 32 lines x 128 entries / 256 threads
+
+struct PanelFetch {
+  double v[kFetch];
+};
+
+__device__ __forceinline__ int find_seg(const Seg* __restrict__ segs, int s0, int s1, long long line) {
+  int lo = s0, hi = s1 - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].off <= line) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// rows r0..r0+31 of vstack(segs) (M x n): element e -> (p = e / n, j = e % n), row-coalesced
+__device__ __forceinline__ void fetch_vrows(PanelFetch& f, const Seg* __restrict__ segs, int s0, int s1, int n,
+                                            long long M, long long r0) {
+  const int tot = kPanel * n;
+  int cur_p = -1;
+  MatRef a{nullptr, 0, 0};
+  double sc = 0.0;
+  long long off = 0;
+#pragma unroll
+  for (int q = 0; q < kFetch; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    double val = 0.0;
+    if (e < tot) {
+      const int p = e / n, j = e - p * n;
+      const long long r = r0 + p;
+      if (r < M) {
+        if (p != cur_p) {
+          const Seg& sg = segs[find_seg(segs, s0, s1, r)];
+          a = sg.a;
+          sc = sg.scale;
+          off = sg.off;
+          cur_p = p;
+        }
+        val = sc * mref(a, r - off, j);
+      }
+    }
+    f.v[q] = val;
+  }
+}
+
+__device__ __forceinline__ void store_vrows(const PanelFetch& f, double* P, int ldp, int n) {
+  const int tot = kPanel * n;
+#pragma unroll
+  for (int q = 0; q < kFetch; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    if (e < tot) {
+      const int p = e / n, j = e - p * n;
+      P[p * ldp + j] = f.v[q];
+    }
+  }
+}
+
+// columns c0..c0+31 of hstack(segs) (m x N): element e -> (i = e / 32, p = e % 32); a thread keeps
+// one column p for all its elements (blockDim is a multiple of 32), so one segment lookup per panel
+__device__ __forceinline__ void fetch_hcols(PanelFetch& f, const Seg* __restrict__ segs, int s0, int s1, int m,
+                                            long long N, long long c0) {
+  const int p = threadIdx.x & 31;
+  const long long c = c0 + p;
+  MatRef a{nullptr, 0, 0};
+  double sc = 0.0;
+  long long lc = 0;
+  const bool live = c < N;
+  if (live) {
+    const Seg& sg = segs[find_seg(segs, s0, s1, c)];
+    a = sg.a;
+    sc = sg.scale;
+    lc = c - sg.off;
+  }
+  const int tot = kPanel * m;
+#pragma unroll
+  for (int q = 0; q < kFetch; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    f.v[q] = (live && e < tot) ? sc * mref(a, e >> 5, lc) : 0.0;
+  }
+}
+
+// store as P[p * ld + i] (transposed: panel rows are the stack's columns) or raw[i * ld + p]
+__device__ __forceinline__ void store_hcols(const PanelFetch& f, double* dst, int ld, int m, bool transpose) {
+  const int tot = kPanel * m;
+#pragma unroll
+  for (int q = 0; q < kFetch; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    if (e < tot) {
+      const int i = e >> 5, p = e & 31;
+      if (transpose) dst[p * ld + i] = f.v[q]; else dst[i * ld + p] = f.v[q];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // qr_r: R factor of vstack(segs) (reference dense.py:145-150 / numpy qr mode="r").
 // ---------------------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kThreads) qr_r_kernel(const QrItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads, 3) qr_r_kernel(const QrItem* __restrict__ items,
                                                         const Seg* __restrict__ segs) {
   extern __shared__ double smem[];
   const QrItem it = items[blockIdx.x];
@@ -271,9 +373,14 @@ __global__ void __launch_bounds__(kThreads) qr_r_kernel(const QrItem* __restrict
   const long long nn = (long long)n * n;
   for (long long e = threadIdx.x; e < nn; e += blockDim.x) R[e] = 0.0;
   __syncthreads();
+  const bool pre = kPanel * n <= kFetch * (int)blockDim.x;
+  PanelFetch f;
+  if (pre) fetch_vrows(f, segs, it.s0, it.s1, n, it.M, 0);
   for (long long r0 = 0; r0 < it.M; r0 += kPanel) {
-    load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P, ldp);
+    if (pre) store_vrows(f, P, ldp, n);
+    else load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P, ldp);
     __syncthreads();
+    if (pre && r0 + kPanel < it.M) fetch_vrows(f, segs, it.s0, it.s1, n, it.M, r0 + kPanel);
     tsqr_absorb(R, n, P, ldp, vb, tb);
   }
   const long long rows = it.M < n ? it.M : n;
@@ -314,45 +421,55 @@ __device__ void jacobi_rows(double* W, int n, int* flag, double* red) {
   }
   const double frozen = red[nw];
   const int np = (n + 1) & ~1;  // even number of players, player n (if odd) is a bye
-  const int npairs = np / 2;
-  // convergence threshold sqrt(n) eps (LAPACK dgesvj): rounding noise of an n-term dot product
-  // never falls below eps, so a pure-eps test can keep rotating to the sweep limit
-  const double tol = kEps * sqrt((double)n);
+  const int npairs = np / 2, m1 = np - 1;
+  // convergence threshold sqrt(n) eps (LAPACK dgesvj); tested squared to avoid square roots
+  const double tol2 = kEps * kEps * (double)n;
+  // two row pairs per warp at a time, one per half-warp (16 lanes, 4-step butterflies)
+  const int half = lane >> 4, hl = lane & 15;
+  const int nslots = 2 * nw;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
-    for (int step = 0; step < np - 1; ++step) {
-      for (int q = warp; q < npairs; q += nw) {
-        // circle method: player 0 fixed, players 1..np-1 rotate by `step`
-        const int a = (q == 0) ? 0 : 1 + (q + step) % (np - 1);
-        const int b = 1 + ((q == 0 ? 0 : np - 1 - q) + step) % (np - 1);
-        if (a >= n || b >= n) continue;
-        double* ra = W + (long long)a * n;
-        double* rb = W + (long long)b * n;
+    for (int step = 0; step < m1; ++step) {
+      for (int q0 = 2 * warp; q0 < npairs; q0 += nslots) {
+        const int q = q0 + half;
+        // circle method: player 0 fixed, players 1..np-1 rotate by `step` (no integer division)
+        int xa = q + step;
+        if (xa >= m1) xa -= m1;
+        int xb = (q == 0 ? 0 : m1 - q) + step;
+        while (xb >= m1) xb -= m1;
+        const int a = (q == 0) ? 0 : 1 + xa;
+        const int b = 1 + xb;
+        const bool live = q < npairs && a < n && b < n;
+        double* ra = W + (long long)(live ? a : 0) * n;
+        double* rb = W + (long long)(live ? b : 0) * n;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int j = lane; j < n; j += 32) {
-          const double x = ra[j], y = rb[j];
-          al = fma(x, x, al);
-          be = fma(y, y, be);
-          ga = fma(x, y, ga);
-        }
+        if (live)
+          for (int j = hl; j < n; j += 16) {
+            const double x = ra[j], y = rb[j];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {  // three independent butterflies, interleaved
+        for (int o = 8; o > 0; o >>= 1) {  // three independent butterflies within the half-warp
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (ga != 0.0 && al > frozen && be > frozen && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+        if (live && ga != 0.0 && al > frozen && be > frozen && ga * ga > tol2 * al * be) {
           const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t);
-          const double s = c * t;
-          for (int j = lane; j < n; j += 32) {
+          const double az = fabs(zeta);
+          const double t0 = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(az, az, 1.0)));
+          const double t = zeta >= 0.0 ? t0 : -t0;
+          const double c = rsqrt(fma(t, t, 1.0));
+          const double sn = c * t;
+          for (int j = hl; j < n; j += 16) {
             const double x = ra[j], y = rb[j];
-            ra[j] = c * x - s * y;
-            rb[j] = s * x + c * y;
+            ra[j] = c * x - sn * y;
+            rb[j] = sn * x + c * y;
           }
-          if (lane == 0) *flag = 1;
+          if (hl == 0) *flag = 1;
         }
         __syncwarp();
       }
@@ -442,7 +559,7 @@ __device__ void load_v_factor(const SvdItem& it, double* V, int ldv, double* tv,
   householder_qr_cols(V, m, kx, ldv, k1, tv, red);
 }
 
-__global__ void __launch_bounds__(kThreads) svd_tsqr_kernel(const SvdItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads, 3) svd_tsqr_kernel(const SvdItem* __restrict__ items,
                                                             const Seg* __restrict__ segs,
                                                             const SvdWork* __restrict__ work, int rsmem) {
   extern __shared__ double smem[];
@@ -472,11 +589,16 @@ __global__ void __launch_bounds__(kThreads) svd_tsqr_kernel(const SvdItem* __res
   __syncthreads();
   const long long per = (N + it.nchunk - 1) / it.nchunk;
   const long long cbeg = w.a * per, cend = min(N, cbeg + per);
+  const bool pre = kPanel * m <= kFetch * (int)blockDim.x;
+  PanelFetch f;
+  if (pre && cbeg < cend) fetch_hcols(f, segs, it.s0, it.s1, m, min(cend, cbeg + kPanel), cbeg);
   for (long long c0 = cbeg; c0 < cend; c0 += kPanel) {
     const long long lim = min(cend, c0 + kPanel);  // columns beyond this chunk load as zero
     if (kx > 0) {
-      load_hpanel(segs, it.s0, it.s1, m, lim, c0, raw, false, kRawLd);
+      if (pre) store_hcols(f, raw, kRawLd, m, false);
+      else load_hpanel(segs, it.s0, it.s1, m, lim, c0, raw, false, kRawLd);
       __syncthreads();
+      if (pre && c0 + kPanel < cend) fetch_hcols(f, segs, it.s0, it.s1, m, min(cend, c0 + 2 * kPanel), c0 + kPanel);
       for (int p = warp; p < kPanel; p += nw)
         for (int j = 0; j < k1; ++j)
           if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], raw, kRawLd, p);
@@ -486,7 +608,10 @@ __global__ void __launch_bounds__(kThreads) svd_tsqr_kernel(const SvdItem* __res
         P[p * ldp + i] = raw[(k1 + i) * kRawLd + p];
       }
     } else {
-      load_hpanel(segs, it.s0, it.s1, m, lim, c0, P, true, ldp);
+      if (pre) store_hcols(f, P, ldp, m, true);
+      else load_hpanel(segs, it.s0, it.s1, m, lim, c0, P, true, ldp);
+      __syncthreads();
+      if (pre && c0 + kPanel < cend) fetch_hcols(f, segs, it.s0, it.s1, m, min(cend, c0 + 2 * kPanel), c0 + kPanel);
     }
     __syncthreads();
     tsqr_absorb(R, n, P, ldp, vb, tb);
@@ -497,7 +622,7 @@ __global__ void __launch_bounds__(kThreads) svd_tsqr_kernel(const SvdItem* __res
   }
 }
 
-__global__ void __launch_bounds__(kThreads) svd_merge_kernel(const SvdItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads, 3) svd_merge_kernel(const SvdItem* __restrict__ items,
                                                              const SvdWork* __restrict__ work, int rsmem) {
   extern __shared__ double smem[];
   const SvdWork w = work[blockIdx.x];
@@ -804,6 +929,190 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
 }
 
 // ---------------------------------------------------------------------------------------------
+// norm_warp_kernel: sigma_1 of a single-segment matrix with m, N <= 64, one warp per matrix.
+// A lives in shared memory; Lanczos on the smaller Gram side (A^T A or A A^T, never formed) runs
+// min(m, N) steps (full length: the tridiagonal carries the whole spectrum, the extreme Ritz value
+// is accurate despite loss of orthogonality), then Sturm multisection on the tridiagonal.
+// An exactly zero matrix returns exactly 0 (the reference's zero-norm skips are exact tests).
+// ---------------------------------------------------------------------------------------------
+
+static constexpr int kNW = 2;            // warps (matrices) per CTA
+static constexpr int kNWMax = 64;        // smaller side (Lanczos vector length) handled here
+static constexpr int kNWMaxH = 128;      // larger side
+static constexpr int kNWCap = 64 * 65;   // A capacity (doubles): m * (N | 1) <= kNWCap
+
+__device__ double warp_lambda_max(const double* d, const double* e, int g) {
+  const int lane = threadIdx.x & 31;
+  double lo = 1e300, hi = -1e300;
+  for (int i = lane; i < g; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < g ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const double span = fmax(fabs(lo), fabs(hi));
+  if (span == 0.0) return 0.0;
+  hi += 2.0 * kEps * span + 1e-300;
+  lo -= 2.0 * kEps * span + 1e-300;
+  for (int round = 0; round < 64; ++round) {
+    if (hi - lo <= 2.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
+    // two points per lane (independent recurrences interleaved): 65-way multisection
+    const double w = (hi - lo) / 65.0;
+    const double x0 = lo + w * (double)(2 * lane + 1), x1 = lo + w * (double)(2 * lane + 2);
+    int c0 = 0, c1 = 0;
+    double q0 = d[0] - x0, q1 = d[0] - x1;
+    c0 += q0 < 0.0;
+    c1 += q1 < 0.0;
+    for (int i = 1; i < g; ++i) {
+      const double e2 = e[i - 1] * e[i - 1];
+      if (q0 == 0.0) q0 = -1e-300;
+      if (q1 == 0.0) q1 = -1e-300;
+      q0 = (d[i] - x0) - e2 / q0;
+      q1 = (d[i] - x1) - e2 / q1;
+      c0 += q0 < 0.0;
+      c1 += q1 < 0.0;
+    }
+    // points in increasing order: p = 2*lane+1 (x0), 2*lane+2 (x1); find the first with count == g
+    const unsigned f0 = __ballot_sync(0xffffffffu, c0 >= g), f1 = __ballot_sync(0xffffffffu, c1 >= g);
+    int first = 65;
+    if (f0) first = min(first, 2 * (__ffs(f0) - 1) + 1);
+    if (f1) first = min(first, 2 * (__ffs(f1) - 1) + 2);
+    const double nhi = first < 65 ? lo + w * first : hi;
+    const double nlo = first < 65 ? lo + w * (first - 1) : lo + w * 64.0;
+    lo = nlo;
+    hi = nhi;
+  }
+  return 0.5 * (lo + hi);
+}
+
+__global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __restrict__ items,
+                                                             const Seg* __restrict__ segs, int nitems) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = blockIdx.x * kNW + warp;
+  if (idx >= nitems) return;
+  double* A = smem + warp * (kNWCap + 3 * kNWMax + kNWMaxH);
+  double* vs = A + kNWCap;          // broadcast vector (length g)
+  double* us = vs + kNWMax;         // intermediate (length h)
+  double* al = us + kNWMaxH;        // Lanczos diagonal
+  double* be = al + kNWMax;         // Lanczos off-diagonal
+  const NormItem it = items[idx];
+  const Seg sg = segs[it.s0];
+  const int m = it.m, N = (int)it.N;
+  const int kNWLd = N | 1;          // odd row stride: lane-per-row access without bank conflicts
+  double amax = 0.0;
+  const int tot = m * N;
+  for (int e0 = 0; e0 < tot; e0 += 8 * 32) {  // 8 independent loads in flight per lane
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * 32 + lane;
+      a[q] = e < tot ? mref(sg.a, e / N, e % N) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * 32 + lane;
+      if (e < tot) {
+        const double v = sg.scale * a[q];
+        A[(e / N) * kNWLd + e % N] = v;
+        amax = fmax(amax, fabs(v));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (amax == 0.0) {
+    if (lane == 0) *it.out = 0.0;
+    return;
+  }
+  const bool colside = N <= m;  // Lanczos vectors live on the smaller side
+  const int g = colside ? N : m, h = colside ? m : N;
+  // deterministic pseudo-random start vector
+  double v0 = 0.0, v1 = 0.0;
+  {
+    unsigned s0 = 2654435761u * (lane + 1) ^ 0x9e3779b9u, s1 = 2654435761u * (lane + 33) ^ 0x85ebca6bu;
+    s0 ^= s0 >> 13; s0 *= 0x5bd1e995u; s0 ^= s0 >> 15;
+    s1 ^= s1 >> 13; s1 *= 0x5bd1e995u; s1 ^= s1 >> 15;
+    v0 = lane < g ? 0.5 + (double)(s0 & 0xffff) / 65536.0 : 0.0;
+    v1 = lane + 32 < g ? 0.5 + (double)(s1 & 0xffff) / 65536.0 : 0.0;
+    const double nv = sqrt(warp_sum(v0 * v0 + v1 * v1));
+    v0 /= nv;
+    v1 /= nv;
+  }
+  double p0 = 0.0, p1 = 0.0, bprev = 0.0;
+  int k = 0;
+  for (; k < g; ++k) {
+    // w = op(v): u = B v (length h), w = B^T u (length g), B = A (colside) or A^T
+    if (lane < g) vs[lane] = v0;
+    if (lane + 32 < g) vs[lane + 32] = v1;
+    __syncwarp();
+    // strides of B (h x g): colside B = A (row r, col j), else B = A^T
+    const int br = colside ? kNWLd : 1, bc = colside ? 1 : kNWLd;
+    for (int r = lane; r < h; r += 32) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // 4 independent FMA chains
+      int j = 0;
+      for (; j + 3 < g; j += 4) {
+        a0 = fma(A[r * br + j * bc], vs[j], a0);
+        a1 = fma(A[r * br + (j + 1) * bc], vs[j + 1], a1);
+        a2 = fma(A[r * br + (j + 2) * bc], vs[j + 2], a2);
+        a3 = fma(A[r * br + (j + 3) * bc], vs[j + 3], a3);
+      }
+      for (; j < g; ++j) a0 = fma(A[r * br + j * bc], vs[j], a0);
+      us[r] = (a0 + a1) + (a2 + a3);
+    }
+    __syncwarp();
+    double w0 = 0.0, w1 = 0.0, x0 = 0.0, x1 = 0.0;
+    const int c0 = lane < g ? lane : 0, c1 = lane + 32 < g ? lane + 32 : 0;
+    int i = 0;
+    for (; i + 1 < h; i += 2) {
+      const double u = us[i], u2 = us[i + 1];
+      w0 = fma(A[i * br + c0 * bc], u, w0);
+      w1 = fma(A[i * br + c1 * bc], u, w1);
+      x0 = fma(A[(i + 1) * br + c0 * bc], u2, x0);
+      x1 = fma(A[(i + 1) * br + c1 * bc], u2, x1);
+    }
+    if (i < h) {
+      w0 = fma(A[i * br + c0 * bc], us[i], w0);
+      w1 = fma(A[i * br + c1 * bc], us[i], w1);
+    }
+    w0 = lane < g ? w0 + x0 : 0.0;
+    w1 = lane + 32 < g ? w1 + x1 : 0.0;
+    const double a = warp_sum(w0 * v0 + w1 * v1);
+    w0 -= a * v0 + bprev * p0;
+    w1 -= a * v1 + bprev * p1;
+    const double b = sqrt(warp_sum(w0 * w0 + w1 * w1));
+    if (lane == 0) al[k] = a;
+    if (k + 1 == g || b <= 1e-15 * (fabs(a) + bprev)) {
+      ++k;
+      break;
+    }
+    if (lane == 0) be[k] = b;
+    p0 = v0;
+    p1 = v1;
+    v0 = w0 / b;
+    v1 = w1 / b;
+    bprev = b;
+  }
+  __syncwarp();
+  const double lam = warp_lambda_max(al, be, k);
+  if (lane == 0) *it.out = sqrt(fmax(lam, 0.0));
+}
+
+size_t norm_warp_smem() { return sizeof(double) * kNW * (kNWCap + 3 * kNWMax + kNWMaxH); }
+
+cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t st) {
+  init_attributes();
+  if (nitems == 0) return cudaSuccess;
+  const size_t sm = norm_warp_smem();
+  norm_warp_kernel<<<(nitems + kNW - 1) / kNW, 32 * kNW, sm, st>>>(items, segs, nitems);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // gather: items (src, count, dst) as int64 triples; one CTA per item (packing for download)
 // ---------------------------------------------------------------------------------------------
 
@@ -816,8 +1125,82 @@ __global__ void gather_kernel(const long long* __restrict__ items) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// asm_expand_kernel: one thread per terminal triple writes its GTerm (see AsmTables)
+// ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ MatRef mt(MatRef m) { return MatRef{m.p, m.cs, m.rs}; }
+
+__global__ void asm_expand_kernel(AsmTables T, int ntrip, GTerm* __restrict__ terms) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntrip) return;
+  const int b = T.tnode[i];
+  const int t = T.node_row[b], r = T.node_col[b];
+  const bool dense = T.node_dense[b] != 0;
+  const int s = T.ts[i], bts = T.tbx[i], bsr = T.tby[i];
+  const char k = T.tk[i];
+  GTerm g;
+  g.alpha = 1.0;
+  g.pad_ = 0;
+  g.d = MatRef{nullptr, 0, 0};
+  if (k == 'a') {  // Y|sr admissible: S_Y, (xv | row factor), (W_Y leaf | Y's basis change)^T
+    g.nf = 3;
+    g.k = T.ky_mid[s];
+    g.k2 = T.kwy_col[r];
+    g.b = T.ycoup[bsr];
+    if (dense) {
+      g.a = T.xv[bts];
+      g.d = mt(T.wyleaf[r]);
+    } else {
+      g.a = T.xadm[bts] ? T.rf[bts] : T.rproj[bts];
+      g.d = mt(T.bcc[r]);
+    }
+  } else if (k == 'b') {  // X|ts admissible
+    g.nf = 3;
+    g.k = T.kx_row[t];
+    g.k2 = T.kwx_mid[s];
+    g.b = T.xcoup[bts];
+    if (dense) {
+      g.a = T.vxleaf[t];
+      g.d = mt(T.wyl[bsr]);
+    } else {
+      g.a = T.bcr[t];
+      g.d = mt(T.cproj[bsr]);
+    }
+  } else {  // both dense
+    g.nf = 2;
+    g.a = T.xnear[bts];
+    g.b = T.ynear[bsr];
+    g.k = T.size_mid[s];
+    g.k2 = 0;
+  }
+  terms[i] = g;
+}
+
+// ---------------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------------
+
+// Opt every kernel into the full 227 KB of dynamic shared memory once.  (Setting the attribute per
+// launch races when two host threads launch the same kernel with different sizes.)
+static void init_attributes() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto opt_in = [](const void* fn) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, fn);  // dynamic limit = 227 KB minus the kernel's static shared memory
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
+      // prefer the largest shared-memory carveout so several CTAs fit per SM
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    };
+    opt_in((const void*)gsum_kernel);
+    opt_in((const void*)qr_r_kernel);
+    opt_in((const void*)svd_tsqr_kernel);
+    opt_in((const void*)svd_merge_kernel);
+    opt_in((const void*)svd_finish_kernel);
+    opt_in((const void*)norm_kernel);
+    opt_in((const void*)norm_warp_kernel);
+  });
+}
 
 size_t gsum_smem(int k2max) {
   return sizeof(double) * (2 * kKc * kLdS + (k2max > 0 ? (size_t)kTile * (k2max + 1) : 0));
@@ -825,9 +1208,9 @@ size_t gsum_smem(int k2max) {
 
 cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
                         cudaStream_t st) {
+  init_attributes();
   if (ntiles == 0) return cudaSuccess;
   const size_t sm = gsum_smem(k2max);
-  cudaFuncSetAttribute(gsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   gsum_kernel<<<ntiles, kThreads, sm, st>>>(outs, terms, tiles, k2max);
   return cudaGetLastError();
 }
@@ -837,9 +1220,9 @@ size_t qr_smem(int n, bool ws) {
 }
 
 cudaError_t launch_qr(const QrItem* items, const Seg* segs, int nitems, int nmax, bool ws, cudaStream_t st) {
+  init_attributes();
   if (nitems == 0) return cudaSuccess;
   const size_t sm = qr_smem(nmax, ws);
-  cudaFuncSetAttribute(qr_r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   qr_r_kernel<<<nitems, kThreads, sm, st>>>(items, segs);
   return cudaGetLastError();
 }
@@ -864,23 +1247,23 @@ size_t svd_finish_smem(int m, int kx, bool rsmem) {
 
 cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork* work, int nwork, size_t smem,
                             bool rsmem, cudaStream_t st) {
+  init_attributes();
   if (nwork == 0) return cudaSuccess;
-  cudaFuncSetAttribute(svd_tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   svd_tsqr_kernel<<<nwork, kThreads, smem, st>>>(items, segs, work, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_svd_merge(const SvdItem* items, const SvdWork* work, int nwork, size_t smem, bool rsmem,
                              cudaStream_t st) {
+  init_attributes();
   if (nwork == 0) return cudaSuccess;
-  cudaFuncSetAttribute(svd_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   svd_merge_kernel<<<nwork, kThreads, smem, st>>>(items, work, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, cudaStream_t st) {
+  init_attributes();
   if (nitems == 0) return cudaSuccess;
-  cudaFuncSetAttribute(svd_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   svd_finish_kernel<<<nitems, kFinishThreads, smem, st>>>(items, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
@@ -893,13 +1276,21 @@ size_t norm_smem(int m, long long N) {
 }
 
 cudaError_t launch_norm(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
+  init_attributes();
   if (nitems == 0) return cudaSuccess;
-  cudaFuncSetAttribute(norm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   norm_kernel<<<nitems, kThreads, smem, st>>>(items, segs);
   return cudaGetLastError();
 }
 
+cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t st) {
+  init_attributes();
+  if (ntrip == 0) return cudaSuccess;
+  asm_expand_kernel<<<(ntrip + 255) / 256, 256, 0, st>>>(T, ntrip, terms);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t st) {
+  init_attributes();
   if (nitems == 0) return cudaSuccess;
   gather_kernel<<<nitems, kThreads, 0, st>>>(items);
   return cudaGetLastError();

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <functional>
+#include <thread>
 
 #include "engine.h"
 
@@ -309,39 +310,105 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
     g.run(C);
   }
-  // all terminal triples (induced.py:286-307), one output per product block
+  // all terminal triples (induced.py:286-307), one output per product block; the terms are
+  // expanded on the GPU from the triple list and per-block operand tables (asm_expand_kernel)
   {
     HostTimer ht2(C, "assemble_triples");
+    const int ntrip = (int)pt.ts.size();
+    const Blocks& BX = *x.h->bt;
+    const Blocks& BY = *y.h->bt;
+    const Tree& mid = x.cols();
+    std::vector<int> tnode(ntrip);
+    for (int b = 0; b < B.nb; ++b)
+      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) tnode[i] = b;
+    std::vector<unsigned char> ndense(B.nb), xadm(BX.nb);
+    for (int b = 0; b < B.nb; ++b) ndense[b] = B.near_leaf(b) ? 1 : 0;
+    const MatRef z{nullptr, 0, 0};
+    std::vector<MatRef> xcoup(BX.nb, z), xnear(BX.nb, z), rfr(BX.nb, z), rproj(BX.nb, z), xvr(BX.nb, z);
+    for (int b = 0; b < BX.nb; ++b) {
+      xadm[b] = BX.adm_leaf(b) ? 1 : 0;
+      if (BX.adm_leaf(b)) xcoup[b] = x.coup(b);
+      if (BX.near_leaf(b)) xnear[b] = x.near(b);
+      rfr[b] = rf[b].ref();
+      if (b < (int)qr.proj.size()) rproj[b] = qr.proj[b].ref();
+      if (b < (int)qr.xv.size()) xvr[b] = qr.xv[b].ref();
+    }
+    std::vector<MatRef> ycoup(BY.nb, z), ynear(BY.nb, z), cproj(BY.nb, z), wyl(BY.nb, z);
+    for (int b = 0; b < BY.nb; ++b) {
+      if (BY.adm_leaf(b)) ycoup[b] = y.coup(b);
+      if (BY.near_leaf(b)) ynear[b] = y.near(b);
+      if (b < (int)qc.proj.size()) cproj[b] = qc.proj[b].ref();
+      if (b < (int)qc.xv.size()) wyl[b] = qc.xv[b].ref();
+    }
+    std::vector<MatRef> vxleaf(rows.n, z), bcr(rows.n, z), wyleaf(cols.n, z), bcc(cols.n, z);
+    for (int t = 0; t < rows.n; ++t) {
+      if (rows.leaf(t)) vxleaf[t] = x.rb().leafm(t).ref();
+      bcr[t] = qr.bc[t].ref();
+    }
+    for (int r = 0; r < cols.n; ++r) {
+      if (cols.leaf(r)) wyleaf[r] = y.cb().leafm(r).ref();
+      bcc[r] = qc.bc[r].ref();
+    }
+    std::vector<int> size_mid(mid.n);
+    for (int s = 0; s < mid.n; ++s) size_mid[s] = mid.size(s);
+    AsmTables T;
+    T.tnode = C.push(tnode);
+    T.ts = C.push(pt.ts);
+    T.tk = C.push(pt.tk);
+    T.tbx = C.push(pt.tbx);
+    T.tby = C.push(pt.tby);
+    T.node_row = C.push(B.row);
+    T.node_col = C.push(B.col);
+    T.node_dense = C.push(ndense);
+    T.xcoup = C.push(xcoup);
+    T.xnear = C.push(xnear);
+    T.xadm = C.push(xadm);
+    T.rf = C.push(rfr);
+    T.rproj = C.push(rproj);
+    T.xv = C.push(xvr);
+    T.ycoup = C.push(ycoup);
+    T.ynear = C.push(ynear);
+    T.cproj = C.push(cproj);
+    T.wyl = C.push(wyl);
+    T.vxleaf = C.push(vxleaf);
+    T.bcr = C.push(bcr);
+    T.wyleaf = C.push(wyleaf);
+    T.bcc = C.push(bcc);
+    T.kx_row = C.push(x.rb().rank);
+    T.kwx_mid = C.push(x.cb().rank);
+    T.ky_mid = C.push(y.rb().rank);
+    T.kwy_col = C.push(y.cb().rank);
+    T.size_mid = C.push(size_mid);
+    GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
+    cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
+    ++C.launches;
     GBatch g;
+    int k2max = 0;
+    for (int k : y.cb().rank) k2max = std::max(k2max, k);
+    for (int k : x.cb().rank) k2max = std::max(k2max, k);
+    if (k2max > 256) throw StructureErr("gsum: 3-factor middle dimension above 256");
+    g.k2max = k2max;
+    double fl = 0.0;
     for (int b = 0; b < B.nb; ++b) {
       const int t = B.row[b], r = B.col[b];
       const bool dense = B.near_leaf(b);
       const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
-      g.out(tgt, false);
-      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
-        const int s = pt.ts[i];
-        const int bts = pt.tbx[i], bsr = pt.tby[i];
-        const char k = pt.tk[i];
-        if (k == 'a') {
-          const MatRef SY = y.coup(bsr);
-          const int ks = y.rb().rank[s], kr = y.cb().rank[r];
-          if (dense) {
-            g.t3(qr.xv[bts].ref(), SY, y.cb().leafm(r).tref(), ks, kr);
+      g.outs.push_back(GOut{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]});
+      if (C.prof)
+        for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+          const int s = pt.ts[i];
+          const double m = tgt.r, n = tgt.c;
+          if (pt.tk[i] == 'c') fl += 2 * m * n * mid.size(s);
+          else if (pt.tk[i] == 'a') {
+            const double k = y.rb().rank[s], k2 = y.cb().rank[r];
+            fl += 2 * m * k * k2 + 2 * m * k2 * n;
           } else {
-            const Mat A = bx.b->adm_leaf(bts) ? rf[bts] : qr.proj[bts];
-            g.t3(A.ref(), SY, qc.bc[r].tref(), ks, kr);
+            const double k = x.rb().rank[t], k2 = x.cb().rank[s];
+            fl += 2 * m * k * k2 + 2 * m * k2 * n;
           }
-        } else if (k == 'b') {
-          const MatRef SX = x.coup(bts);
-          const int kt = x.rb().rank[t], ks = x.cb().rank[s];
-          if (dense) g.t3(x.rb().leafm(t).ref(), SX, qc.xv[bsr].tref(), kt, ks);
-          else g.t3(qr.bc[t].ref(), SX, qc.proj[bsr].tref(), kt, ks);
-        } else {
-          g.t2(x.near(bts), y.near(bsr), x.cols().size(s));
         }
-      }
     }
-    g.run(C);
+    g.run_device_terms(C, d_terms, fl);
   }
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
   HostTimer ht3(C, "assemble_pushdown");
@@ -403,10 +470,35 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   MatStore rwx = basis_weights(C, sc, *x.rb);
   MatStore zxt = total_weights(C, sc, XT, rwx, scaling);
   record(C, e1);
-  Induced qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+  // the row and column bases are independent until the assembly: run them concurrently, the
+  // column pass on a side stream driven by a second host thread
+  auto keep2 = std::make_shared<Arena>(C.st);
+  Induced qr, qc;
+  {
+    Ctx& S = C.side();
+    keep2->st = S.st;
+    keep2->cross_stream = true;
+    std::exception_ptr err;
+    std::thread th([&] {
+      try {
+        qc = induced_rows(S, *keep2, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+        S.sync();
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (err) std::rethrow_exception(err);
+    C.join_side(S);
+  }
   record(C, e2);
-  Induced qc = induced_rows(C, *keep, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
-  record(C, e3);
+  e3 = e2;
   PTree pt;
   {
     HostTimer ht(C, "product_tree");
@@ -415,6 +507,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
   record(C, e4);
   G->owned.push_back(keep);
+  G->owned.push_back(keep2);
   G->own_rows = x.own_rows;
   G->own_cols = y.own_cols;
   if (C.timing) {

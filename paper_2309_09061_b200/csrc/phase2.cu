@@ -4,6 +4,7 @@
 #include <cmath>
 #include <functional>
 #include <map>
+#include <thread>
 
 #include "engine.h"
 
@@ -630,11 +631,36 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     nn = all_norms(C, sc, g, false);
   }
   auto ar = std::make_shared<Arena>(C.st);
-  CState rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, nn);
+  // row and column coarse bases are independent until the final projection: concurrent passes
+  auto ar2 = std::make_shared<Arena>(C.st);
+  CState rs, cs;
+  {
+    Ctx& S = C.side();
+    ar2->st = S.st;
+    ar2->cross_stream = true;
+    std::exception_ptr err;
+    std::thread th([&] {
+      try {
+        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, nn);
+        S.sync();
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, nn);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (err) std::rethrow_exception(err);
+    C.join_side(S);
+  }
   if (C.timing) { e1 = C.event(); cudaEventRecord(e1, C.st); }
-  CState cs = coarse_rows(C, *ar, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, nn);
-  if (C.timing) { e2 = C.event(); cudaEventRecord(e2, C.st); }
+  e2 = e1;
   auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar);
+  Z->owned.push_back(ar2);
   Z->own_rows = g.own_rows;
   Z->own_cols = g.own_cols;
   if (C.timing) {
