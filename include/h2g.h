@@ -50,6 +50,9 @@ int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset);
    (0 gsum, 1 qr_r, 2 svd, 3 norm, 4 gather); out20 = per class {launches, ms, algorithmic flops, bytes} */
 int h2g_ctx_set_profile(h2g_ctx* ctx, int on);
 int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* out20, int reset);
+/* timeline: trace_begin turns on per-launch events; trace_dump writes a chrome://tracing JSON */
+int h2g_ctx_trace_begin(h2g_ctx* ctx);
+int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path);
 
 /* cluster tree (reference ClusterTree, trees.py:34-97): n nodes in preorder */
 int h2g_tree_create(h2g_ctx* ctx, int n, const long long* start, const long long* stop,

@@ -104,6 +104,44 @@ int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset) {
   return (int)out.size();
 }
 
+int h2g_ctx_trace_begin(h2g_ctx* ctx) {
+  return guarded([&] {
+    Ctx& C = ctx->c;
+    C.sync();
+    C.prof = true;
+    C.trace = true;
+    C.trace_recs.clear();
+    C.trace_out = &C.trace_recs;
+    if (!C.trace_base) cuda_check(cudaEventCreate(&C.trace_base), "event");
+    cudaEventRecord(C.trace_base, C.st);
+    cudaEventSynchronize(C.trace_base);
+    C.trace_host0 = std::chrono::steady_clock::now();
+  });
+}
+
+int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path) {
+  return guarded([&] {
+    Ctx& C = ctx->c;
+    C.sync();
+    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather"};
+    FILE* f = fopen(path, "w");
+    if (!f) throw InvalidInput("cannot open trace file");
+    fprintf(f, "{\"traceEvents\":[\n");
+    bool first = true;
+    for (auto& r : C.trace_recs) {
+      const bool host = r.cls < 0;
+      fprintf(f, "%s{\"name\":\"%s\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%d,\"tid\":%d}",
+              first ? "" : ",\n", host ? "host_sync_wait" : names[r.cls], r.t0_us, r.dur_us, host ? 1 : 0, r.tid);
+      first = false;
+    }
+    fprintf(f, "\n]}\n");
+    fclose(f);
+    C.trace = false;
+    C.prof = false;
+    C.trace_out = nullptr;
+  });
+}
+
 int h2g_ctx_synchronize(h2g_ctx* ctx) {
   return guarded([&] { ctx->c.sync(); });
 }

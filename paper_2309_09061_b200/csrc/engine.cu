@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 
 #include "engine.h"
@@ -85,7 +87,14 @@ void Ctx::ensure_read(size_t bytes) {
 
 void Ctx::sync() {
   HostTimer ht(*this, "sync_wait");
+  const auto h0 = std::chrono::steady_clock::now();
   cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  if (trace && trace_out) {
+    const auto h1 = std::chrono::steady_clock::now();
+    trace_out->push_back(TraceRec{-1 - trace_tid, trace_tid,
+                                  std::chrono::duration<double, std::micro>(h0 - trace_host0).count(),
+                                  std::chrono::duration<double, std::micro>(h1 - h0).count()});
+  }
   stage_off = 0;
   ++syncs;
   if (!pending.empty()) drain_prof();
@@ -121,6 +130,11 @@ void Ctx::drain_prof() {
   for (auto& p : pending) {
     float ms = 0;
     cudaEventElapsedTime(&ms, p.a, p.b);
+    if (trace && trace_out && trace_base) {
+      float t0 = 0;
+      cudaEventElapsedTime(&t0, trace_base, p.a);
+      trace_out->push_back(TraceRec{p.cls, trace_tid, 1e3 * t0, 1e3 * ms});
+    }
     KStat& k = kstat[p.cls];
     k.launches += 1;
     k.ms += ms;
@@ -157,6 +171,11 @@ Ctx& Ctx::side() {
   if (!side_) side_.reset(new Ctx(device, nullptr));
   side_->timing = timing;
   side_->prof = prof;
+  side_->trace = trace;
+  side_->trace_tid = 1;
+  side_->trace_base = trace_base;
+  side_->trace_host0 = trace_host0;
+  side_->trace_out = trace_out;
   // the side stream starts after everything queued so far on the main stream
   cudaEvent_t e;
   cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -277,41 +296,60 @@ void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
 
 static constexpr size_t kSmemLimit = 227 * 1024 - 1024;  // minus the kernels' static shared memory
 
+// Pairwise tree of partial-R merges; `parts` = (rbuf, n, nchunk) per item.
+static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>& parts, bool rsmem, size_t smem) {
+  int maxchunk = 1;
+  for (auto& p : parts) maxchunk = std::max(maxchunk, std::get<2>(p));
+  for (int stride = 1; stride < maxchunk; stride *= 2) {
+    std::vector<MergeWork> lvl;
+    for (auto& p : parts) {
+      if (std::get<1>(p) == 0) continue;
+      for (int a = 0; a + stride < std::get<2>(p); a += 2 * stride)
+        lvl.push_back(MergeWork{std::get<0>(p), std::get<1>(p), a, a + stride, 0});
+    }
+    if (lvl.empty()) continue;
+    cuda_check(launch_tsqr_merge(C.push(lvl), (int)lvl.size(), smem, rsmem, C.st), "tsqr_merge");
+    ++C.launches;
+  }
+}
+
 void QrBatch::run(Ctx& C, Arena& scratch) {
-  std::vector<QrItem> small, big;
-  int nsmall = 0, nbig = 0;
+  static constexpr long long kChunkRows = 256;  // rows per chunk CTA (8 panels of 32)
+  std::vector<QrItem> live;
+  bool rsmem = true;
   for (auto& it : items) {
     if (it.n == 0 || it.M == 0) continue;
-    if (qr_smem(it.n, false) <= kSmemLimit) {
-      small.push_back(it);
-      nsmall = std::max(nsmall, it.n);
-    } else {
-      it.ws = scratch.alloc((size_t)it.n * it.n);
-      big.push_back(it);
-      nbig = std::max(nbig, it.n);
-    }
+    it.nchunk = (int)std::max<long long>(1, (it.M + kChunkRows - 1) / kChunkRows);
+    it.rbuf = scratch.alloc((size_t)it.nchunk * it.n * it.n);
+    if (qr_smem(it.n, true) > kSmemLimit || merge_smem(it.n, true) > kSmemLimit) rsmem = false;
+    live.push_back(it);
   }
-  if (small.empty() && big.empty()) { items.clear(); sl.segs.clear(); return; }
-  Seg* d_s = C.push(sl.segs);
+  if (live.empty()) { items.clear(); sl.segs.clear(); return; }
+  size_t sm_chunk = 0, sm_merge = 0;
+  std::vector<SvdWork> work;
+  std::vector<std::tuple<double*, int, int>> parts;
+  for (size_t i = 0; i < live.size(); ++i) {
+    sm_chunk = std::max(sm_chunk, qr_smem(live[i].n, rsmem));
+    sm_merge = std::max(sm_merge, merge_smem(live[i].n, rsmem));
+    for (int c = 0; c < live[i].nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
+    parts.emplace_back(live[i].rbuf, live[i].n, live[i].nchunk);
+  }
   double fl = 0, by = 0;
   if (C.prof)
-    for (auto* v : {&small, &big})
-      for (auto& it : *v) {  // Householder R-only: 2 M n^2 - 2/3 n^3 (M >= n)
-        const double M = (double)it.M, n = it.n;
-        fl += M >= n ? 2 * M * n * n - 2.0 / 3 * n * n * n : 2 * n * M * M - 2.0 / 3 * M * M * M;
-        by += 8 * (M * n + std::min(M, n) * n);
-      }
-  QrItem* d_small = C.push(small);
-  QrItem* d_big = C.push(big);
+    for (auto& it : live) {  // Householder R-only: 2 M n^2 - 2/3 n^3 (M >= n)
+      const double M = (double)it.M, n = it.n;
+      fl += M >= n ? 2 * M * n * n - 2.0 / 3 * n * n * n : 2 * n * M * M - 2.0 / 3 * M * M * M;
+      by += 8 * (M * n + std::min(M, n) * n);
+    }
+  Seg* d_s = C.push(sl.segs);
+  QrItem* d_items = C.push(live);
+  SvdWork* d_work = C.push(work);
   cudaEvent_t ev = C.prof_begin();
-  if (!small.empty()) {
-    cuda_check(launch_qr(d_small, d_s, (int)small.size(), nsmall, false, C.st), "qr_r");
-    ++C.launches;
-  }
-  if (!big.empty()) {
-    cuda_check(launch_qr(d_big, d_s, (int)big.size(), nbig, true, C.st), "qr_r ws");
-    ++C.launches;
-  }
+  cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
+  ++C.launches;
+  run_merges(C, parts, rsmem, sm_merge);
+  cuda_check(launch_qr_out(d_items, (int)live.size(), C.st), "qr_out");
+  ++C.launches;
   C.prof_end(K_QR, ev, fl, by);
   items.clear();
   sl.segs.clear();
@@ -386,38 +424,34 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     it.nchunk = (int)std::max<long long>(1, (it.N + kChunkCols - 1) / kChunkCols);
     it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
     it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
-    if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || svd_merge_smem(n, true) > kSmemLimit ||
+    if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || merge_smem(n, true) > kSmemLimit ||
         svd_finish_smem(it.m, it.kx, true) > kSmemLimit)
       rsmem = false;
     live.push_back(it);
   }
   if (live.empty()) return ranks;
   std::vector<SvdWork> work;
-  std::vector<std::vector<SvdWork>> merges;
-  int maxchunk = 1;
+  std::vector<std::tuple<double*, int, int>> parts;
   for (size_t i = 0; i < live.size(); ++i) {
     const SvdItem& it = live[i];
     const int n = it.m - std::min(it.m, it.kx);
     sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
-    sm_merge = std::max(sm_merge, svd_merge_smem(n, rsmem));
+    sm_merge = std::max(sm_merge, merge_smem(n, rsmem));
     sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, rsmem));
     if (sm_tsqr > kSmemLimit || sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
     for (int c = 0; c < it.nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
-    maxchunk = std::max(maxchunk, it.nchunk);
+    if (n > 0) parts.emplace_back(it.rbuf, n, it.nchunk);
   }
-  for (int stride = 1; stride < maxchunk; stride *= 2) {  // pairwise tree of R merges
-    std::vector<SvdWork> lvl;
-    for (size_t i = 0; i < live.size(); ++i) {
-      if (live[i].m - std::min(live[i].m, live[i].kx) == 0) continue;
-      for (int a = 0; a + stride < live[i].nchunk; a += 2 * stride) lvl.push_back(SvdWork{(int)i, a, a + stride, 0});
-    }
-    merges.push_back(std::move(lvl));
+  static const bool dbg_sweeps = getenv("H2G_DEBUG_SWEEPS") != nullptr;
+  int* d_sw = nullptr;
+  if (dbg_sweeps) {
+    d_sw = (int*)scratch.alloc_bytes(live.size() * sizeof(int));
+    cuda_check(cudaMemsetAsync(d_sw, 0, live.size() * sizeof(int), C.st), "memset");
+    for (size_t i = 0; i < live.size(); ++i) live[i].sweeps_out = d_sw + i;
   }
   Seg* d_s = C.push(sl.segs);
   SvdItem* d_items = C.push(live);
   SvdWork* d_work = C.push(work);
-  std::vector<SvdWork*> d_merge;
-  for (auto& l : merges) d_merge.push_back(C.push(l));
   double fl = 0, by = 0;
   if (C.prof)
     for (auto& it : live) {  // reference ops: full QR of V, Q^T A, gesdd of the remainder
@@ -430,15 +464,22 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   cudaEvent_t ev = C.prof_begin();
   cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
   ++C.launches;
-  for (size_t l = 0; l < merges.size(); ++l) {
-    if (merges[l].empty()) continue;
-    cuda_check(launch_svd_merge(d_items, d_merge[l], (int)merges[l].size(), sm_merge, rsmem, C.st), "svd_merge");
-    ++C.launches;
-  }
+  run_merges(C, parts, rsmem, sm_merge);
   cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, rsmem, C.st), "svd_finish");
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());
+  if (dbg_sweeps) {
+    std::vector<int> sw = C.read(d_sw, live.size());
+    int mx = 0, mxn = 0;
+    double mean = 0;
+    for (size_t i = 0; i < sw.size(); ++i) {
+      mx = std::max(mx, sw[i]);
+      mean += sw[i];
+      mxn = std::max(mxn, live[i].m - std::min(live[i].m, live[i].kx));
+    }
+    fprintf(stderr, "svd batch: %zu items, n<=%d, sweeps max %d mean %.1f\n", sw.size(), mxn, mx, mean / sw.size());
+  }
   items.clear();
   sl.segs.clear();
   return ranks;

@@ -23,18 +23,20 @@ void cuda_check(cudaError_t e, const char* what);
 
 // ------------------------------------------------------------------ kernels (kernels.cu)
 cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
-cudaError_t launch_qr(const QrItem*, const Seg*, int nitems, int nmax, bool ws, cudaStream_t);
+cudaError_t launch_qr_chunks(const QrItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
+                             cudaStream_t);
+cudaError_t launch_tsqr_merge(const MergeWork*, int nwork, size_t smem, bool rsmem, cudaStream_t);
+cudaError_t launch_qr_out(const QrItem*, int nitems, cudaStream_t);
 cudaError_t launch_svd_tsqr(const SvdItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
                             cudaStream_t);
-cudaError_t launch_svd_merge(const SvdItem*, const SvdWork*, int nwork, size_t smem, bool rsmem, cudaStream_t);
 cudaError_t launch_svd_finish(const SvdItem*, int nitems, size_t smem, bool rsmem, cudaStream_t);
 cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
 cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t);
-size_t qr_smem(int n, bool ws);
+size_t qr_smem(int n, bool rsmem);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
-size_t svd_merge_smem(int n, bool rsmem);
+size_t merge_smem(int n, bool rsmem);
 size_t svd_finish_smem(int m, int kx, bool rsmem);
 size_t norm_smem(int m, long long N);
 size_t gsum_smem(int k2max);
@@ -189,6 +191,17 @@ struct Ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> free_ev;
   std::map<std::string, double> htime;  // host-side ms per named section (timing mode)
+  // timeline tracing (profile mode + trace): device intervals per launch, host sync waits
+  struct TraceRec {
+    int cls, tid;
+    double t0_us, dur_us;
+  };
+  bool trace = false;
+  int trace_tid = 0;
+  cudaEvent_t trace_base = nullptr;
+  std::chrono::steady_clock::time_point trace_host0;
+  std::vector<TraceRec>* trace_out = nullptr;  // shared with the side context
+  std::vector<TraceRec> trace_recs;
   cudaEvent_t prof_begin();
   void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
   void drain_prof();

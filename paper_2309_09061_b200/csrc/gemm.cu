@@ -1,0 +1,201 @@
+// Grouped FP64 chain-GEMM on the tensor pipe (DMMA, mma.sync m8n8k4 f64) for sm_100a.
+//
+// Same contract as kernels.cu's gsum_kernel (GOut / GTerm / GTile): one CTA per 64x64 output
+// tile, 4 warps each owning a 32x32 quadrant (4x4 DMMA tiles, 32 accumulators per lane).  The k
+// dimension streams through shared memory in 16-wide chunks with a register prefetch of the next
+// chunk, so global loads overlap the tensor work.  3-factor terms first form T = A*B (64 x k2) in
+// shared memory, then T*D.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "h2g_types.h"
+
+namespace h2g {
+
+namespace {
+
+constexpr int kT = 64;            // output tile
+constexpr int kKC = 16;           // k chunk
+constexpr int kLdA = kKC + 4;     // As[64][20]
+constexpr int kLdB = kT + 8;      // Bs[16][72]
+constexpr int kThr = 128;         // 4 warps
+constexpr int kPerA = kT * kKC / kThr;  // 8 elements per thread per chunk
+constexpr int kPerB = kKC * kT / kThr;  // 8
+
+__device__ __forceinline__ double ld(const MatRef& a, long long i, long long j) {
+  return a.p[i * a.rs + j * a.cs];
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct Acc {
+  double v[4][4][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[r][c][0] = v[r][c][1] = 0.0;
+  }
+};
+
+// chunk loads: A rows i0..i0+63 (only < mt valid), k cols kk..kk+15 (only < kc); B likewise
+__device__ __forceinline__ void fetch_chunk(double (&ra)[kPerA], double (&rb)[kPerB], const MatRef& A, int ai0,
+                                            int mt, const MatRef& B, int bj0, int nt, int kk, int kc, double alpha) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < kPerA; ++q) {
+    const int e = tid + q * kThr;
+    const int i = e / kKC, l = e % kKC;
+    ra[q] = (i < mt && l < kc) ? alpha * ld(A, ai0 + i, kk + l) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kPerB; ++q) {
+    const int e = tid + q * kThr;
+    const int l = e / kT, j = e % kT;
+    rb[q] = (j < nt && l < kc) ? ld(B, kk + l, bj0 + j) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void store_chunk(const double (&ra)[kPerA], const double (&rb)[kPerB], double* As,
+                                            double* Bs) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < kPerA; ++q) {
+    const int e = tid + q * kThr;
+    As[(e / kKC) * kLdA + e % kKC] = ra[q];
+  }
+#pragma unroll
+  for (int q = 0; q < kPerB; ++q) {
+    const int e = tid + q * kThr;
+    Bs[(e / kT) * kLdB + e % kT] = rb[q];
+  }
+}
+
+__device__ __forceinline__ void mma_chunk(Acc& acc, const double* As, const double* Bs, int kc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  for (int kk = 0; kk < kc; kk += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r] = As[(wr + r * 8 + g) * kLdA + kk + t4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) b[c] = Bs[(kk + t4) * kLdB + wc + c * 8 + g];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dmma(acc.v[r][c], a[r], b[c]);
+  }
+}
+
+// acc += alpha * A[ai0:ai0+mt, 0:k] * B[0:k, bj0:bj0+nt]
+__device__ void tile_gemm(Acc& acc, const MatRef& A, int ai0, int mt, const MatRef& B, int bj0, int nt, int k,
+                          double alpha, double* As, double* Bs) {
+  double ra[kPerA], rb[kPerB];
+  if (k <= 0) return;
+  fetch_chunk(ra, rb, A, ai0, mt, B, bj0, nt, 0, min(kKC, k), alpha);
+  for (int kk = 0; kk < k; kk += kKC) {
+    const int kc = min(kKC, k - kk);
+    __syncthreads();  // previous chunk's readers are done
+    store_chunk(ra, rb, As, Bs);
+    __syncthreads();
+    if (kk + kKC < k) fetch_chunk(ra, rb, A, ai0, mt, B, bj0, nt, kk + kKC, min(kKC, k - kk - kKC), alpha);
+    mma_chunk(acc, As, Bs, (kc + 3) & ~3);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThr) gsum_mma_kernel(const GOut* __restrict__ outs,
+                                                         const GTerm* __restrict__ terms,
+                                                         const GTile* __restrict__ tiles, int k2max) {
+  extern __shared__ double smem[];
+  double* As = smem;                 // 64 x kLdA
+  double* Bs = As + kT * kLdA;       // 16 x kLdB
+  double* Ts = Bs + kKC * kLdB;      // 64 x ldT
+  const int ldT = k2max + 4;
+  const GTile tl = tiles[blockIdx.x];
+  const GOut o = outs[tl.out];
+  const int i0 = (tl.tij & 0xffff) * kT, j0 = (tl.tij >> 16) * kT;
+  const int mt = min(kT, o.m - i0), nt = min(kT, o.n - j0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  Acc acc;
+  acc.zero();
+  for (int ti = o.t0; ti < o.t1; ++ti) {
+    const GTerm t = terms[ti];
+    if (t.nf == 1) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+            if (i < mt && j < nt) acc.v[r][c][h] += t.alpha * ld(t.a, i0 + i, j0 + j);
+          }
+    } else if (t.nf == 2) {
+      tile_gemm(acc, t.a, i0, mt, t.b, j0, nt, t.k, t.alpha, As, Bs);
+    } else {
+      // T = alpha * A[i0:i0+mt, :] * B (mt x k2) into shared memory, 64 columns at a time
+      for (int js = 0; js < t.k2; js += kT) {
+        Acc ta;
+        ta.zero();
+        const int ns = min(kT, t.k2 - js);
+        tile_gemm(ta, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+              if (j < ns) Ts[i * ldT + js + j] = ta.v[r][c][h];
+            }
+      }
+      __syncthreads();
+      const MatRef T{Ts, ldT, 1};
+      tile_gemm(acc, T, 0, mt, t.d, j0, nt, t.k2, 1.0, As, Bs);
+      __syncthreads();  // Ts is rewritten by the next 3-factor term
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+        if (i < mt && j < nt) {
+          double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+          *dst = (o.beta ? *dst : 0.0) + acc.v[r][c][h];
+        }
+      }
+}
+
+size_t gsum_mma_smem(int k2max) {
+  return sizeof(double) * ((size_t)kT * kLdA + (size_t)kKC * kLdB + (k2max > 0 ? (size_t)kT * (k2max + 4) : 0));
+}
+
+cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
+                            cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)gsum_mma_kernel);
+    cudaFuncSetAttribute((const void*)gsum_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - (int)fa.sharedSizeBytes);
+    cudaFuncSetAttribute((const void*)gsum_mma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  });
+  if (ntiles == 0) return cudaSuccess;
+  gsum_mma_kernel<<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
+  return cudaGetLastError();
+}
+
+}  // namespace h2g

@@ -48,10 +48,16 @@ struct Seg {
 
 // R-only QR of vstack(segs[s0:s1]) (M x n); writes min(M, n) x n rows (ld n) to out.
 struct QrItem {
-  int s0, s1, n, pad_;
+  int s0, s1, n, nchunk;  // nchunk row chunks (>= 1), each reduced by its own CTA
   long long M;
   double* out;
-  double* ws;  // optional global workspace (n x n) when R does not fit shared memory
+  double* rbuf;  // nchunk x (n x n) partial R factors
+};
+
+// Tree merge of two partial R factors: rbuf[a] <- R([rbuf[a]; rbuf[b]]) (n x n each).
+struct MergeWork {
+  double* rbuf;
+  int n, a, b, pad_;
 };
 
 // Truncated SVD of hstack(segs[s0:s1]) (m x N), optionally protecting range(V) (m x kx)
@@ -74,6 +80,8 @@ struct SvdItem {
   double* sig_out;  // optional: sorted singular values of B (capacity m)
   double* rbuf;     // nchunk x (n x n) partial R factors, n = m - min(m, kx)
   double* vws;      // m x kx Householder vectors of V + kx coefficients
+  int* sweeps_out;  // optional diagnostic: Jacobi sweeps used
+  int pad2_;
 };
 
 // Work units of the SVD pipeline: stage-1 chunk (item, chunk) and tree merges R_a <- [R_a; R_b].

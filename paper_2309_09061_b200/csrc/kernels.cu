@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "h2g_types.h"
@@ -357,36 +358,78 @@ __device__ __forceinline__ void store_hcols(const PanelFetch& f, double* dst, in
 }
 
 // ---------------------------------------------------------------------------------------------
-// qr_r: R factor of vstack(segs) (reference dense.py:145-150 / numpy qr mode="r").
+// qr_r: R factor of vstack(segs) (reference dense.py:145-150 / numpy qr mode="r"), as a chunked
+// TSQR: qr_chunk_kernel reduces 256-row chunks (one CTA each) to partial R factors,
+// tsqr_merge_kernel combines them pairwise, qr_out_kernel writes the first min(M, n) rows.
 // ---------------------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(kThreads, 3) qr_r_kernel(const QrItem* __restrict__ items,
-                                                        const Seg* __restrict__ segs) {
+__global__ void __launch_bounds__(kThreads, 3) qr_chunk_kernel(const QrItem* __restrict__ items,
+                                                             const Seg* __restrict__ segs,
+                                                             const SvdWork* __restrict__ work, int rsmem) {
   extern __shared__ double smem[];
-  const QrItem it = items[blockIdx.x];
+  const SvdWork w = work[blockIdx.x];
+  const QrItem it = items[w.item];
   const int n = it.n;
-  const int ldp = n | 1;               // odd row stride: lanes walk P's rows without bank conflicts
+  const int ldp = n | 1;               // odd row stride: conflict-free column access
   double* P = smem;                    // 32 x ldp
   double* vb = P + kPanel * ldp;       // 64
   double* tb = vb + 64;                // 2 (+pad)
-  double* R = it.ws ? it.ws : tb + 4;  // n x n
+  double* R = rsmem ? tb + 4 : it.rbuf + (long long)w.a * n * n;
   const long long nn = (long long)n * n;
   for (long long e = threadIdx.x; e < nn; e += blockDim.x) R[e] = 0.0;
   __syncthreads();
+  const long long per = (it.M + it.nchunk - 1) / it.nchunk;
+  const long long rbeg = w.a * per, rend = min(it.M, rbeg + per);
   const bool pre = kPanel * n <= kFetch * (int)blockDim.x;
   PanelFetch f;
-  if (pre) fetch_vrows(f, segs, it.s0, it.s1, n, it.M, 0);
-  for (long long r0 = 0; r0 < it.M; r0 += kPanel) {
+  if (pre && rbeg < rend) fetch_vrows(f, segs, it.s0, it.s1, n, rend, rbeg);
+  for (long long r0 = rbeg; r0 < rend; r0 += kPanel) {
     if (pre) store_vrows(f, P, ldp, n);
-    else load_vpanel(segs, it.s0, it.s1, n, it.M, r0, P, ldp);
+    else load_vpanel(segs, it.s0, it.s1, n, rend, r0, P, ldp);
     __syncthreads();
-    if (pre && r0 + kPanel < it.M) fetch_vrows(f, segs, it.s0, it.s1, n, it.M, r0 + kPanel);
+    if (pre && r0 + kPanel < rend) fetch_vrows(f, segs, it.s0, it.s1, n, rend, r0 + kPanel);
     tsqr_absorb(R, n, P, ldp, vb, tb);
   }
+  if (rsmem) {
+    double* dst = it.rbuf + (long long)w.a * n * n;
+    for (long long e = threadIdx.x; e < nn; e += blockDim.x) dst[e] = R[e];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 3) tsqr_merge_kernel(const MergeWork* __restrict__ work, int rsmem) {
+  extern __shared__ double smem[];
+  const MergeWork w = work[blockIdx.x];
+  const int n = w.n;
+  const int ldp = n | 1;
+  double* P = smem;               // 32 x ldp
+  double* vb = P + kPanel * ldp;  // 64
+  double* tb = vb + 64;           // 4
+  double* Ra = w.rbuf + (long long)w.a * n * n;
+  const double* Rb = w.rbuf + (long long)w.b * n * n;
+  double* R = rsmem ? tb + 4 : Ra;
+  if (rsmem)
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = Ra[e];
+  for (int r0 = 0; r0 < n; r0 += kPanel) {
+    for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
+      const int p = e / n, j = e % n;
+      P[p * ldp + j] = (r0 + p < n) ? Rb[(long long)(r0 + p) * n + j] : 0.0;
+    }
+    __syncthreads();
+    tsqr_absorb(R, n, P, ldp, vb, tb, r0);
+  }
+  if (rsmem) {
+    __syncthreads();
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) Ra[e] = R[e];
+  }
+}
+
+__global__ void qr_out_kernel(const QrItem* __restrict__ items) {
+  const QrItem it = items[blockIdx.x];
+  const int n = it.n;
   const long long rows = it.M < n ? it.M : n;
   for (long long e = threadIdx.x; e < rows * n; e += blockDim.x) {
     const long long i = e / n, j = e % n;
-    it.out[e] = j >= i ? R[i * n + j] : 0.0;
+    it.out[e] = j >= i ? it.rbuf[i * n + j] : 0.0;
   }
 }
 
@@ -396,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 3) qr_r_kernel(const QrItem* __restr
 // orthonormal regardless of the row norms.  Round-robin pairing, one pair per warp at a time.
 // ---------------------------------------------------------------------------------------------
 
-__device__ void jacobi_rows(double* W, int n, int* flag, double* red) {
+__device__ int jacobi_rows(double* W, int n, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   // Rows whose norm is below eps * (largest row norm) can never pass the truncation threshold
   // (thr >= max(rows, cols) eps sigma_1); rotating against them moves the other row by less than
@@ -477,8 +520,9 @@ __device__ void jacobi_rows(double* W, int n, int* flag, double* red) {
     }
     const int any = *flag;
     __syncthreads();
-    if (!any) break;
+    if (!any) return sweep + 1;
   }
+  return 40;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -622,36 +666,6 @@ __global__ void __launch_bounds__(kThreads, 3) svd_tsqr_kernel(const SvdItem* __
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) svd_merge_kernel(const SvdItem* __restrict__ items,
-                                                             const SvdWork* __restrict__ work, int rsmem) {
-  extern __shared__ double smem[];
-  const SvdWork w = work[blockIdx.x];
-  const SvdItem it = items[w.item];
-  const int n = svd_n(it);
-  const int ldp = n | 1;
-  double* P = smem;               // 32 x ldp
-  double* vb = P + kPanel * ldp;  // 64
-  double* tb = vb + 64;         // 4
-  double* Ra = it.rbuf + (long long)w.a * n * n;
-  const double* Rb = it.rbuf + (long long)w.b * n * n;
-  double* R = rsmem ? tb + 4 : Ra;
-  if (rsmem) {
-    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = Ra[e];
-  }
-  for (int r0 = 0; r0 < n; r0 += kPanel) {
-    for (int e = threadIdx.x; e < kPanel * n; e += blockDim.x) {
-      const int p = e / n, j = e % n;
-      P[p * ldp + j] = (r0 + p < n) ? Rb[(long long)(r0 + p) * n + j] : 0.0;
-    }
-    __syncthreads();
-    tsqr_absorb(R, n, P, ldp, vb, tb, r0);
-  }
-  if (rsmem) {
-    __syncthreads();
-    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) Ra[e] = R[e];
-  }
-}
-
 static constexpr int kFinishThreads = 512;  // Jacobi: more warps = fewer row pairs per warp per step
 
 __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
@@ -679,7 +693,8 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
       for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
     __syncthreads();
     // B = R^T Q_B^T: left singular vectors of B are the normalised rows of R after Jacobi
-    jacobi_rows(R, n, &flag, jred);
+    const int sw = jacobi_rows(R, n, &flag, jred);
+    if (it.sweeps_out && threadIdx.x == 0) *it.sweeps_out = sw;
     for (int i = warp; i < n; i += nw) {
       double s = 0.0;
       for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * n + j], R[(long long)i * n + j], s);
@@ -1193,9 +1208,9 @@ static void init_attributes() {
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     };
     opt_in((const void*)gsum_kernel);
-    opt_in((const void*)qr_r_kernel);
+    opt_in((const void*)qr_chunk_kernel);
+    opt_in((const void*)tsqr_merge_kernel);
     opt_in((const void*)svd_tsqr_kernel);
-    opt_in((const void*)svd_merge_kernel);
     opt_in((const void*)svd_finish_kernel);
     opt_in((const void*)norm_kernel);
     opt_in((const void*)norm_warp_kernel);
@@ -1206,8 +1221,14 @@ size_t gsum_smem(int k2max) {
   return sizeof(double) * (2 * kKc * kLdS + (k2max > 0 ? (size_t)kTile * (k2max + 1) : 0));
 }
 
+cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
+                            cudaStream_t st);
+
 cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
                         cudaStream_t st) {
+  // tensor-pipe (DMMA) version by default; H2G_GSUM_LEGACY=1 selects the DFMA register-tile kernel
+  static const bool legacy = getenv("H2G_GSUM_LEGACY") != nullptr;
+  if (!legacy) return launch_gsum_mma(outs, terms, tiles, ntiles, k2max, st);
   init_attributes();
   if (ntiles == 0) return cudaSuccess;
   const size_t sm = gsum_smem(k2max);
@@ -1215,15 +1236,28 @@ cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles
   return cudaGetLastError();
 }
 
-size_t qr_smem(int n, bool ws) {
-  return sizeof(double) * ((size_t)kPanel * (n | 1) + 64 + 4 + (ws ? 0 : (size_t)n * n));
+size_t qr_smem(int n, bool rsmem) {
+  return sizeof(double) * ((size_t)kPanel * (n | 1) + 64 + 4 + (rsmem ? (size_t)n * n : 0));
 }
 
-cudaError_t launch_qr(const QrItem* items, const Seg* segs, int nitems, int nmax, bool ws, cudaStream_t st) {
+cudaError_t launch_qr_chunks(const QrItem* items, const Seg* segs, const SvdWork* work, int nwork, size_t smem,
+                             bool rsmem, cudaStream_t st) {
   init_attributes();
+  if (nwork == 0) return cudaSuccess;
+  qr_chunk_kernel<<<nwork, kThreads, smem, st>>>(items, segs, work, rsmem ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tsqr_merge(const MergeWork* work, int nwork, size_t smem, bool rsmem, cudaStream_t st) {
+  init_attributes();
+  if (nwork == 0) return cudaSuccess;
+  tsqr_merge_kernel<<<nwork, kThreads, smem, st>>>(work, rsmem ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qr_out(const QrItem* items, int nitems, cudaStream_t st) {
   if (nitems == 0) return cudaSuccess;
-  const size_t sm = qr_smem(nmax, ws);
-  qr_r_kernel<<<nitems, kThreads, sm, st>>>(items, segs);
+  qr_out_kernel<<<nitems, kThreads, 0, st>>>(items);
   return cudaGetLastError();
 }
 
@@ -1235,7 +1269,7 @@ size_t svd_tsqr_smem(int m, int kx, bool rsmem) {
   return d * sizeof(double);
 }
 
-size_t svd_merge_smem(int n, bool rsmem) {
+size_t merge_smem(int n, bool rsmem) {
   return sizeof(double) * ((size_t)kPanel * (n | 1) + 68 + (rsmem ? (size_t)n * n : 0));
 }
 
@@ -1250,14 +1284,6 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
   init_attributes();
   if (nwork == 0) return cudaSuccess;
   svd_tsqr_kernel<<<nwork, kThreads, smem, st>>>(items, segs, work, rsmem ? 1 : 0);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_svd_merge(const SvdItem* items, const SvdWork* work, int nwork, size_t smem, bool rsmem,
-                             cudaStream_t st) {
-  init_attributes();
-  if (nwork == 0) return cudaSuccess;
-  svd_merge_kernel<<<nwork, kThreads, smem, st>>>(items, work, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 

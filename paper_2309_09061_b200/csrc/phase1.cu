@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <functional>
+#include <future>
 #include <thread>
 
 #include "engine.h"
@@ -461,6 +462,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr, e4 = nullptr;
   record(C, e0);
+  // T^XY is pure structure: build it on a host thread while the GPU computes weights and bases
+  auto pt_future = std::async(std::launch::async, [&x, &y] {
+    return product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+  });
   auto keep = std::make_shared<Arena>(C.st);
   Arena sc(C.st);
   HView X{&x, false}, Y{&y, false}, XT{&x, true}, YT{&y, true};
@@ -501,8 +506,8 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   e3 = e2;
   PTree pt;
   {
-    HostTimer ht(C, "product_tree");
-    pt = product_tree(X.bv(), Y.bv());
+    HostTimer ht(C, "product_tree_wait");
+    pt = pt_future.get();
   }
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
   record(C, e4);

@@ -83,6 +83,12 @@ class Context:
                 out[k] = float(v)
         return out
 
+    def trace_begin(self):
+        N.check(self.lib.h2g_ctx_trace_begin(self.h))
+
+    def trace_dump(self, path: str):
+        N.check(self.lib.h2g_ctx_trace_dump(self.h, path.encode()))
+
     def synchronize(self):
         N.check(self.lib.h2g_ctx_synchronize(self.h))
 

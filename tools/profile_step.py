@@ -26,3 +26,8 @@ s2 = ctx.stage_times()
 print(f"step {t*1e3:.1f} ms", {k: round(s1[k] * 1e3, 2) for k in ("t_setup", "t1_row", "t1_col", "t1_mat")},
       {k: round(s2[k] * 1e3, 2) for k in ("t2_row", "t2_col", "t2_mat")})
 print("host ms", {k: round(v, 1) for k, v in ctx.host_times().items()})
+if os.environ.get("H2G_TRACE"):
+    ctx.trace_begin()
+    g = P.multiply(dx, dy, spec["eps"], ctx=ctx)
+    z = P.coarsen(g, dx.block_tree, spec["eps"], ctx=ctx)
+    ctx.trace_dump(os.environ["H2G_TRACE"])
