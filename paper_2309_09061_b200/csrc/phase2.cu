@@ -1,9 +1,12 @@
 // Phase 2 of the product: adaptive re-compression onto the prescribed block tree (Figs. 4-5) and
 // the final projection (reference coarsening.py:36-445), plus input recompression.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <map>
+#include <unordered_map>
 #include <thread>
 
 #include "engine.h"
@@ -11,108 +14,152 @@
 namespace h2g {
 
 // ------------------------------------------------------------------ column trees (trees.py:362-406)
+// Flat column tree: children of a node are contiguous (k0[u] .. k0[u] + nk[u] - 1); node 0 is the
+// root.  Matrices live on the leaves.  (The reference's ColumnTree objects, built and discarded per
+// block, become index arithmetic here.)
 struct CT {
-  std::vector<int> cl;
+  std::vector<int> cl, k0, nk;
   std::vector<char> adm;
-  std::vector<std::vector<int>> kids;
   std::vector<Mat> mat;
   int add(int c, bool a, Mat m = Mat{}) {
     cl.push_back(c);
     adm.push_back(a ? 1 : 0);
-    kids.emplace_back();
+    k0.push_back(0);
+    nk.push_back(0);
     mat.push_back(m);
     return (int)cl.size() - 1;
   }
-  bool leaf(int u) const { return kids[u].empty(); }
+  void set(int u, int c, bool a, Mat m) {
+    cl[u] = c;
+    adm[u] = a ? 1 : 0;
+    mat[u] = m;
+  }
+  int reserve_kids(int u, int n) {  // allocates n contiguous child slots of u
+    const int base = (int)cl.size();
+    for (int i = 0; i < n; ++i) add(-1, true);
+    k0[u] = base;
+    nk[u] = n;
+    return base;
+  }
+  bool leaf(int u) const { return nk[u] == 0; }
+  int kid(int u, int i) const { return k0[u] + i; }
+  void clear() {
+    cl.clear();
+    k0.clear();
+    nk.clear();
+    adm.clear();
+    mat.clear();
+  }
   void leaves(int u, std::vector<int>& out) const {
     if (leaf(u)) { out.push_back(u); return; }
-    for (int k : kids[u]) leaves(k, out);
+    for (int i = 0; i < nk[u]; ++i) leaves(k0[u] + i, out);
   }
 };
 using CTP = std::shared_ptr<CT>;
+struct CTRef {  // a column tree inside a pooled flat tree
+  const CT* t = nullptr;
+  int root = -1;
+};
 
-static int ct_copy(const CT& a, int u, CT& out, bool with_mats) {
-  const int v = out.add(a.cl[u], a.adm[u], with_mats ? a.mat[u] : Mat{});
-  for (int k : a.kids[u]) {
-    const int w = ct_copy(a, k, out, with_mats);
-    out.kids[v].push_back(w);
+static int ct_copy(const CT& a, int u, CT& out, bool with_mats, int slot = -1) {
+  if (slot < 0) slot = out.add(a.cl[u], a.adm[u], with_mats ? a.mat[u] : Mat{});
+  else out.set(slot, a.cl[u], a.adm[u], with_mats ? a.mat[u] : Mat{});
+  if (!a.leaf(u)) {
+    const int n = a.nk[u];
+    const int base = out.reserve_kids(slot, n);
+    for (int i = 0; i < n; ++i) ct_copy(a, a.kid(u, i), out, with_mats, base + i);
   }
-  return v;
+  return slot;
 }
 
 // Structure-only union (coarsening.py:89-105).
-static int ct_union(const CT* a, int ua, const CT* b, int ub, CT& out) {
-  if (!a) return ct_copy(*b, ub, out, false);
-  if (!b) return ct_copy(*a, ua, out, false);
+static int ct_union(const CT* a, int ua, const CT* b, int ub, CT& out, int slot = -1) {
+  if (!a) return ct_copy(*b, ub, out, false, slot);
+  if (!b) return ct_copy(*a, ua, out, false, slot);
   if (a->cl[ua] != b->cl[ub]) throw StructureErr("column trees rooted at different clusters");
   const bool ak = !a->leaf(ua), bk = !b->leaf(ub);
   if (ak && bk) {
-    const int v = out.add(a->cl[ua], true);
-    const size_t n = std::min(a->kids[ua].size(), b->kids[ub].size());
-    for (size_t i = 0; i < n; ++i) {
-      const int w = ct_union(a, a->kids[ua][i], b, b->kids[ub][i], out);
-      out.kids[v].push_back(w);
-    }
-    return v;
+    if (slot < 0) slot = out.add(a->cl[ua], true);
+    else out.set(slot, a->cl[ua], true, Mat{});
+    const int n = std::min(a->nk[ua], b->nk[ub]);
+    const int base = out.reserve_kids(slot, n);
+    for (int i = 0; i < n; ++i) ct_union(a, a->kid(ua, i), b, b->kid(ub, i), out, base + i);
+    return slot;
   }
-  if (ak) return ct_copy(*a, ua, out, false);
-  if (bk) return ct_copy(*b, ub, out, false);
-  return out.add(a->cl[ua], a->adm[ua] && b->adm[ub]);
+  if (ak) return ct_copy(*a, ua, out, false, slot);
+  if (bk) return ct_copy(*b, ub, out, false, slot);
+  if (slot < 0) return out.add(a->cl[ua], a->adm[ua] && b->adm[ub]);
+  out.set(slot, a->cl[ua], a->adm[ua] && b->adm[ub], Mat{});
+  return slot;
 }
 
 // Deferred products  dst = src * F_{path[0]}^T * ... * F_{path[-1]}^T (* W_leaf^T)  (match_column,
-// coarsening.py:108-136), resolved with memoised prefix products in dependency waves.
+// coarsening.py:108-136), resolved with memoised prefix products in dependency waves.  Paths live in
+// one shared pool.
 struct Jobs {
   struct J {
     Mat dst, src;
-    std::vector<int> path;
+    int p0, plen;
     bool conv;
     int leafcl;
   };
   std::vector<J> v;
+  std::vector<int> pool;
 };
 
-static void ct_push_down(const Mat& src, std::vector<int>& path, const CT& T, int tu, int ro, Jobs& J) {
+static void ct_push_down(const Mat& src, int* path, int depth, const CT& T, int tu, int ro, Jobs& J) {
   if (!T.leaf(tu)) {
-    for (int tc : T.kids[tu]) {
-      path.push_back(T.cl[tc]);
-      ct_push_down(src, path, T, tc, ro, J);
-      path.pop_back();
+    if (depth >= 62) throw StructureErr("column tree deeper than 62 levels");
+    for (int i = 0; i < T.nk[tu]; ++i) {
+      const int tc = T.kid(tu, i);
+      path[depth] = T.cl[tc];
+      ct_push_down(src, path, depth + 1, T, tc, ro, J);
     }
     return;
   }
-  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, path, !T.adm[tu], T.cl[tu]});
+  const int p0 = (int)J.pool.size();
+  J.pool.insert(J.pool.end(), path, path + depth);
+  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, p0, depth, !T.adm[tu], T.cl[tu]});
 }
 
 static void ct_match(const CT& P, int pu, const CT& T, int tu, int ro, Jobs& J) {
   if (P.cl[pu] != T.cl[tu]) throw InvalidInput("representation and target roots differ");
   if (!P.leaf(pu)) {
     if (T.leaf(tu)) throw StructureErr("match_column: target coarser than representation");
-    for (size_t i = 0; i < P.kids[pu].size(); ++i) ct_match(P, P.kids[pu][i], T, T.kids[tu][i], ro, J);
+    for (int i = 0; i < P.nk[pu]; ++i) ct_match(P, P.kid(pu, i), T, T.kid(tu, i), ro, J);
     return;
   }
   const Mat& src = P.mat[pu];
   if (!T.leaf(tu)) {
-    std::vector<int> path;
-    for (int tc : T.kids[tu]) {
-      path.assign(1, T.cl[tc]);
-      ct_push_down(src, path, T, tc, ro, J);
+    int path[64];
+    for (int i = 0; i < T.nk[tu]; ++i) {
+      const int tc = T.kid(tu, i);
+      path[0] = T.cl[tc];
+      ct_push_down(src, path, 1, T, tc, ro, J);
     }
     return;
   }
-  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, {}, P.adm[pu] && !T.adm[tu], T.cl[tu]});
+  J.v.push_back(Jobs::J{T.mat[tu].band(ro, src.r), src, 0, 0, P.adm[pu] && !T.adm[tu], T.cl[tu]});
 }
 
+struct PtrClusterHash {
+  size_t operator()(const std::pair<const double*, int>& k) const {
+    return std::hash<const void*>()(k.first) * 1000003u ^ (size_t)k.second;
+  }
+};
+
 static void resolve_jobs(Ctx& C, Arena& sc, Jobs& J, const Basis& w) {
-  std::map<std::pair<const double*, int>, Mat> inter;
+  std::unordered_map<std::pair<const double*, int>, Mat, PtrClusterHash> inter;
+  inter.reserve(J.v.size());
   std::vector<std::vector<std::pair<const Jobs::J*, int>>> waves;
   for (const auto& j : J.v) {
-    const int nf = (int)j.path.size() + (j.conv ? 1 : 0);
+    const int* path = J.pool.data() + j.p0;
+    const int nf = j.plen + (j.conv ? 1 : 0);
     const int L = nf - 2;
     for (int i = 0; i < L; ++i) {
-      auto key = std::make_pair((const double*)j.src.p, j.path[i]);
+      auto key = std::make_pair((const double*)j.src.p, path[i]);
       if (inter.count(key)) continue;
-      inter[key] = Mat{sc.alloc((size_t)j.src.r * w.rank[j.path[i]]), j.src.r, w.rank[j.path[i]]};
+      inter[key] = Mat{sc.alloc((size_t)j.src.r * w.rank[path[i]]), j.src.r, w.rank[path[i]]};
       if ((int)waves.size() <= i) waves.resize(i + 1);
       waves[i].emplace_back(&j, i);
     }
@@ -121,28 +168,40 @@ static void resolve_jobs(Ctx& C, Arena& sc, Jobs& J, const Basis& w) {
     GBatch g;
     for (auto& pr : wave) {
       const Jobs::J& j = *pr.first;
+      const int* path = J.pool.data() + j.p0;
       const int i = pr.second;
-      const Mat in = i == 0 ? j.src : inter[std::make_pair((const double*)j.src.p, j.path[i - 1])];
-      g.out(inter[std::make_pair((const double*)j.src.p, j.path[i])], false);
-      g.t2(in.ref(), w.xferm(j.path[i]).tref(), in.c);
+      const Mat in = i == 0 ? j.src : inter[std::make_pair((const double*)j.src.p, path[i - 1])];
+      g.out(inter[std::make_pair((const double*)j.src.p, path[i])], false);
+      g.t2(in.ref(), w.xferm(path[i]).tref(), in.c);
     }
     g.run(C);
   }
   GBatch g;
+  g.outs.reserve(J.v.size());
+  g.terms.reserve(J.v.size());
   for (const auto& j : J.v) {
-    const int nf = (int)j.path.size() + (j.conv ? 1 : 0);
+    const int* path = J.pool.data() + j.p0;
+    const int nf = j.plen + (j.conv ? 1 : 0);
     const int L = std::max(0, nf - 2);
-    const Mat base = L > 0 ? inter[std::make_pair((const double*)j.src.p, j.path[L - 1])] : j.src;
-    std::vector<std::pair<MatRef, int>> f;  // remaining factors with their column counts
-    for (size_t i = L; i < j.path.size(); ++i) f.emplace_back(w.xferm(j.path[i]).tref(), w.rank[j.path[i]]);
-    if (j.conv) f.emplace_back(w.leafm(j.leafcl).tref(), w.tree->size(j.leafcl));
+    const Mat base = L > 0 ? inter[std::make_pair((const double*)j.src.p, path[L - 1])] : j.src;
+    MatRef f[2];
+    int fc[2], nfac = 0;
+    for (int i = L; i < j.plen; ++i) {
+      f[nfac] = w.xferm(path[i]).tref();
+      fc[nfac++] = w.rank[path[i]];
+    }
+    if (j.conv) {
+      f[nfac] = w.leafm(j.leafcl).tref();
+      fc[nfac++] = w.tree->size(j.leafcl);
+    }
     g.out(j.dst, false);
-    if (f.empty()) g.t1(base.ref());
-    else if (f.size() == 1) g.t2(base.ref(), f[0].first, base.c);
-    else g.t3(base.ref(), f[0].first, f[1].first, base.c, f[0].second);
+    if (nfac == 0) g.t1(base.ref());
+    else if (nfac == 1) g.t2(base.ref(), f[0], base.c);
+    else g.t3(base.ref(), f[0], f[1], base.c, fc[0]);
   }
   g.run(C);
   J.v.clear();
+  J.pool.clear();
 }
 
 // ------------------------------------------------------------------ coverage (coarsening.py:160-184)
@@ -175,7 +234,8 @@ static std::vector<char> coverage(BView pt, BView coarse) {
 struct CState {
   std::shared_ptr<Basis> q;
   MatStore r, z;
-  std::vector<CTP> reps;
+  std::vector<CTRef> reps;
+  std::vector<std::unique_ptr<CT>> pools;  // owners of the stored representations
 };
 
 // Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
@@ -205,7 +265,10 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   q.xfer.assign(tr.n, nullptr);
   S.r.assign(tr.n, Mat{});
   S.z.assign(tr.n, Mat{});
-  S.reps.assign(pt.nb, nullptr);
+  S.reps.assign(pt.nb, CTRef{});
+  CT mpool, singles, acc, nxt, tg[8];  // per-level scratch trees (capacity reused)
+  std::vector<int> mroot(pt.nb, -1);
+  std::vector<double> msc(pt.nb, 0.0);
   Arena sc(C.st);
 
   // top-down condensation weights Z_t (coarsening.py:231-245)
@@ -247,6 +310,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   for (int lev = tr.depth; lev >= 0; --lev) {
     const std::vector<int>& L = tr.by_level[lev];
     const size_t nl = L.size();
+    HostTimer htv(C, "p2_vz_plan");
     GBatch g1, g2;
     std::vector<Mat> V(nl), VZ(nl);
     for (size_t li = 0; li < nl; ++li) {
@@ -282,99 +346,111 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     }
     g1.run(C);
     g2.run(C);
+    htv.~HostTimer();
+    new (&htv) HostTimer(C, "p2_dummy");
 
-    // merged representations of subdivided covered blocks (coarsening.py:260-279)
-    std::map<int, CTP> merged;
+    // merged representations of subdivided covered blocks (coarsening.py:260-279); all column
+    // trees of the level live in pooled flat trees (no per-block allocations)
+    mpool.clear();
+    std::vector<int> mblocks;
     Jobs J;
+    {
+    HostTimer htm(C, "p2_merge_plan");
     for (size_t li = 0; li < nl; ++li) {
       const int t = L[li];
       if (tr.leaf(t)) continue;
       for (int b : sub_cov[t]) {
-        std::vector<int> order;
-        std::map<int, std::vector<std::pair<CTP, int>>> groups;  // r2 -> (part, rows)
+        // children of (t, r) are chil(t) x (chil(r) or {r}): group by column r2, first appearance
+        int order[8], ngroup = 0;
+        CTRef gpart[8][8];
+        int grows[8][8], gcnt[8] = {0};
+        singles.clear();  // one-leaf column trees for admissible children (R_t2 S_b2)
+        if (pt.nkids(b) > 8) throw StructureErr("product block with more than 8 children");
         for (int i = 0; i < pt.nkids(b); ++i) {
           const int b2 = pt.kid(b, i);
           const int r2 = pv.col(b2);
-          CTP part;
+          CTRef part;
           if (pt.adm_leaf(b2)) {
-            part = std::make_shared<CT>();
-            part->add(r2, true, lm[b2]);
+            part = CTRef{&singles, singles.add(r2, true, lm[b2])};
           } else {
             part = S.reps[b2];
-            if (!part) throw StructureErr("missing child representation");
+            if (!part.t) throw StructureErr("missing child representation");
           }
-          if (!groups.count(r2)) order.push_back(r2);
-          groups[r2].emplace_back(part, q.rank[pv.row(b2)]);
+          int gi = 0;
+          while (gi < ngroup && order[gi] != r2) ++gi;
+          if (gi == ngroup) order[ngroup++] = r2;
+          gpart[gi][gcnt[gi]] = part;
+          grows[gi][gcnt[gi]++] = q.rank[pv.row(b2)];
         }
-        std::map<int, CTP> per;
-        for (int r2 : order) {
-          auto& parts = groups[r2];
-          CTP tgt = std::make_shared<CT>();
-          {
-            CT acc;
-            ct_union(nullptr, 0, parts[0].first.get(), 0, acc);
-            for (size_t i = 1; i < parts.size(); ++i) {
-              CT nxt;
-              ct_union(&acc, 0, parts[i].first.get(), 0, nxt);
-              acc = std::move(nxt);
+        for (int gi = 0; gi < ngroup; ++gi) {
+          CT& tgt = tg[gi];
+          tgt.clear();
+          if (gcnt[gi] == 1) {
+            ct_copy(*gpart[gi][0].t, gpart[gi][0].root, tgt, false);
+          } else {
+            acc.clear();
+            ct_union(nullptr, 0, gpart[gi][0].t, gpart[gi][0].root, acc);
+            for (int i = 1; i < gcnt[gi]; ++i) {
+              nxt.clear();
+              ct_union(&acc, 0, gpart[gi][i].t, gpart[gi][i].root, nxt);
+              std::swap(acc, nxt);
             }
-            *tgt = std::move(acc);
+            ct_copy(acc, 0, tgt, false);
           }
           int rows = 0;
-          for (auto& pr : parts) rows += pr.second;
-          std::vector<int> lv;
-          tgt->leaves(0, lv);
-          for (int u : lv) {
-            const int c = tgt->cl[u];
-            const int cols = tgt->adm[u] ? w1.rank[c] : w1.tree->size(c);
-            tgt->mat[u] = Mat{sc.alloc((size_t)rows * cols), rows, cols};
+          for (int i = 0; i < gcnt[gi]; ++i) rows += grows[gi][i];
+          for (int u = 0; u < (int)tgt.cl.size(); ++u) {
+            if (!tgt.leaf(u)) continue;
+            const int c = tgt.cl[u];
+            const int cols = tgt.adm[u] ? w1.rank[c] : w1.tree->size(c);
+            tgt.mat[u] = Mat{sc.alloc((size_t)rows * cols), rows, cols};
           }
           int ro = 0;
-          for (auto& pr : parts) {
-            ct_match(*pr.first, 0, *tgt, 0, ro, J);
-            ro += pr.second;
+          for (int i = 0; i < gcnt[gi]; ++i) {
+            ct_match(*gpart[gi][i].t, gpart[gi][i].root, tgt, 0, ro, J);
+            ro += grows[gi][i];
           }
-          per[r2] = tgt;
         }
         const int r = pv.col(b);
-        if (order.size() == 1 && order[0] == r) {
-          merged[b] = per[r];
+        if (ngroup == 1 && order[0] == r) {
+          mroot[b] = ct_copy(tg[0], 0, mpool, true);
         } else {
-          CTP w = std::make_shared<CT>();
-          const int root = w->add(r, true);
-          for (int r2 : order) {
-            const int k = ct_copy(*per[r2], 0, *w, true);
-            w->kids[root].push_back(k);
-          }
-          merged[b] = w;
+          const int root = mpool.add(r, true);
+          const int base = mpool.reserve_kids(root, ngroup);
+          for (int gi = 0; gi < ngroup; ++gi) ct_copy(tg[gi], 0, mpool, true, base + gi);
+          mroot[b] = root;
         }
+        mblocks.push_back(b);
       }
     }
+    static const bool dbg_jobs = getenv("H2G_DEBUG_JOBS") != nullptr;
+    if (dbg_jobs)
+      fprintf(stderr, "level %d: %zu merged reps, %zu nodes, %zu jobs, path pool %zu\n", lev, mblocks.size(),
+              mpool.cl.size(), J.v.size(), J.pool.size());
     resolve_jobs(C, sc, J, w1);
+    }
 
     // scales of the flattened merged reps (coarsening.py:316-317)
-    std::map<int, double> msc;
-    if (scale && !merged.empty()) {
+    std::vector<int> lv;
+    if (scale && !mblocks.empty()) {
       NormBatch nbat;
-      std::vector<int> ids;
-      for (auto& kv : merged) {
-        std::vector<int> lv;
-        kv.second->leaves(0, lv);
+      for (int b : mblocks) {
+        lv.clear();
+        mpool.leaves(mroot[b], lv);
         NormItem it{};
         it.s0 = nbat.sl.begin();
         long long N = 0;
         for (int u : lv) {
-          nbat.sl.add(kv.second->mat[u].ref(), kv.second->mat[u].c);
-          N += kv.second->mat[u].c;
+          nbat.sl.add(mpool.mat[u].ref(), mpool.mat[u].c);
+          N += mpool.mat[u].c;
         }
         it.s1 = nbat.sl.begin();
-        it.m = lv.empty() ? 0 : kv.second->mat[lv[0]].r;
+        it.m = lv.empty() ? 0 : mpool.mat[lv[0]].r;
         it.N = N;
         nbat.items.push_back(it);
-        ids.push_back(kv.first);
       }
       auto v = nbat.run(C, sc);
-      for (size_t i = 0; i < ids.size(); ++i) msc[ids[i]] = v[i];
+      for (size_t i = 0; i < mblocks.size(); ++i) msc[mblocks[i]] = v[i];
     }
 
     // truncated SVDs of C_t = [V Z^T | scaled columns] (coarsening.py:294-326)
@@ -396,14 +472,13 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
         }
       } else {
         for (int b : sub_cov[t]) {
-          const CT& M = *merged[b];
-          std::vector<int> lv;
-          M.leaves(0, lv);
+          lv.clear();
+          mpool.leaves(mroot[b], lv);
           const double nv = scale ? msc[b] : 0.0;
           const double s = (scale && nv > 0.0) ? 1.0 / nv : 1.0;
           for (int u : lv) {
-            sv.sl.add(M.mat[u].ref(), M.mat[u].c, s);
-            N += M.mat[u].c;
+            sv.sl.add(mpool.mat[u].ref(), mpool.mat[u].c, s);
+            N += mpool.mat[u].c;
           }
         }
       }
@@ -420,7 +495,11 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     }
     std::vector<int> rk = sv.run(C, sc);
 
+    HostTimer htp(C, "p2_post");
+    S.pools.emplace_back(new CT());
+    CT& rp = *S.pools.back();  // this level's stored representations
     GBatch gp, gq;
+    std::vector<int> lv2;
     for (size_t li = 0; li < nl; ++li) {
       const int t = L[li];
       const int k = rk[li];
@@ -436,9 +515,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
           Mat rep{out.alloc((size_t)k * w1.tree->size(r)), k, w1.tree->size(r)};
           gp.out(rep, false);
           gp.t2(Q.tref(), g.near(b), Q.r);
-          CTP c = std::make_shared<CT>();
-          c->add(r, false, rep);
-          S.reps[b] = c;
+          S.reps[b] = CTRef{&rp, rp.add(r, false, rep)};
         }
       } else {
         int off = 0;
@@ -448,27 +525,28 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
           off += q.rank[c];
         }
         for (int b : sub_cov[t]) {  // stored reps are Q^T (unscaled rep) (coarsening.py:327-328)
-          const CT& M = *merged[b];
-          CTP c = std::make_shared<CT>();
-          ct_copy(M, 0, *c, false);
-          std::vector<int> lv;
-          c->leaves(0, lv);
-          for (int u : lv) {
-            const Mat& src = M.mat[u];
-            c->mat[u] = Mat{out.alloc((size_t)k * src.c), k, src.c};
-            gp.out(c->mat[u], false);
+          const int root = ct_copy(mpool, mroot[b], rp, false);
+          lv.clear();
+          lv2.clear();
+          mpool.leaves(mroot[b], lv);
+          rp.leaves(root, lv2);
+          for (size_t i = 0; i < lv.size(); ++i) {
+            const Mat& src = mpool.mat[lv[i]];
+            rp.mat[lv2[i]] = Mat{out.alloc((size_t)k * src.c), k, src.c};
+            gp.out(rp.mat[lv2[i]], false);
             gp.t2(Q.tref(), src.ref(), Q.r);
           }
-          S.reps[b] = c;
+          S.reps[b] = CTRef{&rp, root};
         }
       }
     }
     gp.run(C);
+    HostTimer htc(C, "p2_compose");
     // compose_leaf_rep for subdivided covered blocks at leaf row clusters (coarsening.py:281-290)
     for (size_t li = 0; li < nl; ++li) {
       const int t = L[li];
       if (!tr.leaf(t)) continue;
-      std::function<int(CT&, int)> build = [&](CT& T, int b) -> int {
+      std::function<int(CT&, int, int)> build = [&](CT& T, int b, int slot) -> int {
         const int r = pv.col(b);
         if (pt.adm_leaf(b)) {
           if (!lm[b].p) {
@@ -476,21 +554,25 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
             gq.out(lm[b], false);
             gq.t2(S.r[t].ref(), g.coup(b), S.r[t].c);
           }
-          return T.add(r, true, lm[b]);
+          if (slot < 0) return T.add(r, true, lm[b]);
+          T.set(slot, r, true, lm[b]);
+          return slot;
         }
-        if (pt.near_leaf(b)) return T.add(r, false, S.reps[b]->mat[0]);
-        const int v = T.add(r, true);
-        for (int i = 0; i < pt.nkids(b); ++i) {
-          const int w = build(T, pt.kid(b, i));
-          T.kids[v].push_back(w);
+        if (pt.near_leaf(b)) {
+          const Mat nm = S.reps[b].t->mat[S.reps[b].root];
+          if (slot < 0) return T.add(r, false, nm);
+          T.set(slot, r, false, nm);
+          return slot;
         }
-        return v;
+        if (slot < 0) slot = T.add(r, true);
+        else T.set(slot, r, true, Mat{});
+        const int base = T.reserve_kids(slot, pt.nkids(b));
+        for (int i = 0; i < pt.nkids(b); ++i) build(T, pt.kid(b, i), base + i);
+        return slot;
       };
       std::function<void(int)> all = [&](int b) {
         if (pt.leaf(b)) return;
-        CTP c = std::make_shared<CT>();
-        build(*c, b);
-        S.reps[b] = c;
+        S.reps[b] = CTRef{&rp, build(rp, b, -1)};
         for (int i = 0; i < pt.nkids(b); ++i) all(pt.kid(b, i));
       };
       for (int b : sub_cov[t]) all(b);
@@ -542,10 +624,11 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     if (!cb.adm_leaf(b)) continue;
     const int pb = pt.find(cb.row[b], cb.col[b]);
     if (pt.adm_leaf(pb)) continue;
-    const CT& rep = *rs.reps[pb];
+    const CTRef rr = rs.reps[pb];
+    if (!rr.t) throw StructureErr("missing representation of a covered product block");
     std::vector<int> lv;
-    rep.leaves(0, lv);
-    for (int u : lv) need(cb.col[b], rep.cl[u]);
+    rr.t->leaves(rr.root, lv);
+    for (int u : lv) need(cb.col[b], rr.t->cl[u]);
   }
   for (auto& wave : waves) {
     GBatch gw;
@@ -569,9 +652,9 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
       if (pt.adm_leaf(pb)) {
         g1.t3(rs.r[t].ref(), g.coup(pb), cs.r[r].tref(), rs.r[t].c, cs.r[r].c);
       } else {
-        const CT& rep = *rs.reps[pb];
+        const CT& rep = *rs.reps[pb].t;
         std::vector<int> lv;
-        rep.leaves(0, lv);
+        rep.leaves(rs.reps[pb].root, lv);
         for (int u : lv) {  // lift (coarsening.py:374-382)
           const int c = rep.cl[u];
           const Mat& M = rep.mat[u];
@@ -594,13 +677,15 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   return Z;
 }
 
-static std::vector<double> all_norms(Ctx& C, Arena& sc, const H2& g, bool coupling) {
+// sigma_1 of every coupling and nearfield block of g in one batch (coarsening.py:342-351)
+static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, std::vector<double>& nn) {
   const Blocks& B = *g.bt;
   NormBatch nb;
   std::vector<int> ids;
   HView v{&g, false};
   for (int b = 0; b < B.nb; ++b) {
-    if (coupling ? !B.adm_leaf(b) : !B.near_leaf(b)) continue;
+    if (!B.leaf(b)) continue;
+    const bool coupling = B.adm[b];
     const int t = B.row[b], s = B.col[b];
     const int m = coupling ? g.rb->rank[t] : B.rows->size(t);
     const int n = coupling ? g.cb->rank[s] : B.cols->size(s);
@@ -613,10 +698,10 @@ static std::vector<double> all_norms(Ctx& C, Arena& sc, const H2& g, bool coupli
     nb.items.push_back(it);
     ids.push_back(b);
   }
-  std::vector<double> out(B.nb, 0.0);
+  cn.assign(B.nb, 0.0);
+  nn.assign(B.nb, 0.0);
   auto vals = nb.run(C, sc);
-  for (size_t i = 0; i < ids.size(); ++i) out[ids[i]] = vals[i];
-  return out;
+  for (size_t i = 0; i < ids.size(); ++i) (B.adm[ids[i]] ? cn : nn)[ids[i]] = vals[i];
 }
 
 // Phase-2 driver (reference coarsening.py:408-422).
@@ -626,10 +711,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   Arena sc(C.st);
   std::vector<double> cn, nn;
-  if (scale) {
-    cn = all_norms(C, sc, g, true);
-    nn = all_norms(C, sc, g, false);
-  }
+  if (scale) all_norms(C, sc, g, cn, nn);
   auto ar = std::make_shared<Arena>(C.st);
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
