@@ -666,13 +666,110 @@ __global__ void __launch_bounds__(kThreads, 3) svd_tsqr_kernel(const SvdItem* __
   }
 }
 
+// Householder QR with column pivoting of W (n x n, row-major), in place; only the triangular factor
+// is kept.  perm[c] = original column of column c.  Used as the Jacobi preconditioner
+// (Drmac-Veselic): W Pi = Q1 R1, and the rows of R1 are graded by the pivoting, so one-sided Jacobi
+// on them needs a few sweeps instead of ~15.  Left singular vectors of W^T = Pi x those of R1^T.
+__device__ void qrcp_rows_precondition(double* W, int n, int* perm, double* cn, double* cn0, double* vh,
+                                       double* red, int* ired) {
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int c = tid; c < n; c += nt) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(W[(long long)i * n + c], W[(long long)i * n + c], s);
+    cn[c] = cn0[c] = s;
+    perm[c] = c;
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    double best = -1.0;
+    int bi = j;
+    for (int c = j + tid; c < n; c += nt)
+      if (cn[c] > best) { best = cn[c]; bi = c; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { red[warp] = best; ired[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = -1.0;
+      int p = j;
+      for (int w = 0; w < nw; ++w)
+        if (red[w] > b || (red[w] == b && ired[w] < p)) { b = red[w]; p = ired[w]; }
+      ired[nw] = p;
+    }
+    __syncthreads();
+    const int p = ired[nw];
+    if (p != j) {
+      for (int i = tid; i < n; i += nt) {
+        const double a = W[(long long)i * n + j];
+        W[(long long)i * n + j] = W[(long long)i * n + p];
+        W[(long long)i * n + p] = a;
+      }
+      if (tid == 0) {
+        double t = cn[j]; cn[j] = cn[p]; cn[p] = t;
+        t = cn0[j]; cn0[j] = cn0[p]; cn0[p] = t;
+        const int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {  // reflector for column j, rows j..n-1
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < n; i += 32) ss = fma(W[(long long)i * n + j], W[(long long)i * n + j], ss);
+      ss = warp_sum(ss);
+      const double alpha = W[(long long)j * n + j];
+      double tau = 0.0, scale = 0.0;
+      if (ss != 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        const double beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int i = j + 1 + lane; i < n; i += 32) {
+        vh[i] = W[(long long)i * n + j] * scale;
+        W[(long long)i * n + j] = 0.0;
+      }
+      if (lane == 0) {
+        if (ss != 0.0) W[(long long)j * n + j] = alpha >= 0.0 ? -sqrt(alpha * alpha + ss) : sqrt(alpha * alpha + ss);
+        red[nw + 1] = tau;
+      }
+    }
+    __syncthreads();
+    const double tau = red[nw + 1];
+    for (int c = j + 1 + tid; c < n; c += nt) {
+      if (tau != 0.0) {
+        double w0 = W[(long long)j * n + c], w1 = 0.0;
+        int i = j + 1;
+        for (; i + 1 < n; i += 2) {
+          w0 = fma(vh[i], W[(long long)i * n + c], w0);
+          w1 = fma(vh[i + 1], W[(long long)(i + 1) * n + c], w1);
+        }
+        if (i < n) w0 = fma(vh[i], W[(long long)i * n + c], w0);
+        const double tw = tau * (w0 + w1);
+        W[(long long)j * n + c] -= tw;
+        for (int i2 = j + 1; i2 < n; ++i2) W[(long long)i2 * n + c] -= tw * vh[i2];
+      }
+      const double rj = W[(long long)j * n + c];
+      cn[c] -= rj * rj;
+      if (cn[c] <= 1e-2 * cn0[c]) {  // cancellation: recompute the trailing norm exactly
+        double s2 = 0.0;
+        for (int i2 = j + 1; i2 < n; ++i2) s2 = fma(W[(long long)i2 * n + c], W[(long long)i2 * n + c], s2);
+        cn[c] = cn0[c] = s2;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 static constexpr int kFinishThreads = 512;  // Jacobi: more warps = fewer row pairs per warp per step
 
 __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
   extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
-  __shared__ double jred[kFinishThreads / 32 + 1];
+  __shared__ double jred[kFinishThreads / 32 + 2];
   const SvdItem it = items[blockIdx.x];
   const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
   const long long N = it.N;
@@ -682,7 +779,13 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
   double* tv = V + (long long)m * ldv;       // kx + 1
   double* sig = tv + kx + 1;                 // n
   int* ord = (int*)(sig + n);                // n ints
-  double* R = rsmem ? sig + n + (n / 2 + 1) : it.rbuf;
+  double* cn = sig + n + (n / 2 + 1);        // QRCP column norms (n), reference norms (n), reflector (n)
+  double* cn0 = cn + n;
+  double* vh = cn0 + n;
+  int* perm = (int*)(vh + n);                // n ints
+  int* iperm = perm + n;                     // n ints
+  double* R = rsmem ? vh + n + n + 1 : it.rbuf;
+  __shared__ int ired[kFinishThreads / 32 + 2];
   if (kx > 0) {
     for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
     for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
@@ -692,7 +795,11 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
     if (rsmem)
       for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
     __syncthreads();
-    // B = R^T Q_B^T: left singular vectors of B are the normalised rows of R after Jacobi
+    // B = R^T Q_B^T: left singular vectors of B = those of R^T.  QRCP preconditioning R Pi = Q1 R1,
+    // then the left singular vectors of R^T are Pi x the normalised rows of R1 after row Jacobi.
+    qrcp_rows_precondition(R, n, perm, cn, cn0, vh, jred, ired);
+    for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
+    __syncthreads();
     const int sw = jacobi_rows(R, n, &flag, jred);
     if (it.sweeps_out && threadIdx.x == 0) *it.sweeps_out = sw;
     for (int i = warp; i < n; i += nw) {
@@ -736,7 +843,7 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
       val = (i == j) ? 1.0 : 0.0;
     } else {
       const int src = ord[j - k1];
-      val = (i < k1) ? 0.0 : R[(long long)src * n + (i - k1)] / sig[src];
+      val = (i < k1) ? 0.0 : R[(long long)src * n + iperm[i - k1]] / sig[src];
     }
     Q[e] = val;
   }
@@ -1276,7 +1383,8 @@ size_t merge_smem(int n, bool rsmem) {
 size_t svd_finish_smem(int m, int kx, bool rsmem) {
   const int k1 = m < kx ? m : kx;
   const int n = m - k1;
-  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + n + (n / 2 + 1) + (rsmem ? (size_t)n * n : 0));
+  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + n + (n / 2 + 1) + 4 * (size_t)n + 1 +
+                           (rsmem ? (size_t)n * n : 0));
 }
 
 cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork* work, int nwork, size_t smem,
