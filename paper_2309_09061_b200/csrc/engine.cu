@@ -71,6 +71,11 @@ Ctx::Ctx(int dev, cudaStream_t s) : device(dev), st(s) {
 
 Ctx::~Ctx() {
   cudaStreamSynchronize(st);
+  if (up_stream) {
+    cudaStreamSynchronize(up_stream);
+    cudaStreamDestroy(up_stream);
+  }
+  if (up_host) cudaFreeHost(up_host);
   for (auto e : evpool) cudaEventDestroy(e);
   cudaFreeHost(hstage);
   cudaFree(dstage);
@@ -695,6 +700,50 @@ PTree product_tree(BView bx, BView by) {
   bt->finalize();
   P.bt = bt;
   return P;
+}
+
+// Planner-thread epilogue: distinct dense-target operand blocks, and the triple arrays copied to the
+// device on a private stream (overlapping the GPU's basis construction).
+void ptree_prepare(PTree& P, Ctx& C, int nbx, int nby) {
+  const Blocks& B = *P.bt;
+  const int nt = (int)P.ts.size();
+  std::vector<char> seenx(nbx, 0), seeny(nby, 0);
+  for (int b = 0; b < B.nb; ++b) {
+    if (!B.near_leaf(b)) continue;
+    for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
+      if (P.tk[i] == 'a' && !seenx[P.tbx[i]]) { seenx[P.tbx[i]] = 1; P.need_xv.push_back(P.tbx[i]); }
+      if (P.tk[i] == 'b' && !seeny[P.tby[i]]) { seeny[P.tby[i]] = 1; P.need_wy.push_back(P.tby[i]); }
+    }
+  }
+  if (nt == 0) return;
+  const size_t n4 = (size_t)nt * 4, pad = 256;
+  const size_t bytes = 4 * ((n4 + pad - 1) / pad * pad) + nt + pad;
+  if (!C.up_stream) cuda_check(cudaStreamCreateWithFlags(&C.up_stream, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamSynchronize(C.up_stream), "up sync");
+  if (bytes > C.up_cap) {
+    if (C.up_host) cudaFreeHost(C.up_host);
+    C.up_cap = bytes * 2;
+    cuda_check(cudaMallocHost(&C.up_host, C.up_cap), "cudaMallocHost");
+  }
+  const size_t stride = (n4 + pad - 1) / pad * pad;
+  char* h = C.up_host;
+  int* htnode = (int*)h;
+  for (int b = 0; b < B.nb; ++b)
+    for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) htnode[i] = b;
+  memcpy(h + stride, P.ts.data(), n4);
+  memcpy(h + 2 * stride, P.tbx.data(), n4);
+  memcpy(h + 3 * stride, P.tby.data(), n4);
+  memcpy(h + 4 * stride, P.tk.data(), nt);
+  cuda_check(cudaMallocAsync(&P.dev.block, bytes, C.up_stream), "cudaMallocAsync");
+  cuda_check(cudaMemcpyAsync(P.dev.block, h, bytes, cudaMemcpyHostToDevice, C.up_stream), "upload");
+  char* d = (char*)P.dev.block;
+  P.dev.tnode = (int*)d;
+  P.dev.ts = (int*)(d + stride);
+  P.dev.tbx = (int*)(d + 2 * stride);
+  P.dev.tby = (int*)(d + 3 * stride);
+  P.dev.tk = d + 4 * stride;
+  cuda_check(cudaEventCreateWithFlags(&P.dev.ready, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(P.dev.ready, C.up_stream), "event");
 }
 
 // ============================================================================ setup stages

@@ -207,6 +207,9 @@ struct Ctx {
   void drain_prof();
 
   std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
+  cudaStream_t up_stream = nullptr;  // structure uploads from the planner thread
+  char* up_host = nullptr;
+  size_t up_cap = 0;
   Ctx(int dev, cudaStream_t s);
   ~Ctx();
   Ctx& side();
@@ -323,7 +326,17 @@ struct PTree {  // product block tree with the classified triples per node
   std::vector<int> ts;    // middle cluster
   std::vector<char> tk;   // kind 'a' 'b' 'c'
   std::vector<int> tbx, tby;  // block ids of X|ts and Y|sr
+  // filled by the asynchronous planner thread: distinct X / Y blocks feeding dense targets
+  // (kinds a / b) and the triple arrays already copied to the device
+  std::vector<int> need_xv, need_wy;
+  struct Dev {
+    int *tnode = nullptr, *ts = nullptr, *tbx = nullptr, *tby = nullptr;
+    char* tk = nullptr;
+    void* block = nullptr;
+    cudaEvent_t ready = nullptr;
+  } dev;
 };
+void ptree_prepare(PTree& P, Ctx& C, int nbx, int nby);
 
 // ------------------------------------------------------------------ stages
 std::shared_ptr<Tree> make_tree(int n, const long long* start, const long long* stop, const long long* cptr,

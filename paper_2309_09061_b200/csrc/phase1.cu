@@ -280,17 +280,9 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   }
   // memoised leaf products needed by dense targets, and row factors of admissible X blocks
   HostTimer ht1(C, "assemble_xv_rf");
-  std::vector<int> need_xv, need_wy;
-  for (int b = 0; b < B.nb; ++b) {
-    if (!B.near_leaf(b)) continue;
-    for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
-      if (pt.tk[i] == 'a') need_xv.push_back(pt.tbx[i]);
-      if (pt.tk[i] == 'b') need_wy.push_back(pt.tby[i]);
-    }
-  }
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
-  xv_compute(C, sc, x, y, P, need_xv, qr.xv);
-  xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, need_wy, qc.xv);
+  xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
+  xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, pt.need_wy, qc.xv);
   std::vector<Mat> rf(x.h->bt->nb);
   {
     GBatch g;
@@ -319,9 +311,6 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     const Blocks& BX = *x.h->bt;
     const Blocks& BY = *y.h->bt;
     const Tree& mid = x.cols();
-    std::vector<int> tnode(ntrip);
-    for (int b = 0; b < B.nb; ++b)
-      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) tnode[i] = b;
     std::vector<unsigned char> ndense(B.nb), xadm(BX.nb);
     for (int b = 0; b < B.nb; ++b) ndense[b] = B.near_leaf(b) ? 1 : 0;
     const MatRef z{nullptr, 0, 0};
@@ -353,11 +342,12 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     std::vector<int> size_mid(mid.n);
     for (int s = 0; s < mid.n; ++s) size_mid[s] = mid.size(s);
     AsmTables T;
-    T.tnode = C.push(tnode);
-    T.ts = C.push(pt.ts);
-    T.tk = C.push(pt.tk);
-    T.tbx = C.push(pt.tbx);
-    T.tby = C.push(pt.tby);
+    T.tnode = pt.dev.tnode;
+    T.ts = pt.dev.ts;
+    T.tk = pt.dev.tk;
+    T.tbx = pt.dev.tbx;
+    T.tby = pt.dev.tby;
+    if (pt.dev.ready) cuda_check(cudaStreamWaitEvent(C.st, pt.dev.ready, 0), "wait upload");
     T.node_row = C.push(B.row);
     T.node_col = C.push(B.col);
     T.node_dense = C.push(ndense);
@@ -383,6 +373,14 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
     ++C.launches;
+    if (pt.dev.block) {  // the triple arrays are consumed: release them in stream order
+      cudaFreeAsync(pt.dev.block, C.st);
+      pt.dev.block = nullptr;
+    }
+    if (pt.dev.ready) {
+      cudaEventDestroy(pt.dev.ready);
+      pt.dev.ready = nullptr;
+    }
     GBatch g;
     int k2max = 0;
     for (int k : y.cb().rank) k2max = std::max(k2max, k);
@@ -463,8 +461,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr, e4 = nullptr;
   record(C, e0);
   // T^XY is pure structure: build it on a host thread while the GPU computes weights and bases
-  auto pt_future = std::async(std::launch::async, [&x, &y] {
-    return product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+  auto pt_future = std::async(std::launch::async, [&x, &y, &C] {
+    PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+    ptree_prepare(pt, C, x.bt->nb, y.bt->nb);
+    return pt;
   });
   auto keep = std::make_shared<Arena>(C.st);
   Arena sc(C.st);
