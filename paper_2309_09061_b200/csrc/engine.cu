@@ -360,26 +360,21 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   sl.segs.clear();
 }
 
-std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {
-  std::vector<double> res(items.size(), 0.0);
-  if (items.empty()) return res;
-  double* d_out = scratch.alloc(items.size());
-  cuda_check(cudaMemsetAsync(d_out, 0, items.size() * sizeof(double), C.st), "memset");
+void NormBatch::run_async(Ctx& C) {
   size_t smem = 0;
-  std::vector<NormItem> big, small;  // small: single segment, both sides <= 64 (warp Lanczos)
-  for (size_t i = 0; i < items.size(); ++i) {
-    items[i].out = d_out + i;
-    if (items[i].m == 0 || items[i].N == 0) continue;
-    const long long mn = std::min<long long>(items[i].m, items[i].N), mx = std::max<long long>(items[i].m, items[i].N);
-    if (items[i].s1 - items[i].s0 == 1 && mn <= 64 && mx <= 128 && items[i].m * (items[i].N | 1) <= 64 * 65) {
-      small.push_back(items[i]);
+  std::vector<NormItem> big, small;  // small: single segment, both sides <= 64 / 128 (warp Lanczos)
+  for (auto& it : items) {
+    if (it.m == 0 || it.N == 0) continue;
+    const long long mn = std::min<long long>(it.m, it.N), mx = std::max<long long>(it.m, it.N);
+    if (it.s1 - it.s0 == 1 && mn <= 64 && mx <= 128 && it.m * (it.N | 1) <= 64 * 65) {
+      small.push_back(it);
       continue;
     }
-    const bool rowside = (items[i].m <= items[i].N) || (items[i].m <= 160);
-    const long long g = rowside ? items[i].m : items[i].N;
+    const bool rowside = (it.m <= it.N) || (it.m <= 160);
+    const long long g = rowside ? it.m : it.N;
     if (g > 180) throw StructureErr("spectral norm: both sides above 180");
-    smem = std::max(smem, norm_smem(items[i].m, items[i].N));
-    big.push_back(items[i]);
+    smem = std::max(smem, norm_smem(it.m, it.N));
+    big.push_back(it);
   }
   if (!big.empty() || !small.empty()) {
     double fl = 0, by = 0;
@@ -403,12 +398,20 @@ std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {
       ++C.launches;
     }
     C.prof_end(K_NORM, ev, fl, by);
-    std::vector<double> vals = C.read(d_out, items.size());
-    for (size_t i = 0; i < items.size(); ++i) res[i] = vals[i];
   }
   items.clear();
   sl.segs.clear();
-  return res;
+}
+
+std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {
+  std::vector<double> res(items.size(), 0.0);
+  if (items.empty()) return res;
+  double* d_out = scratch.alloc(items.size());
+  cuda_check(cudaMemsetAsync(d_out, 0, items.size() * sizeof(double), C.st), "memset");
+  for (size_t i = 0; i < items.size(); ++i) items[i].out = d_out + i;
+  const size_t n = items.size();
+  run_async(C);
+  return C.read(d_out, n);
 }
 
 std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {

@@ -266,9 +266,9 @@ struct SegList {  // segments of the batch's items; begin() opens (and closes) a
     cur = 0;
     return (int)segs.size();
   }
-  void add(MatRef a, int w, double scale = 1.0) {
+  void add(MatRef a, int w, double scale = 1.0, const double* sdiv = nullptr) {
     if (w > 0) {
-      segs.push_back(Seg{a, w, 0, scale, cur});
+      segs.push_back(Seg{a, w, 0, scale, cur, sdiv});
       cur += w;
     }
   }
@@ -285,6 +285,8 @@ struct NormBatch {
   SegList sl;
   std::vector<NormItem> items;
   std::vector<double> run(Ctx& C, Arena& scratch);  // sync + values
+  // no host synchronisation: each item writes sigma_1 to its preset `out` (caller zero-fills)
+  void run_async(Ctx& C);
 };
 
 struct SvdBatch {

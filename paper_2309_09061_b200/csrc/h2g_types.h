@@ -43,7 +43,8 @@ struct Seg {
   int w;
   int pad_;
   double scale;
-  long long off;  // first stacked line of this segment within its item
+  long long off;       // first stacked line of this segment within its item
+  const double* sdiv;  // optional device scalar: the segment is divided by *sdiv when *sdiv > 0
 };
 
 // R-only QR of vstack(segs[s0:s1]) (M x n); writes min(M, n) x n rows (ld n) to out.

@@ -34,6 +34,14 @@ __device__ __forceinline__ double mref(const MatRef& a, long long i, long long j
   return a.p[i * a.rs + j * a.cs];
 }
 
+// effective scale of a segment: host factor times 1 / (device norm) when given and positive
+// (reference coarsening.py:247-252 `scaled`: divide only when nrm > 0)
+__device__ __forceinline__ double seg_scale(const Seg& sg) {
+  if (!sg.sdiv) return sg.scale;
+  const double d = *sg.sdiv;
+  return d > 0.0 ? sg.scale / d : sg.scale;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -232,7 +240,7 @@ __device__ void load_hpanel(const Seg* segs, int s0, int s1, int m, long long N,
     const Seg sg = segs[s];
     const long long lc = c - off;
     for (int i = lane; i < m; i += 32) {
-      const double val = sg.scale * mref(sg.a, i, lc);
+      const double val = seg_scale(sg) * mref(sg.a, i, lc);
       if (transpose_rows) dst[p * ldd + i] = val; else dst[i * ldd + p] = val;
     }
   }
@@ -256,7 +264,8 @@ __device__ void load_vpanel(const Seg* segs, int s0, int s1, int n, long long M,
     }
     const Seg sg = segs[s];
     const long long lr = r - off;
-    for (int j = lane; j < n; j += 32) P[p * ldp + j] = sg.scale * mref(sg.a, lr, j);
+    const double ssc = seg_scale(sg);
+    for (int j = lane; j < n; j += 32) P[p * ldp + j] = ssc * mref(sg.a, lr, j);
   }
 }
 
@@ -297,7 +306,7 @@ __device__ __forceinline__ void fetch_vrows(PanelFetch& f, const Seg* __restrict
         if (p != cur_p) {
           const Seg& sg = segs[find_seg(segs, s0, s1, r)];
           a = sg.a;
-          sc = sg.scale;
+          sc = seg_scale(sg);
           off = sg.off;
           cur_p = p;
         }
@@ -333,7 +342,7 @@ __device__ __forceinline__ void fetch_hcols(PanelFetch& f, const Seg* __restrict
   if (live) {
     const Seg& sg = segs[find_seg(segs, s0, s1, c)];
     a = sg.a;
-    sc = sg.scale;
+    sc = seg_scale(sg);
     lc = c - sg.off;
   }
   const int tot = kPanel * m;
@@ -968,7 +977,7 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
         for (int s = it.s0; s < it.s1; ++s) {
           const Seg sg = segs[s];
           for (int c = lane; c < sg.w; c += 32)
-            Pn[pr * N + off + c] = (r < m) ? sg.scale * mref(sg.a, r, c) : 0.0;
+            Pn[pr * N + off + c] = (r < m) ? seg_scale(sg) * mref(sg.a, r, c) : 0.0;
           off += sg.w;
         }
       }
@@ -1139,7 +1148,7 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
     for (int q = 0; q < 8; ++q) {
       const int e = e0 + q * 32 + lane;
       if (e < tot) {
-        const double v = sg.scale * a[q];
+        const double v = seg_scale(sg) * a[q];
         A[(e / N) * kNWLd + e % N] = v;
         amax = fmax(amax, fabs(v));
       }

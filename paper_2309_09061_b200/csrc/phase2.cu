@@ -240,7 +240,7 @@ struct CState {
 
 // Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
 static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
-                          const std::vector<double>& cn, const std::vector<double>& nn) {
+                          const std::vector<double>& cn, const double* d_nn) {
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   const BView pv = g.bv();
   const Blocks& pt = *g.h->bt;
@@ -268,8 +268,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   S.reps.assign(pt.nb, CTRef{});
   CT mpool, singles, acc, nxt, tg[8];  // per-level scratch trees (capacity reused)
   std::vector<int> mroot(pt.nb, -1);
-  std::vector<double> msc(pt.nb, 0.0);
   Arena sc(C.st);
+  double* d_msc = sc.alloc(std::max(1, pt.nb));  // sigma_1 of merged reps, per block
 
   // top-down condensation weights Z_t (coarsening.py:231-245)
   for (int lev = 0; lev <= tr.depth; ++lev) {
@@ -430,10 +430,11 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     resolve_jobs(C, sc, J, w1);
     }
 
-    // scales of the flattened merged reps (coarsening.py:316-317)
+    // scales of the flattened merged reps (coarsening.py:316-317), kept on the device
     std::vector<int> lv;
     if (scale && !mblocks.empty()) {
       NormBatch nbat;
+      cuda_check(cudaMemsetAsync(d_msc, 0, sizeof(double) * pt.nb, C.st), "memset");
       for (int b : mblocks) {
         lv.clear();
         mpool.leaves(mroot[b], lv);
@@ -447,10 +448,10 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
         it.s1 = nbat.sl.begin();
         it.m = lv.empty() ? 0 : mpool.mat[lv[0]].r;
         it.N = N;
+        it.out = d_msc + b;
         nbat.items.push_back(it);
       }
-      auto v = nbat.run(C, sc);
-      for (size_t i = 0; i < mblocks.size(); ++i) msc[mblocks[i]] = v[i];
+      nbat.run_async(C);
     }
 
     // truncated SVDs of C_t = [V Z^T | scaled columns] (coarsening.py:294-326)
@@ -466,18 +467,15 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       if (tr.leaf(t)) {
         for (int b : near_cov[t]) {
           const int w = w1.tree->size(pv.col(b));
-          const double s = (scale && nn[b] > 0.0) ? 1.0 / nn[b] : 1.0;
-          sv.sl.add(g.near(b), w, s);
+          sv.sl.add(g.near(b), w, 1.0, scale ? d_nn + b : nullptr);
           N += w;
         }
       } else {
         for (int b : sub_cov[t]) {
           lv.clear();
           mpool.leaves(mroot[b], lv);
-          const double nv = scale ? msc[b] : 0.0;
-          const double s = (scale && nv > 0.0) ? 1.0 / nv : 1.0;
           for (int u : lv) {
-            sv.sl.add(mpool.mat[u].ref(), mpool.mat[u].c, s);
+            sv.sl.add(mpool.mat[u].ref(), mpool.mat[u].c, 1.0, scale ? d_msc + b : nullptr);
             N += mpool.mat[u].c;
           }
         }
@@ -677,31 +675,36 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   return Z;
 }
 
-// sigma_1 of every coupling and nearfield block of g in one batch (coarsening.py:342-351)
-static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, std::vector<double>& nn) {
+// sigma_1 of every coupling (synchronously: their exact zeros skip rows of the Z stacks) and every
+// nearfield block of g (asynchronously into a device array: they only scale SVD segments)
+// (coarsening.py:342-351)
+static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn) {
   const Blocks& B = *g.bt;
-  NormBatch nb;
+  NormBatch nbn, nbc;
   std::vector<int> ids;
   HView v{&g, false};
+  cuda_check(cudaMemsetAsync(d_nn, 0, sizeof(double) * B.nb, C.st), "memset");
   for (int b = 0; b < B.nb; ++b) {
     if (!B.leaf(b)) continue;
     const bool coupling = B.adm[b];
     const int t = B.row[b], s = B.col[b];
     const int m = coupling ? g.rb->rank[t] : B.rows->size(t);
     const int n = coupling ? g.cb->rank[s] : B.cols->size(s);
+    NormBatch& nb = coupling ? nbc : nbn;
     NormItem it{};
     it.s0 = nb.sl.begin();
     nb.sl.add(coupling ? v.coup(b) : v.near(b), n);
     it.s1 = nb.sl.begin();
     it.m = m;
     it.N = n;
+    if (!coupling) it.out = d_nn + b;
     nb.items.push_back(it);
-    ids.push_back(b);
+    if (coupling) ids.push_back(b);
   }
+  nbn.run_async(C);
   cn.assign(B.nb, 0.0);
-  nn.assign(B.nb, 0.0);
-  auto vals = nb.run(C, sc);
-  for (size_t i = 0; i < ids.size(); ++i) (B.adm[ids[i]] ? cn : nn)[ids[i]] = vals[i];
+  auto vals = nbc.run(C, sc);
+  for (size_t i = 0; i < ids.size(); ++i) cn[ids[i]] = vals[i];
 }
 
 // Phase-2 driver (reference coarsening.py:408-422).
@@ -710,8 +713,9 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   Arena sc(C.st);
-  std::vector<double> cn, nn;
-  if (scale) all_norms(C, sc, g, cn, nn);
+  std::vector<double> cn;
+  double* d_nn = sc.alloc(std::max(1, g.bt->nb));
+  if (scale) all_norms(C, sc, g, cn, d_nn);
   auto ar = std::make_shared<Arena>(C.st);
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
@@ -723,14 +727,14 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     std::exception_ptr err;
     std::thread th([&] {
       try {
-        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, nn);
+        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn);
         S.sync();
       } catch (...) {
         err = std::current_exception();
       }
     });
     try {
-      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, nn);
+      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn);
     } catch (...) {
       th.join();
       throw;
