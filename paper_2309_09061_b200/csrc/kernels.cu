@@ -155,56 +155,72 @@ __global__ void __launch_bounds__(kThreads) gsum_kernel(const GOut* __restrict__
 // P (32 x n) the next rows.
 // ---------------------------------------------------------------------------------------------
 
-// Reflector j from column j of P (one lane per panel row) and R[j][j]; run by one whole warp.
-__device__ __forceinline__ void tsqr_make(double* R, int n, double* P, int ldp, int j, double* vb, double* tb) {
-  const int lane = threadIdx.x & 31;
-  const double x = P[lane * ldp + j];
-  const double s = warp_sum(x * x);
-  const double alpha = R[(long long)j * n + j];
-  double v = 0.0, tau = 0.0;
-  if (s != 0.0) {
-    const double nrm = sqrt(alpha * alpha + s);
-    const double beta = alpha >= 0.0 ? -nrm : nrm;
-    tau = (beta - alpha) / beta;
-    v = x / (alpha - beta);
-    if (lane == 0) R[(long long)j * n + j] = beta;
-  }
-  vb[lane] = v;
-  if (lane == 0) *tb = tau;
-}
-
-// [R; P] -> R' (structured TSQR step).  One thread per trailing column applies reflector j with a
-// 32-term dot product and a 32-term update (no shuffles); the warp holding the owner of column j+1
-// then builds reflector j+1 cooperatively (lane per panel row).  One barrier per column; needs
-// n - 1 <= kThreads.  Columns < jstart of P are known to be zero (triangular panels in merges).
+// [R; P] -> R' (structured TSQR step).  A quad of lanes owns one trailing column (lane q of the
+// quad holds panel rows 8q..8q+7): reflector j is applied with an 8-term partial dot product, a
+// 2-step quad reduction and an 8-term update.  Column j+1 is always the first column of quad 0,
+// which right after its update builds reflector j+1 from the same registers' rows (norm, beta,
+// tau, v) -- the per-column critical path is a handful of dependent FMAs.  One barrier per
+// column; columns < jstart of P are known to be zero (triangular panels in merges).
 __device__ void tsqr_absorb(double* R, int n, double* P, int ldp, double* vb /*64*/, double* tb /*2*/,
                             int jstart = 0) {
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  const int quad = tid >> 2, q = tid & 3, r0 = q * 8;
+  constexpr int kQuads = kThreads / 4;
   if (jstart >= n) return;
-  if (warp == ((jstart & (kThreads - 1)) >> 5)) tsqr_make(R, n, P, ldp, jstart, vb + (jstart & 1) * 32, tb + (jstart & 1));
+  auto make = [&](int j, double* v, double* t) {  // quad 0 only
+    double x[8], s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i] = P[(r0 + i) * ldp + j];
+      s = fma(x[i], x[i], s);
+    }
+    s += __shfl_xor_sync(0x0000000fu, s, 1);
+    s += __shfl_xor_sync(0x0000000fu, s, 2);
+    const double alpha = R[(long long)j * n + j];
+    double tau = 0.0, scale = 0.0;
+    if (s != 0.0) {
+      const double nrm = sqrt(alpha * alpha + s);
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+      if (q == 0) R[(long long)j * n + j] = beta;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[r0 + i] = x[i] * scale;
+    if (q == 0) *t = tau;
+  };
+  if (quad == 0) make(jstart, vb + (jstart & 1) * 32, tb + (jstart & 1));
   __syncthreads();
   for (int j = jstart; j < n; ++j) {
     const int cur = j & 1;
     const double tau = tb[cur];
     const double* v = vb + cur * 32;
-    const int c = j + 1 + ((tid - (j + 1)) & (kThreads - 1));  // this thread's column (at most one)
-    if (tau != 0.0 && c < n) {
-      double w0 = R[(long long)j * n + c], w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    if (tau != 0.0) {
+      double vr[8];
 #pragma unroll
-      for (int i = 0; i < kPanel; i += 4) {
-        w0 = fma(v[i], P[i * ldp + c], w0);
-        w1 = fma(v[i + 1], P[(i + 1) * ldp + c], w1);
-        w2 = fma(v[i + 2], P[(i + 2) * ldp + c], w2);
-        w3 = fma(v[i + 3], P[(i + 3) * ldp + c], w3);
+      for (int i = 0; i < 8; ++i) vr[i] = v[r0 + i];
+      const int wq = quad & 7;  // quad within the warp: all lanes of a warp iterate together
+      for (int cb = j + 1 + (quad - wq); cb < n; cb += kQuads) {
+        const int c = cb + wq;
+        const bool act = c < n;
+        double w = 0.0;
+        if (act) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w = fma(vr[i], P[(r0 + i) * ldp + c], w);
+        }
+        w += __shfl_xor_sync(0xffffffffu, w, 1);
+        w += __shfl_xor_sync(0xffffffffu, w, 2);
+        if (act) {
+          const double tw = tau * (w + R[(long long)j * n + c]);
+          if (q == 0) R[(long long)j * n + c] -= tw;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) P[(r0 + i) * ldp + c] -= tw * vr[i];
+        }
       }
-      const double tw = tau * ((w0 + w1) + (w2 + w3));
-      R[(long long)j * n + c] -= tw;
-#pragma unroll 8
-      for (int i = 0; i < kPanel; ++i) P[i * ldp + c] -= tw * v[i];
     }
-    if (j + 1 < n && warp == (((j + 1) & (kThreads - 1)) >> 5)) {
-      __syncwarp();
-      tsqr_make(R, n, P, ldp, j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
+    if (quad == 0 && j + 1 < n) {
+      __syncwarp(0x0000000fu);
+      make(j + 1, vb + (cur ^ 1) * 32, tb + (cur ^ 1));
     }
     __syncthreads();
   }
