@@ -1110,18 +1110,33 @@ __device__ double warp_lambda_max(const double* d, const double* e, int g) {
     // two points per lane (independent recurrences interleaved): 65-way multisection
     const double w = (hi - lo) / 65.0;
     const double x0 = lo + w * (double)(2 * lane + 1), x1 = lo + w * (double)(2 * lane + 2);
+    // Sturm counts without divisions: leading minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2},
+    // rescaled every 8 steps; #sign changes of (1, p_1, .., p_g) = #eigenvalues below x
     int c0 = 0, c1 = 0;
-    double q0 = d[0] - x0, q1 = d[0] - x1;
-    c0 += q0 < 0.0;
-    c1 += q1 < 0.0;
+    double pa0 = 1.0, pb0 = d[0] - x0, pa1 = 1.0, pb1 = d[0] - x1;
+    if (pb0 == 0.0) pb0 = -1e-300;
+    if (pb1 == 0.0) pb1 = -1e-300;
+    c0 += pb0 < 0.0;
+    c1 += pb1 < 0.0;
     for (int i = 1; i < g; ++i) {
       const double e2 = e[i - 1] * e[i - 1];
-      if (q0 == 0.0) q0 = -1e-300;
-      if (q1 == 0.0) q1 = -1e-300;
-      q0 = (d[i] - x0) - e2 / q0;
-      q1 = (d[i] - x1) - e2 / q1;
-      c0 += q0 < 0.0;
-      c1 += q1 < 0.0;
+      double n0 = fma(d[i] - x0, pb0, -e2 * pa0);
+      double n1 = fma(d[i] - x1, pb1, -e2 * pa1);
+      if (n0 == 0.0) n0 = -1e-300 * pb0;
+      if (n1 == 0.0) n1 = -1e-300 * pb1;
+      c0 += (n0 < 0.0) != (pb0 < 0.0);
+      c1 += (n1 < 0.0) != (pb1 < 0.0);
+      pa0 = pb0;
+      pb0 = n0;
+      pa1 = pb1;
+      pb1 = n1;
+      if ((i & 7) == 0) {
+        const double s0 = fabs(pa0) + fabs(pb0), s1 = fabs(pa1) + fabs(pb1);
+        if (s0 > 1e150) { pa0 *= 1e-150; pb0 *= 1e-150; }
+        else if (s0 < 1e-150) { pa0 *= 1e150; pb0 *= 1e150; }
+        if (s1 > 1e150) { pa1 *= 1e-150; pb1 *= 1e-150; }
+        else if (s1 < 1e-150) { pa1 *= 1e150; pb1 *= 1e150; }
+      }
     }
     // points in increasing order: p = 2*lane+1 (x0), 2*lane+2 (x1); find the first with count == g
     const unsigned f0 = __ballot_sync(0xffffffffu, c0 >= g), f1 = __ballot_sync(0xffffffffu, c1 >= g);
@@ -1152,23 +1167,29 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
   const int m = it.m, N = (int)it.N;
   const int kNWLd = N | 1;          // odd row stride: lane-per-row access without bank conflicts
   double amax = 0.0;
-  const int tot = m * N;
-  for (int e0 = 0; e0 < tot; e0 += 8 * 32) {  // 8 independent loads in flight per lane
-    double a[8];
+  const double ssc = seg_scale(sg);
+  const double* ap = sg.a.p;
+  const int ars = sg.a.rs, acs = sg.a.cs;
+  for (int i0 = 0; i0 < m; i0 += 4) {  // 4 rows x up to 4 column chunks of loads in flight per lane
+    double a[4][4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = e0 + q * 32 + lane;
-      a[q] = e < tot ? mref(sg.a, e / N, e % N) : 0.0;
-    }
+    for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = e0 + q * 32 + lane;
-      if (e < tot) {
-        const double v = seg_scale(sg) * a[q];
-        A[(e / N) * kNWLd + e % N] = v;
-        amax = fmax(amax, fabs(v));
+      for (int jj = 0; jj < 4; ++jj) {
+        const int i = i0 + ii, j = lane + 32 * jj;
+        a[ii][jj] = (i < m && j < N) ? ap[i * ars + j * acs] : 0.0;
       }
-    }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int i = i0 + ii, j = lane + 32 * jj;
+        if (i < m && j < N) {
+          const double v = ssc * a[ii][jj];
+          A[i * kNWLd + j] = v;
+          amax = fmax(amax, fabs(v));
+        }
+      }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -1197,37 +1218,75 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
     if (lane < g) vs[lane] = v0;
     if (lane + 32 < g) vs[lane + 32] = v1;
     __syncwarp();
-    // strides of B (h x g): colside B = A (row r, col j), else B = A^T
-    const int br = colside ? kNWLd : 1, bc = colside ? 1 : kNWLd;
-    for (int r = lane; r < h; r += 32) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // 4 independent FMA chains
-      int j = 0;
-      for (; j + 3 < g; j += 4) {
-        a0 = fma(A[r * br + j * bc], vs[j], a0);
-        a1 = fma(A[r * br + (j + 1) * bc], vs[j + 1], a1);
-        a2 = fma(A[r * br + (j + 2) * bc], vs[j + 2], a2);
-        a3 = fma(A[r * br + (j + 3) * bc], vs[j + 3], a3);
+    // B (h x g) = A (colside) or A^T; u = B v (lane per row of B), w = B^T u (lane per column of B)
+    double w0 = 0.0, w1 = 0.0;
+    if (colside) {
+      for (int r = lane; r < h; r += 32) {
+        const double* ar = A + r * kNWLd;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 3 < g; j += 4) {
+          a0 = fma(ar[j], vs[j], a0);
+          a1 = fma(ar[j + 1], vs[j + 1], a1);
+          a2 = fma(ar[j + 2], vs[j + 2], a2);
+          a3 = fma(ar[j + 3], vs[j + 3], a3);
+        }
+        for (; j < g; ++j) a0 = fma(ar[j], vs[j], a0);
+        us[r] = (a0 + a1) + (a2 + a3);
       }
-      for (; j < g; ++j) a0 = fma(A[r * br + j * bc], vs[j], a0);
-      us[r] = (a0 + a1) + (a2 + a3);
+      __syncwarp();
+      double x0 = 0.0, x1 = 0.0;
+      const int c0 = lane < g ? lane : 0, c1 = lane + 32 < g ? lane + 32 : 0;
+      int i = 0;
+      for (; i + 1 < h; i += 2) {
+        const double u = us[i], u2 = us[i + 1];
+        const double* a0p = A + i * kNWLd;
+        w0 = fma(a0p[c0], u, w0);
+        w1 = fma(a0p[c1], u, w1);
+        x0 = fma(a0p[kNWLd + c0], u2, x0);
+        x1 = fma(a0p[kNWLd + c1], u2, x1);
+      }
+      if (i < h) {
+        w0 = fma(A[i * kNWLd + c0], us[i], w0);
+        w1 = fma(A[i * kNWLd + c1], us[i], w1);
+      }
+      w0 += x0;
+      w1 += x1;
+    } else {
+      for (int r = lane; r < h; r += 32) {  // row r of A^T = column r of A
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 3 < g; j += 4) {
+          a0 = fma(A[j * kNWLd + r], vs[j], a0);
+          a1 = fma(A[(j + 1) * kNWLd + r], vs[j + 1], a1);
+          a2 = fma(A[(j + 2) * kNWLd + r], vs[j + 2], a2);
+          a3 = fma(A[(j + 3) * kNWLd + r], vs[j + 3], a3);
+        }
+        for (; j < g; ++j) a0 = fma(A[j * kNWLd + r], vs[j], a0);
+        us[r] = (a0 + a1) + (a2 + a3);
+      }
+      __syncwarp();
+      double x0 = 0.0, x1 = 0.0;
+      const int c0 = lane < g ? lane : 0, c1 = lane + 32 < g ? lane + 32 : 0;
+      const double* r0p = A + c0 * kNWLd;
+      const double* r1p = A + c1 * kNWLd;
+      int i = 0;
+      for (; i + 1 < h; i += 2) {
+        const double u = us[i], u2 = us[i + 1];
+        w0 = fma(r0p[i], u, w0);
+        w1 = fma(r1p[i], u, w1);
+        x0 = fma(r0p[i + 1], u2, x0);
+        x1 = fma(r1p[i + 1], u2, x1);
+      }
+      if (i < h) {
+        w0 = fma(r0p[i], us[i], w0);
+        w1 = fma(r1p[i], us[i], w1);
+      }
+      w0 += x0;
+      w1 += x1;
     }
-    __syncwarp();
-    double w0 = 0.0, w1 = 0.0, x0 = 0.0, x1 = 0.0;
-    const int c0 = lane < g ? lane : 0, c1 = lane + 32 < g ? lane + 32 : 0;
-    int i = 0;
-    for (; i + 1 < h; i += 2) {
-      const double u = us[i], u2 = us[i + 1];
-      w0 = fma(A[i * br + c0 * bc], u, w0);
-      w1 = fma(A[i * br + c1 * bc], u, w1);
-      x0 = fma(A[(i + 1) * br + c0 * bc], u2, x0);
-      x1 = fma(A[(i + 1) * br + c1 * bc], u2, x1);
-    }
-    if (i < h) {
-      w0 = fma(A[i * br + c0 * bc], us[i], w0);
-      w1 = fma(A[i * br + c1 * bc], us[i], w1);
-    }
-    w0 = lane < g ? w0 + x0 : 0.0;
-    w1 = lane + 32 < g ? w1 + x1 : 0.0;
+    w0 = lane < g ? w0 : 0.0;
+    w1 = lane + 32 < g ? w1 : 0.0;
     const double a = warp_sum(w0 * v0 + w1 * v1);
     w0 -= a * v0 + bprev * p0;
     w1 -= a * v1 + bprev * p1;
