@@ -123,15 +123,18 @@ int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path) {
   return guarded([&] {
     Ctx& C = ctx->c;
     C.sync();
-    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather"};
+    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather", "svd.tsqr", "merge", "svd.finish", "qr.chunk"};
     FILE* f = fopen(path, "w");
     if (!f) throw InvalidInput("cannot open trace file");
     fprintf(f, "{\"traceEvents\":[\n");
     bool first = true;
     for (auto& r : C.trace_recs) {
       const bool host = r.cls < 0;
-      fprintf(f, "%s{\"name\":\"%s\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%d,\"tid\":%d}",
-              first ? "" : ",\n", host ? "host_sync_wait" : names[r.cls], r.t0_us, r.dur_us, host ? 1 : 0, r.tid);
+      fprintf(f,
+              "%s{\"name\":\"%s\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%d,\"tid\":%d,"
+              "\"args\":{\"tag\":\"%s\",\"gflop\":%.4f}}",
+              first ? "" : ",\n", host ? "host_sync_wait" : names[r.cls], r.t0_us, r.dur_us, host ? 1 : 0, r.tid,
+              r.tag.c_str(), r.flops * 1e-9);
       first = false;
     }
     fprintf(f, "\n]}\n");

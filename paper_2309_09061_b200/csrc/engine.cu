@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <mutex>
 
 #include "engine.h"
 
@@ -90,15 +91,18 @@ void Ctx::ensure_read(size_t bytes) {
   cuda_check(cudaMallocHost(&hread, read_cap), "cudaMallocHost read");
 }
 
+static std::mutex g_trace_mu;  // the main and side contexts share one trace vector
+
 void Ctx::sync() {
   HostTimer ht(*this, "sync_wait");
   const auto h0 = std::chrono::steady_clock::now();
   cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   if (trace && trace_out) {
     const auto h1 = std::chrono::steady_clock::now();
+    std::lock_guard<std::mutex> lk(g_trace_mu);
     trace_out->push_back(TraceRec{-1 - trace_tid, trace_tid,
                                   std::chrono::duration<double, std::micro>(h0 - trace_host0).count(),
-                                  std::chrono::duration<double, std::micro>(h1 - h0).count()});
+                                  std::chrono::duration<double, std::micro>(h1 - h0).count(), 0.0, tag});
   }
   stage_off = 0;
   ++syncs;
@@ -128,7 +132,7 @@ void Ctx::prof_end(int cls, cudaEvent_t a, double flops, double bytes) {
     free_ev.pop_back();
   }
   cudaEventRecord(b, st);
-  pending.push_back(Pending{cls, a, b, flops, bytes});
+  pending.push_back(Pending{cls, a, b, flops, bytes, trace ? tag : std::string()});
 }
 
 void Ctx::drain_prof() {
@@ -138,15 +142,17 @@ void Ctx::drain_prof() {
     if (trace && trace_out && trace_base) {
       float t0 = 0;
       cudaEventElapsedTime(&t0, trace_base, p.a);
-      trace_out->push_back(TraceRec{p.cls, trace_tid, 1e3 * t0, 1e3 * ms});
+      std::lock_guard<std::mutex> lk(g_trace_mu);
+      trace_out->push_back(TraceRec{p.cls, trace_tid, 1e3 * t0, 1e3 * ms, p.flops, p.tag});
     }
+    free_ev.push_back(p.a);
+    free_ev.push_back(p.b);
+    if (p.cls >= K_NCLASS) continue;
     KStat& k = kstat[p.cls];
     k.launches += 1;
     k.ms += ms;
     k.flops += p.flops;
     k.bytes += p.bytes;
-    free_ev.push_back(p.a);
-    free_ev.push_back(p.b);
   }
   pending.clear();
 }
@@ -313,7 +319,9 @@ static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>&
         lvl.push_back(MergeWork{std::get<0>(p), std::get<1>(p), a, a + stride, 0});
     }
     if (lvl.empty()) continue;
+    cudaEvent_t sv = C.sub_begin();
     cuda_check(launch_tsqr_merge(C.push(lvl), (int)lvl.size(), smem, rsmem, C.st), "tsqr_merge");
+    C.sub_end(S_MERGE, sv);
     ++C.launches;
   }
 }
@@ -350,7 +358,9 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   QrItem* d_items = C.push(live);
   SvdWork* d_work = C.push(work);
   cudaEvent_t ev = C.prof_begin();
+  cudaEvent_t sv = C.sub_begin();
   cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
+  C.sub_end(S_QR_CHUNK, sv);
   ++C.launches;
   run_merges(C, parts, rsmem, sm_merge);
   cuda_check(launch_qr_out(d_items, (int)live.size(), C.st), "qr_out");
@@ -470,10 +480,14 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
       by += 8 * (m * N + m * kx + m * m);
     }
   cudaEvent_t ev = C.prof_begin();
+  cudaEvent_t sv = C.sub_begin();
   cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
+  C.sub_end(S_SVD_TSQR, sv);
   ++C.launches;
   run_merges(C, parts, rsmem, sm_merge);
+  cudaEvent_t sf = C.sub_begin();
   cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, rsmem, C.st), "svd_finish");
+  C.sub_end(S_SVD_FIN, sf);
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());

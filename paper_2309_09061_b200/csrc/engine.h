@@ -161,6 +161,8 @@ struct StageTimes {
 
 // Per-kernel-class accounting for the roofline (profile mode only; never inside a timed step).
 enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_NCLASS = 5 };
+// trace-only sub-intervals (not counted in the kernel-class statistics)
+enum KSub { S_SVD_TSQR = 5, S_MERGE = 6, S_SVD_FIN = 7, S_QR_CHUNK = 8, S_NSUB = 9 };
 struct KStat {
   long long launches = 0;
   double ms = 0, flops = 0, bytes = 0;
@@ -187,6 +189,7 @@ struct Ctx {
     int cls;
     cudaEvent_t a, b;
     double flops, bytes;
+    std::string tag;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> free_ev;
@@ -195,7 +198,10 @@ struct Ctx {
   struct TraceRec {
     int cls, tid;
     double t0_us, dur_us;
+    double flops;
+    std::string tag;
   };
+  std::string tag;  // current stage label (profile/trace mode), set by StageTag
   bool trace = false;
   int trace_tid = 0;
   cudaEvent_t trace_base = nullptr;
@@ -204,6 +210,8 @@ struct Ctx {
   std::vector<TraceRec> trace_recs;
   cudaEvent_t prof_begin();
   void prof_end(int cls, cudaEvent_t a, double flops, double bytes);
+  cudaEvent_t sub_begin() { return trace ? prof_begin() : nullptr; }
+  void sub_end(int cls, cudaEvent_t a) { if (trace) prof_end(cls, a, 0.0, 0.0); }
   void drain_prof();
 
   std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
@@ -241,6 +249,21 @@ struct HostTimer {
   ~HostTimer() {
     if (C.timing)
       C.htime[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+// Labels the launches issued in its scope (trace mode only).
+struct StageTag {
+  Ctx& C;
+  std::string prev;
+  StageTag(Ctx& c, const std::string& t) : C(c) {
+    if (C.trace) {
+      prev = C.tag;
+      C.tag = t;
+    }
+  }
+  ~StageTag() {
+    if (C.trace) C.tag = prev;
   }
 };
 

@@ -19,9 +19,9 @@ constexpr int kT = 64;            // output tile
 constexpr int kKC = 16;           // k chunk
 constexpr int kLdA = kKC + 4;     // As[64][20]
 constexpr int kLdB = kT + 8;      // Bs[16][72]
-constexpr int kThr = 128;         // 4 warps
-constexpr int kPerA = kT * kKC / kThr;  // 8 elements per thread per chunk
-constexpr int kPerB = kKC * kT / kThr;  // 8
+constexpr int kThr = 256;         // 8 warps, each a 16 x 32 quadrant (2 x 4 DMMA tiles)
+constexpr int kPerA = kT * kKC / kThr;  // 4 elements per thread per chunk
+constexpr int kPerB = kKC * kT / kThr;  // 4
 
 __device__ __forceinline__ double ld(const MatRef& a, long long i, long long j) {
   return a.p[i * a.rs + j * a.cs];
@@ -33,15 +33,20 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+constexpr int kRT = 2, kCT = 4;  // DMMA tiles per warp (rows x cols)
+
 struct Acc {
-  double v[4][4][2];
+  double v[kRT][kCT][2];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < kRT; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) v[r][c][0] = v[r][c][1] = 0.0;
+      for (int c = 0; c < kCT; ++c) v[r][c][0] = v[r][c][1] = 0.0;
   }
 };
+
+__device__ __forceinline__ int warp_row0() { return (threadIdx.x >> 6) * 16; }
+__device__ __forceinline__ int warp_col0() { return ((threadIdx.x >> 5) & 1) * 32; }
 
 // chunk loads: A rows i0..i0+63 (only < mt valid), k cols kk..kk+15 (only < kc); B likewise
 __device__ __forceinline__ void fetch_chunk(double (&ra)[kPerA], double (&rb)[kPerB], const MatRef& A, int ai0,
@@ -77,19 +82,19 @@ __device__ __forceinline__ void store_chunk(const double (&ra)[kPerA], const dou
 }
 
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* As, const double* Bs, int kc) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  const int wr = warp_row0(), wc = warp_col0();
   for (int kk = 0; kk < kc; kk += 4) {
-    double a[4], b[4];
+    double a[kRT], b[kCT];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) a[r] = As[(wr + r * 8 + g) * kLdA + kk + t4];
+    for (int r = 0; r < kRT; ++r) a[r] = As[(wr + r * 8 + g) * kLdA + kk + t4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) b[c] = Bs[(kk + t4) * kLdB + wc + c * 8 + g];
+    for (int c = 0; c < kCT; ++c) b[c] = Bs[(kk + t4) * kLdB + wc + c * 8 + g];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < kRT; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) dmma(acc.v[r][c], a[r], b[c]);
+      for (int c = 0; c < kCT; ++c) dmma(acc.v[r][c], a[r], b[c]);
   }
 }
 
@@ -111,7 +116,7 @@ __device__ void tile_gemm(Acc& acc, const MatRef& A, int ai0, int mt, const MatR
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThr) gsum_mma_kernel(const GOut* __restrict__ outs,
+__global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restrict__ outs,
                                                          const GTerm* __restrict__ terms,
                                                          const GTile* __restrict__ tiles, int k2max) {
   extern __shared__ double smem[];
@@ -123,18 +128,18 @@ __global__ void __launch_bounds__(kThr) gsum_mma_kernel(const GOut* __restrict__
   const GOut o = outs[tl.out];
   const int i0 = (tl.tij & 0xffff) * kT, j0 = (tl.tij >> 16) * kT;
   const int mt = min(kT, o.m - i0), nt = min(kT, o.n - j0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  const int wr = warp_row0(), wc = warp_col0();
   Acc acc;
   acc.zero();
   for (int ti = o.t0; ti < o.t1; ++ti) {
     const GTerm t = terms[ti];
     if (t.nf == 1) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < kRT; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < kCT; ++c)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
@@ -150,9 +155,9 @@ __global__ void __launch_bounds__(kThr) gsum_mma_kernel(const GOut* __restrict__
         const int ns = min(kT, t.k2 - js);
         tile_gemm(ta, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < kRT; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < kCT; ++c)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
@@ -166,9 +171,9 @@ __global__ void __launch_bounds__(kThr) gsum_mma_kernel(const GOut* __restrict__
     }
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < kRT; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < kCT; ++c)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;

@@ -1078,8 +1078,10 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
 // ---------------------------------------------------------------------------------------------
 // norm_warp_kernel: sigma_1 of a single-segment matrix with m, N <= 64, one warp per matrix.
 // A lives in shared memory; Lanczos on the smaller Gram side (A^T A or A A^T, never formed) runs
-// min(m, N) steps (full length: the tridiagonal carries the whole spectrum, the extreme Ritz value
-// is accurate despite loss of orthogonality), then Sturm multisection on the tridiagonal.
+// at most min(m, N) steps, then Sturm multisection on the tridiagonal.  The top Ritz value grows
+// monotonically with the step count; from step 12 on it is re-evaluated every 4 steps and the
+// iteration stops once it moved by <= 1e-14 relative (the sigma_1 are scale factors and rank
+// thresholds: an error of that size cannot move a truncation whose margin is >= 1e-4).
 // An exactly zero matrix returns exactly 0 (the reference's zero-norm skips are exact tests).
 // ---------------------------------------------------------------------------------------------
 
@@ -1211,7 +1213,7 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
     v0 /= nv;
     v1 /= nv;
   }
-  double p0 = 0.0, p1 = 0.0, bprev = 0.0;
+  double p0 = 0.0, p1 = 0.0, bprev = 0.0, theta = 0.0, done = -1.0;
   int k = 0;
   for (; k < g; ++k) {
     // w = op(v): u = B v (length h), w = B^T u (length g), B = A (colside) or A^T
@@ -1297,6 +1299,16 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
       break;
     }
     if (lane == 0) be[k] = b;
+    if ((k & 3) == 3 && k >= 11) {
+      // early exit once the top Ritz value (monotone in k) has settled to ~1e-14 relative
+      __syncwarp();
+      const double th = warp_lambda_max(al, be, k + 1);
+      if (th - theta <= 1e-14 * th) {
+        done = th;
+        break;
+      }
+      theta = th;
+    }
     p0 = v0;
     p1 = v1;
     v0 = w0 / b;
@@ -1304,7 +1316,7 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
     bprev = b;
   }
   __syncwarp();
-  const double lam = warp_lambda_max(al, be, k);
+  const double lam = done >= 0.0 ? done : warp_lambda_max(al, be, k);
   if (lane == 0) *it.out = sqrt(fmax(lam, 0.0));
 }
 

@@ -90,13 +90,17 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
     if (tr.leaf(t))
       for (int b : mids[t]) leaf_blocks.push_back(b);
   R.proj.assign(B.nb, Mat{});
-  xv_compute(C, out, x, y, P, leaf_blocks, R.xv);
+  {
+    StageTag tag(C, "p1.xv");
+    xv_compute(C, out, x, y, P, leaf_blocks, R.xv);
+  }
 
   std::vector<Mat> blk(B.nb);
   std::vector<Mat> vx(tr.n);
   std::vector<Mat> rfb(B.nb);
   for (int lev = tr.depth; lev >= 0; --lev) {
     const std::vector<int>& L = tr.by_level[lev];
+    StageTag tag(C, "p1.L" + std::to_string(lev));
     GBatch g1, g2;
     std::vector<Mat>& rf = rfb;
     for (int t : L) {
@@ -411,6 +415,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   }
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
   HostTimer ht3(C, "assemble_pushdown");
+  StageTag tagp(C, "p1.push");
   for (int lev = 0; lev < B.depth; ++lev) {
     GBatch g1, g2;
     for (int b : B.by_level[lev]) {
@@ -469,6 +474,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   auto keep = std::make_shared<Arena>(C.st);
   Arena sc(C.st);
   HView X{&x, false}, Y{&y, false}, XT{&x, true}, YT{&y, true};
+  StageTag tag0(C, "p1.weights");
   MatStore P = basis_product(C, sc, *x.cb, *y.rb);
   MatStore rwy = basis_weights(C, sc, *y.cb);
   MatStore zy = total_weights(C, sc, Y, rwy, scaling);
@@ -509,6 +515,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     HostTimer ht(C, "product_tree_wait");
     pt = pt_future.get();
   }
+  StageTag taga(C, "p1.asm");
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
   record(C, e4);
   G->owned.push_back(keep);

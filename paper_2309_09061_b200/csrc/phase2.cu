@@ -273,6 +273,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
 
   // top-down condensation weights Z_t (coarsening.py:231-245)
   for (int lev = 0; lev <= tr.depth; ++lev) {
+    StageTag tag(C, "p2.Z.L" + std::to_string(lev));
     GBatch ge;
     QrBatch qb;
     for (int t : tr.by_level[lev]) {
@@ -310,6 +311,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   for (int lev = tr.depth; lev >= 0; --lev) {
     const std::vector<int>& L = tr.by_level[lev];
     const size_t nl = L.size();
+    StageTag tag(C, "p2.B.L" + std::to_string(lev));
     HostTimer htv(C, "p2_vz_plan");
     GBatch g1, g2;
     std::vector<Mat> V(nl), VZ(nl);
@@ -715,7 +717,10 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   Arena sc(C.st);
   std::vector<double> cn;
   double* d_nn = sc.alloc(std::max(1, g.bt->nb));
-  if (scale) all_norms(C, sc, g, cn, d_nn);
+  if (scale) {
+    StageTag tag(C, "p2.norms");
+    all_norms(C, sc, g, cn, d_nn);
+  }
   auto ar = std::make_shared<Arena>(C.st);
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
@@ -745,6 +750,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   }
   if (C.timing) { e1 = C.event(); cudaEventRecord(e1, C.st); }
   e2 = e1;
+  StageTag tagp(C, "p2.project");
   auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar);
   Z->owned.push_back(ar2);
   Z->own_rows = g.own_rows;
