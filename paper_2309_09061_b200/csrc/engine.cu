@@ -326,12 +326,79 @@ static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>&
   }
 }
 
+// Register-tile TSQR (tileqr.cu) handles R factors up to 128 columns; H2G_NO_TILE=1 forces the
+// panel kernels (A/B comparisons).
+static bool tile_path(int n) {
+  static const bool off = getenv("H2G_NO_TILE") != nullptr;
+  return !off && n <= 128;
+}
+
+// Tiles (128 lines) per chunk CTA: one tile each while the grid is below ~2 CTAs per SM (latency
+// bound), more once there are many (each extra tile per CTA saves a merge).
+static int tiles_per_cta(long long total_tiles) {
+  const long long slots = 148 * 2;
+  return (int)std::max<long long>(1, std::min<long long>(8, total_tiles / slots));
+}
+
+static void run_tile_merges(Ctx& C, const std::vector<std::tuple<double*, int, int, int>>& parts,
+                            const TileItem* d_items, int nmax) {
+  int maxchunk = 1;
+  for (auto& p : parts) maxchunk = std::max(maxchunk, std::get<2>(p));
+  for (int stride = 1; stride < maxchunk; stride *= 2) {
+    std::vector<TileWork> lvl;
+    for (auto& p : parts) {
+      const int n = std::get<1>(p);
+      double* rb = std::get<0>(p);
+      for (int a = 0; a + stride < std::get<2>(p); a += 2 * stride) {
+        TileWork w{};
+        w.item = std::get<3>(p);
+        w.rinit = rb + (size_t)a * n * n;
+        w.rsrc = rb + (size_t)(a + stride) * n * n;
+        w.rout = rb + (size_t)a * n * n;
+        lvl.push_back(w);
+      }
+    }
+    if (lvl.empty()) continue;
+    cudaEvent_t sv = C.sub_begin();
+    cuda_check(launch_tile_absorb(d_items, nullptr, C.push(lvl), (int)lvl.size(), nmax, C.st), "tile_merge");
+    C.sub_end(S_MERGE, sv);
+    ++C.launches;
+  }
+}
+
 void QrBatch::run(Ctx& C, Arena& scratch) {
   static constexpr long long kChunkRows = 256;  // rows per chunk CTA (8 panels of 32)
   std::vector<QrItem> live;
   bool rsmem = true;
+  long long tile_total = 0;
+  for (auto& it : items)
+    if (it.n > 0 && it.M > 0 && tile_path(it.n)) tile_total += (it.M + 127) / 128;
+  const int tpc = tiles_per_cta(tile_total);
+  std::vector<TileItem> titems;
+  std::vector<TileWork> twork;
+  std::vector<std::tuple<double*, int, int, int>> tparts;
+  int tnmax = 0;
   for (auto& it : items) {
     if (it.n == 0 || it.M == 0) continue;
+    if (tile_path(it.n)) {
+      const long long per = 128LL * tpc;
+      it.nchunk = (int)((it.M + per - 1) / per);
+      it.rbuf = scratch.alloc((size_t)it.nchunk * it.n * it.n);
+      const int ti = (int)titems.size();
+      titems.push_back(TileItem{it.s0, it.s1, it.n, it.n, 0, 0, nullptr});
+      for (int c = 0; c < it.nchunk; ++c) {
+        TileWork w{};
+        w.item = ti;
+        w.l0 = c * per;
+        w.l1 = std::min(it.M, w.l0 + per);
+        w.rout = it.rbuf + (size_t)c * it.n * it.n;
+        twork.push_back(w);
+      }
+      tparts.emplace_back(it.rbuf, it.n, it.nchunk, ti);
+      tnmax = std::max(tnmax, it.n);
+      live.push_back(it);
+      continue;
+    }
     it.nchunk = (int)std::max<long long>(1, (it.M + kChunkRows - 1) / kChunkRows);
     it.rbuf = scratch.alloc((size_t)it.nchunk * it.n * it.n);
     if (qr_smem(it.n, true) > kSmemLimit || merge_smem(it.n, true) > kSmemLimit) rsmem = false;
@@ -342,6 +409,7 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
   for (size_t i = 0; i < live.size(); ++i) {
+    if (tile_path(live[i].n)) continue;
     sm_chunk = std::max(sm_chunk, qr_smem(live[i].n, rsmem));
     sm_merge = std::max(sm_merge, merge_smem(live[i].n, rsmem));
     for (int c = 0; c < live[i].nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
@@ -359,10 +427,19 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   SvdWork* d_work = C.push(work);
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
-  cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
+  if (!work.empty()) {
+    cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
+    ++C.launches;
+  }
+  const TileItem* d_ti = nullptr;
+  if (!twork.empty()) {
+    d_ti = C.push(titems);
+    cuda_check(launch_tile_absorb(d_ti, d_s, C.push(twork), (int)twork.size(), tnmax, C.st), "tile_absorb");
+    ++C.launches;
+  }
   C.sub_end(S_QR_CHUNK, sv);
-  ++C.launches;
   run_merges(C, parts, rsmem, sm_merge);
+  if (!tparts.empty()) run_tile_merges(C, tparts, d_ti, tnmax);
   cuda_check(launch_qr_out(d_items, (int)live.size(), C.st), "qr_out");
   ++C.launches;
   C.prof_end(K_QR, ev, fl, by);
@@ -431,41 +508,80 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   cuda_check(cudaMemsetAsync(d_rank, 0, items.size() * sizeof(int), C.st), "memset");
   static constexpr long long kChunkCols = 256;  // columns per stage-1 CTA (8 panels of 32)
   std::vector<SvdItem> live;
-  bool rsmem = true;
-  size_t sm_tsqr = 0, sm_merge = 0, sm_fin = 0;
+  bool rsmem = true, fin_rsmem = true;
+  size_t sm_tsqr = 0, sm_merge = 0, sm_fin = 0, sm_prep = 0;
+  long long tile_total = 0;
+  for (auto& it : items) {
+    const int n = it.m - std::min(it.m, it.kx);
+    if (it.m > 0 && tile_path(n)) tile_total += std::max<long long>(1, (it.N + 127) / 128);
+  }
+  const int tpc = tiles_per_cta(tile_total);
+  std::vector<TileItem> titems;
+  std::vector<TileWork> twork;
+  std::vector<std::tuple<double*, int, int, int>> tparts;
+  std::vector<int> prep_ids;
+  int tnmax = 0;
   for (size_t i = 0; i < items.size(); ++i) {
     SvdItem& it = items[i];
     it.rank_out = d_rank + i;
     if (it.m == 0) continue;
     const int k1 = std::min(it.m, it.kx);
     const int n = it.m - k1;
+    it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
+    if (svd_finish_smem(it.m, it.kx, true) > kSmemLimit) fin_rsmem = false;
+    if (tile_path(n)) {
+      const long long per = 128LL * tpc;
+      it.nchunk = (int)std::max<long long>(1, (it.N + per - 1) / per);
+      it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
+      it.q2 = (it.kx > 0 && n > 0) ? scratch.alloc((size_t)it.m * n) : nullptr;
+      if (it.kx > 0) {
+        prep_ids.push_back((int)live.size());
+        sm_prep = std::max(sm_prep, svd_prep_smem(it.m, it.kx));
+      }
+      if (n > 0) {
+        const int ti = (int)titems.size();
+        titems.push_back(TileItem{it.s0, it.s1, n, it.kx > 0 ? it.m : n, 1, 0, it.q2});
+        for (int c = 0; c < it.nchunk; ++c) {
+          TileWork w{};
+          w.item = ti;
+          w.l0 = c * per;
+          w.l1 = std::min(it.N, w.l0 + per);
+          w.rout = it.rbuf + (size_t)c * n * n;
+          twork.push_back(w);
+        }
+        tparts.emplace_back(it.rbuf, n, it.nchunk, ti);
+        tnmax = std::max(tnmax, n);
+      }
+      live.push_back(it);
+      continue;
+    }
     it.nchunk = (int)std::max<long long>(1, (it.N + kChunkCols - 1) / kChunkCols);
     it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
-    it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
-    if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || merge_smem(n, true) > kSmemLimit ||
-        svd_finish_smem(it.m, it.kx, true) > kSmemLimit)
-      rsmem = false;
+    if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || merge_smem(n, true) > kSmemLimit) rsmem = false;
     live.push_back(it);
   }
   if (live.empty()) return ranks;
+  if (sm_prep > kSmemLimit) throw StructureErr("svd: protected basis too large for shared memory");
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
   for (size_t i = 0; i < live.size(); ++i) {
     const SvdItem& it = live[i];
     const int n = it.m - std::min(it.m, it.kx);
+    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem));
+    if (sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
+    if (tile_path(n)) continue;
     sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
     sm_merge = std::max(sm_merge, merge_smem(n, rsmem));
-    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, rsmem));
-    if (sm_tsqr > kSmemLimit || sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
+    if (sm_tsqr > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
     for (int c = 0; c < it.nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
     if (n > 0) parts.emplace_back(it.rbuf, n, it.nchunk);
   }
   static const bool dbg_sweeps = getenv("H2G_DEBUG_SWEEPS") != nullptr;
   int* d_sw = nullptr;
   if (dbg_sweeps) {
-    d_sw = (int*)scratch.alloc_bytes(live.size() * sizeof(int));
-    cuda_check(cudaMemsetAsync(d_sw, 0, live.size() * sizeof(int), C.st), "memset");
-    for (size_t i = 0; i < live.size(); ++i) live[i].sweeps_out = d_sw + i;
+    d_sw = (int*)scratch.alloc_bytes(live.size() * 4 * sizeof(int));
+    cuda_check(cudaMemsetAsync(d_sw, 0, live.size() * 4 * sizeof(int), C.st), "memset");
+    for (size_t i = 0; i < live.size(); ++i) live[i].sweeps_out = d_sw + 4 * i;
   }
   Seg* d_s = C.push(sl.segs);
   SvdItem* d_items = C.push(live);
@@ -481,26 +597,45 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     }
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
-  cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
+  if (!work.empty()) {
+    cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
+    ++C.launches;
+  }
+  if (!prep_ids.empty()) {
+    cuda_check(launch_svd_prep(d_items, C.push(prep_ids), (int)prep_ids.size(), sm_prep, C.st), "svd_prep");
+    ++C.launches;
+  }
+  const TileItem* d_ti = nullptr;
+  if (!twork.empty()) {
+    d_ti = C.push(titems);
+    cuda_check(launch_tile_absorb(d_ti, d_s, C.push(twork), (int)twork.size(), tnmax, C.st), "tile_absorb");
+    ++C.launches;
+  }
   C.sub_end(S_SVD_TSQR, sv);
-  ++C.launches;
   run_merges(C, parts, rsmem, sm_merge);
+  if (!tparts.empty()) run_tile_merges(C, tparts, d_ti, tnmax);
   cudaEvent_t sf = C.sub_begin();
-  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, rsmem, C.st), "svd_finish");
+  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, C.st), "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());
   if (dbg_sweeps) {
-    std::vector<int> sw = C.read(d_sw, live.size());
+    std::vector<int> sw = C.read(d_sw, live.size() * 4);
     int mx = 0, mxn = 0;
-    double mean = 0;
-    for (size_t i = 0; i < sw.size(); ++i) {
-      mx = std::max(mx, sw[i]);
-      mean += sw[i];
-      mxn = std::max(mxn, live[i].m - std::min(live[i].m, live[i].kx));
+    double mean = 0, mn = 0, mnr = 0, mk = 0, mN = 0;
+    const size_t ni = live.size();
+    for (size_t i = 0; i < ni; ++i) {
+      mx = std::max(mx, sw[4 * i]);
+      mean += sw[4 * i];
+      mn += sw[4 * i + 1];
+      mnr += sw[4 * i + 2];
+      mk += sw[4 * i + 3];
+      mN += (double)live[i].N;
+      mxn = std::max(mxn, sw[4 * i + 1]);
     }
-    fprintf(stderr, "svd batch: %zu items, n<=%d, sweeps max %d mean %.1f\n", sw.size(), mxn, mx, mean / sw.size());
+    fprintf(stderr, "svd batch: %zu items, n<=%d, mean n %.1f live %.1f k2 %.1f N %.0f, sweeps max %d mean %.1f\n",
+            ni, mxn, mn / ni, mnr / ni, mk / ni, mN / ni, mx, mean / ni);
   }
   items.clear();
   sl.segs.clear();

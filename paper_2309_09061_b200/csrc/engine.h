@@ -34,6 +34,10 @@ cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cu
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
 cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t);
+cudaError_t launch_tile_absorb(const TileItem*, const Seg*, const TileWork*, int nwork, int nmax, cudaStream_t);
+cudaError_t launch_svd_prep(const SvdItem*, const int* ids, int nids, size_t smem, cudaStream_t);
+size_t tile_absorb_smem(int n);
+size_t svd_prep_smem(int m, int kx);
 size_t qr_smem(int n, bool rsmem);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t merge_smem(int n, bool rsmem);

@@ -81,8 +81,27 @@ struct SvdItem {
   double* sig_out;  // optional: sorted singular values of B (capacity m)
   double* rbuf;     // nchunk x (n x n) partial R factors, n = m - min(m, kx)
   double* vws;      // m x kx Householder vectors of V + kx coefficients
-  int* sweeps_out;  // optional diagnostic: Jacobi sweeps used
+  int* sweeps_out;  // optional diagnostic: Jacobi sweeps used, n, live rows, k2
   int pad2_;
+  double* q2;       // tile path with kx > 0: Q_V[:, k1:] (m x n), written by svd_prep_kernel
+};
+
+// Register-tile TSQR (tileqr.cu): one item = one stacked operand reduced to an n x n R factor
+// (n <= 128).  Lines are rows of vstack(segs) (hcols = 0) or columns of hstack(segs)
+// (hcols = 1); each line contributes kdim source entries, projected onto q2 (kdim x n) if given.
+struct TileItem {
+  int s0, s1, n, kdim, hcols, pad_;
+  const double* q2;
+};
+
+// One CTA: absorb lines [l0, l1) (128 per tile) into R (starting from rinit, else zero) and
+// write R to rout; with rsrc the single tile is the n x n factor rsrc (tree merge).
+struct TileWork {
+  int item, pad_;
+  long long l0, l1;
+  const double* rinit;
+  const double* rsrc;
+  double* rout;
 };
 
 // Work units of the SVD pipeline: stage-1 chunk (item, chunk) and tree merges R_a <- [R_a; R_b].

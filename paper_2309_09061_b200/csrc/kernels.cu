@@ -464,7 +464,7 @@ __global__ void qr_out_kernel(const QrItem* __restrict__ items) {
 // orthonormal regardless of the row norms.  Round-robin pairing, one pair per warp at a time.
 // ---------------------------------------------------------------------------------------------
 
-__device__ int jacobi_rows(double* W, int n, int* flag, double* red) {
+__device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   // Rows whose norm is below eps * (largest row norm) can never pass the truncation threshold
   // (thr >= max(rows, cols) eps sigma_1); rotating against them moves the other row by less than
@@ -472,7 +472,7 @@ __device__ int jacobi_rows(double* W, int n, int* flag, double* red) {
   // inputs keep the sweep loop busy orthogonalising rounding noise.
   {
     double mx = 0.0;
-    for (int i = warp; i < n; i += nw) {
+    for (int i = warp; i < nr; i += nw) {
       double s = 0.0;
       for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * n + j], W[(long long)i * n + j], s);
       s = warp_sum(s);
@@ -488,7 +488,7 @@ __device__ int jacobi_rows(double* W, int n, int* flag, double* red) {
     __syncthreads();
   }
   const double frozen = red[nw];
-  const int np = (n + 1) & ~1;  // even number of players, player n (if odd) is a bye
+  const int np = (nr + 1) & ~1;  // even number of players, player nr (if odd) is a bye
   const int npairs = np / 2, m1 = np - 1;
   // convergence threshold sqrt(n) eps (LAPACK dgesvj); tested squared to avoid square roots
   const double tol2 = kEps * kEps * (double)n;
@@ -508,7 +508,7 @@ __device__ int jacobi_rows(double* W, int n, int* flag, double* red) {
         while (xb >= m1) xb -= m1;
         const int a = (q == 0) ? 0 : 1 + xa;
         const int b = 1 + xb;
-        const bool live = q < npairs && a < n && b < n;
+        const bool live = q < npairs && a < nr && b < nr;
         double* ra = W + (long long)(live ? a : 0) * n;
         double* rb = W + (long long)(live ? b : 0) * n;
         double al = 0.0, be = 0.0, ga = 0.0;
@@ -695,9 +695,10 @@ __global__ void __launch_bounds__(kThreads, 3) svd_tsqr_kernel(const SvdItem* __
 // is kept.  perm[c] = original column of column c.  Used as the Jacobi preconditioner
 // (Drmac-Veselic): W Pi = Q1 R1, and the rows of R1 are graded by the pivoting, so one-sided Jacobi
 // on them needs a few sweeps instead of ~15.  Left singular vectors of W^T = Pi x those of R1^T.
-__device__ void qrcp_rows_precondition(double* W, int n, int* perm, double* cn, double* cn0, double* vh,
-                                       double* red, int* ired) {
+__device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, double* cn0, double* vh,
+                                      double* red, int* ired) {
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  double cn0_first = 0.0;
   for (int c = tid; c < n; c += nt) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = fma(W[(long long)i * n + c], W[(long long)i * n + c], s);
@@ -727,6 +728,15 @@ __device__ void qrcp_rows_precondition(double* W, int n, int* perm, double* cn, 
     }
     __syncthreads();
     const int p = ired[nw];
+    {
+      // Early stop: once the trailing block (rows j.., columns j..) has Frobenius norm^2
+      // <= (n - j) max cn <= eps^2 r_00^2 / 4, its rows sit below the Jacobi freeze level
+      // (eps x largest row norm; row 0 of R1 has norm >= |r_00|): they would never be rotated and
+      // can never pass the truncation threshold, so they are left unreduced and excluded.
+      const double bst = cn[p];
+      if (j == 0) cn0_first = bst;
+      else if ((double)(n - j) * bst * 4.0 <= kEps * kEps * cn0_first) return j;
+    }
     if (p != j) {
       for (int i = tid; i < n; i += nt) {
         const double a = W[(long long)i * n + j];
@@ -786,6 +796,7 @@ __device__ void qrcp_rows_precondition(double* W, int n, int* perm, double* cn, 
     }
     __syncthreads();
   }
+  return n;
 }
 
 static constexpr int kFinishThreads = 512;  // Jacobi: more warps = fewer row pairs per warp per step
@@ -822,11 +833,15 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
     __syncthreads();
     // B = R^T Q_B^T: left singular vectors of B = those of R^T.  QRCP preconditioning R Pi = Q1 R1,
     // then the left singular vectors of R^T are Pi x the normalised rows of R1 after row Jacobi.
-    qrcp_rows_precondition(R, n, perm, cn, cn0, vh, jred, ired);
+    const int nr = qrcp_rows_precondition(R, n, perm, cn, cn0, vh, jred, ired);
     for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
     __syncthreads();
-    const int sw = jacobi_rows(R, n, &flag, jred);
-    if (it.sweeps_out && threadIdx.x == 0) *it.sweeps_out = sw;
+    const int sw = jacobi_rows(R, nr, n, &flag, jred);
+    if (it.sweeps_out && threadIdx.x == 0) {
+      it.sweeps_out[0] = sw;
+      it.sweeps_out[1] = n;
+      it.sweeps_out[2] = nr;
+    }
     for (int i = warp; i < n; i += nw) {
       double s = 0.0;
       for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * n + j], R[(long long)i * n + j], s);
@@ -857,6 +872,7 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
     k2 = s_k2;
     if (it.sig_out)
       for (int i = threadIdx.x; i < n; i += blockDim.x) it.sig_out[i] = sig[ord[i]];
+    if (it.sweeps_out && threadIdx.x == 0) it.sweeps_out[3] = k2;
   }
   __syncthreads();
   const int kt = k1 + k2;
