@@ -123,7 +123,7 @@ int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path) {
   return guarded([&] {
     Ctx& C = ctx->c;
     C.sync();
-    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather", "svd.tsqr", "merge", "svd.finish", "qr.chunk"};
+    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather", "svd.tsqr", "merge", "svd.finish", "qr.chunk", "misc"};
     FILE* f = fopen(path, "w");
     if (!f) throw InvalidInput("cannot open trace file");
     fprintf(f, "{\"traceEvents\":[\n");

@@ -579,9 +579,9 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   static const bool dbg_sweeps = getenv("H2G_DEBUG_SWEEPS") != nullptr;
   int* d_sw = nullptr;
   if (dbg_sweeps) {
-    d_sw = (int*)scratch.alloc_bytes(live.size() * 4 * sizeof(int));
-    cuda_check(cudaMemsetAsync(d_sw, 0, live.size() * 4 * sizeof(int), C.st), "memset");
-    for (size_t i = 0; i < live.size(); ++i) live[i].sweeps_out = d_sw + 4 * i;
+    d_sw = (int*)scratch.alloc_bytes(live.size() * 8 * sizeof(int));
+    cuda_check(cudaMemsetAsync(d_sw, 0, live.size() * 8 * sizeof(int), C.st), "memset");
+    for (size_t i = 0; i < live.size(); ++i) live[i].sweeps_out = d_sw + 8 * i;
   }
   Seg* d_s = C.push(sl.segs);
   SvdItem* d_items = C.push(live);
@@ -621,21 +621,25 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());
   if (dbg_sweeps) {
-    std::vector<int> sw = C.read(d_sw, live.size() * 4);
+    std::vector<int> sw = C.read(d_sw, live.size() * 8);
     int mx = 0, mxn = 0;
-    double mean = 0, mn = 0, mnr = 0, mk = 0, mN = 0;
+    double mean = 0, mn = 0, mnr = 0, mk = 0, mN = 0, ph[4] = {0, 0, 0, 0};
     const size_t ni = live.size();
     for (size_t i = 0; i < ni; ++i) {
-      mx = std::max(mx, sw[4 * i]);
-      mean += sw[4 * i];
-      mn += sw[4 * i + 1];
-      mnr += sw[4 * i + 2];
-      mk += sw[4 * i + 3];
+      const int* r = &sw[8 * i];
+      mx = std::max(mx, r[0]);
+      mean += r[0];
+      mn += r[1];
+      mnr += r[2];
+      mk += r[3];
+      for (int q = 0; q < 4; ++q) ph[q] = std::max(ph[q], (double)r[4 + q]);
       mN += (double)live[i].N;
-      mxn = std::max(mxn, sw[4 * i + 1]);
+      mxn = std::max(mxn, r[1]);
     }
-    fprintf(stderr, "svd batch: %zu items, n<=%d, mean n %.1f live %.1f k2 %.1f N %.0f, sweeps max %d mean %.1f\n",
-            ni, mxn, mn / ni, mnr / ni, mk / ni, mN / ni, mx, mean / ni);
+    fprintf(stderr,
+            "svd batch: %zu items, n<=%d, mean n %.1f live %.1f k2 %.1f N %.0f, sweeps max %d mean %.1f | max kcyc "
+            "load %.0f qrcp %.0f jacobi %.0f out %.0f\n",
+            ni, mxn, mn / ni, mnr / ni, mk / ni, mN / ni, mx, mean / ni, ph[0], ph[1], ph[2], ph[3]);
   }
   items.clear();
   sl.segs.clear();
@@ -856,12 +860,19 @@ PTree product_tree(BView bx, BView by) {
 
 // Planner-thread epilogue: distinct dense-target operand blocks, and the triple arrays copied to the
 // device on a private stream (overlapping the GPU's basis construction).
-void ptree_prepare(PTree& P, Ctx& C, int nbx, int nby) {
+void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
   const Blocks& B = *P.bt;
   const int nt = (int)P.ts.size();
-  std::vector<char> seenx(nbx, 0), seeny(nby, 0);
+  const int nbx = BX.nb;
+  std::vector<char> seenx(nbx, 0), seeny(nby, 0), seenf(nbx, 0);
   for (int b = 0; b < B.nb; ++b) {
-    if (!B.near_leaf(b)) continue;
+    if (!B.near_leaf(b)) {
+      for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
+        const int bts = P.tbx[i];
+        if (P.tk[i] == 'a' && BX.adm_leaf(bts) && !seenf[bts]) { seenf[bts] = 1; P.rf_blocks.push_back(bts); }
+      }
+      continue;
+    }
     for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
       if (P.tk[i] == 'a' && !seenx[P.tbx[i]]) { seenx[P.tbx[i]] = 1; P.need_xv.push_back(P.tbx[i]); }
       if (P.tk[i] == 'b' && !seeny[P.tby[i]]) { seeny[P.tby[i]] = 1; P.need_wy.push_back(P.tby[i]); }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -166,7 +167,7 @@ struct StageTimes {
 // Per-kernel-class accounting for the roofline (profile mode only; never inside a timed step).
 enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_NCLASS = 5 };
 // trace-only sub-intervals (not counted in the kernel-class statistics)
-enum KSub { S_SVD_TSQR = 5, S_MERGE = 6, S_SVD_FIN = 7, S_QR_CHUNK = 8, S_NSUB = 9 };
+enum KSub { S_SVD_TSQR = 5, S_MERGE = 6, S_SVD_FIN = 7, S_QR_CHUNK = 8, S_MISC = 9, S_NSUB = 10 };
 struct KStat {
   long long launches = 0;
   double ms = 0, flops = 0, bytes = 0;
@@ -255,6 +256,12 @@ struct HostTimer {
       C.htime[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 };
+
+// H2G_SERIAL=1: run the row and column passes one after the other on the main stream (profiling).
+inline bool serial_passes() {
+  static const bool on = getenv("H2G_SERIAL") != nullptr;
+  return on;
+}
 
 // Labels the launches issued in its scope (trace mode only).
 struct StageTag {
@@ -358,6 +365,7 @@ struct PTree {  // product block tree with the classified triples per node
   // filled by the asynchronous planner thread: distinct X / Y blocks feeding dense targets
   // (kinds a / b) and the triple arrays already copied to the device
   std::vector<int> need_xv, need_wy;
+  std::vector<int> rf_blocks;  // distinct admissible-leaf X blocks of kind-a triples on non-dense targets
   struct Dev {
     int *tnode = nullptr, *ts = nullptr, *tbx = nullptr, *tby = nullptr;
     char* tk = nullptr;
@@ -365,7 +373,7 @@ struct PTree {  // product block tree with the classified triples per node
     cudaEvent_t ready = nullptr;
   } dev;
 };
-void ptree_prepare(PTree& P, Ctx& C, int nbx, int nby);
+void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby);
 
 // ------------------------------------------------------------------ stages
 std::shared_ptr<Tree> make_tree(int n, const long long* start, const long long* stop, const long long* cptr,

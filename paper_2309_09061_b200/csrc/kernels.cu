@@ -464,6 +464,28 @@ __global__ void qr_out_kernel(const QrItem* __restrict__ items) {
 // orthonormal regardless of the row norms.  Round-robin pairing, one pair per warp at a time.
 // ---------------------------------------------------------------------------------------------
 
+// Rotation of the row pair (a, b) with Gram entries al = |a|^2, be = |b|^2, ga = a.b:
+// t = sign(d) 2ga / (|d| + hypot(d, 2ga)), d = be - al (the smaller root of t^2 + 2 zeta t - 1,
+// zeta = d / 2ga; Rutishauser), c = 1 / sqrt(1 + t^2), s = c t.  One sqrt, one division, one rsqrt.
+__device__ __forceinline__ void jacobi_rotation(double al, double be, double ga, double& c, double& sn) {
+  const double d = be - al, g2 = 2.0 * ga;
+  const double ad = fabs(d), ag = fabs(g2);
+  double t;
+  if (ad > 1e150 || ag > 1e150) {  // avoid overflow of d^2 + g2^2
+    const double zeta = d / g2, az = fabs(zeta);
+    const double t0 = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(az, az, 1.0)));
+    t = zeta >= 0.0 ? t0 : -t0;
+  } else {
+    const double r = sqrt(fma(d, d, g2 * g2));
+    t = g2 / (ad + r);
+    if (d < 0.0) t = -t;
+  }
+  c = rsqrt(fma(t, t, 1.0));
+  sn = c * t;
+}
+
+// NPL > 0: rows of length n <= 16 NPL held in registers per half-warp (unrolled); NPL = 0: loops.
+template <int NPL>
 __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   // Rows whose norm is below eps * (largest row norm) can never pass the truncation threshold
@@ -492,54 +514,76 @@ __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
   const int npairs = np / 2, m1 = np - 1;
   // convergence threshold sqrt(n) eps (LAPACK dgesvj); tested squared to avoid square roots
   const double tol2 = kEps * kEps * (double)n;
-  // two row pairs per warp at a time, one per half-warp (16 lanes, 4-step butterflies)
+  // one row pair per half-warp (16 lanes, 4-step butterflies)
   const int half = lane >> 4, hl = lane & 15;
-  const int nslots = 2 * nw;
+  const int slot = 2 * warp + half, nslots = 2 * nw;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int step = 0; step < m1; ++step) {
-      for (int q0 = 2 * warp; q0 < npairs; q0 += nslots) {
-        const int q = q0 + half;
+      for (int q = slot; q < npairs; q += nslots) {
         // circle method: player 0 fixed, players 1..np-1 rotate by `step` (no integer division)
         int xa = q + step;
         if (xa >= m1) xa -= m1;
         int xb = (q == 0 ? 0 : m1 - q) + step;
-        while (xb >= m1) xb -= m1;
+        if (xb >= m1) xb -= m1;
+        if (xb >= m1) xb -= m1;
         const int a = (q == 0) ? 0 : 1 + xa;
         const int b = 1 + xb;
-        const bool live = q < npairs && a < nr && b < nr;
-        double* ra = W + (long long)(live ? a : 0) * n;
-        double* rb = W + (long long)(live ? b : 0) * n;
+        if (a >= nr || b >= nr) continue;  // bye (odd nr): uniform per half-warp
+        double* ra = W + (long long)a * n;
+        double* rb = W + (long long)b * n;
         double al = 0.0, be = 0.0, ga = 0.0;
-        if (live)
+        double xav[NPL > 0 ? NPL : 1], xbv[NPL > 0 ? NPL : 1];
+        if (NPL > 0) {
+#pragma unroll
+          for (int k = 0; k < NPL; ++k) {
+            const int j = hl + 16 * k;
+            xav[k] = j < n ? ra[j] : 0.0;
+            xbv[k] = j < n ? rb[j] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < NPL; ++k) {
+            al = fma(xav[k], xav[k], al);
+            be = fma(xbv[k], xbv[k], be);
+            ga = fma(xav[k], xbv[k], ga);
+          }
+        } else {
           for (int j = hl; j < n; j += 16) {
             const double x = ra[j], y = rb[j];
             al = fma(x, x, al);
             be = fma(y, y, be);
             ga = fma(x, y, ga);
           }
+        }
+        const unsigned hmask = 0xffffu << (16 * half);
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {  // three independent butterflies within the half-warp
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          al += __shfl_xor_sync(hmask, al, o);
+          be += __shfl_xor_sync(hmask, be, o);
+          ga += __shfl_xor_sync(hmask, ga, o);
         }
-        if (live && ga != 0.0 && al > frozen && be > frozen && ga * ga > tol2 * al * be) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double az = fabs(zeta);
-          const double t0 = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(az, az, 1.0)));
-          const double t = zeta >= 0.0 ? t0 : -t0;
-          const double c = rsqrt(fma(t, t, 1.0));
-          const double sn = c * t;
-          for (int j = hl; j < n; j += 16) {
-            const double x = ra[j], y = rb[j];
-            ra[j] = c * x - sn * y;
-            rb[j] = sn * x + c * y;
+        if (ga != 0.0 && al > frozen && be > frozen && ga * ga > tol2 * al * be) {
+          double c, sn;
+          jacobi_rotation(al, be, ga, c, sn);
+          if (NPL > 0) {
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) {
+              const int j = hl + 16 * k;
+              if (j < n) {
+                ra[j] = c * xav[k] - sn * xbv[k];
+                rb[j] = sn * xav[k] + c * xbv[k];
+              }
+            }
+          } else {
+            for (int j = hl; j < n; j += 16) {
+              const double x = ra[j], y = rb[j];
+              ra[j] = c * x - sn * y;
+              rb[j] = sn * x + c * y;
+            }
           }
           if (hl == 0) *flag = 1;
         }
-        __syncwarp();
       }
       __syncthreads();
     }
@@ -827,16 +871,21 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
     for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
   }
   int k2 = 0;
+  long long tk[5] = {clock64(), 0, 0, 0, 0};  // phase timestamps (diagnostic output only)
   if (n > 0 && N > 0) {
     if (rsmem)
       for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
     __syncthreads();
+    tk[1] = clock64();
     // B = R^T Q_B^T: left singular vectors of B = those of R^T.  QRCP preconditioning R Pi = Q1 R1,
     // then the left singular vectors of R^T are Pi x the normalised rows of R1 after row Jacobi.
     const int nr = qrcp_rows_precondition(R, n, perm, cn, cn0, vh, jred, ired);
     for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
     __syncthreads();
-    const int sw = jacobi_rows(R, nr, n, &flag, jred);
+    tk[2] = clock64();
+    const int sw = n <= 64 ? jacobi_rows<4>(R, nr, n, &flag, jred)
+                   : n <= 128 ? jacobi_rows<8>(R, nr, n, &flag, jred) : jacobi_rows<0>(R, nr, n, &flag, jred);
+    tk[3] = clock64();
     if (it.sweeps_out && threadIdx.x == 0) {
       it.sweeps_out[0] = sw;
       it.sweeps_out[1] = n;
@@ -902,6 +951,10 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
     }
   }
   if (threadIdx.x == 0) *it.rank_out = kt;
+  if (it.sweeps_out && threadIdx.x == 0 && tk[3] > 0) {
+    tk[4] = clock64();
+    for (int q = 1; q < 5; ++q) it.sweeps_out[3 + q] = (int)((tk[q] - tk[q - 1]) / 1000);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -285,25 +285,25 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   // memoised leaf products needed by dense targets, and row factors of admissible X blocks
   HostTimer ht1(C, "assemble_xv_rf");
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
-  xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
-  xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, pt.need_wy, qc.xv);
+  {
+    HostTimer hx(C, "asm_xv1");
+    xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
+  }
+  {
+    HostTimer hx(C, "asm_xv2");
+    xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, pt.need_wy, qc.xv);
+  }
   std::vector<Mat> rf(x.h->bt->nb);
   {
+    HostTimer hx(C, "asm_rf");
     GBatch g;
-    for (int b = 0; b < B.nb; ++b) {
-      if (B.near_leaf(b)) continue;
-      const int t = B.row[b];
-      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
-        if (pt.tk[i] != 'a') continue;
-        const int s = pt.ts[i];
-        const int bts = pt.tbx[i];
-        if (!bx.b->adm_leaf(bts) || rf[bts].p) continue;
-        // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
-        Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
-        g.out(m, false);
-        g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
-        rf[bts] = m;
-      }
+    for (int bts : pt.rf_blocks) {  // (planner thread: distinct X blocks of kind-a triples)
+      const int t = x.row(bts), s = x.col(bts);
+      // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
+      Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
+      g.out(m, false);
+      g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
+      rf[bts] = m;
     }
     g.run(C);
   }
@@ -343,6 +343,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       if (cols.leaf(r)) wyleaf[r] = y.cb().leafm(r).ref();
       bcc[r] = qc.bc[r].ref();
     }
+    HostTimer htt(C, "asm_tables");
     std::vector<int> size_mid(mid.n);
     for (int s = 0; s < mid.n; ++s) size_mid[s] = mid.size(s);
     AsmTables T;
@@ -351,6 +352,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     T.tk = pt.dev.tk;
     T.tbx = pt.dev.tbx;
     T.tby = pt.dev.tby;
+    cudaEvent_t sw = C.sub_begin();
     if (pt.dev.ready) cuda_check(cudaStreamWaitEvent(C.st, pt.dev.ready, 0), "wait upload");
     T.node_row = C.push(B.row);
     T.node_col = C.push(B.col);
@@ -376,6 +378,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     T.size_mid = C.push(size_mid);
     GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
+    C.sub_end(S_MISC, sw);
     ++C.launches;
     if (pt.dev.block) {  // the triple arrays are consumed: release them in stream order
       cudaFreeAsync(pt.dev.block, C.st);
@@ -385,6 +388,8 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       cudaEventDestroy(pt.dev.ready);
       pt.dev.ready = nullptr;
     }
+    htt.~HostTimer();
+    new (&htt) HostTimer(C, "asm_outs");
     GBatch g;
     int k2max = 0;
     for (int k : y.cb().rank) k2max = std::max(k2max, k);
@@ -468,7 +473,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   // T^XY is pure structure: build it on a host thread while the GPU computes weights and bases
   auto pt_future = std::async(std::launch::async, [&x, &y, &C] {
     PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
-    ptree_prepare(pt, C, x.bt->nb, y.bt->nb);
+    ptree_prepare(pt, C, *x.bt, y.bt->nb);
     return pt;
   });
   auto keep = std::make_shared<Arena>(C.st);
@@ -485,7 +490,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   // column pass on a side stream driven by a second host thread
   auto keep2 = std::make_shared<Arena>(C.st);
   Induced qr, qc;
-  {
+  if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
+    qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+    qc = induced_rows(C, *keep2, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+  } else {
     Ctx& S = C.side();
     keep2->st = S.st;
     keep2->cross_stream = true;

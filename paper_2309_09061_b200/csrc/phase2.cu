@@ -725,7 +725,10 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
   CState rs, cs;
-  {
+  if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
+    rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn);
+    cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn);
+  } else {
     Ctx& S = C.side();
     ar2->st = S.st;
     ar2->cross_stream = true;
