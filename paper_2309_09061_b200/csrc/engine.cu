@@ -863,6 +863,29 @@ PTree product_tree(BView bx, BView by) {
 void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
   const Blocks& B = *P.bt;
   const int nt = (int)P.ts.size();
+  // order each node's triples c, a, b (stable): the assembly sums kind-a terms into one T and
+  // kind-b terms into one U before applying their shared factor (GOut ka / kb)
+  {
+    std::vector<int> ts2(nt), tbx2(nt), tby2(nt);
+    std::vector<char> tk2(nt);
+    for (int b = 0; b < B.nb; ++b) {
+      int o = P.tptr[b];
+      for (const char kind : {'c', 'a', 'b'})
+        for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i)
+          if (P.tk[i] == kind) {
+            ts2[o] = P.ts[i];
+            tbx2[o] = P.tbx[i];
+            tby2[o] = P.tby[i];
+            tk2[o] = kind;
+            ++o;
+          }
+      if (o != P.tptr[b + 1]) throw StructureErr("product tree: unknown triple kind");
+    }
+    P.ts.swap(ts2);
+    P.tbx.swap(tbx2);
+    P.tby.swap(tby2);
+    P.tk.swap(tk2);
+  }
   const int nbx = BX.nb;
   std::vector<char> seenx(nbx, 0), seeny(nby, 0), seenf(nbx, 0);
   for (int b = 0; b < B.nb; ++b) {

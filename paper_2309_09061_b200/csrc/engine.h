@@ -44,7 +44,6 @@ size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t merge_smem(int n, bool rsmem);
 size_t svd_finish_smem(int m, int kx, bool rsmem);
 size_t norm_smem(int m, long long N);
-size_t gsum_smem(int k2max);
 
 // ------------------------------------------------------------------ structure
 struct Tree {

@@ -116,6 +116,22 @@ __device__ void tile_gemm(Acc& acc, const MatRef& A, int ai0, int mt, const MatR
 
 }  // namespace
 
+// Spill an accumulator into shared memory (rows < nr, cols < nc) with leading dimension ld.
+__device__ __forceinline__ void acc_to_smem(const Acc& a, double* S, int ld, int nr, int nc) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = warp_row0(), wc = warp_col0();
+#pragma unroll
+  for (int r = 0; r < kRT; ++r)
+#pragma unroll
+    for (int c = 0; c < kCT; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+        if (i < nr && j < nc) S[i * ld + j] = a.v[r][c][h];
+      }
+}
+
 __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restrict__ outs,
                                                          const GTerm* __restrict__ terms,
                                                          const GTile* __restrict__ tiles, int k2max) {
@@ -131,10 +147,26 @@ __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restric
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int wr = warp_row0(), wc = warp_col0();
-  Acc acc;
+  Acc acc, aux;  // aux: 3-factor intermediate, or the open nf = 4 / 5 group sum
   acc.zero();
+  int grp = 0;
+  auto flush = [&]() {
+    __syncthreads();  // Ts may still be read by an earlier product
+    if (grp == 4) {   // C += T (mt x ka) * da
+      acc_to_smem(aux, Ts, ldT, kT, o.ka);
+      __syncthreads();
+      tile_gemm(acc, MatRef{Ts, ldT, 1}, 0, mt, o.da, j0, nt, o.ka, 1.0, As, Bs);
+    } else {          // C += ab (mt x kb) * U
+      acc_to_smem(aux, Ts, ldT, o.kb, kT);
+      __syncthreads();
+      tile_gemm(acc, o.ab, i0, mt, MatRef{Ts, ldT, 1}, 0, nt, o.kb, 1.0, As, Bs);
+    }
+    __syncthreads();
+    grp = 0;
+  };
   for (int ti = o.t0; ti < o.t1; ++ti) {
     const GTerm t = terms[ti];
+    if (grp && t.nf != grp) flush();
     if (t.nf == 1) {
 #pragma unroll
       for (int r = 0; r < kRT; ++r)
@@ -147,22 +179,19 @@ __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restric
           }
     } else if (t.nf == 2) {
       tile_gemm(acc, t.a, i0, mt, t.b, j0, nt, t.k, t.alpha, As, Bs);
+    } else if (t.nf == 4) {
+      if (!grp) { aux.zero(); grp = 4; }
+      tile_gemm(aux, t.a, i0, mt, t.b, 0, o.ka, t.k, t.alpha, As, Bs);
+    } else if (t.nf == 5) {
+      if (!grp) { aux.zero(); grp = 5; }
+      tile_gemm(aux, t.a, 0, o.kb, t.b, j0, nt, t.k, t.alpha, As, Bs);
     } else {
       // T = alpha * A[i0:i0+mt, :] * B (mt x k2) into shared memory, 64 columns at a time
       for (int js = 0; js < t.k2; js += kT) {
-        Acc ta;
-        ta.zero();
+        aux.zero();
         const int ns = min(kT, t.k2 - js);
-        tile_gemm(ta, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
-#pragma unroll
-        for (int r = 0; r < kRT; ++r)
-#pragma unroll
-          for (int c = 0; c < kCT; ++c)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
-              if (j < ns) Ts[i * ldT + js + j] = ta.v[r][c][h];
-            }
+        tile_gemm(aux, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
+        acc_to_smem(aux, Ts + js, ldT, kT, ns);
       }
       __syncthreads();
       const MatRef T{Ts, ldT, 1};
@@ -170,6 +199,7 @@ __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restric
       __syncthreads();  // Ts is rewritten by the next 3-factor term
     }
   }
+  if (grp) flush();
 #pragma unroll
   for (int r = 0; r < kRT; ++r)
 #pragma unroll

@@ -25,10 +25,17 @@ struct GTerm {
 };
 
 // One output matrix: C (m x n, row-major, ldc) = (beta ? C : 0) + sum_{t0 <= i < t1} term_i
+// Grouped 3-factor terms (product assembly, reference induced.py:286-307 regrouped):
+//   nf = 4: T (m x ka) += alpha * A B, consecutive terms, flushed once as C += T * da
+//   nf = 5: U (kb x n) += alpha * A B, consecutive terms, flushed once as C += ab * U
+// (the kind-a terms of one target share their right factor, the kind-b terms their left one).
 struct GOut {
   double* c;
   int ldc, m, n, beta;
   int t0, t1;
+  int ka = 0, kb = 0;
+  MatRef da = {nullptr, 0, 0};
+  MatRef ab = {nullptr, 0, 0};
 };
 
 // One 64 x 64 output tile of a GOut.
@@ -151,6 +158,7 @@ struct AsmTables {
   const int* ky_mid;     // rank of V_Y per middle cluster
   const int* kwy_col;    // rank of W_Y per column cluster
   const int* size_mid;   // middle cluster sizes
+  int grouped;           // emit nf = 4 / 5 group terms where the shared factor has rank <= 64
 };
 
 }  // namespace h2g

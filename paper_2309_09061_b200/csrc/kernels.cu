@@ -1,6 +1,6 @@
 // Batched FP64 kernels for the adaptive H^2 product on sm_100a.
 //
-//   gsum_kernel  : grouped small-matrix chain products C (+)= sum alpha * A*B(*D)   (all GEMM work)
+//   (grouped chain products C (+)= sum alpha * A*B(*D): gemm.cu, DMMA)
 //   qr_r_kernel  : R factor of a stacked tall matrix, streamed in 32-row panels    (dense.py:145-150)
 //   svd_*_kernel : protected, QR-preconditioned one-sided Jacobi truncated SVD    (dense.py:77-101,
 //                  induced.py:115-146, coarsening.py:294-326)
@@ -23,9 +23,6 @@ namespace h2g {
 static void init_attributes();
 
 static constexpr int kThreads = 256;
-static constexpr int kTile = 64;   // gsum output tile
-static constexpr int kKc = 16;     // gsum k-chunk
-static constexpr int kLdS = kTile + 2;
 static constexpr int kPanel = 32;  // TSQR / Gram panel rows (one per lane)
 static constexpr int kRawLd = kPanel + 1;  // odd stride of the m x 32 protect panel
 static constexpr double kEps = 2.220446049250313e-16;
@@ -46,108 +43,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-// ---------------------------------------------------------------------------------------------
-// gsum: 64x64 output tile per CTA, 4x4 per thread (rows ty+16r, cols tx+16c), k streamed in
-// 16-wide chunks through shared memory.
-// ---------------------------------------------------------------------------------------------
-
-__device__ __forceinline__ void tile_mma(double (&acc)[4][4], const MatRef& A, int ai0, int mt,
-                                         const MatRef& B, int bj0, int nt, int k, double alpha,
-                                         double* As, double* Bs) {
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (int kk = 0; kk < k; kk += kKc) {
-    const int kc = min(kKc, k - kk);
-    for (int e = tid; e < kTile * kKc; e += kThreads) {
-      const int l = e % kKc, i = e / kKc;
-      As[l * kLdS + i] = (i < mt && l < kc) ? alpha * mref(A, ai0 + i, kk + l) : 0.0;
-    }
-    for (int e = tid; e < kTile * kKc; e += kThreads) {
-      const int j = e % kTile, l = e / kTile;
-      Bs[l * kLdS + j] = (j < nt && l < kc) ? mref(B, kk + l, bj0 + j) : 0.0;
-    }
-    __syncthreads();
-    for (int l = 0; l < kc; ++l) {
-      double a[4], b[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = As[l * kLdS + ty + 16 * r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = Bs[l * kLdS + tx + 16 * c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) gsum_kernel(const GOut* __restrict__ outs,
-                                                        const GTerm* __restrict__ terms,
-                                                        const GTile* __restrict__ tiles,
-                                                        int k2max) {
-  extern __shared__ double smem[];
-  double* As = smem;
-  double* Bs = As + kKc * kLdS;
-  double* Ts = Bs + kKc * kLdS;  // kTile x (k2max + 1)
-  const int ldT = k2max + 1;
-  const GTile tl = tiles[blockIdx.x];
-  const GOut o = outs[tl.out];
-  const int i0 = (tl.tij & 0xffff) * kTile, j0 = (tl.tij >> 16) * kTile;
-  const int mt = min(kTile, o.m - i0), nt = min(kTile, o.n - j0);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-
-  for (int ti = o.t0; ti < o.t1; ++ti) {
-    const GTerm t = terms[ti];
-    if (t.nf == 1) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i = ty + 16 * r, j = tx + 16 * c;
-          if (i < mt && j < nt) acc[r][c] += t.alpha * mref(t.a, i0 + i, j0 + j);
-        }
-    } else if (t.nf == 2) {
-      tile_mma(acc, t.a, i0, mt, t.b, j0, nt, t.k, t.alpha, As, Bs);
-    } else {
-      // T = alpha * A[i0:i0+mt, :] * B  (mt x k2) into shared memory, 64 columns at a time
-      for (int js = 0; js < t.k2; js += kTile) {
-        double tacc[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tacc[r][c] = 0.0;
-        const int ns = min(kTile, t.k2 - js);
-        tile_mma(tacc, t.a, i0, mt, t.b, js, ns, t.k, t.alpha, As, Bs);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int i = ty + 16 * r, j = tx + 16 * c;
-            if (j < ns) Ts[i * ldT + js + j] = tacc[r][c];
-          }
-      }
-      __syncthreads();
-      MatRef T{Ts, ldT, 1};
-      tile_mma(acc, T, 0, mt, t.d, j0, nt, t.k2, 1.0, As, Bs);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = ty + 16 * r, j = tx + 16 * c;
-      if (i < mt && j < nt) {
-        double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
-        *dst = (o.beta ? *dst : 0.0) + acc[r][c];
-      }
-    }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1429,7 +1324,19 @@ __global__ void asm_expand_kernel(AsmTables T, int ntrip, GTerm* __restrict__ te
   g.alpha = 1.0;
   g.pad_ = 0;
   g.d = MatRef{nullptr, 0, 0};
-  if (k == 'a') {  // Y|sr admissible: S_Y, (xv | row factor), (W_Y leaf | Y's basis change)^T
+  if (k == 'a' && T.grouped && T.kwy_col[r] <= 64) {  // T += (xv | row factor) S_Y; flushed * D_r
+    g.nf = 4;
+    g.k = T.ky_mid[s];
+    g.k2 = 0;
+    g.b = T.ycoup[bsr];
+    g.a = dense ? T.xv[bts] : (T.xadm[bts] ? T.rf[bts] : T.rproj[bts]);
+  } else if (k == 'b' && T.grouped && T.kx_row[t] <= 64) {  // U += S_X (W_X,s-side)^T; flushed A_t *
+    g.nf = 5;
+    g.k = T.kwx_mid[s];
+    g.k2 = 0;
+    g.a = T.xcoup[bts];
+    g.b = dense ? mt(T.wyl[bsr]) : mt(T.cproj[bsr]);
+  } else if (k == 'a') {  // Y|sr admissible: S_Y, (xv | row factor), (W_Y leaf | Y's basis change)^T
     g.nf = 3;
     g.k = T.ky_mid[s];
     g.k2 = T.kwy_col[r];
@@ -1479,7 +1386,6 @@ static void init_attributes() {
       // prefer the largest shared-memory carveout so several CTAs fit per SM
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     };
-    opt_in((const void*)gsum_kernel);
     opt_in((const void*)qr_chunk_kernel);
     opt_in((const void*)tsqr_merge_kernel);
     opt_in((const void*)svd_tsqr_kernel);
@@ -1489,23 +1395,12 @@ static void init_attributes() {
   });
 }
 
-size_t gsum_smem(int k2max) {
-  return sizeof(double) * (2 * kKc * kLdS + (k2max > 0 ? (size_t)kTile * (k2max + 1) : 0));
-}
-
 cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
                             cudaStream_t st);
 
 cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
                         cudaStream_t st) {
-  // tensor-pipe (DMMA) version by default; H2G_GSUM_LEGACY=1 selects the DFMA register-tile kernel
-  static const bool legacy = getenv("H2G_GSUM_LEGACY") != nullptr;
-  if (!legacy) return launch_gsum_mma(outs, terms, tiles, ntiles, k2max, st);
-  init_attributes();
-  if (ntiles == 0) return cudaSuccess;
-  const size_t sm = gsum_smem(k2max);
-  gsum_kernel<<<ntiles, kThreads, sm, st>>>(outs, terms, tiles, k2max);
-  return cudaGetLastError();
+  return launch_gsum_mma(outs, terms, tiles, ntiles, k2max, st);
 }
 
 size_t qr_smem(int n, bool rsmem) {

@@ -376,6 +376,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     T.ky_mid = C.push(y.rb().rank);
     T.kwy_col = C.push(y.cb().rank);
     T.size_mid = C.push(size_mid);
+    T.grouped = 1;
     GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
     C.sub_end(S_MISC, sw);
@@ -395,13 +396,24 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     for (int k : y.cb().rank) k2max = std::max(k2max, k);
     for (int k : x.cb().rank) k2max = std::max(k2max, k);
     if (k2max > 256) throw StructureErr("gsum: 3-factor middle dimension above 256");
-    g.k2max = k2max;
+    g.k2max = std::max(k2max, 64);  // group sums T (64 x ka) / U (kb x 64) share the Ts buffer
     double fl = 0.0;
     for (int b = 0; b < B.nb; ++b) {
       const int t = B.row[b], r = B.col[b];
       const bool dense = B.near_leaf(b);
       const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
-      g.outs.push_back(GOut{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]});
+      GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
+      // grouped kind-a / kind-b terms (asm_expand_kernel emits nf = 4 / 5 under the same rule)
+      const int ka = y.cb().rank[r], kb = x.rb().rank[t];
+      if (ka <= 64) {
+        o.ka = ka;
+        o.da = dense ? y.cb().leafm(r).tref() : qc.bc[r].tref();
+      }
+      if (kb <= 64) {
+        o.kb = kb;
+        o.ab = dense ? x.rb().leafm(t).ref() : qr.bc[t].ref();
+      }
+      g.outs.push_back(o);
       if (C.prof)
         for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
           const int s = pt.ts[i];
@@ -415,6 +427,39 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
             fl += 2 * m * k * k2 + 2 * m * k2 * n;
           }
         }
+    }
+    static const bool dbg_asm = getenv("H2G_DEBUG_ASM") != nullptr;
+    if (dbg_asm) {  // output-shape census of the assembly launch (algorithmic vs 64x64-tile work)
+      auto up = [](double v, double q) { return std::ceil(v / q) * q; };
+      double cnt[2] = {0, 0}, mn[2] = {0, 0}, nt[2] = {0, 0}, alg[2] = {0, 0}, pad[2] = {0, 0};
+      for (int b = 0; b < B.nb; ++b) {
+        const int t = B.row[b], r = B.col[b];
+        const int d = B.near_leaf(b) ? 1 : 0;
+        const double m = d ? rows.size(t) : Q.rank[t], n = d ? cols.size(r) : W.rank[r];
+        if (m == 0 || n == 0) continue;
+        cnt[d] += 1;
+        mn[d] += m * n;
+        nt[d] += pt.tptr[b + 1] - pt.tptr[b];
+        const double tiles = up(m, 64) * up(n, 64) / 4096.0;
+        for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+          const int s = pt.ts[i];
+          double k, k2 = 0;
+          if (pt.tk[i] == 'c') k = mid.size(s);
+          else if (pt.tk[i] == 'a') { k = y.rb().rank[s]; k2 = y.cb().rank[r]; }
+          else { k = x.rb().rank[t]; k2 = x.cb().rank[s]; }
+          if (k2 == 0) {
+            alg[d] += 2 * m * n * k;
+            pad[d] += tiles * 2 * 4096 * up(k, 16);
+          } else {
+            alg[d] += 2 * m * k * k2 + 2 * m * k2 * n;
+            pad[d] += tiles * (2 * 64 * up(k2, 64) * up(k, 16) + 2 * 4096 * up(k2, 16));
+          }
+        }
+      }
+      for (int d = 0; d < 2; ++d)
+        fprintf(stderr, "asm %s: %.0f outputs, mean m*n %.0f, mean terms %.1f, alg %.2f GF, tile work %.2f GF\n",
+                d ? "dense" : "coupling", cnt[d], mn[d] / std::max(1.0, cnt[d]), nt[d] / std::max(1.0, cnt[d]),
+                alg[d] * 1e-9, pad[d] * 1e-9);
     }
     g.run_device_terms(C, d_terms, fl);
   }
