@@ -271,20 +271,40 @@ def main():
     stages.update({k: st2[k] for k in ("t2_row", "t2_col", "t2_mat")})
     zr, zc = z.download().row_basis.rank, None
 
-    # end to end through the public API: host H2Matrix in, host H2Matrix out
-    xh = dx.download()
-    yh = xh if dy is dx else dy.download()
-    h2d = dx.packed_bytes() + (0 if dy is dx else dy.packed_bytes())
-    P.multiply_coarsen(xh, yh, eps, ctx=ctx)
+    # end to end through the C-ABI boundary on HOST buffers: X (and Y) in the packed layout in
+    # pinned host memory -> h2g_h2_upload -> multiply -> coarsen -> h2g_h2_download into pinned
+    # host buffers; every step uploads its inputs and downloads Z
+    def pinned_copy(d):
+        out = {}
+        for k, v in d.items():
+            if k.startswith(("rows.", "cols.", "bt.")):
+                continue
+            t = torch.empty(len(v), dtype=torch.float64 if k.endswith("data") else torch.int64, pin_memory=True)
+            a = t.numpy()
+            a[:] = v
+            out[k] = a
+        return out
+
+    def payload(d):  # every host array the step copies (data + offset tables)
+        return sum(v.nbytes for v in d.values())
+
+    xp = pinned_copy(dx.download_packed())
+    yp = None if dy is dx else pinned_copy(dy.download_packed())
+    bt_x = dx.block_tree
+    bt_y = None if dy is dx else dy.block_tree
+    zshape = z.packed_shapes()
+    zout = {k: torch.empty(n, dtype=torch.float64 if k.endswith("data") else torch.int64,
+                           pin_memory=True).numpy() for k, n in zshape.items()}
+    P.multiply_coarsen_packed(xp, bt_x, yp, bt_y, eps, coarse=bt_x, out=zout, ctx=ctx)
     torch.cuda.synchronize()
     e2e_t = []
     for _ in range(max(1, min(args.steps, 3))):
         t0 = time.perf_counter()
-        zh = P.multiply_coarsen(xh, yh, eps, ctx=ctx)
+        zp = P.multiply_coarsen_packed(xp, bt_x, yp, bt_y, eps, coarse=bt_x, out=zout, ctx=ctx)
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = reduce_max(sum(e2e_t) / len(e2e_t), torch.device("cuda", local))
-    from paper_2309_09061_b200.h2 import storage_bytes
-    d2h = storage_bytes(zh)
+    h2d = payload(xp) + (payload(yp) if yp is not None else 0)
+    d2h = payload(zp)
 
     # roofline: dominant kernel class by device time in the profiled step
     peak_fp64 = fp64_peak_tflops()

@@ -16,7 +16,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # GPU entry points import the native binding lazily (the CPU test tier imports this package)
-    if name in ("multiply", "coarsen", "recompress", "multiply_coarsen"):
+    if name in ("multiply", "coarsen", "recompress", "multiply_coarsen", "multiply_coarsen_packed"):
         from . import api
         return getattr(api, name)
     if name in ("Context", "DeviceH2", "default_context"):

@@ -18,7 +18,7 @@ from .errors import InvalidInputError
 from .h2 import H2Matrix
 from .trees import BlockTree, same_cluster_tree
 
-__all__ = ["multiply", "coarsen", "recompress", "multiply_coarsen"]
+__all__ = ["multiply", "coarsen", "recompress", "multiply_coarsen", "multiply_coarsen_packed"]
 
 
 def _ctx(ctx):
@@ -93,3 +93,18 @@ def multiply_coarsen(x, y, tol: float, *, coarse: BlockTree | None = None, max_r
     g = multiply(dx, dy, tol, max_rank=max_rank, ctx=ctx)
     z = coarsen(g, coarse if coarse is not None else dx.block_tree, tol, max_rank=max_rank, ctx=ctx)
     return z.download() if hx else z
+
+
+def multiply_coarsen_packed(xp: dict, x_tree: BlockTree, yp: dict | None = None, y_tree: BlockTree | None = None,
+                            tol: float = 0.0, *, coarse: BlockTree | None = None, max_rank: int | None = None,
+                            out: dict | None = None, ctx: Context | None = None) -> dict:
+    """The product on HOST buffers in the packed layout (packed.py; the arrays the C ABI
+    h2g_h2_upload / h2g_h2_download take): upload X (and Y; None = Y is X), multiply, coarsen onto
+    `coarse` (default X's block tree), download Z into `out` (preallocated, e.g. pinned, arrays of
+    DeviceH2.packed_shapes() length) or fresh arrays.  Z's block tree is `coarse`."""
+    _check_tol(tol)
+    ctx = _ctx(ctx)
+    dx = DeviceH2.upload_packed(xp, x_tree, ctx)
+    dy = dx if yp is None else DeviceH2.upload_packed(yp, y_tree if y_tree is not None else x_tree, ctx)
+    z = multiply_coarsen(dx, dy, tol, coarse=coarse, max_rank=max_rank, ctx=ctx)
+    return z.download_packed(out)

@@ -615,7 +615,9 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   run_merges(C, parts, rsmem, sm_merge);
   if (!tparts.empty()) run_tile_merges(C, tparts, d_ti, tnmax);
   cudaEvent_t sf = C.sub_begin();
-  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, C.st), "svd_finish");
+  int fin_nmax = 0;
+  for (auto& it : live) fin_nmax = std::max(fin_nmax, it.m - std::min(it.m, it.kx));
+  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, fin_nmax, C.st), "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);

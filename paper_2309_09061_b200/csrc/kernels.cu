@@ -738,13 +738,13 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
   return n;
 }
 
-static constexpr int kFinishThreads = 512;  // Jacobi: more warps = fewer row pairs per warp per step
-
-__global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
+// NT = 512 for n <= 64, 1024 above: one Jacobi row pair per half-warp per step (n <= 128)
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
   extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
-  __shared__ double jred[kFinishThreads / 32 + 2];
+  __shared__ double jred[NT / 32 + 2];
   const SvdItem it = items[blockIdx.x];
   const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
   const long long N = it.N;
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(kFinishThreads) svd_finish_kernel(const SvdIte
   int* perm = (int*)(vh + n);                // n ints
   int* iperm = perm + n;                     // n ints
   double* R = rsmem ? vh + n + n + 1 : it.rbuf;
-  __shared__ int ired[kFinishThreads / 32 + 2];
+  __shared__ int ired[NT / 32 + 2];
   if (kx > 0) {
     for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
     for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
@@ -1389,7 +1389,8 @@ static void init_attributes() {
     opt_in((const void*)qr_chunk_kernel);
     opt_in((const void*)tsqr_merge_kernel);
     opt_in((const void*)svd_tsqr_kernel);
-    opt_in((const void*)svd_finish_kernel);
+    opt_in((const void*)svd_finish_kernel<512>);
+    opt_in((const void*)svd_finish_kernel<1024>);
     opt_in((const void*)norm_kernel);
     opt_in((const void*)norm_warp_kernel);
   });
@@ -1455,10 +1456,11 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
   return cudaGetLastError();
 }
 
-cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, cudaStream_t st) {
+cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, int nmax, cudaStream_t st) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
-  svd_finish_kernel<<<nitems, kFinishThreads, smem, st>>>(items, rsmem ? 1 : 0);
+  if (nmax > 64) svd_finish_kernel<1024><<<nitems, 1024, smem, st>>>(items, rsmem ? 1 : 0);
+  else svd_finish_kernel<512><<<nitems, 512, smem, st>>>(items, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -147,20 +147,30 @@ class DeviceH2:
 
     @classmethod
     def upload(cls, g: H2Matrix, ctx: Context | None = None) -> "DeviceH2":
+        return cls.upload_packed(pack_h2(g), g.block_tree, ctx, share=g.row_basis is g.col_basis)
+
+    @classmethod
+    def upload_packed(cls, d: dict, block_tree: BlockTree, ctx: Context | None = None, *,
+                      share: bool = False) -> "DeviceH2":
+        """Upload from the packed layout (packed.py keys rb.*, cb.*, coup_*, near_*) over the
+        C ABI h2g_h2_upload.  Host arrays are copied as given; pinned arrays (e.g.
+        torch.empty(..., pin_memory=True).numpy()) transfer at full link bandwidth."""
         ctx = ctx or default_context()
-        d = pack_h2(g)
-        share = g.row_basis is g.col_basis
         a = {k: (N.f64(v) if k.endswith("data") else N.i64(v)) for k, v in d.items()
              if not k.startswith(("rows.", "cols.", "bt."))}
+        if share and "cb.rank" not in a:
+            for k in ("rank", "leaf_off", "xfer_off", "data"):
+                a["cb." + k] = a["rb." + k]
+        g = block_tree
         h = N.P()
         N.check(ctx.lib.h2g_h2_upload(
-            ctx.h, ctx.blocks(g.block_tree),
+            ctx.h, ctx.blocks(g),
             a["rb.rank"][1], a["rb.leaf_off"][1], a["rb.xfer_off"][1], a["rb.data"][1], len(a["rb.data"][0]),
             a["cb.rank"][1], a["cb.leaf_off"][1], a["cb.xfer_off"][1], a["cb.data"][1], len(a["cb.data"][0]),
             1 if share else 0,
             a["coup_off"][1], a["coup_data"][1], len(a["coup_data"][0]),
             a["near_off"][1], a["near_data"][1], len(a["near_data"][0]), C.byref(h)))
-        return cls(ctx, h, g.block_tree, g.block_tree.rows, g.block_tree.cols)
+        return cls(ctx, h, g, g.rows, g.cols)
 
     def sizes(self):
         out = np.zeros(8, np.int64)
@@ -182,18 +192,34 @@ class DeviceH2:
             self._bt = BlockTree(self.rows, self.cols, row, col, kids, adm.astype(bool))
         return self._bt
 
-    def to_packed(self) -> dict:
+    def packed_shapes(self) -> dict:
+        """Array lengths of the packed layout of this matrix (keys as in packed.py)."""
         s = self.sizes()
         nb, nr, nc = int(s[0]), int(s[1]), int(s[2])
         d = {}
         for p, n, ln in (("rb.", nr, s[3]), ("cb.", nc, s[4])):
-            d[p + "rank"] = np.zeros(n, np.int64)
-            d[p + "leaf_off"] = np.zeros(n, np.int64)
-            d[p + "xfer_off"] = np.zeros(n, np.int64)
-            d[p + "data"] = np.zeros(int(ln))
-        d["coup_off"], d["coup_data"] = np.zeros(nb, np.int64), np.zeros(int(s[5]))
-        d["near_off"], d["near_data"] = np.zeros(nb, np.int64), np.zeros(int(s[6]))
+            d[p + "rank"] = d[p + "leaf_off"] = d[p + "xfer_off"] = n
+            d[p + "data"] = int(ln)
+        d["coup_off"], d["coup_data"] = nb, int(s[5])
+        d["near_off"], d["near_data"] = nb, int(s[6])
+        return d
 
+    def download_packed(self, out: dict | None = None) -> dict:
+        """Download into the packed layout over the C ABI h2g_h2_download (device gather, one
+        copy per family).  `out` may hold preallocated (e.g. pinned) arrays of at least
+        packed_shapes() length; float64 for *data, int64 otherwise."""
+        shp = self.packed_shapes()
+        d = {}
+        for k, n in shp.items():
+            a = None if out is None else out.get(k)
+            dt = np.float64 if k.endswith("data") else np.int64
+            if a is None or a.dtype != dt or a.size < n or not a.flags.c_contiguous:
+                a = np.zeros(n, dt)
+            d[k] = a[:n]
+        self._download_into(d)
+        return d
+
+    def _download_into(self, d: dict):
         def ip(k):
             return d[k].ctypes.data_as(N.I64P)
 
@@ -204,6 +230,9 @@ class DeviceH2:
             self.ctx.h, self.h, ip("rb.rank"), ip("rb.leaf_off"), ip("rb.xfer_off"), fp("rb.data"),
             ip("cb.rank"), ip("cb.leaf_off"), ip("cb.xfer_off"), fp("cb.data"),
             ip("coup_off"), fp("coup_data"), ip("near_off"), fp("near_data")))
+
+    def to_packed(self) -> dict:
+        d = self.download_packed()
         bt = self.block_tree
         f = bt.flat()
         d["bt.row"], d["bt.col"] = f["row"], f["col"]

@@ -164,3 +164,24 @@ def test_native_library_loaded_from_repo():
     P.multiply_coarsen(x, y, 1e-3)
     maps = open("/proc/self/maps").read()
     assert os.path.realpath(_native.LIB_PATH) in maps
+
+
+def test_packed_host_buffer_path():
+    """multiply_coarsen_packed (packed host buffers over the C ABI) equals the object path."""
+    P = _P()
+    import torch
+    from paper_2309_09061_b200.packed import pack_h2, unpack_h2
+    d = load("rand_s0_tol1e-3")
+    x, y, eps = _inputs(d)
+    z = P.multiply_coarsen(x, y, eps)
+    xp, yp = pack_h2(x), pack_h2(y)
+    pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in xp.items() if k.endswith("data")}
+    xp.update(pinned)
+    zp = P.multiply_coarsen_packed(xp, x.block_tree, yp, y.block_tree, eps)
+    zp.update({"bt.row": d["x/bt.row"], "bt.col": d["x/bt.col"], "bt.child_ptr": d["x/bt.child_ptr"],
+               "bt.child_idx": d["x/bt.child_idx"], "bt.adm": d["x/bt.adm"]})
+    z2 = unpack_h2(zp, rows=x.block_tree.rows, cols=x.block_tree.cols)
+    assert list(z2.row_basis.rank) == list(z.row_basis.rank)
+    v = np.random.default_rng(3).standard_normal(x.shape[1])
+    from paper_2309_09061_b200.h2 import h2_matvec_host
+    assert rel(h2_matvec_host(z2, v), h2_matvec_host(z, v)) <= 1e-13
