@@ -489,6 +489,100 @@ __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
   return 40;
 }
 
+// Octet variant: one row pair per 8 lanes (64 pairs per 512-thread CTA, i.e. n <= 128), NPL =
+// ceil(n / 8) entries per lane.  Against the half-warp version it halves the lanes per pair, so
+// every step is one round and the three butterflies cost 3 levels per 4 pairs instead of 4 levels
+// per 2 -- the step is then bound by the FP64 pipe rather than by shuffles and issue overhead.
+template <int NPL>
+__device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  {
+    double mx = 0.0;
+    for (int i = warp; i < nr; i += nw) {
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * n + j], W[(long long)i * n + j], s);
+      s = warp_sum(s);
+      mx = fmax(mx, s);
+    }
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < nw; ++w) m = fmax(m, red[w]);
+      red[nw] = m * kEps * kEps;
+    }
+    __syncthreads();
+  }
+  const double frozen = red[nw];
+  const int np = (nr + 1) & ~1;
+  const int npairs = np / 2, m1 = np - 1;
+  const double tol2 = kEps * kEps * (double)n;
+  const int q = threadIdx.x >> 3, ol = lane & 7;
+  const unsigned omask = 0xffu << (lane & 24);
+  const bool act = q < npairs;
+  // circle method positions of this octet's pair, advanced by one per step (no divisions)
+  int xa = q, xb = q == 0 ? 0 : m1 - q;
+  if (xb >= m1) xb -= m1;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int step = 0; step < m1; ++step) {
+      const int a = (q == 0) ? 0 : 1 + xa;
+      const int b = 1 + xb;
+      if (act && a < nr && b < nr) {
+        double* ra = W + a * n;
+        double* rb = W + b * n;
+        double x[NPL], y[NPL];
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+          const int j = ol + 8 * k;
+          x[k] = j < n ? ra[j] : 0.0;
+          y[k] = j < n ? rb[j] : 0.0;
+        }
+        double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NPL; k += 2) {
+          al0 = fma(x[k], x[k], al0);
+          be0 = fma(y[k], y[k], be0);
+          ga0 = fma(x[k], y[k], ga0);
+          if (k + 1 < NPL) {
+            al1 = fma(x[k + 1], x[k + 1], al1);
+            be1 = fma(y[k + 1], y[k + 1], be1);
+            ga1 = fma(x[k + 1], y[k + 1], ga1);
+          }
+        }
+        double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(omask, al, o);
+          be += __shfl_xor_sync(omask, be, o);
+          ga += __shfl_xor_sync(omask, ga, o);
+        }
+        if (ga != 0.0 && al > frozen && be > frozen && ga * ga > tol2 * al * be) {
+          double c, sn;
+          jacobi_rotation(al, be, ga, c, sn);
+#pragma unroll
+          for (int k = 0; k < NPL; ++k) {
+            const int j = ol + 8 * k;
+            if (j < n) {
+              ra[j] = c * x[k] - sn * y[k];
+              rb[j] = sn * x[k] + c * y[k];
+            }
+          }
+          if (ol == 0) *flag = 1;
+        }
+      }
+      if (++xa == m1) xa = 0;
+      if (++xb == m1) xb = 0;
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) return sweep + 1;
+  }
+  return 40;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Truncated SVD pipeline (see SvdItem), split so one wide matrix spreads over many CTAs:
 //   svd_tsqr_kernel   one CTA per (item, column chunk): Householder QR of the protected V,
@@ -738,9 +832,10 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
   return n;
 }
 
-// NT = 512 for n <= 64, 1024 above: one Jacobi row pair per half-warp per step (n <= 128)
-template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
+// NPLO: octet-Jacobi entries per lane (8: n <= 64, 16: n <= 128), 0: half-warp loop (n > 128)
+static constexpr int NT = 512;
+template <int NPLO>
+__global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
   extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
@@ -778,8 +873,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) svd_finish_kernel(const SvdItem
     for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
     __syncthreads();
     tk[2] = clock64();
-    const int sw = n <= 64 ? jacobi_rows<4>(R, nr, n, &flag, jred)
-                   : n <= 128 ? jacobi_rows<8>(R, nr, n, &flag, jred) : jacobi_rows<0>(R, nr, n, &flag, jred);
+    const int sw = (NPLO > 0 && n <= 8 * NPLO) ? jacobi_rows_oct<(NPLO > 0 ? NPLO : 1)>(R, nr, n, &flag, jred)
+                                                : jacobi_rows<0>(R, nr, n, &flag, jred);
     tk[3] = clock64();
     if (it.sweeps_out && threadIdx.x == 0) {
       it.sweeps_out[0] = sw;
@@ -1389,8 +1484,9 @@ static void init_attributes() {
     opt_in((const void*)qr_chunk_kernel);
     opt_in((const void*)tsqr_merge_kernel);
     opt_in((const void*)svd_tsqr_kernel);
-    opt_in((const void*)svd_finish_kernel<512>);
-    opt_in((const void*)svd_finish_kernel<1024>);
+    opt_in((const void*)svd_finish_kernel<0>);
+    opt_in((const void*)svd_finish_kernel<8>);
+    opt_in((const void*)svd_finish_kernel<16>);
     opt_in((const void*)norm_kernel);
     opt_in((const void*)norm_warp_kernel);
   });
@@ -1459,8 +1555,9 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
 cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, int nmax, cudaStream_t st) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
-  if (nmax > 64) svd_finish_kernel<1024><<<nitems, 1024, smem, st>>>(items, rsmem ? 1 : 0);
-  else svd_finish_kernel<512><<<nitems, 512, smem, st>>>(items, rsmem ? 1 : 0);
+  if (nmax <= 64) svd_finish_kernel<8><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
+  else if (nmax <= 128) svd_finish_kernel<16><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
+  else svd_finish_kernel<0><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
   return cudaGetLastError();
 }
 
