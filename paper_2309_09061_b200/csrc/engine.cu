@@ -333,11 +333,34 @@ static bool tile_path(int n) {
   return !off && n <= 128;
 }
 
-// Tiles (128 lines) per chunk CTA: one tile each while the grid is below ~2 CTAs per SM (latency
-// bound), more once there are many (each extra tile per CTA saves a merge).
-static int tiles_per_cta(long long total_tiles) {
+// Tiles (128 lines) per chunk CTA.  Time model in units of one tile absorb, `slots` concurrent
+// CTAs: chunk stage ceil(ctas / slots) x tpc, then each pairwise merge level ceil(merges / slots).
+// Pick tpc in {1, 2, 4, 8} minimising it (few items: many short CTAs; many items: fewer merges).
+static int tiles_per_cta(const std::vector<long long>& lines) {
   const long long slots = 148 * 2;
-  return (int)std::max<long long>(1, std::min<long long>(8, total_tiles / slots));
+  int best = 1;
+  double bcost = 1e300;
+  for (int tpc = 1; tpc <= 8; tpc *= 2) {
+    std::vector<long long> ch;
+    long long ctas = 0;
+    for (long long M : lines) {
+      ch.push_back(std::max<long long>(1, (M + 128LL * tpc - 1) / (128LL * tpc)));
+      ctas += ch.back();
+    }
+    double cost = std::ceil((double)ctas / slots) * tpc;
+    for (;;) {  // merge levels: every item with c > 1 partial factors merges floor(c / 2) pairs
+      long long merges = 0;
+      for (long long& c : ch)
+        if (c > 1) {
+          merges += c / 2;
+          c = (c + 1) / 2;
+        }
+      if (!merges) break;
+      cost += std::ceil((double)merges / slots);
+    }
+    if (cost < bcost - 1e-9) { bcost = cost; best = tpc; }
+  }
+  return best;
 }
 
 static void run_tile_merges(Ctx& C, const std::vector<std::tuple<double*, int, int, int>>& parts,
@@ -370,10 +393,10 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   static constexpr long long kChunkRows = 256;  // rows per chunk CTA (8 panels of 32)
   std::vector<QrItem> live;
   bool rsmem = true;
-  long long tile_total = 0;
+  std::vector<long long> tile_lines;
   for (auto& it : items)
-    if (it.n > 0 && it.M > 0 && tile_path(it.n)) tile_total += (it.M + 127) / 128;
-  const int tpc = tiles_per_cta(tile_total);
+    if (it.n > 0 && it.M > 0 && tile_path(it.n)) tile_lines.push_back(it.M);
+  const int tpc = tiles_per_cta(tile_lines);
   std::vector<TileItem> titems;
   std::vector<TileWork> twork;
   std::vector<std::tuple<double*, int, int, int>> tparts;
@@ -405,6 +428,18 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
     live.push_back(it);
   }
   if (live.empty()) { items.clear(); sl.segs.clear(); return; }
+  static const bool dbg_qr = getenv("H2G_DEBUG_SWEEPS") != nullptr;
+  if (dbg_qr) {
+    double mn = 0, mM = 0, mc = 0;
+    int mxn = 0, mxc = 0;
+    for (auto& it : live) {
+      mn += it.n; mM += (double)it.M; mc += it.nchunk;
+      mxn = std::max(mxn, it.n); mxc = std::max(mxc, it.nchunk);
+    }
+    const double ni = (double)live.size();
+    fprintf(stderr, "qr batch: %zu items, n mean %.1f max %d, M mean %.0f, chunks mean %.1f max %d, tiles/cta %d\n",
+            live.size(), mn / ni, mxn, mM / ni, mc / ni, mxc, tpc);
+  }
   size_t sm_chunk = 0, sm_merge = 0;
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
@@ -510,12 +545,12 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<SvdItem> live;
   bool rsmem = true, fin_rsmem = true;
   size_t sm_tsqr = 0, sm_merge = 0, sm_fin = 0, sm_prep = 0;
-  long long tile_total = 0;
+  std::vector<long long> tile_lines;
   for (auto& it : items) {
     const int n = it.m - std::min(it.m, it.kx);
-    if (it.m > 0 && tile_path(n)) tile_total += std::max<long long>(1, (it.N + 127) / 128);
+    if (it.m > 0 && n > 0 && tile_path(n)) tile_lines.push_back(it.N);
   }
-  const int tpc = tiles_per_cta(tile_total);
+  const int tpc = tiles_per_cta(tile_lines);
   std::vector<TileItem> titems;
   std::vector<TileWork> twork;
   std::vector<std::tuple<double*, int, int, int>> tparts;

@@ -526,18 +526,26 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   HView X{&x, false}, Y{&y, false}, XT{&x, true}, YT{&y, true};
   StageTag tag0(C, "p1.weights");
   MatStore P = basis_product(C, sc, *x.cb, *y.rb);
-  MatStore rwy = basis_weights(C, sc, *y.cb);
-  MatStore zy = total_weights(C, sc, Y, rwy, scaling);
-  MatStore rwx = basis_weights(C, sc, *x.rb);
-  MatStore zxt = total_weights(C, sc, XT, rwx, scaling);
   record(C, e1);
   // the row and column bases are independent until the assembly: run them concurrently, the
   // column pass on a side stream driven by a second host thread
   auto keep2 = std::make_shared<Arena>(C.st);
   Induced qr, qc;
+  // each pass first forms its own total weights (weights.py:60-101): Z_Y for the rows, Z_X^T for
+  // the columns
+  auto row_pass = [&](Ctx& c, Arena& out, Arena& scr) {
+    MatStore rwy = basis_weights(c, scr, *y.cb);
+    MatStore zy = total_weights(c, scr, Y, rwy, scaling);
+    return induced_rows(c, out, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+  };
+  auto col_pass = [&](Ctx& c, Arena& out, Arena& scr) {
+    MatStore rwx = basis_weights(c, scr, *x.rb);
+    MatStore zxt = total_weights(c, scr, XT, rwx, scaling);
+    return induced_rows(c, out, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+  };
   if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
-    qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
-    qc = induced_rows(C, *keep2, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+    qr = row_pass(C, *keep, sc);
+    qc = col_pass(C, *keep2, sc);
   } else {
     Ctx& S = C.side();
     keep2->st = S.st;
@@ -545,14 +553,16 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     std::exception_ptr err;
     std::thread th([&] {
       try {
-        qc = induced_rows(S, *keep2, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+        StageTag tg(S, "p1.weights");
+        Arena sc2(S.st);
+        qc = col_pass(S, *keep2, sc2);
         S.sync();
       } catch (...) {
         err = std::current_exception();
       }
     });
     try {
-      qr = induced_rows(C, *keep, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+      qr = row_pass(C, *keep, sc);
     } catch (...) {
       th.join();
       throw;
