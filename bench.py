@@ -244,10 +244,12 @@ def main():
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
     e0.record(stream)
     for _ in range(args.steps):
         z = step()
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     e1.synchronize()
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -321,6 +323,29 @@ def main():
                               "frac_of_step": (1e3 * total_flops / (peak_fp64 * 1e12)) / ms},
                 "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src}
 
+    # accuracy of the full-size product: the reference's 20-step power-iteration estimate of
+    # |XY - Z|_2 / |XY|_2 (bench.py:147-174), every matvec on the GPU
+    eps2 = P.estimate_relative_spectral_error(dx, dy, z, steps=20, seed=0)
+    # H^2 matvec: HBM bound, every stored entry of Z read once per product
+    vz = torch.randn(n, dtype=torch.float64, device=torch.device("cuda", local))
+    for _ in range(3):
+        z.matvec(vz)
+    torch.cuda.synchronize()
+    ctx.kernel_stats(reset=True)
+    ctx.set_profile(True)
+    mv_reps = 10
+    for _ in range(mv_reps):
+        z.matvec(vz)
+    ctx.synchronize()
+    ctx.set_profile(False)
+    mvs = ctx.kernel_stats(reset=True)["mv"]
+    mv_ms = mvs["ms"] / mv_reps
+    mv_bytes = mvs["bytes"] / mv_reps
+    matvec = {"kernel": "mv_kernel", "ms": mv_ms, "launches": mvs["launches"] // mv_reps,
+              "bytes": mv_bytes, "achieved_gbs": mv_bytes / (mv_ms / 1e3) / 1e9 if mv_ms > 0 else 0.0,
+              "peak_gbs": hbm, "frac": (mv_bytes / (mv_ms / 1e3) / 1e9) / hbm if mv_ms > 0 else 0.0,
+              "note": "Z v on the c-config product Z; bytes = matrix entries read (x/y traffic excluded)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_n = args.cpu_sample_n
@@ -350,6 +375,9 @@ def main():
             "cpu_baseline": cpu,
             "stages_s": stages,
             "ranks": {"final_max": int(max(zr)), "final_mean": float(sum(zr) / len(zr))},
+            "accuracy": {"eps2_power_iteration": eps2, "steps": 20, "seed": 0, "eps": eps,
+                         "estimator": "reference bench.py:147-174 on GPU matvecs"},
+            "matvec": matvec,
             "setup_s": {"build_inputs": t_build, "upload_recompress": t_prep},
         }
         if args.profile_json:

@@ -47,9 +47,10 @@ int h2g_ctx_synchronize(h2g_ctx* ctx);
 /* host-side time per named section in timing mode, as "name=ms;..." (returns the full length) */
 int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset);
 /* profile mode: CUDA events around every batched launch, accumulated per kernel class
-   (0 gsum, 1 qr_r, 2 svd, 3 norm, 4 gather); out20 = per class {launches, ms, algorithmic flops, bytes} */
+   (0 gsum, 1 qr_r, 2 svd, 3 norm, 4 gather, 5 mv); out24 = per class {launches, ms, algorithmic flops,
+   bytes} */
 int h2g_ctx_set_profile(h2g_ctx* ctx, int on);
-int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* out20, int reset);
+int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* out24, int reset);
 /* timeline: trace_begin turns on per-launch events; trace_dump writes a chrome://tracing JSON */
 int h2g_ctx_trace_begin(h2g_ctx* ctx);
 int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path);
@@ -98,6 +99,10 @@ int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max
                 h2g_h2** z);
 /* orthogonalise + coarsen onto the own block tree */
 int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z);
+/* y <- (accumulate ? y : 0) + alpha * op(G) x, op = identity (trans = 0) or transpose (trans = 1);
+   x and y are DEVICE vectors (length cols / rows of op(G)), computed on the context's stream.
+   Replaces h2mul.h2_matvec / h2_matvec_adjoint (h2.py:224-267). */
+int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, double alpha, int accumulate);
 
 const char* h2g_last_error(void);
 

@@ -25,6 +25,7 @@ __all__ = [
     "o_multiply", "o_coverage", "o_coarse_rows", "o_coarse_cols",
     "o_project_final", "o_coarsen", "o_orthogonalize", "o_recompress",
     "o_matvec", "o_matvec_t", "o_to_dense", "o_from_packed", "o_to_packed",
+    "o_spectral_norm_est", "o_relative_spectral_error",
     "o_run_stages", "OracleError",
 ]
 
@@ -926,6 +927,46 @@ def o_matvec(g, x):
 def o_matvec_t(g, x):
     """y = G^T x (h2.py:247-267)."""
     return o_matvec(g.T(), x)
+
+
+def o_spectral_norm_est(apply, apply_t, dim, steps, rng):
+    """Power iteration on A^T A, sigma_1 estimate |A v| (bench.py:126-144)."""
+    v = rng.standard_normal(dim)
+    nv = np.linalg.norm(v)
+    if nv == 0 or dim == 0:
+        return 0.0
+    v = v / nv
+    sigma = 0.0
+    for _ in range(steps):
+        w = apply(v)
+        sigma = float(np.linalg.norm(w))
+        if sigma == 0.0:
+            return 0.0
+        v = apply_t(w)
+        nv = float(np.linalg.norm(v))
+        if nv == 0.0:
+            return sigma
+        v = v / nv
+    return sigma
+
+
+def o_relative_spectral_error(x, y, g, steps=20, seed=0):
+    """|XY - G|_2 / |XY|_2 by the same power iteration for both norms (bench.py:147-174)."""
+    rng = np.random.default_rng(seed)
+    n_k = y.shape[1]
+
+    def xy(v):
+        return o_matvec(x, o_matvec(y, v))
+
+    def xy_t(v):
+        return o_matvec_t(y, o_matvec_t(x, v))
+
+    denom = o_spectral_norm_est(xy, xy_t, n_k, steps, rng)
+    numer = o_spectral_norm_est(lambda v: xy(v) - o_matvec(g, v), lambda v: xy_t(v) - o_matvec_t(g, v),
+                                n_k, steps, rng)
+    if denom == 0.0:
+        return 0.0 if numer == 0.0 else float("inf")
+    return numer / denom
 
 
 def o_to_dense(g):

@@ -19,6 +19,9 @@ def __getattr__(name):
     if name in ("multiply", "coarsen", "recompress", "multiply_coarsen", "multiply_coarsen_packed"):
         from . import api
         return getattr(api, name)
+    if name in ("estimate_relative_spectral_error", "h2_matvec", "h2_matvec_adjoint"):
+        from . import errest
+        return getattr(errest, name)
     if name in ("Context", "DeviceH2", "default_context"):
         from . import device
         return getattr(device, name)

@@ -123,7 +123,7 @@ int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path) {
   return guarded([&] {
     Ctx& C = ctx->c;
     C.sync();
-    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather", "svd.tsqr", "merge", "svd.finish", "qr.chunk", "misc"};
+    static const char* names[] = {"gsum", "qr_r", "svd", "norm", "gather", "mv", "svd.tsqr", "merge", "svd.finish", "qr.chunk", "misc"};
     FILE* f = fopen(path, "w");
     if (!f) throw InvalidInput("cannot open trace file");
     fprintf(f, "{\"traceEvents\":[\n");
@@ -393,6 +393,13 @@ int h2g_blocks_structure(h2g_blocks* bb, long long* sizes2, long long* row, long
     }
     cptr[B.nb] = B.cptr[B.nb];
     for (size_t i = 0; i < B.cidx.size(); ++i) cidx[i] = B.cidx[i];
+  });
+}
+
+int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, double alpha, int accumulate) {
+  return guarded([&] {
+    if (!x || !y) throw InvalidInput("matvec: null vector");
+    h2_matvec(ctx->c, HView{g->h.get(), trans != 0}, x, y, alpha, accumulate != 0);
   });
 }
 

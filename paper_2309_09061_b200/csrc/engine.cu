@@ -9,7 +9,10 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <functional>
+#include <memory>
+#include <thread>
 #include <mutex>
 
 #include "engine.h"
@@ -800,43 +803,50 @@ static inline char classify(BView bx, BView by, int bts, int bsr) {
 }
 
 // Product block tree T^XY with the per-node terminal triples (trees.py:314-359, induced.py:280-326).
-PTree product_tree(BView bx, BView by) {
-  const Tree& rows = bx.rows();
-  const Tree& mid = bx.cols();
-  const Tree& cols = by.cols();
-  if (!mid.same(by.rows())) throw InvalidInput("factors do not share the middle cluster tree");
-  PTree P;
-  auto bt = std::make_shared<Blocks>();
-  bt->rows = &rows;
-  bt->cols = &cols;
+//
+// The recursion `rec(t, r, middles)` is a depth-first preorder walk.  It is built in parallel: a
+// breadth-first prefix expands the top frames until there are enough independent subtrees, each
+// subtree is built by its own host thread with the same per-node logic, and the pieces are
+// stitched back in exact preorder (prefix node, then its children's subtrees in slot order), so
+// block ids, children and triple order are identical to the sequential walk.
+namespace {
+
+struct PtMid {
+  int s, hx, hy;  // middle cluster and hint blocks (parents of X|ts, Y|sr)
+};
+struct PtFrame {
+  int t, r, parent, slot, m0, m1;  // middles in `pool[m0:m1]`
+};
+
+struct PtBuilder {
+  BView bx, by;
+  const Tree *rows, *mid, *cols;
+  std::vector<PtMid> pool;
+  std::vector<int> row, col;
+  std::vector<unsigned char> adm;
   std::vector<std::vector<int>> kids;
-  struct Mid {
-    int s, hx, hy;  // middle cluster and hint blocks (parents of X|ts, Y|sr)
-  };
-  struct Frame {
-    int t, r, parent, slot, m0, m1;  // middles in `pool[m0:m1]`
-  };
-  std::vector<Mid> pool{Mid{0, 0, 0}};
-  std::vector<Frame> stack{Frame{0, 0, -1, 0, 0, 1}};
+  std::vector<int> tptr, ts, tbx, tby;
+  std::vector<char> tk;
   struct Live {
     int s, bts, bsr;
   };
   std::vector<Live> pend, open;
-  P.tptr.reserve(1 << 16);
-  while (!stack.empty()) {
-    const Frame f = stack.back();
-    stack.pop_back();
-    const int b = (int)bt->row.size();
+
+  PtBuilder(BView x, BView y) : bx(x), by(y), rows(&x.rows()), mid(&x.cols()), cols(&y.cols()) {}
+
+  // creates node for frame f (linking it to its parent slot) and appends its child frames
+  int node(const PtFrame& f, std::vector<PtFrame>& out) {
+    const int b = (int)row.size();
     if (f.parent >= 0) kids[f.parent][f.slot] = b;
-    bt->row.push_back(f.t);
-    bt->col.push_back(f.r);
-    bt->adm.push_back(1);
+    row.push_back(f.t);
+    col.push_back(f.r);
+    adm.push_back(1);
     kids.emplace_back();
-    P.tptr.push_back((int)P.ts.size());
-    const bool both_leaf = rows.leaf(f.t) && cols.leaf(f.r);
+    tptr.push_back((int)ts.size());
+    const bool both_leaf = rows->leaf(f.t) && cols->leaf(f.r);
     pend.clear();
     for (int i = f.m0; i < f.m1; ++i) {
-      const Mid& m = pool[i];
+      const PtMid& m = pool[i];
       pend.push_back(Live{m.s, locate(bx, m.hx, f.t, m.s), locate(by, m.hy, m.s, f.r)});
     }
     open.clear();
@@ -847,8 +857,8 @@ PTree product_tree(BView bx, BView by) {
       const char k = classify(bx, by, l.bts, l.bsr);
       if (k == 'n') {
         if (both_leaf) {  // both clusters exhausted: chase the middle only (trees.py:343-345)
-          for (int i = 0; i < mid.nkids(l.s); ++i) {
-            const int s2 = mid.kid(l.s, i);
+          for (int i = 0; i < mid->nkids(l.s); ++i) {
+            const int s2 = mid->kid(l.s, i);
             pend.push_back(Live{s2, locate(bx, l.bts, f.t, s2), locate(by, l.bsr, s2, f.r)});
           }
         } else {
@@ -857,32 +867,158 @@ PTree product_tree(BView bx, BView by) {
         continue;
       }
       if (k == 'c') dense = true;
-      P.ts.push_back(l.s);
-      P.tk.push_back(k);
-      P.tbx.push_back(l.bts);
-      P.tby.push_back(l.bsr);
+      ts.push_back(l.s);
+      tk.push_back(k);
+      tbx.push_back(l.bts);
+      tby.push_back(l.bsr);
     }
     if (!open.empty()) {
       const int m0 = (int)pool.size();
       for (const Live& l : open) {  // _sub_middles (trees.py:303-311)
-        if (!bx.b->leaf(l.bts) && !by.b->leaf(l.bsr) && mid.nkids(l.s) > 0) {
-          for (int i = 0; i < mid.nkids(l.s); ++i) pool.push_back(Mid{mid.kid(l.s, i), l.bts, l.bsr});
+        if (!bx.b->leaf(l.bts) && !by.b->leaf(l.bsr) && mid->nkids(l.s) > 0) {
+          for (int i = 0; i < mid->nkids(l.s); ++i) pool.push_back(PtMid{mid->kid(l.s, i), l.bts, l.bsr});
         } else {
-          pool.push_back(Mid{l.s, l.bts, l.bsr});
+          pool.push_back(PtMid{l.s, l.bts, l.bsr});
         }
       }
       const int m1 = (int)pool.size();
-      const int nt = std::max(1, rows.nkids(f.t)), nr = std::max(1, cols.nkids(f.r));
+      const int nt = std::max(1, rows->nkids(f.t)), nr = std::max(1, cols->nkids(f.r));
       kids[b].assign(nt * nr, -1);
-      for (int i = nt * nr - 1; i >= 0; --i) {
-        const int t2 = rows.nkids(f.t) ? rows.kid(f.t, i / nr) : f.t;
-        const int r2 = cols.nkids(f.r) ? cols.kid(f.r, i % nr) : f.r;
-        stack.push_back(Frame{t2, r2, b, i, m0, m1});
+      for (int i = 0; i < nt * nr; ++i) {
+        const int t2 = rows->nkids(f.t) ? rows->kid(f.t, i / nr) : f.t;
+        const int r2 = cols->nkids(f.r) ? cols->kid(f.r, i % nr) : f.r;
+        out.push_back(PtFrame{t2, r2, b, i, m0, m1});
       }
     } else if (dense) {
-      bt->adm[b] = 0;
+      adm[b] = 0;
     }
+    return b;
   }
+
+  // sequential preorder walk from `root` (its middles already in pool[root.m0:root.m1])
+  void dfs(const PtFrame& root) {
+    std::vector<PtFrame> stack{root}, tmp;
+    while (!stack.empty()) {
+      const PtFrame f = stack.back();
+      stack.pop_back();
+      tmp.clear();
+      node(f, tmp);
+      for (int i = (int)tmp.size() - 1; i >= 0; --i) stack.push_back(tmp[i]);  // slot 0 first
+    }
+    tptr.push_back((int)ts.size());
+  }
+};
+
+}  // namespace
+
+PTree product_tree(BView bx, BView by) {
+  const Tree& rows = bx.rows();
+  const Tree& cols = by.cols();
+  if (!bx.cols().same(by.rows())) throw InvalidInput("factors do not share the middle cluster tree");
+  // breadth-first prefix until there are enough subtrees for the worker threads
+  PtBuilder pre(bx, by);
+  pre.pool.push_back(PtMid{0, 0, 0});
+  std::vector<PtFrame> level{PtFrame{0, 0, -1, 0, 0, 1}}, next;
+  // prefix children: >= 0 prefix node, < 0: -(1 + fragment index)
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t want = std::max<size_t>(1, 8 * (size_t)std::min(hw, 16u));
+  std::vector<PtFrame> frags;
+  while (!level.empty()) {
+    if (level.size() >= want) {
+      for (const PtFrame& f : level) {
+        pre.kids[f.parent][f.slot] = -1 - (int)frags.size();
+        frags.push_back(f);
+      }
+      break;
+    }
+    next.clear();
+    for (const PtFrame& f : level) pre.node(f, next);
+    level.swap(next);
+  }
+  pre.tptr.push_back((int)pre.ts.size());
+  // subtrees in parallel
+  std::vector<std::unique_ptr<PtBuilder>> fb(frags.size());
+  {
+    std::atomic<size_t> nextf{0};
+    std::exception_ptr err;
+    std::mutex emu;
+    auto work = [&] {
+      try {
+        for (size_t i; (i = nextf.fetch_add(1)) < frags.size();) {
+          auto B = std::make_unique<PtBuilder>(bx, by);
+          const PtFrame& f = frags[i];
+          B->pool.assign(pre.pool.begin() + f.m0, pre.pool.begin() + f.m1);
+          B->dfs(PtFrame{f.t, f.r, -1, 0, 0, f.m1 - f.m0});
+          fb[i] = std::move(B);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(emu);
+        if (!err) err = std::current_exception();
+      }
+    };
+    const int nth = (int)std::min<size_t>(frags.size(), std::min(hw, 16u));
+    std::vector<std::thread> th;
+    for (int k = 1; k < nth; ++k) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    if (err) std::rethrow_exception(err);
+  }
+  // stitch in preorder
+  PTree P;
+  auto bt = std::make_shared<Blocks>();
+  bt->rows = &rows;
+  bt->cols = &cols;
+  size_t nnodes = pre.row.size(), ntrip = pre.ts.size();
+  for (auto& B : fb) {
+    nnodes += B->row.size();
+    ntrip += B->ts.size();
+  }
+  bt->row.reserve(nnodes);
+  bt->col.reserve(nnodes);
+  bt->adm.reserve(nnodes);
+  P.tptr.reserve(nnodes + 1);
+  P.ts.reserve(ntrip);
+  P.tk.reserve(ntrip);
+  P.tbx.reserve(ntrip);
+  P.tby.reserve(ntrip);
+  std::vector<std::vector<int>> kids;
+  kids.reserve(nnodes);
+  auto append = [&](const PtBuilder& B, int b, int base) {
+    bt->row.push_back(B.row[b]);
+    bt->col.push_back(B.col[b]);
+    bt->adm.push_back(B.adm[b]);
+    P.tptr.push_back((int)P.ts.size());
+    for (int i = B.tptr[b]; i < B.tptr[b + 1]; ++i) {
+      P.ts.push_back(B.ts[i]);
+      P.tk.push_back(B.tk[i]);
+      P.tbx.push_back(B.tbx[i]);
+      P.tby.push_back(B.tby[i]);
+    }
+    kids.emplace_back(B.kids[b]);
+    if (base)
+      for (int& c : kids.back()) c += base;
+  };
+  std::function<int(int)> emit = [&](int p) -> int {
+    const int g = (int)bt->row.size();
+    append(pre, p, 0);
+    const std::vector<int> ch = pre.kids[p];
+    for (size_t i = 0; i < ch.size(); ++i) {
+      int gid;
+      if (ch[i] >= 0) {
+        gid = emit(ch[i]);
+      } else {
+        const PtBuilder& B = *fb[-1 - ch[i]];
+        gid = (int)bt->row.size();
+        for (int b = 0; b < (int)B.row.size(); ++b) append(B, b, gid);
+      }
+      kids[g][i] = gid;
+    }
+    return g;
+  };
+  if (pre.row.empty()) {  // the root itself was a fragment (cannot happen: want >= 1 frame > 0)
+    throw StructureErr("product tree: empty prefix");
+  }
+  emit(0);
   P.tptr.push_back((int)P.ts.size());
   bt->nb = (int)bt->row.size();
   bt->cptr.assign(bt->nb + 1, 0);

@@ -164,9 +164,9 @@ struct StageTimes {
 };
 
 // Per-kernel-class accounting for the roofline (profile mode only; never inside a timed step).
-enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_NCLASS = 5 };
+enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_MV = 5, K_NCLASS = 6 };
 // trace-only sub-intervals (not counted in the kernel-class statistics)
-enum KSub { S_SVD_TSQR = 5, S_MERGE = 6, S_SVD_FIN = 7, S_QR_CHUNK = 8, S_MISC = 9, S_NSUB = 10 };
+enum KSub { S_SVD_TSQR = 6, S_MERGE = 7, S_SVD_FIN = 8, S_QR_CHUNK = 9, S_MISC = 10, S_NSUB = 11 };
 struct KStat {
   long long launches = 0;
   double ms = 0, flops = 0, bytes = 0;
@@ -328,6 +328,32 @@ struct SvdBatch {
   std::vector<int> run(Ctx& C, Arena& scratch);  // sync + ranks (k1 + k2)
 };
 
+// Batched small GEMVs (matvec.cu): y (m) = (beta ? y : 0) + sum alpha * A (m x k) x (k).
+struct MvTerm {
+  MatRef a;
+  const double* x;
+  int k, pad_;
+  double alpha;
+};
+struct MvOut {
+  double* y;
+  int m, t0, t1, beta;
+};
+struct MvBatch {
+  std::vector<MvOut> outs;
+  std::vector<MvTerm> terms;
+  double bytes_a = 0.0;  // matrix bytes read (profile ledger)
+  void out(double* y, int m, bool beta) {
+    outs.push_back(MvOut{y, m, (int)terms.size(), (int)terms.size(), beta ? 1 : 0});
+  }
+  void term(MatRef a, const double* x, int k, double alpha, double elems) {
+    terms.push_back(MvTerm{a, x, k, 0, alpha});
+    outs.back().t1 = (int)terms.size();
+    bytes_a += 8.0 * elems;
+  }
+  void run(Ctx& C);
+};
+
 using MatStore = std::vector<Mat>;
 struct PRef {  // basis product view (transposed for the column pass)
   const MatStore* P;
@@ -393,6 +419,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
 std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling);
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale);
+void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool accumulate);
 std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank);
 
 }  // namespace h2g

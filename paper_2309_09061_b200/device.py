@@ -62,13 +62,13 @@ class Context:
         N.check(self.lib.h2g_ctx_counters(self.h, out.ctypes.data_as(N.I64P), 1 if reset else 0))
         return {"launches": int(out[0]), "syncs": int(out[1])}
 
-    KCLASSES = ("gsum", "qr_r", "svd", "norm", "gather")
+    KCLASSES = ("gsum", "qr_r", "svd", "norm", "gather", "mv")
 
     def set_profile(self, on: bool):
         N.check(self.lib.h2g_ctx_set_profile(self.h, 1 if on else 0))
 
     def kernel_stats(self, reset: bool = True) -> dict:
-        out = np.zeros(20)
+        out = np.zeros(4 * len(self.KCLASSES))
         N.check(self.lib.h2g_ctx_kernel_stats(self.h, out.ctypes.data_as(N.F64P), 1 if reset else 0))
         return {k: {"launches": int(out[4 * i]), "ms": float(out[4 * i + 1]), "flops": float(out[4 * i + 2]),
                     "bytes": float(out[4 * i + 3])} for i, k in enumerate(self.KCLASSES)}
@@ -243,6 +243,36 @@ class DeviceH2:
     def download(self) -> H2Matrix:
         """Host H2Matrix with the reference's container interface."""
         return unpack_h2(self.to_packed(), rows=self.rows, cols=self.cols)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (int(self.rows.stop[0] - self.rows.start[0]), int(self.cols.stop[0] - self.cols.start[0]))
+
+    def matvec(self, x, *, trans: bool = False, alpha: float = 1.0, out=None, accumulate: bool = False):
+        """op(G) x on the GPU through the C ABI h2g_matvec (reference h2_matvec / h2_matvec_adjoint,
+        h2.py:224-267).  x: CUDA float64 tensor of length cols (rows if trans); returns a CUDA
+        tensor (out, if given, accumulated into when accumulate=True)."""
+        import torch
+        nr, nc = self.shape
+        nin, nout = (nr, nc) if trans else (nc, nr)
+        dev = torch.device("cuda", self.ctx.device)
+        x = torch.as_tensor(x, dtype=torch.float64, device=dev).contiguous()
+        if x.shape != (nin,):
+            raise InvalidInputError(f"x has shape {tuple(x.shape)}, expected ({nin},)")
+        if out is None:
+            if accumulate:
+                raise InvalidInputError("accumulate=True needs out")
+            out = torch.empty(nout, dtype=torch.float64, device=dev)
+        elif out.shape != (nout,) or out.dtype != torch.float64 or not out.is_contiguous():
+            raise InvalidInputError(f"out must be a contiguous float64 tensor of shape ({nout},)")
+        cur = torch.cuda.current_stream(dev)
+        self.ctx.stream.wait_stream(cur)
+        x.record_stream(self.ctx.stream)
+        out.record_stream(self.ctx.stream)
+        N.check(self.ctx.lib.h2g_matvec(self.ctx.h, self.h, 1 if trans else 0, C.c_void_p(x.data_ptr()),
+                                        C.c_void_p(out.data_ptr()), float(alpha), 1 if accumulate else 0))
+        cur.wait_stream(self.ctx.stream)
+        return out
 
     def packed_bytes(self) -> int:
         """Bytes of the packed float64 payload (bases + couplings + nearfield)."""

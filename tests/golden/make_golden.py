@@ -205,6 +205,9 @@ def run_reference(h2mul, x, y, eps, out, probes, x_raw=None, y_raw=None, keep_z=
         if x_raw is not None:
             xr.append(h2mul.h2_matvec(x_raw, v))
             yr.append(h2mul.h2_matvec(y_raw, v))
+    # the reference's own power-iteration error estimate |XY - Z|_2 / |XY|_2 (bench.py:147-174)
+    from h2mul.bench import estimate_relative_spectral_error
+    out["est.eps2"] = np.asarray([estimate_relative_spectral_error(x, y, z, steps=20, seed=0)])
     out["probe.v"] = np.asarray(vs)
     out["probe.zv"] = np.asarray(zv)
     out["probe.gv"] = np.asarray(gv_)
@@ -288,7 +291,8 @@ def random_pair_case(h2mul, seed, n, leaf, dim, tol, rank=3):
 
 def main():
     h2mul, hp = _ref()
-    os.makedirs(HERE, exist_ok=True)
+    out_dir = os.environ.get("GOLDEN_OUT", HERE)
+    os.makedirs(out_dir, exist_ok=True)
     cases = {}
     for name in ("c1", "c2", "c3", "c4", "c5"):
         cases[name] = config_case(name, h2mul, hp)
@@ -297,7 +301,7 @@ def main():
     cases["rand_s2_2d"] = random_pair_case(h2mul, 2, 96, 6, 2, 1e-4)
     cases["rand_s3_2d_tol0"] = random_pair_case(h2mul, 3, 64, 5, 2, 0.0)
     for name, out in cases.items():
-        path = os.path.join(HERE, f"{name}.npz")
+        path = os.path.join(out_dir, f"{name}.npz")
         np.savez_compressed(path, **out)
         print(f"{name}: {os.path.getsize(path) / 1e6:.2f} MB, ranks induced "
               f"{out['rank.induced_row'].max()} final {out['rank.final_row'].max()}, "

@@ -185,3 +185,43 @@ def test_packed_host_buffer_path():
     v = np.random.default_rng(3).standard_normal(x.shape[1])
     from paper_2309_09061_b200.h2 import h2_matvec_host
     assert rel(h2_matvec_host(z2, v), h2_matvec_host(z, v)) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["rand_s0_tol1e-3", "c1"])
+def test_gpu_matvec_matches_host(name):
+    """GPU h2_matvec / adjoint (h2.py:224-267) against the host restatement on Z and X."""
+    P = _P()
+    import torch
+    from paper_2309_09061_b200.h2 import h2_matvec_host
+    d = load(name)
+    x, y, eps = _inputs(d)
+    dx = P.DeviceH2.upload(x)
+    z = P.coarsen(P.multiply(dx, P.DeviceH2.upload(y) if y is not x else dx, eps), dx.block_tree, eps)
+    zh = z.download()
+    rng = np.random.default_rng(5)
+    for g, gh in ((dx, x), (z, zh)):
+        nr, nc = g.shape
+        v = rng.standard_normal(nc)
+        u = rng.standard_normal(nr)
+        gv = g.matvec(torch.from_numpy(v).cuda()).cpu().numpy()
+        assert rel(gv, h2_matvec_host(gh, v)) <= 1e-13
+        gtu = g.matvec(torch.from_numpy(u).cuda(), trans=True).cpu().numpy()
+        # adjoint identity <G v, u> = <v, G^T u>
+        assert abs(gv @ u - v @ gtu) <= 1e-12 * np.linalg.norm(gv) * np.linalg.norm(u)
+
+
+@pytest.mark.parametrize("name", RANDOM_CASES + CONFIG_CASES)
+def test_gpu_error_estimate_matches_reference(name):
+    """GPU power-iteration |XY - Z|_2 / |XY|_2 (bench.py:147-174) against the reference's own value."""
+    P = _P()
+    d = load(name)
+    x, y, eps = _inputs(d)
+    dx = P.DeviceH2.upload(x)
+    dy = dx if y is x else P.DeviceH2.upload(y)
+    z = P.coarsen(P.multiply(dx, dy, eps), dx.block_tree, eps)
+    est = P.estimate_relative_spectral_error(dx, dy, z, steps=20, seed=0)
+    ref = float(d["est.eps2"][0])
+    if ref <= 1e-12:  # exact product (tol 0 or ranks below the tolerance): rounding noise only
+        assert est <= 1e-12
+    else:
+        assert abs(est - ref) <= 1e-4 * ref

@@ -51,3 +51,13 @@ def test_oracle_matches_reference_rebuilt_inputs(name):
     x, y = golden_inputs_oracle(d)
     assert x.rb.rank == list(d["rank.x_row"]) and y.cb.rank == list(d["rank.y_col"])
     _check_case(d, x, y)
+
+
+@pytest.mark.parametrize("name", ["c1", "rand_s0_tol1e-3", "rand_s2_2d"])
+def test_oracle_error_estimate_matches_reference(name):
+    """The oracle's power-iteration estimate (bench.py:147-174) on the reference's own X, Y, Z."""
+    import oracle as O
+    d = load(name)
+    x, y, z = O.o_from_packed(d, "x/"), O.o_from_packed(d, "y/"), O.o_from_packed(d, "z/")
+    est = O.o_relative_spectral_error(x, y, z, steps=20, seed=0)
+    assert abs(est - float(d["est.eps2"][0])) <= 1e-8 * float(d["est.eps2"][0])
