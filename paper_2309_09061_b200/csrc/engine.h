@@ -132,6 +132,7 @@ struct H2 {
   std::shared_ptr<Basis> rb, cb;
   std::vector<double*> coup, near;
   std::vector<ArenaPtr> owned;
+  ArenaPtr near_owner;  // arena holding the nearfield blocks (shared by a coarsened result)
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
   std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
 };

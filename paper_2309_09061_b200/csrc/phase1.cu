@@ -262,6 +262,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   G->cb = qc.q;
   auto ar = std::make_shared<Arena>(C.st);
   G->owned.push_back(ar);
+  G->near_owner = ar;
   Arena sc(C.st);
   const Blocks& B = *pt.bt;
   const Tree& rows = *B.rows;

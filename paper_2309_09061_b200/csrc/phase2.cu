@@ -593,6 +593,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   Z->rb = rs.q;
   Z->cb = cs.q;
   Z->owned.push_back(ar);
+  if (g.h->near_owner) Z->owned.push_back(g.h->near_owner);  // dense blocks shared with the product
   const Blocks& cb = *coarse;
   const Blocks& pt = *g.h->bt;
   const Basis& qr = *rs.q;
@@ -602,23 +603,26 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   Z->near.assign(cb.nb, nullptr);
   Arena sc(C.st);
   // chain(r, c) = F'_c F'_parent ... (k'_c x k'_r), memoised, depth >= 2 materialised in waves
-  std::map<std::pair<int, int>, Mat> chain;
+  std::unordered_map<long long, Mat> chain;
+  chain.reserve(1024);
+  auto ckey = [&](int r, int c) { return (long long)r * ctree.n + c; };
   std::vector<std::vector<std::pair<int, int>>> waves;
   std::function<void(int, int)> need = [&](int r, int c) {
     if (ctree.parent[c] == r || c == r) return;
-    auto key = std::make_pair(r, c);
+    const long long key = ckey(r, c);
     if (chain.count(key)) return;
     need(r, ctree.parent[c]);
     int d = 0;
     for (int u = c; u != r; u = ctree.parent[u]) ++d;
     chain[key] = Mat{sc.alloc((size_t)qc.rank[c] * qc.rank[r]), qc.rank[c], qc.rank[r]};
     if ((int)waves.size() <= d) waves.resize(d + 1);
-    waves[d].push_back(key);
+    waves[d].push_back(std::make_pair(r, c));
   };
   auto chain_ref = [&](int r, int c) -> Mat {
     if (ctree.parent[c] == r) return qc.xferm(c);
-    return chain[std::make_pair(r, c)];
+    return chain[ckey(r, c)];
   };
+  std::vector<int> lv;
   // collect the needed chains
   for (int b = 0; b < cb.nb; ++b) {
     if (!cb.adm_leaf(b)) continue;
@@ -626,7 +630,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     if (pt.adm_leaf(pb)) continue;
     const CTRef rr = rs.reps[pb];
     if (!rr.t) throw StructureErr("missing representation of a covered product block");
-    std::vector<int> lv;
+    lv.clear();
     rr.t->leaves(rr.root, lv);
     for (int u : lv) need(cb.col[b], rr.t->cl[u]);
   }
@@ -634,7 +638,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     GBatch gw;
     for (auto& key : wave) {
       const int r = key.first, c = key.second;
-      gw.out(chain[key], false);
+      gw.out(chain[ckey(r, c)], false);
       const Mat up = chain_ref(r, ctree.parent[c]);
       gw.t2(qc.xferm(c).ref(), up.ref(), qc.rank[ctree.parent[c]]);
     }
@@ -653,7 +657,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
         g1.t3(rs.r[t].ref(), g.coup(pb), cs.r[r].tref(), rs.r[t].c, cs.r[r].c);
       } else {
         const CT& rep = *rs.reps[pb].t;
-        std::vector<int> lv;
+        lv.clear();
         rep.leaves(rs.reps[pb].root, lv);
         for (int u : lv) {  // lift (coarsening.py:374-382)
           const int c = rep.cl[u];
@@ -663,6 +667,10 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
           else g1.t3(M.ref(), X, chain_ref(r, c).ref(), M.c, qc.rank[c]);
         }
       }
+    } else if (pt.near_leaf(pb) && !g.T && g.h->near_owner) {
+      // the reference copies G's dense block (coarsening.py:397-398); device matrices are immutable,
+      // so Z shares it (its arena stays alive with Z) instead of copying
+      Z->near[b] = g.h->near[pb];
     } else {
       const int nr = cb.rows->size(t), nc = ctree.size(r);
       Mat N{ar->alloc((size_t)nr * nc), nr, nc};
