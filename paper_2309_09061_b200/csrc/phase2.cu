@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <functional>
+#include <future>
 #include <map>
 #include <unordered_map>
 #include <thread>
@@ -238,24 +239,42 @@ struct CState {
   std::vector<std::unique_ptr<CT>> pools;  // owners of the stored representations
 };
 
-// Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
-static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
-                          const std::vector<double>& cn, const double* d_nn) {
-  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
-  const BView pv = g.bv();
-  const Blocks& pt = *g.h->bt;
+// Structure-only preparation of one pass (runs on a host thread while the norms are computed):
+// coverage of T^XY by the coarse tree and the per-row-cluster block lists.
+struct CPrep {
+  std::vector<std::vector<int>> row_adm, near_cov, sub_cov;
+};
+
+static CPrep prep_rows(BView pv, BView coarse) {
   validate_coarse(pv, coarse);
   const std::vector<char> cov = coverage(pv, coarse);
   const Tree& tr = pv.rows();
-  const Basis& v1 = g.rb();
-  const Basis& w1 = g.cb();
-  std::vector<std::vector<int>> row_adm(tr.n), near_cov(tr.n), sub_cov(tr.n);
+  const Blocks& pt = *pv.b;
+  CPrep P;
+  P.row_adm.resize(tr.n);
+  P.near_cov.resize(tr.n);
+  P.sub_cov.resize(tr.n);
   for (int b = 0; b < pt.nb; ++b) {
     const int t = pv.row(b);
-    if (pt.adm_leaf(b)) row_adm[t].push_back(b);
-    else if (pt.near_leaf(b)) { if (cov[b]) near_cov[t].push_back(b); }
-    else if (cov[b]) sub_cov[t].push_back(b);
+    if (pt.adm_leaf(b)) P.row_adm[t].push_back(b);
+    else if (pt.near_leaf(b)) { if (cov[b]) P.near_cov[t].push_back(b); }
+    else if (cov[b]) P.sub_cov[t].push_back(b);
   }
+  return P;
+}
+
+// Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
+static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
+                          const std::vector<double>& cn, const double* d_nn, const CPrep& prep) {
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  const BView pv = g.bv();
+  const Blocks& pt = *g.h->bt;
+  const Tree& tr = pv.rows();
+  const Basis& v1 = g.rb();
+  const Basis& w1 = g.cb();
+  const std::vector<std::vector<int>>& row_adm = prep.row_adm;
+  const std::vector<std::vector<int>>& near_cov = prep.near_cov;
+  const std::vector<std::vector<int>>& sub_cov = prep.sub_cov;
   CState S;
   S.q = std::make_shared<Basis>();
   Basis& q = *S.q;
@@ -722,6 +741,12 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
                             bool scale) {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  // structure of both passes on host threads while the block norms run on the GPU
+  const BView gv{g.bt.get(), false}, gvt{g.bt.get(), true};
+  const BView cvw{coarse.get(), false}, cvt{coarse.get(), true};
+  auto prep_r = std::async(std::launch::async, [gv, cvw] { return prep_rows(gv, cvw); });
+  auto prep_c = std::async(std::launch::async, [gvt, cvt] { return prep_rows(gvt, cvt); });
   Arena sc(C.st);
   std::vector<double> cn;
   double* d_nn = sc.alloc(std::max(1, g.bt->nb));
@@ -729,13 +754,17 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     StageTag tag(C, "p2.norms");
     all_norms(C, sc, g, cn, d_nn);
   }
+  prep_r.wait();
+  prep_c.wait();
   auto ar = std::make_shared<Arena>(C.st);
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
   CState rs, cs;
   if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
-    rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn);
-    cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn);
+    rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
+                     prep_r.get());
+    cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
+                     prep_c.get());
   } else {
     Ctx& S = C.side();
     ar2->st = S.st;
@@ -743,14 +772,16 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     std::exception_ptr err;
     std::thread th([&] {
       try {
-        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn);
+        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
+                         prep_c.get());
         S.sync();
       } catch (...) {
         err = std::current_exception();
       }
     });
     try {
-      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn);
+      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
+                       prep_r.get());
     } catch (...) {
       th.join();
       throw;
