@@ -56,7 +56,11 @@ __device__ __forceinline__ void fetch_chunk(double (&ra)[kPerA], double (&rb)[kP
   for (int q = 0; q < kPerA; ++q) {
     const int e = tid + q * kThr;
     const int i = e / kKC, l = e % kKC;
-    ra[q] = (i < mt && l < kc) ? alpha * ld(A, ai0 + i, kk + l) : 0.0;
+    ra[q] = (i < mt && l < kc) ? ld(A, ai0 + i, kk + l) : 0.0;
+  }
+  if (alpha != 1.0) {  // uniform per term; most terms have alpha = 1
+#pragma unroll
+    for (int q = 0; q < kPerA; ++q) ra[q] *= alpha;
   }
 #pragma unroll
   for (int q = 0; q < kPerB; ++q) {

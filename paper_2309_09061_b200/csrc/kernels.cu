@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
 // norm_warp_kernel: sigma_1 of a single-segment matrix with m, N <= 64, one warp per matrix.
 // A lives in shared memory; Lanczos on the smaller Gram side (A^T A or A A^T, never formed) runs
 // at most min(m, N) steps, then Sturm multisection on the tridiagonal.  The top Ritz value grows
-// monotonically with the step count; from step 12 on it is re-evaluated every 4 steps and the
+// monotonically with the step count; from step 6 on it is re-evaluated every 2 steps and the
 // iteration stops once it moved by <= 1e-14 relative (the sigma_1 are scale factors and rank
 // thresholds: an error of that size cannot move a truncation whose margin is >= 1e-4).
 // An exactly zero matrix returns exactly 0 (the reference's zero-norm skips are exact tests).
@@ -1358,7 +1358,7 @@ __global__ void __launch_bounds__(32 * kNW) norm_warp_kernel(const NormItem* __r
       break;
     }
     if (lane == 0) be[k] = b;
-    if ((k & 3) == 3 && k >= 11) {
+    if ((k & 1) == 1 && k >= 5) {
       // early exit once the top Ritz value (monotone in k) has settled to ~1e-14 relative
       __syncwarp();
       const double th = warp_lambda_max(al, be, k + 1);
