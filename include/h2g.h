@@ -99,6 +99,15 @@ int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max
                 h2g_h2** z);
 /* orthogonalise + coarsen onto the own block tree */
 int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z);
+/* Interpolation H^2 matrix of a point-kernel problem with the couplings and nearfield blocks
+   evaluated on the GPU (reference problems.py:295-332): kernel 0 = -log r, 1 = 1/(4 pi r),
+   2 = 1/r, 3 = exp(-r)/r; points (n x dim) and weights (n) in cluster-tree order; the shared
+   interpolation basis in the packed layout (rank / leaf_off / xfer_off / data); node_off / nodes =
+   per-cluster Chebyshev grid (rank x dim, row-major) used for the couplings. Host arrays. */
+int h2g_h2_build_kernel(h2g_ctx* ctx, h2g_blocks* bt, int kernel, int dim, const double* points,
+                        const double* weights, const long long* rank, const long long* leaf_off,
+                        const long long* xfer_off, const double* basis, long long basis_len,
+                        const long long* node_off, const double* nodes, long long nodes_len, h2g_h2** out);
 /* y <- (accumulate ? y : 0) + alpha * op(G) x, op = identity (trans = 0) or transpose (trans = 1);
    x and y are DEVICE vectors (length cols / rows of op(G)), computed on the context's stream.
    Replaces h2mul.h2_matvec / h2_matvec_adjoint (h2.py:224-267). */

@@ -26,6 +26,8 @@ U8P = C.POINTER(C.c_ubyte)
 SIGNATURES = {
     "h2g_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
     "h2g_matvec": (C.c_int, [P, P, C.c_int, P, P, C.c_double, C.c_int]),
+    "h2g_h2_build_kernel": (C.c_int, [P, P, C.c_int, C.c_int, F64P, F64P, I64P, I64P, I64P, F64P, C.c_longlong,
+                                      I64P, F64P, C.c_longlong, C.POINTER(P)]),
     "h2g_ctx_destroy": (C.c_int, [P]),
     "h2g_ctx_set_timing": (C.c_int, [P, C.c_int]),
     "h2g_ctx_stage_times": (C.c_int, [P, F64P]),

@@ -396,6 +396,19 @@ int h2g_blocks_structure(h2g_blocks* bb, long long* sizes2, long long* row, long
   });
 }
 
+int h2g_h2_build_kernel(h2g_ctx* ctx, h2g_blocks* bt, int kernel, int dim, const double* points,
+                        const double* weights, const long long* rank, const long long* loff, const long long* xoff,
+                        const double* basis, long long basis_len, const long long* node_off, const double* nodes,
+                        long long nodes_len, h2g_h2** out) {
+  return guarded([&] {
+    auto h = build_kernel_h2(ctx->c, bt->b, kernel, dim, points, weights, rank, loff, xoff, basis, basis_len,
+                             node_off, nodes, nodes_len);
+    h->own_rows = bt->rows;
+    h->own_cols = bt->cols;
+    *out = new h2g_h2{h};
+  });
+}
+
 int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, double alpha, int accumulate) {
   return guarded([&] {
     if (!x || !y) throw InvalidInput("matvec: null vector");

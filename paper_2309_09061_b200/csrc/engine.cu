@@ -486,8 +486,11 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
 }
 
 void NormBatch::run_async(Ctx& C) {
-  size_t smem = 0;
-  std::vector<NormItem> big, small;  // small: single segment, both sides <= 64 / 128 (warp Lanczos)
+  size_t smem = 0, smem_g = 0;
+  // small: single segment, both sides <= 64 / 128 (warp Lanczos); big: CTA Gram in shared memory;
+  // huge: CTA Gram in global scratch
+  std::vector<NormItem> big, small, huge;
+  std::unique_ptr<Arena> local;
   for (auto& it : items) {
     if (it.m == 0 || it.N == 0) continue;
     const long long mn = std::min<long long>(it.m, it.N), mx = std::max<long long>(it.m, it.N);
@@ -497,14 +500,24 @@ void NormBatch::run_async(Ctx& C) {
     }
     const bool rowside = (it.m <= it.N) || (it.m <= 160);
     const long long g = rowside ? it.m : it.N;
-    if (g > 180) throw StructureErr("spectral norm: both sides above 180");
-    smem = std::max(smem, norm_smem(it.m, it.N));
-    big.push_back(it);
+    if (norm_smem(it.m, it.N, true) <= kSmemLimit) {
+      smem = std::max(smem, norm_smem(it.m, it.N, true));
+      big.push_back(it);
+      continue;
+    }
+    if (norm_smem(it.m, it.N, false) > kSmemLimit) throw StructureErr("spectral norm: panel too wide for shared memory");
+    if (!scratch) {
+      local.reset(new Arena(C.st));
+      scratch = local.get();
+    }
+    it.gbuf = scratch->alloc((size_t)g * g);
+    smem_g = std::max(smem_g, norm_smem(it.m, it.N, false));
+    huge.push_back(it);
   }
-  if (!big.empty() || !small.empty()) {
+  if (!big.empty() || !small.empty() || !huge.empty()) {
     double fl = 0, by = 0;
     if (C.prof)
-      for (auto* v : {&big, &small})
+      for (auto* v : {&big, &small, &huge})
         for (auto& it : *v) {  // Gram on the short side + tridiagonalisation (reference's work)
           const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
           fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
@@ -522,10 +535,15 @@ void NormBatch::run_async(Ctx& C) {
       cuda_check(launch_norm_warp(d_small, d_s, (int)small.size(), C.st), "norm_warp");
       ++C.launches;
     }
+    if (!huge.empty()) {
+      cuda_check(launch_norm(C.push(huge), d_s, (int)huge.size(), smem_g, C.st), "norm(global gram)");
+      ++C.launches;
+    }
     C.prof_end(K_NORM, ev, fl, by);
   }
   items.clear();
   sl.segs.clear();
+  if (local) scratch = nullptr;
 }
 
 std::vector<double> NormBatch::run(Ctx& C, Arena& scratch) {

@@ -43,7 +43,7 @@ size_t qr_smem(int n, bool rsmem);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t merge_smem(int n, bool rsmem);
 size_t svd_finish_smem(int m, int kx, bool rsmem);
-size_t norm_smem(int m, long long N);
+size_t norm_smem(int m, long long N, bool gram_in_smem = true);
 
 // ------------------------------------------------------------------ structure
 struct Tree {
@@ -321,6 +321,7 @@ struct NormBatch {
   std::vector<double> run(Ctx& C, Arena& scratch);  // sync + values
   // no host synchronisation: each item writes sigma_1 to its preset `out` (caller zero-fills)
   void run_async(Ctx& C);
+  Arena* scratch = nullptr;  // for Gram matrices of large items (else a local arena)
 };
 
 struct SvdBatch {
@@ -421,6 +422,11 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale);
 void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool accumulate);
+std::shared_ptr<H2> build_kernel_h2(Ctx& C, std::shared_ptr<const Blocks> bt, int kind, int dim,
+                                    const double* points, const double* weights, const long long* rank,
+                                    const long long* loff, const long long* xoff, const double* basis,
+                                    long long basis_len, const long long* node_off, const double* nodes,
+                                    long long nodes_len);
 std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank);
 
 }  // namespace h2g

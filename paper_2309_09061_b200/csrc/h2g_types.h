@@ -121,6 +121,7 @@ struct NormItem {
   int s0, s1, m, pad_;
   long long N;
   double* out;
+  double* gbuf;  // optional global scratch for the Gram matrix (large items); null: shared memory
 };
 
 // Device-side expansion of the product assembly (reference induced.py:286-307): one GTerm per

@@ -1020,8 +1020,8 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
   }
   const bool rowside = (m <= N) || (m <= 160);
   const int g = rowside ? m : (int)N;
-  double* G = smem;                       // g x g
-  double* Pn = G + (long long)g * g;      // 32 x max(m, N) panel
+  double* G = it.gbuf ? it.gbuf : smem;                  // g x g (global scratch for large items)
+  double* Pn = it.gbuf ? smem : G + (long long)g * g;    // 32 x max(m, N) panel
   double* d = Pn + kPanel * (rowside ? m : (int)N);
   double* e = d + g;
   double* v = e + g;
@@ -1561,11 +1561,11 @@ cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, boo
   return cudaGetLastError();
 }
 
-size_t norm_smem(int m, long long N) {
+size_t norm_smem(int m, long long N, bool gram_in_smem) {
   const bool rowside = (m <= N) || (m <= 160);
   const int g = rowside ? m : (int)N;
   const int w = rowside ? m : (int)N;
-  return sizeof(double) * ((size_t)g * g + (size_t)kPanel * w + 4 * (size_t)g);
+  return sizeof(double) * ((gram_in_smem ? (size_t)g * g : 0) + (size_t)kPanel * w + 4 * (size_t)g);
 }
 
 cudaError_t launch_norm(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {

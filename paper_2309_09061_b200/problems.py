@@ -18,7 +18,7 @@ from .errors import InvalidInputError
 from .h2 import ClusterBasis, H2Matrix
 from .trees import build_block_tree, build_cluster_tree
 
-__all__ = ["CONFIGS", "KERNEL_FNS", "make_points", "build_interpolation_h2", "build_config"]
+__all__ = ["CONFIGS", "KERNEL_FNS", "make_points", "build_interpolation_h2", "build_config", "build_config_device"]
 
 _FLAT_AXIS = 1e-8  # reference problems.py:40
 
@@ -174,3 +174,69 @@ def build_config(name: str, n: int | None = None, seed: int = 0):
     else:
         y = build_interpolation_h2(tree, blocks, w, KERNEL_FNS[spec["kernel_y"]], spec["order"])
     return x, y, spec
+
+
+KERNEL_IDS = {"log": 0, "slp": 1, "inv_r": 2, "exp_r": 3}  # h2g_h2_build_kernel ids
+
+
+def _interp_basis_packed(tree, weights_perm, order):
+    """Host interpolation basis in the packed layout plus the per-cluster Chebyshev grids."""
+    interp = _TensorInterp(tree, order)
+    rank = np.asarray([interp.points[t].shape[0] for t in range(tree.nnodes)], dtype=np.int64)
+    f = tree.flat()
+    loff = np.full(tree.nnodes, -1, np.int64)
+    xoff = np.full(tree.nnodes, -1, np.int64)
+    chunks, off = [], 0
+    for t in range(tree.nnodes):
+        if tree.is_leaf(t):
+            sl = tree.index_range(t)
+            m = interp.eval(t, tree.points[sl]) * weights_perm[sl, None]
+            loff[t] = off
+            chunks.append(m.ravel())
+            off += m.size
+    for t in range(tree.nnodes):
+        p = f["parent"][t]
+        if p >= 0:
+            m = interp.eval(p, interp.points[t])
+            xoff[t] = off
+            chunks.append(m.ravel())
+            off += m.size
+    data = np.concatenate(chunks) if chunks else np.zeros(0)
+    noff = np.zeros(tree.nnodes, np.int64)
+    grids, o = [], 0
+    for t in range(tree.nnodes):
+        noff[t] = o
+        grids.append(np.ascontiguousarray(interp.points[t], dtype=np.float64).ravel())
+        o += interp.points[t].size
+    return rank, loff, xoff, data, noff, np.concatenate(grids)
+
+
+def build_config_device(name: str, n: int | None = None, seed: int = 0, ctx=None):
+    """Raw inputs X, Y of a BASELINE config built on the GPU: structure and the
+    small interpolation bases on the host, the couplings and nearfield blocks evaluated by
+    h2g_h2_build_kernel.  Returns (dx_raw, dy_raw, spec) as DeviceH2 (dy is dx when X = Y)."""
+    import ctypes as C
+    from . import _native as N
+    from .device import DeviceH2, default_context
+    spec = dict(CONFIGS[name])
+    n = spec["n"] if n is None else int(n)
+    spec["n"] = n
+    ctx = ctx or default_context()
+    pts, wts = make_points(spec["geometry"], n, seed)
+    tree = build_cluster_tree(pts, spec["leaf"])
+    blocks = build_block_tree(tree, tree, spec["eta"])
+    w = np.ascontiguousarray(wts[tree.perm], dtype=np.float64)
+    P = np.ascontiguousarray(tree.points, dtype=np.float64)
+    rank, loff, xoff, data, noff, nodes = _interp_basis_packed(tree, w, spec["order"])
+    hb = ctx.blocks(blocks)
+
+    def make(kernel):
+        h = N.P()
+        N.check(ctx.lib.h2g_h2_build_kernel(
+            ctx.h, hb, KERNEL_IDS[kernel], P.shape[1], N.f64(P)[1], N.f64(w)[1], N.i64(rank)[1], N.i64(loff)[1],
+            N.i64(xoff)[1], N.f64(data)[1], len(data), N.i64(noff)[1], N.f64(nodes)[1], len(nodes), C.byref(h)))
+        return DeviceH2(ctx, h, blocks, tree, tree)
+
+    dx = make(spec["kernel_x"])
+    dy = dx if spec["kernel_y"] == spec["kernel_x"] else make(spec["kernel_y"])
+    return dx, dy, spec

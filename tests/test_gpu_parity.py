@@ -225,3 +225,23 @@ def test_gpu_error_estimate_matches_reference(name):
         assert est <= 1e-12
     else:
         assert abs(est - ref) <= 1e-4 * ref
+
+
+@pytest.mark.parametrize("name,n", [("c2", 2048), ("c3", 2048), ("c4", 4096)])
+def test_gpu_input_builder_matches_host(name, n):
+    """GPU kernel evaluation (h2g_h2_build_kernel) reproduces the host builder (problems.py:295-332),
+    and its recompressed input has the reference's per-cluster ranks."""
+    P = _P()
+    import torch
+    from paper_2309_09061_b200.problems import build_config, build_config_device
+    xr, yr, spec = build_config(name, n=n)
+    dxr, dyr, _ = build_config_device(name, n=n)
+    hx = P.DeviceH2.upload(xr)
+    v = torch.from_numpy(np.random.default_rng(7).standard_normal(n)).cuda()
+    assert rel(dxr.matvec(v).cpu().numpy(), hx.matvec(v).cpu().numpy()) <= 1e-13
+    if yr is not xr:
+        hy = P.DeviceH2.upload(yr)
+        assert rel(dyr.matvec(v).cpu().numpy(), hy.matvec(v).cpu().numpy()) <= 1e-13
+    d = load(name)
+    x = P.recompress(dxr, spec["eps"])
+    assert list(x.download().row_basis.rank) == list(d["rank.x_row"])
