@@ -489,13 +489,19 @@ void NormBatch::run_async(Ctx& C) {
   size_t smem = 0, smem_g = 0;
   // small: single segment, both sides <= 64 / 128 (warp Lanczos); big: CTA Gram in shared memory;
   // huge: CTA Gram in global scratch
-  std::vector<NormItem> big, small, huge;
+  std::vector<NormItem> big, small, huge, mid;  // mid: single segment up to 128 x 128 (CTA Lanczos)
+  size_t smem_mid = 0;
   std::unique_ptr<Arena> local;
   for (auto& it : items) {
     if (it.m == 0 || it.N == 0) continue;
     const long long mn = std::min<long long>(it.m, it.N), mx = std::max<long long>(it.m, it.N);
     if (it.s1 - it.s0 == 1 && mn <= 64 && mx <= 128 && it.m * (it.N | 1) <= 64 * 65) {
       small.push_back(it);
+      continue;
+    }
+    if (it.s1 - it.s0 == 1 && it.m <= 128 && it.N <= 128) {
+      smem_mid = std::max(smem_mid, norm_cta_smem(it.m, (int)it.N));
+      mid.push_back(it);
       continue;
     }
     const bool rowside = (it.m <= it.N) || (it.m <= 160);
@@ -514,10 +520,10 @@ void NormBatch::run_async(Ctx& C) {
     smem_g = std::max(smem_g, norm_smem(it.m, it.N, false));
     huge.push_back(it);
   }
-  if (!big.empty() || !small.empty() || !huge.empty()) {
+  if (!big.empty() || !small.empty() || !huge.empty() || !mid.empty()) {
     double fl = 0, by = 0;
     if (C.prof)
-      for (auto* v : {&big, &small, &huge})
+      for (auto* v : {&big, &small, &huge, &mid})
         for (auto& it : *v) {  // Gram on the short side + tridiagonalisation (reference's work)
           const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
           fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
@@ -537,6 +543,10 @@ void NormBatch::run_async(Ctx& C) {
     }
     if (!huge.empty()) {
       cuda_check(launch_norm(C.push(huge), d_s, (int)huge.size(), smem_g, C.st), "norm(global gram)");
+      ++C.launches;
+    }
+    if (!mid.empty()) {
+      cuda_check(launch_norm_cta(C.push(mid), d_s, (int)mid.size(), smem_mid, C.st), "norm_cta");
       ++C.launches;
     }
     C.prof_end(K_NORM, ev, fl, by);

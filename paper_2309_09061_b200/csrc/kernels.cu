@@ -1390,6 +1390,168 @@ cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems,
 }
 
 // ---------------------------------------------------------------------------------------------
+// norm_cta_kernel: sigma_1 of a single-segment matrix with m, N <= 128 (e.g. 128 x 128 nearfield
+// blocks): one CTA per matrix, A in shared memory, Lanczos on the smaller Gram side with the same
+// early exit as the warp version.  Matvecs: thread per row (u = B v) and thread per column
+// (w = B^T u), each split over two thread halves; odd row stride keeps both conflict-free.
+// ---------------------------------------------------------------------------------------------
+
+static constexpr int kNC = 128;  // max side
+static constexpr int kNCThreads = 256;
+
+__global__ void __launch_bounds__(kNCThreads) norm_cta_kernel(const NormItem* __restrict__ items,
+                                                              const Seg* __restrict__ segs) {
+  extern __shared__ double smem[];
+  __shared__ double red[kNCThreads / 32 + 2];
+  __shared__ double lam_s;
+  __shared__ int stop_s;
+  const NormItem it = items[blockIdx.x];
+  const Seg sg = segs[it.s0];
+  const int m = it.m, N = (int)it.N, ld = N | 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  double* A = smem;                  // m x ld
+  double* v = A + (size_t)m * ld;    // g
+  double* u = v + kNC;               // h
+  double* part = u + kNC;            // 2 x kNC partial sums
+  double* al = part + 2 * kNC;       // Lanczos diagonal
+  double* be = al + kNC;             // off-diagonal
+  const double ssc = seg_scale(sg);
+  double amax = 0.0;
+  for (int e = tid; e < m * N; e += blockDim.x) {
+    const int i = e / N, j = e % N;
+    const double x = ssc * mref(sg.a, i, j);
+    A[i * ld + j] = x;
+    amax = fmax(amax, fabs(x));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) red[warp] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int w = 0; w < nw; ++w) a = fmax(a, red[w]);
+    red[nw] = a;
+  }
+  __syncthreads();
+  if (red[nw] == 0.0) {
+    if (tid == 0) *it.out = 0.0;
+    return;
+  }
+  const bool colside = N <= m;  // Lanczos vectors on the smaller side
+  const int g = colside ? N : m, h = colside ? m : N;
+  // deterministic pseudo-random positive start vector (as norm_warp_kernel)
+  for (int i = tid; i < g; i += blockDim.x) {
+    unsigned x = 2654435761u * (i + 1) ^ (i < 32 ? 0x9e3779b9u : 0x85ebca6bu);
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    v[i] = 0.5 + (double)(x & 0xffff) / 65536.0;
+  }
+  __syncthreads();
+  auto block_sum = [&](double x) -> double {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = x;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    return s;
+  };
+  {
+    const double nv = sqrt(block_sum(tid < g ? v[tid] * v[tid] : 0.0));
+    if (tid < g) v[tid] /= nv;
+    __syncthreads();
+  }
+  const int half = tid >> 7, hi = tid & 127;  // two halves of 128 threads
+  double vprev = 0.0, bprev = 0.0, theta = 0.0, done = -1.0;
+  int k = 0;
+  for (; k < g; ++k) {
+    // u = B v (length h), B = A (colside) or A^T: thread per entry, k-range split in halves
+    if (hi < h) {
+      double s0 = 0.0, s1 = 0.0;
+      const int j0 = half ? g / 2 : 0, j1 = half ? g : g / 2;
+      int j = j0;
+      if (colside) {
+        const double* ar = A + hi * ld;
+        for (; j + 1 < j1; j += 2) { s0 = fma(ar[j], v[j], s0); s1 = fma(ar[j + 1], v[j + 1], s1); }
+        if (j < j1) s0 = fma(ar[j], v[j], s0);
+      } else {
+        for (; j + 1 < j1; j += 2) { s0 = fma(A[j * ld + hi], v[j], s0); s1 = fma(A[(j + 1) * ld + hi], v[j + 1], s1); }
+        if (j < j1) s0 = fma(A[j * ld + hi], v[j], s0);
+      }
+      part[half * kNC + hi] = s0 + s1;
+    }
+    __syncthreads();
+    if (tid < h) u[tid] = part[tid] + part[kNC + tid];
+    __syncthreads();
+    // w = B^T u (length g)
+    double wv = 0.0;
+    if (hi < g) {
+      double s0 = 0.0, s1 = 0.0;
+      const int i0 = half ? h / 2 : 0, i1 = half ? h : h / 2;
+      int i = i0;
+      if (colside) {
+        for (; i + 1 < i1; i += 2) { s0 = fma(A[i * ld + hi], u[i], s0); s1 = fma(A[(i + 1) * ld + hi], u[i + 1], s1); }
+        if (i < i1) s0 = fma(A[i * ld + hi], u[i], s0);
+      } else {
+        const double* ar = A + hi * ld;
+        for (; i + 1 < i1; i += 2) { s0 = fma(ar[i], u[i], s0); s1 = fma(ar[i + 1], u[i + 1], s1); }
+        if (i < i1) s0 = fma(ar[i], u[i], s0);
+      }
+      part[half * kNC + hi] = s0 + s1;
+    }
+    __syncthreads();
+    const double vi = tid < g ? v[tid] : 0.0;
+    if (tid < g) wv = part[tid] + part[kNC + tid];
+    const double a = block_sum(wv * vi);
+    if (tid < g) wv -= a * vi + bprev * vprev;
+    const double b = sqrt(block_sum(tid < g ? wv * wv : 0.0));
+    if (tid == 0) al[k] = a;
+    if (k + 1 == g || b <= 1e-15 * (fabs(a) + bprev)) {
+      ++k;
+      break;
+    }
+    if (tid == 0) be[k] = b;
+    if ((k & 1) == 1 && k >= 5) {  // top Ritz value settled to 1e-14 relative: stop
+      __syncthreads();
+      if (warp == 0) {
+        const double th = warp_lambda_max(al, be, k + 1);
+        if (lane == 0) {
+          lam_s = th;
+          stop_s = th - theta <= 1e-14 * th;
+        }
+      }
+      __syncthreads();
+      if (stop_s) {
+        done = lam_s;
+        break;
+      }
+      theta = lam_s;
+    }
+    vprev = vi;
+    bprev = b;
+    __syncthreads();
+    if (tid < g) v[tid] = wv / b;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double lam = done >= 0.0 ? done : warp_lambda_max(al, be, k);
+    if (lane == 0) *it.out = sqrt(fmax(lam, 0.0));
+  }
+}
+
+size_t norm_cta_smem(int m, int N) {
+  return sizeof(double) * ((size_t)m * (N | 1) + 6 * (size_t)kNC);
+}
+
+cudaError_t launch_norm_cta(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
+  init_attributes();
+  if (nitems == 0) return cudaSuccess;
+  norm_cta_kernel<<<nitems, kNCThreads, smem, st>>>(items, segs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // gather: items (src, count, dst) as int64 triples; one CTA per item (packing for download)
 // ---------------------------------------------------------------------------------------------
 
@@ -1489,6 +1651,7 @@ static void init_attributes() {
     opt_in((const void*)svd_finish_kernel<16>);
     opt_in((const void*)norm_kernel);
     opt_in((const void*)norm_warp_kernel);
+    opt_in((const void*)norm_cta_kernel);
   });
 }
 
