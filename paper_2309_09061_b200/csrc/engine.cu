@@ -411,7 +411,7 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
       it.nchunk = (int)((it.M + per - 1) / per);
       it.rbuf = scratch.alloc((size_t)it.nchunk * it.n * it.n);
       const int ti = (int)titems.size();
-      titems.push_back(TileItem{it.s0, it.s1, it.n, it.n, 0, 0, nullptr});
+      titems.push_back(TileItem{it.s0, it.s1, it.n, it.n, 0, 0, nullptr});  // no projection
       for (int c = 0; c < it.nchunk; ++c) {
         TileWork w{};
         w.item = ti;
@@ -599,14 +599,15 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
       const long long per = 128LL * tpc;
       it.nchunk = (int)std::max<long long>(1, (it.N + per - 1) / per);
       it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
-      it.q2 = (it.kx > 0 && n > 0) ? scratch.alloc((size_t)it.m * n) : nullptr;
+      it.q2 = it.kx > 0 ? scratch.alloc((size_t)it.m * it.m) : nullptr;
       if (it.kx > 0) {
         prep_ids.push_back((int)live.size());
-        sm_prep = std::max(sm_prep, svd_prep_smem(it.m, it.kx));
+        const size_t full = svd_prep_smem(it.m, it.kx, true);
+        sm_prep = std::max(sm_prep, full <= kSmemLimit ? full : svd_prep_smem(it.m, it.kx, false));
       }
       if (n > 0) {
         const int ti = (int)titems.size();
-        titems.push_back(TileItem{it.s0, it.s1, n, it.kx > 0 ? it.m : n, 1, 0, it.q2});
+        titems.push_back(TileItem{it.s0, it.s1, n, it.kx > 0 ? it.m : n, 1, it.m, it.q2 ? it.q2 + k1 : nullptr});
         for (int c = 0; c < it.nchunk; ++c) {
           TileWork w{};
           w.item = ti;

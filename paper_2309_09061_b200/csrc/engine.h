@@ -40,7 +40,7 @@ cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaS
 cudaError_t launch_tile_absorb(const TileItem*, const Seg*, const TileWork*, int nwork, int nmax, cudaStream_t);
 cudaError_t launch_svd_prep(const SvdItem*, const int* ids, int nids, size_t smem, cudaStream_t);
 size_t tile_absorb_smem(int n);
-size_t svd_prep_smem(int m, int kx);
+size_t svd_prep_smem(int m, int kx, bool with_q = true);
 size_t qr_smem(int n, bool rsmem);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t merge_smem(int n, bool rsmem);

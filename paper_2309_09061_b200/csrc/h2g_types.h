@@ -90,15 +90,15 @@ struct SvdItem {
   double* vws;      // m x kx Householder vectors of V + kx coefficients
   int* sweeps_out;  // optional diagnostic: Jacobi sweeps used, n, live rows, k2
   int pad2_;
-  double* q2;       // tile path with kx > 0: Q_V[:, k1:] (m x n), written by svd_prep_kernel
+  double* q2;       // tile path with kx > 0: explicit Q_V (m x m), written by svd_prep_kernel
 };
 
 // Register-tile TSQR (tileqr.cu): one item = one stacked operand reduced to an n x n R factor
 // (n <= 128).  Lines are rows of vstack(segs) (hcols = 0) or columns of hstack(segs)
 // (hcols = 1); each line contributes kdim source entries, projected onto q2 (kdim x n) if given.
 struct TileItem {
-  int s0, s1, n, kdim, hcols, pad_;
-  const double* q2;
+  int s0, s1, n, kdim, hcols, q2ld;
+  const double* q2;  // kdim x n, leading dimension q2ld
 };
 
 // One CTA: absorb lines [l0, l1) (128 per tile) into R (starting from rinit, else zero) and

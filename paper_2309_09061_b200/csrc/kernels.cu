@@ -366,13 +366,17 @@ __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga,
   const double d = be - al, g2 = 2.0 * ga;
   const double ad = fabs(d), ag = fabs(g2);
   double t;
-  if (ad > 1e150 || ag > 1e150) {  // avoid overflow of d^2 + g2^2
+  const double mx = fmax(ad, ag);
+  if (mx > 1e150 || mx < 1e-150) {  // far from 1: scale-free form (no over/underflow of d^2 + g2^2)
     const double zeta = d / g2, az = fabs(zeta);
     const double t0 = az > 1e150 ? 0.5 / az : 1.0 / (az + sqrt(fma(az, az, 1.0)));
     t = zeta >= 0.0 ? t0 : -t0;
   } else {
-    const double r = sqrt(fma(d, d, g2 * g2));
-    t = g2 / (ad + r);
+    // r = |(d, g2)| and 1 / (|d| + r) by reciprocal square root / reciprocal (short dependent
+    // chains); t only steers the rotation, its orthogonality comes from c = 1 / sqrt(1 + t^2)
+    const double r2 = fma(d, d, g2 * g2);
+    const double r = r2 * rsqrt(r2);
+    t = g2 * __drcp_rn(ad + r);
     if (d < 0.0) t = -t;
   }
   c = rsqrt(fma(t, t, 1.0));
@@ -916,6 +920,31 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
   __syncthreads();
   const int kt = k1 + k2;
   double* Q = it.q_out;  // m x kt
+  if (it.q2) {
+    // explicit Q_V from svd_prep_kernel: Q_t = [Q_V[:, :k1] | Q_V[:, k1:] U], U = normalised rows of
+    // R1 (singular order) mapped back through the column pivoting -- one small product instead of
+    // k1 sequential reflector applications per column
+    for (long long e = threadIdx.x; e < (long long)m * kt; e += blockDim.x) {
+      const int i = (int)(e / kt), j = (int)(e % kt);
+      const double* qrow = it.q2 + (long long)i * m;
+      double val;
+      if (j < k1) {
+        val = qrow[j];
+      } else {
+        const int src = ord[j - k1];
+        const double* rr = R + (long long)src * n;
+        double s0 = 0.0, s1 = 0.0;
+        int l = 0;
+        for (; l + 1 < n; l += 2) {
+          s0 = fma(qrow[k1 + l], rr[iperm[l]], s0);
+          s1 = fma(qrow[k1 + l + 1], rr[iperm[l + 1]], s1);
+        }
+        if (l < n) s0 = fma(qrow[k1 + l], rr[iperm[l]], s0);
+        val = (s0 + s1) / sig[src];
+      }
+      Q[e] = val;
+    }
+  } else {
   for (long long e = threadIdx.x; e < (long long)m * kt; e += blockDim.x) {
     const int i = (int)(e / kt), j = (int)(e % kt);
     double val;
@@ -933,6 +962,7 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
     for (int c = warp; c < kt; c += nw)
       for (int j = k1 - 1; j >= 0; --j)
         if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], Q, kt, c);
+  }
   }
   if (it.bc_out) {
     for (int e = threadIdx.x; e < kt * kx; e += blockDim.x) {

@@ -76,7 +76,8 @@ size_t tile_absorb_smem(int n) {
 }
 
 // Staged slice element (k, r): source column k0 + k of line r (k < kk_lim), zero beyond.
-__device__ __forceinline__ void stage_slice(const Layout& L, int hcols, int k0, int kdim, const double* q2, int n) {
+__device__ __forceinline__ void stage_slice(const Layout& L, int hcols, int k0, int kdim, const double* q2, int q2ld,
+                                            int n) {
   const int nt = blockDim.x;
   const int klim = min(kKs, kdim - k0);
   for (int e = threadIdx.x; e < kKs * kRows; e += nt) {
@@ -91,7 +92,7 @@ __device__ __forceinline__ void stage_slice(const Layout& L, int hcols, int k0, 
   if (q2)
     for (int e = threadIdx.x; e < kKs * n; e += nt) {
       const int k = e / n, c = e % n;
-      L.Qs[e] = k < klim ? q2[(long long)(k0 + k) * n + c] : 0.0;
+      L.Qs[e] = k < klim ? q2[(long long)(k0 + k) * q2ld + c] : 0.0;
     }
 }
 
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
       }
       __syncthreads();
       for (int k0 = 0; k0 < it.kdim; k0 += kKs) {
-        stage_slice(L, it.hcols, k0, it.kdim, it.q2, n);
+        stage_slice(L, it.hcols, k0, it.kdim, it.q2, it.q2ld, n);
         __syncthreads();
         if (live) {
           const double* a = L.As + sub * kSubLd;
@@ -239,8 +240,9 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
 }
 
 // Protected-SVD preparation, one CTA per item with kx > 0: Householder QR of V (m x kx) into
-// it.vws (reflectors + tau, consumed by svd_finish_kernel) and Q2 = Q_V[:, k1:] (m x n, row
-// major) into it.q2, the projection the tiles apply (B^T = A^T Q2).
+// it.vws (reflectors + tau) and the explicit Q_V (m x m, row major) into it.q2: its last n
+// columns Q2 = Q_V[:, k1:] are the projection the tiles apply (B^T = A^T Q2), its first k1 and
+// Q2 U give svd_finish_kernel's output Q_t = Q_V [[I, 0], [0, U]] as one product.
 __device__ void prep_qr_cols(double* V, int m, int kx, int ldv, int k1, double* tv, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = 0; j < k1; ++j) {
@@ -285,29 +287,33 @@ __device__ void prep_qr_cols(double* V, int m, int kx, int ldv, int k1, double* 
   }
 }
 
-__global__ void __launch_bounds__(512) svd_prep_kernel(const SvdItem* __restrict__ items, const int* __restrict__ ids) {
+__global__ void __launch_bounds__(512) svd_prep_kernel(const SvdItem* __restrict__ items, const int* __restrict__ ids,
+                                                       size_t smem_bytes) {
   extern __shared__ double smem[];
   __shared__ double red[20];
   const SvdItem it = items[ids[blockIdx.x]];
-  const int m = it.m, kx = it.kx, k1 = min(m, kx), n = m - k1;
-  const int ldv = kx | 1, ldx = n | 1;
+  const int m = it.m, kx = it.kx, k1 = min(m, kx);
+  const int ldv = kx | 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   double* V = smem;
   double* tv = V + (size_t)m * ldv;
-  double* X = tv + kx + 1;
+  // Q_V built in shared memory when it fits, else in place in the output buffer
+  const bool xs = sizeof(double) * ((size_t)m * ldv + kx + 1 + (size_t)m * (m | 1)) <= smem_bytes;
+  const int ldx = xs ? (m | 1) : m;
+  double* X = xs ? tv + kx + 1 : it.q2;
   for (int e = threadIdx.x; e < m * kx; e += blockDim.x) V[(e / kx) * ldv + e % kx] = it.v.p[(long long)(e / kx) * it.v.rs + (long long)(e % kx) * it.v.cs];
   __syncthreads();
   prep_qr_cols(V, m, kx, ldv, k1, tv, red);
   for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) it.vws[e] = V[e];
   for (int e = threadIdx.x; e < kx; e += blockDim.x) it.vws[m * ldv + e] = tv[e];
-  if (n == 0 || !it.q2) return;
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    X[i * ldx + j] = (i == k1 + j) ? 1.0 : 0.0;
+  if (!it.q2) return;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e % m;
+    X[i * ldx + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // Q2 = H_0 H_1 .. H_{k1-1} E: reflectors in reverse order, one warp per column
-  for (int c = warp; c < n; c += nw)
+  // Q_V = H_0 H_1 .. H_{k1-1} I (m x m): reflectors in reverse order, one warp per column
+  for (int c = warp; c < m; c += nw)
     for (int j = k1 - 1; j >= 0; --j) {
       const double tau = tv[j];
       if (tau == 0.0) continue;
@@ -322,12 +328,12 @@ __global__ void __launch_bounds__(512) svd_prep_kernel(const SvdItem* __restrict
       __syncwarp();
     }
   __syncthreads();
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) it.q2[e] = X[(e / n) * ldx + e % n];
+  if (xs)
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) it.q2[e] = X[(e / m) * ldx + e % m];
 }
 
-size_t svd_prep_smem(int m, int kx) {
-  const int k1 = m < kx ? m : kx, n = m - k1;
-  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + (size_t)m * (n | 1));
+size_t svd_prep_smem(int m, int kx, bool with_q) {
+  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + (with_q ? (size_t)m * (m | 1) : 0));
 }
 
 static void tile_attributes() {
@@ -354,7 +360,7 @@ cudaError_t launch_tile_absorb(const TileItem* items, const Seg* segs, const Til
 cudaError_t launch_svd_prep(const SvdItem* items, const int* ids, int nids, size_t smem, cudaStream_t st) {
   tile_attributes();
   if (nids == 0) return cudaSuccess;
-  svd_prep_kernel<<<nids, 512, smem, st>>>(items, ids);
+  svd_prep_kernel<<<nids, 512, smem, st>>>(items, ids, smem);
   return cudaGetLastError();
 }
 
