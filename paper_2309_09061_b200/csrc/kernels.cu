@@ -796,8 +796,8 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
       if (ss != 0.0) {
         const double nrm = sqrt(alpha * alpha + ss);
         const double beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+        tau = (beta - alpha) * __drcp_rn(beta);
+        scale = __drcp_rn(alpha - beta);
       }
       for (int i = j + 1 + lane; i < n; i += 32) {
         vh[i] = W[(long long)i * n + j] * scale;
@@ -810,25 +810,49 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
     }
     __syncthreads();
     const double tau = red[nw + 1];
-    for (int c = j + 1 + tid; c < n; c += nt) {
-      if (tau != 0.0) {
-        double w0 = W[(long long)j * n + c], w1 = 0.0;
-        int i = j + 1;
-        for (; i + 1 < n; i += 2) {
-          w0 = fma(vh[i], W[(long long)i * n + c], w0);
-          w1 = fma(vh[i + 1], W[(long long)(i + 1) * n + c], w1);
+    // trailing update: four threads per column (rows split by residue mod 4, quad shuffles),
+    // so the dependent chain per column is a quarter of the remaining rows
+    {
+      const int sub = tid & 3;
+      const unsigned qmask = 0xfu << (lane & ~3);
+      for (int cb = j + 1; cb < n; cb += nt / 4) {
+        const int c = cb + (tid >> 2);
+        const bool act = c < n;
+        double tw = 0.0;
+        if (tau != 0.0) {
+          double w0 = 0.0, w1 = 0.0;
+          if (act) {
+            int i = j + 1 + sub;
+            for (; i + 4 < n; i += 8) {
+              w0 = fma(vh[i], W[(long long)i * n + c], w0);
+              w1 = fma(vh[i + 4], W[(long long)(i + 4) * n + c], w1);
+            }
+            if (i < n) w0 = fma(vh[i], W[(long long)i * n + c], w0);
+          }
+          double wv = w0 + w1;
+          wv += __shfl_xor_sync(qmask, wv, 1);
+          wv += __shfl_xor_sync(qmask, wv, 2);
+          if (act) {
+            tw = tau * (wv + W[(long long)j * n + c]);
+            for (int i2 = j + 1 + sub; i2 < n; i2 += 4) W[(long long)i2 * n + c] -= tw * vh[i2];
+          }
+          __syncwarp(qmask);  // row j of column c read by all four before the update below
+          if (act && sub == 0) W[(long long)j * n + c] -= tw;
+          __syncwarp(qmask);
         }
-        if (i < n) w0 = fma(vh[i], W[(long long)i * n + c], w0);
-        const double tw = tau * (w0 + w1);
-        W[(long long)j * n + c] -= tw;
-        for (int i2 = j + 1; i2 < n; ++i2) W[(long long)i2 * n + c] -= tw * vh[i2];
-      }
-      const double rj = W[(long long)j * n + c];
-      cn[c] -= rj * rj;
-      if (cn[c] <= 1e-2 * cn0[c]) {  // cancellation: recompute the trailing norm exactly
-        double s2 = 0.0;
-        for (int i2 = j + 1; i2 < n; ++i2) s2 = fma(W[(long long)i2 * n + c], W[(long long)i2 * n + c], s2);
-        cn[c] = cn0[c] = s2;
+        if (act) {
+          const double rj = W[(long long)j * n + c];
+          const bool recompute = cn[c] - rj * rj <= 1e-2 * cn0[c];
+          __syncwarp(qmask);
+          if (sub == 0) cn[c] -= rj * rj;
+          if (recompute) {  // cancellation: recompute the trailing norm exactly
+            double s2 = 0.0;
+            for (int i2 = j + 1 + sub; i2 < n; i2 += 4) s2 = fma(W[(long long)i2 * n + c], W[(long long)i2 * n + c], s2);
+            s2 += __shfl_xor_sync(qmask, s2, 1);
+            s2 += __shfl_xor_sync(qmask, s2, 2);
+            if (sub == 0) cn[c] = cn0[c] = s2;
+          }
+        }
       }
     }
     __syncthreads();

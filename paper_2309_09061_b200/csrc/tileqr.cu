@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
                                                           const TileWork* __restrict__ work) {
   extern __shared__ double smem[];
   __shared__ double tbuf[2];
+  __shared__ int s_sa, s_sb;
+  __shared__ long long g_off[kRows];  // staged segments of the current tile
+  __shared__ const double* g_p[kRows];
+  __shared__ int g_rs[kRows], g_cs[kRows];
+  __shared__ double g_sc[kRows];
   const TileWork w = work[blockIdx.x];
   const TileItem it = items[w.item];
   const int n = it.n;
@@ -126,19 +131,49 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
       }
       __syncthreads();
     } else {
-      // per-line source descriptors
+      // per-line source descriptors: the segments covering this tile's lines are located once
+      // (two binary searches in global memory) and staged in shared memory, every line then
+      // searches the staged offsets
+      const long long llast = min(l + kRows, w.l1) - 1;
+      if (t == 0) s_sa = llast >= l ? find_seg(segs, it.s0, it.s1, l) : 0;
+      if (t == 32 || (blockDim.x <= 32 && t == 0)) s_sb = llast >= l ? find_seg(segs, it.s0, it.s1, llast) : -1;
+      __syncthreads();
+      const int sa = s_sa, nseg = s_sb - s_sa + 1;
+      const bool staged = nseg <= kRows;
+      if (staged)
+        for (int i = t; i < nseg; i += blockDim.x) {
+          const Seg sg = segs[sa + i];
+          g_off[i] = sg.off;
+          g_p[i] = sg.a.p;
+          g_rs[i] = sg.a.rs;
+          g_cs[i] = sg.a.cs;
+          g_sc[i] = seg_scale(sg);
+        }
+      __syncthreads();
       for (int r = t; r < kRows; r += blockDim.x) {
         const long long line = l + r;
         const double* p = nullptr;
         long long st = 0;
         double sc = 0.0;
         if (line < w.l1) {
-          const int s = find_seg(segs, it.s0, it.s1, line);
-          const Seg sg = segs[s];
-          const long long loc = line - sg.off;
-          sc = seg_scale(sg);
-          if (it.hcols) { p = sg.a.p + loc * sg.a.cs; st = sg.a.rs; }
-          else { p = sg.a.p + loc * sg.a.rs; st = sg.a.cs; }
+          if (staged) {
+            int lo = 0, hi = nseg - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (g_off[mid] <= line) lo = mid; else hi = mid - 1;
+            }
+            const long long loc = line - g_off[lo];
+            sc = g_sc[lo];
+            if (it.hcols) { p = g_p[lo] + loc * g_cs[lo]; st = g_rs[lo]; }
+            else { p = g_p[lo] + loc * g_rs[lo]; st = g_cs[lo]; }
+          } else {
+            const int sidx = find_seg(segs, it.s0, it.s1, line);
+            const Seg sg = segs[sidx];
+            const long long loc = line - sg.off;
+            sc = seg_scale(sg);
+            if (it.hcols) { p = sg.a.p + loc * sg.a.cs; st = sg.a.rs; }
+            else { p = sg.a.p + loc * sg.a.rs; st = sg.a.cs; }
+          }
         }
         L.rp[r] = p;
         L.rst[r] = st;
@@ -181,9 +216,16 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
     for (int j = 0; j < n; ++j) {
       double* v = L.vb + buf * kLineLd;
       if (c == j) {
-        double s = 0.0;
+        // critical path of the step: four partial sums, reciprocals instead of divisions
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int i = 0; i < kRpt; ++i) s = fma(x[i], x[i], s);
+        for (int i = 0; i < kRpt; i += 4) {
+          s0 = fma(x[i], x[i], s0);
+          s1 = fma(x[i + 1], x[i + 1], s1);
+          s2 = fma(x[i + 2], x[i + 2], s2);
+          s3 = fma(x[i + 3], x[i + 3], s3);
+        }
+        double s = (s0 + s1) + (s2 + s3);
         s += __shfl_xor_sync(gmask, s, 1);
         s += __shfl_xor_sync(gmask, s, 2);
         const double alpha = L.R[j * n + j];
@@ -191,8 +233,8 @@ __global__ void __launch_bounds__(512) tile_absorb_kernel(const TileItem* __rest
         if (s != 0.0) {
           const double nrm = sqrt(fma(alpha, alpha, s));
           beta = alpha >= 0.0 ? -nrm : nrm;
-          tau = (beta - alpha) / beta;
-          scale = 1.0 / (alpha - beta);
+          tau = (beta - alpha) * __drcp_rn(beta);
+          scale = __drcp_rn(alpha - beta);
         }
         __syncwarp(gmask);  // every lane of the group has read R_jj
         if (sub == 0) L.R[j * n + j] = beta;
