@@ -129,6 +129,7 @@ std::shared_ptr<H2> build_kernel_h2(Ctx& C, std::shared_ptr<const Blocks> bt, in
   }
   if (!ev.empty()) {
     EvalBlock* d_ev = C.push(ev);
+    C.flush();
     eval_blocks_kernel<<<(unsigned)ev.size(), 256, 0, C.st>>>(d_ev, kind, dim);
     cuda_check(cudaGetLastError(), "eval_blocks_kernel");
     ++C.launches;

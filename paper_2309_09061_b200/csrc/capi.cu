@@ -310,6 +310,7 @@ struct Gather {
     double* d = ar.alloc(total);
     for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(d + items[i]);
     long long* di = C.push(items);
+    C.flush();
     cuda_check(launch_gather(di, (int)(items.size() / 3), C.st), "gather");
     cuda_check(cudaMemcpyAsync(host, d, total * sizeof(double), cudaMemcpyDeviceToHost, C.st), "download");
   }

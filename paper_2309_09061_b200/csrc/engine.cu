@@ -97,6 +97,7 @@ void Ctx::ensure_read(size_t bytes) {
 static std::mutex g_trace_mu;  // the main and side contexts share one trace vector
 
 void Ctx::sync() {
+  flush();
   HostTimer ht(*this, "sync_wait");
   const auto h0 = std::chrono::steady_clock::now();
   cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
@@ -108,6 +109,7 @@ void Ctx::sync() {
                                   std::chrono::duration<double, std::micro>(h1 - h0).count(), 0.0, tag});
   }
   stage_off = 0;
+  stage_flushed = 0;
   ++syncs;
   if (!pending.empty()) drain_prof();
 }
@@ -163,7 +165,7 @@ void Ctx::drain_prof() {
 void* Ctx::stage(const void* src, size_t bytes) {
   const size_t need = (bytes + 255) & ~size_t(255);
   if (stage_off + need > stage_cap) {
-    sync();
+    sync();  // flushes and drains: the whole buffer is free again
     if (need > stage_cap) {
       cudaFreeHost(hstage);
       cudaFree(dstage);
@@ -176,9 +178,17 @@ void* Ctx::stage(const void* src, size_t bytes) {
   char* d = dstage + stage_off;
   HostTimer ht(*this, "stage_memcpy");
   memcpy(h, src, bytes);
-  cuda_check(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st), "stage copy");
-  stage_off += need;
+  stage_off += need;  // copied to the device by the next flush() (one transfer per launch)
   return d;
+}
+
+void Ctx::flush() {
+  if (stage_off > stage_flushed) {
+    cuda_check(cudaMemcpyAsync(dstage + stage_flushed, hstage + stage_flushed, stage_off - stage_flushed,
+                               cudaMemcpyHostToDevice, st),
+               "stage copy");
+    stage_flushed = stage_off;
+  }
 }
 
 Ctx& Ctx::side() {
@@ -277,6 +287,7 @@ void GBatch::run(Ctx& C) {
     }
   }
   cudaEvent_t ev = C.prof_begin();
+  C.flush();
   cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
   C.prof_end(K_GSUM, ev, fl, by);
   ++C.launches;
@@ -299,6 +310,7 @@ void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
     GOut* d_o = C.push(outs);
     GTile* d_l = C.push(tiles);
     cudaEvent_t ev = C.prof_begin();
+    C.flush();
     cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st), "gsum");
     C.prof_end(K_GSUM, ev, flops_hint, 0.0);
     ++C.launches;
@@ -323,7 +335,9 @@ static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>&
     }
     if (lvl.empty()) continue;
     cudaEvent_t sv = C.sub_begin();
-    cuda_check(launch_tsqr_merge(C.push(lvl), (int)lvl.size(), smem, rsmem, C.st), "tsqr_merge");
+    MergeWork* d_lvl = C.push(lvl);
+    C.flush();
+    cuda_check(launch_tsqr_merge(d_lvl, (int)lvl.size(), smem, rsmem, C.st), "tsqr_merge");
     C.sub_end(S_MERGE, sv);
     ++C.launches;
   }
@@ -386,7 +400,9 @@ static void run_tile_merges(Ctx& C, const std::vector<std::tuple<double*, int, i
     }
     if (lvl.empty()) continue;
     cudaEvent_t sv = C.sub_begin();
-    cuda_check(launch_tile_absorb(d_items, nullptr, C.push(lvl), (int)lvl.size(), nmax, C.st), "tile_merge");
+    TileWork* d_lvl = C.push(lvl);
+    C.flush();
+    cuda_check(launch_tile_absorb(d_items, nullptr, d_lvl, (int)lvl.size(), nmax, C.st), "tile_merge");
     C.sub_end(S_MERGE, sv);
     ++C.launches;
   }
@@ -466,18 +482,22 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
   if (!work.empty()) {
+    C.flush();
     cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
     ++C.launches;
   }
   const TileItem* d_ti = nullptr;
   if (!twork.empty()) {
     d_ti = C.push(titems);
-    cuda_check(launch_tile_absorb(d_ti, d_s, C.push(twork), (int)twork.size(), tnmax, C.st), "tile_absorb");
+    TileWork* d_tw = C.push(twork);
+    C.flush();
+    cuda_check(launch_tile_absorb(d_ti, d_s, d_tw, (int)twork.size(), tnmax, C.st), "tile_absorb");
     ++C.launches;
   }
   C.sub_end(S_QR_CHUNK, sv);
   run_merges(C, parts, rsmem, sm_merge);
   if (!tparts.empty()) run_tile_merges(C, tparts, d_ti, tnmax);
+  C.flush();
   cuda_check(launch_qr_out(d_items, (int)live.size(), C.st), "qr_out");
   ++C.launches;
   C.prof_end(K_QR, ev, fl, by);
@@ -534,19 +554,25 @@ void NormBatch::run_async(Ctx& C) {
     NormItem* d_small = C.push(small);
     cudaEvent_t ev = C.prof_begin();
     if (!big.empty()) {
+      C.flush();
       cuda_check(launch_norm(d_big, d_s, (int)big.size(), smem, C.st), "norm");
       ++C.launches;
     }
     if (!small.empty()) {
+      C.flush();
       cuda_check(launch_norm_warp(d_small, d_s, (int)small.size(), C.st), "norm_warp");
       ++C.launches;
     }
     if (!huge.empty()) {
-      cuda_check(launch_norm(C.push(huge), d_s, (int)huge.size(), smem_g, C.st), "norm(global gram)");
+      NormItem* d_huge = C.push(huge);
+      C.flush();
+      cuda_check(launch_norm(d_huge, d_s, (int)huge.size(), smem_g, C.st), "norm(global gram)");
       ++C.launches;
     }
     if (!mid.empty()) {
-      cuda_check(launch_norm_cta(C.push(mid), d_s, (int)mid.size(), smem_mid, C.st), "norm_cta");
+      NormItem* d_mid = C.push(mid);
+      C.flush();
+      cuda_check(launch_norm_cta(d_mid, d_s, (int)mid.size(), smem_mid, C.st), "norm_cta");
       ++C.launches;
     }
     C.prof_end(K_NORM, ev, fl, by);
@@ -665,17 +691,22 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
   if (!work.empty()) {
+    C.flush();
     cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
     ++C.launches;
   }
   if (!prep_ids.empty()) {
-    cuda_check(launch_svd_prep(d_items, C.push(prep_ids), (int)prep_ids.size(), sm_prep, C.st), "svd_prep");
+    int* d_ids = C.push(prep_ids);
+    C.flush();
+    cuda_check(launch_svd_prep(d_items, d_ids, (int)prep_ids.size(), sm_prep, C.st), "svd_prep");
     ++C.launches;
   }
   const TileItem* d_ti = nullptr;
   if (!twork.empty()) {
     d_ti = C.push(titems);
-    cuda_check(launch_tile_absorb(d_ti, d_s, C.push(twork), (int)twork.size(), tnmax, C.st), "tile_absorb");
+    TileWork* d_tw = C.push(twork);
+    C.flush();
+    cuda_check(launch_tile_absorb(d_ti, d_s, d_tw, (int)twork.size(), tnmax, C.st), "tile_absorb");
     ++C.launches;
   }
   C.sub_end(S_SVD_TSQR, sv);
@@ -684,6 +715,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   cudaEvent_t sf = C.sub_begin();
   int fin_nmax = 0;
   for (auto& it : live) fin_nmax = std::max(fin_nmax, it.m - std::min(it.m, it.kx));
+  C.flush();
   cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, fin_nmax, C.st), "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;

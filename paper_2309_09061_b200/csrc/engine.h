@@ -182,7 +182,7 @@ struct Ctx {
   // pinned host staging and device staging for descriptors (reset at every host sync)
   char* hstage = nullptr;
   char* dstage = nullptr;
-  size_t stage_cap = 0, stage_off = 0;
+  size_t stage_cap = 0, stage_off = 0, stage_flushed = 0;
   char* hread = nullptr;  // pinned read-back area
   size_t read_cap = 0;
   long long launches = 0;  // kernels launched since the last reset
@@ -229,7 +229,8 @@ struct Ctx {
   ~Ctx();
   Ctx& side();
   void join_side(Ctx& S);  // main stream waits for the side stream's queued work
-  void* stage(const void* src, size_t bytes);  // returns device pointer (async copy enqueued)
+  void* stage(const void* src, size_t bytes);  // returns device pointer (copied at the next flush())
+  void flush();  // enqueue the host->device copy of everything staged since the last flush
   template <class T> T* push(const std::vector<T>& v) {
     return v.empty() ? nullptr : (T*)stage(v.data(), v.size() * sizeof(T));
   }

@@ -129,6 +129,7 @@ void MvBatch::run(Ctx& C) {
     MvTerm* d_t = C.push(terms);
     MvChunk* d_c = C.push(ch);
     int* d_p = C.push(cptr);
+    C.flush();
     ev = C.prof_begin();
     mv_chunk_kernel<<<(unsigned)ch.size(), kMvThreads, smem, C.st>>>(d_o, d_c, d_t, part, ldacc);
     cuda_check(cudaGetLastError(), "mv_chunk_kernel");
@@ -138,6 +139,7 @@ void MvBatch::run(Ctx& C) {
   } else {
     MvOut* d_o = C.push(outs);
     MvTerm* d_t = terms.empty() ? nullptr : C.push(terms);
+    C.flush();
     ev = C.prof_begin();
     mv_kernel<<<(unsigned)outs.size(), kMvThreads, smem, C.st>>>(d_o, d_t, ldacc);
     cuda_check(cudaGetLastError(), "mv_kernel");

@@ -379,6 +379,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     T.size_mid = C.push(size_mid);
     T.grouped = 1;
     GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
+    C.flush();
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
     C.sub_end(S_MISC, sw);
     ++C.launches;
