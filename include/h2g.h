@@ -75,6 +75,17 @@ int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt,
                   const double* cb_data, long long cb_len, int share_bases,
                   const long long* coup_off, const double* coup_data, long long coup_len,
                   const long long* near_off, const double* near_data, long long near_len, h2g_h2** out);
+/* same, but the nearfield array is copied asynchronously on the context's copy stream: the call
+   returns once bases and couplings are enqueued; kernels that read the nearfield wait for it on
+   the device. near_data must stay valid until the next synchronising call on the context
+   (h2g_h2_download, h2g_ctx_synchronize). */
+int h2g_h2_upload_async(h2g_ctx* ctx, h2g_blocks* bt,
+                        const long long* rb_rank, const long long* rb_leaf_off, const long long* rb_xfer_off,
+                        const double* rb_data, long long rb_len,
+                        const long long* cb_rank, const long long* cb_leaf_off, const long long* cb_xfer_off,
+                        const double* cb_data, long long cb_len, int share_bases,
+                        const long long* coup_off, const double* coup_data, long long coup_len,
+                        const long long* near_off, const double* near_data, long long near_len, h2g_h2** out);
 void h2g_h2_destroy(h2g_h2* h);
 /* out8 = {nblocks, row-tree nodes, col-tree nodes, rb_len, cb_len, coup_len, near_len, block child_idx len} */
 int h2g_h2_sizes(h2g_h2* h, long long* out8);

@@ -45,6 +45,9 @@ SIGNATURES = {
     "h2g_h2_upload": (C.c_int, [P, P, I64P, I64P, I64P, F64P, C.c_longlong, I64P, I64P, I64P, F64P,
                                 C.c_longlong, C.c_int, I64P, F64P, C.c_longlong, I64P, F64P, C.c_longlong,
                                 C.POINTER(P)]),
+    "h2g_h2_upload_async": (C.c_int, [P, P, I64P, I64P, I64P, F64P, C.c_longlong, I64P, I64P, I64P, F64P,
+                                C.c_longlong, C.c_int, I64P, F64P, C.c_longlong, I64P, F64P, C.c_longlong,
+                                C.POINTER(P)]),
     "h2g_h2_destroy": (None, [P]),
     "h2g_h2_sizes": (C.c_int, [P, I64P]),
     "h2g_h2_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, U8P]),

@@ -104,7 +104,9 @@ def multiply_coarsen_packed(xp: dict, x_tree: BlockTree, yp: dict | None = None,
     DeviceH2.packed_shapes() length) or fresh arrays.  Z's block tree is `coarse`."""
     _check_tol(tol)
     ctx = _ctx(ctx)
-    dx = DeviceH2.upload_packed(xp, x_tree, ctx)
-    dy = dx if yp is None else DeviceH2.upload_packed(yp, y_tree if y_tree is not None else x_tree, ctx)
+    # nearfield arrays stream in on the copy stream while the weights and bases are computed
+    dx = DeviceH2.upload_packed(xp, x_tree, ctx, asynchronous=True)
+    dy = dx if yp is None else DeviceH2.upload_packed(yp, y_tree if y_tree is not None else x_tree, ctx,
+                                                      asynchronous=True)
     z = multiply_coarsen(dx, dy, tol, coarse=coarse, max_rank=max_rank, ctx=ctx)
     return z.download_packed(out)

@@ -199,11 +199,12 @@ static std::shared_ptr<Basis> upload_basis(Ctx& C, Arena& ar, const Tree* tree, 
   return B;
 }
 
-int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
-                  const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
-                  const long long* cb_loff, const long long* cb_xoff, const double* cb_data, long long cb_len,
-                  int share, const long long* coup_off, const double* coup_data, long long coup_len,
-                  const long long* near_off, const double* near_data, long long near_len, h2g_h2** out) {
+static int upload_impl(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
+                       const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
+                       const long long* cb_loff, const long long* cb_xoff, const double* cb_data, long long cb_len,
+                       int share, const long long* coup_off, const double* coup_data, long long coup_len,
+                       const long long* near_off, const double* near_data, long long near_len, h2g_h2** out,
+                       bool async_near) {
   return guarded([&] {
     Ctx& C = ctx->c;
     auto h = std::make_shared<H2>();
@@ -224,8 +225,22 @@ int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const 
     double* dn = ar->alloc(near_len > 0 ? near_len : 1);
     if (coup_len > 0)
       cuda_check(cudaMemcpyAsync(dc, coup_data, coup_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
-    if (near_len > 0)
-      cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
+    if (near_len > 0) {
+      if (async_near) {  // the nearfield streams in on the copy stream while the product starts
+        if (!C.up_stream) cuda_check(cudaStreamCreateWithFlags(&C.up_stream, cudaStreamNonBlocking), "stream");
+        cudaEvent_t alloc_done;
+        cuda_check(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(alloc_done, C.st), "event");
+        cuda_check(cudaStreamWaitEvent(C.up_stream, alloc_done, 0), "wait");
+        cudaEventDestroy(alloc_done);
+        cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.up_stream),
+                   "upload");
+        cuda_check(cudaEventCreateWithFlags(&h->near_ready, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(h->near_ready, C.up_stream), "event");
+      } else {
+        cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
+      }
+    }
     h->coup.assign(B.nb, nullptr);
     h->near.assign(B.nb, nullptr);
     for (int b = 0; b < B.nb; ++b) {
@@ -241,9 +256,27 @@ int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const 
         h->near[b] = dn + near_off[b];
       }
     }
-    C.sync();  // host arrays may be released by the caller after return
+    if (!async_near) C.sync();  // host arrays may be released by the caller after return
     *out = new h2g_h2{h};
   });
+}
+
+int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
+                  const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
+                  const long long* cb_loff, const long long* cb_xoff, const double* cb_data, long long cb_len,
+                  int share, const long long* coup_off, const double* coup_data, long long coup_len,
+                  const long long* near_off, const double* near_data, long long near_len, h2g_h2** out) {
+  return upload_impl(ctx, bt, rb_rank, rb_loff, rb_xoff, rb_data, rb_len, cb_rank, cb_loff, cb_xoff, cb_data, cb_len,
+                     share, coup_off, coup_data, coup_len, near_off, near_data, near_len, out, false);
+}
+
+int h2g_h2_upload_async(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
+                        const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
+                        const long long* cb_loff, const long long* cb_xoff, const double* cb_data, long long cb_len,
+                        int share, const long long* coup_off, const double* coup_data, long long coup_len,
+                        const long long* near_off, const double* near_data, long long near_len, h2g_h2** out) {
+  return upload_impl(ctx, bt, rb_rank, rb_loff, rb_xoff, rb_data, rb_len, cb_rank, cb_loff, cb_xoff, cb_data, cb_len,
+                     share, coup_off, coup_data, coup_len, near_off, near_data, near_len, out, true);
 }
 
 void h2g_h2_destroy(h2g_h2* h) { delete h; }
@@ -342,6 +375,7 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_
     Ctx& C = ctx->c;
     const H2& h = *hh->h;
     const Blocks& B = *h.bt;
+    wait_near(C, h);
     Arena ar(C.st);
     Gather gr, gc, gcp, gn;
     pack_basis(*h.rb, rb_rank, rb_loff, rb_xoff, gr);

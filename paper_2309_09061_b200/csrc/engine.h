@@ -135,6 +135,10 @@ struct H2 {
   std::vector<double*> coup, near;
   std::vector<ArenaPtr> owned;
   ArenaPtr near_owner;  // arena holding the nearfield blocks (shared by a coarsened result)
+  cudaEvent_t near_ready = nullptr;  // asynchronous upload: the nearfield copy completes at this event
+  ~H2() {
+    if (near_ready) cudaEventDestroy(near_ready);
+  }
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
   std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
 };
@@ -425,6 +429,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale);
 void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool accumulate);
+// make the context's stream wait for an asynchronously uploaded nearfield (no-op otherwise)
+inline void wait_near(Ctx& C, const H2& h) {
+  if (h.near_ready) cuda_check(cudaStreamWaitEvent(C.st, h.near_ready, 0), "wait nearfield upload");
+}
 std::shared_ptr<H2> build_kernel_h2(Ctx& C, std::shared_ptr<const Blocks> bt, int kind, int dim,
                                     const double* points, const double* weights, const long long* rank,
                                     const long long* loff, const long long* xoff, const double* basis,

@@ -162,6 +162,7 @@ void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool a
   const Basis& CB = g.cb();
   const BView bv = g.bv();
   const Blocks& B = *g.h->bt;
+  wait_near(C, *g.h);
   Arena sc(C.st);
   std::vector<long long> xo(ct.n), yo(rt.n);
   long long nx = 0, ny = 0;

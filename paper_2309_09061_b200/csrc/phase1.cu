@@ -76,6 +76,8 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
   for (int b = 0; b < B.nb; ++b)
     if (!B.adm_leaf(b)) mids[x.row(b)].push_back(b);
 
+  wait_near(C, *x.h);  // X|ts and Y|sr dense blocks are read from here on
+  wait_near(C, *y.h);
   Induced R;
   R.q = std::make_shared<Basis>();
   Basis& q = *R.q;

@@ -742,6 +742,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  wait_near(C, g);
   // structure of both passes on host threads while the block norms run on the GPU
   const BView gv{g.bt.get(), false}, gvt{g.bt.get(), true};
   const BView cvw{coarse.get(), false}, cvt{coarse.get(), true};

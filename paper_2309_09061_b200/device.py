@@ -151,7 +151,7 @@ class DeviceH2:
 
     @classmethod
     def upload_packed(cls, d: dict, block_tree: BlockTree, ctx: Context | None = None, *,
-                      share: bool = False) -> "DeviceH2":
+                      share: bool = False, asynchronous: bool = False) -> "DeviceH2":
         """Upload from the packed layout (packed.py keys rb.*, cb.*, coup_*, near_*) over the
         C ABI h2g_h2_upload.  Host arrays are copied as given; pinned arrays (e.g.
         torch.empty(..., pin_memory=True).numpy()) transfer at full link bandwidth."""
@@ -163,14 +163,18 @@ class DeviceH2:
                 a["cb." + k] = a["rb." + k]
         g = block_tree
         h = N.P()
-        N.check(ctx.lib.h2g_h2_upload(
+        fn = ctx.lib.h2g_h2_upload_async if asynchronous else ctx.lib.h2g_h2_upload
+        N.check(fn(
             ctx.h, ctx.blocks(g),
             a["rb.rank"][1], a["rb.leaf_off"][1], a["rb.xfer_off"][1], a["rb.data"][1], len(a["rb.data"][0]),
             a["cb.rank"][1], a["cb.leaf_off"][1], a["cb.xfer_off"][1], a["cb.data"][1], len(a["cb.data"][0]),
             1 if share else 0,
             a["coup_off"][1], a["coup_data"][1], len(a["coup_data"][0]),
             a["near_off"][1], a["near_data"][1], len(a["near_data"][0]), C.byref(h)))
-        return cls(ctx, h, g, g.rows, g.cols)
+        out = cls(ctx, h, g, g.rows, g.cols)
+        if asynchronous:  # the nearfield copy reads these host arrays until the next synchronisation
+            out._host_keep = a
+        return out
 
     def sizes(self):
         out = np.zeros(8, np.int64)
