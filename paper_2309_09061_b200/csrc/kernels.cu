@@ -862,8 +862,10 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
 
 // NPLO: octet-Jacobi entries per lane (8: n <= 64, 16: n <= 128), 0: half-warp loop (n > 128)
 static constexpr int NT = 512;
-template <int NPLO>
-__global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items, int rsmem) {
+// RS: R in shared memory (compile-time, so every access to it is an LDS/STS rather than a generic
+// load), else R is worked on in place in global memory (items too large for shared memory).
+template <int NPLO, bool RS>
+__global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items) {
   extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
@@ -882,7 +884,7 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
   double* vh = cn0 + n;
   int* perm = (int*)(vh + n);                // n ints
   int* iperm = perm + n;                     // n ints
-  double* R = rsmem ? vh + n + n + 1 : it.rbuf;
+  double* R = RS ? vh + n + n + 1 : it.rbuf;
   __shared__ int ired[NT / 32 + 2];
   if (kx > 0) {
     for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
@@ -891,7 +893,7 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
   int k2 = 0;
   long long tk[5] = {clock64(), 0, 0, 0, 0};  // phase timestamps (diagnostic output only)
   if (n > 0 && N > 0) {
-    if (rsmem)
+    if (RS)
       for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
     __syncthreads();
     tk[1] = clock64();
@@ -1700,9 +1702,12 @@ static void init_attributes() {
     opt_in((const void*)qr_chunk_kernel);
     opt_in((const void*)tsqr_merge_kernel);
     opt_in((const void*)svd_tsqr_kernel);
-    opt_in((const void*)svd_finish_kernel<0>);
-    opt_in((const void*)svd_finish_kernel<8>);
-    opt_in((const void*)svd_finish_kernel<16>);
+    opt_in((const void*)svd_finish_kernel<0, true>);
+    opt_in((const void*)svd_finish_kernel<8, true>);
+    opt_in((const void*)svd_finish_kernel<16, true>);
+    opt_in((const void*)svd_finish_kernel<0, false>);
+    opt_in((const void*)svd_finish_kernel<8, false>);
+    opt_in((const void*)svd_finish_kernel<16, false>);
     opt_in((const void*)norm_kernel);
     opt_in((const void*)norm_warp_kernel);
     opt_in((const void*)norm_cta_kernel);
@@ -1772,9 +1777,15 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
 cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, int nmax, cudaStream_t st) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
-  if (nmax <= 64) svd_finish_kernel<8><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
-  else if (nmax <= 128) svd_finish_kernel<16><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
-  else svd_finish_kernel<0><<<nitems, NT, smem, st>>>(items, rsmem ? 1 : 0);
+  if (rsmem) {
+    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items);
+    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items);
+    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items);
+  } else {
+    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items);
+    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items);
+    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items);
+  }
   return cudaGetLastError();
 }
 
