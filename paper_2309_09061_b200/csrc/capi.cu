@@ -1,5 +1,8 @@
 // extern "C" boundary (include/h2g.h): handles, upload / download in the packed layout, status codes.
+#include <malloc.h>
+
 #include <cstring>
+#include <mutex>
 
 #include "../../include/h2g.h"
 #include "engine.h"
@@ -48,7 +51,16 @@ extern "C" {
 const char* h2g_last_error(void) { return g_err.c_str(); }
 
 int h2g_ctx_create(int device, void* stream, h2g_ctx** out) {
-  return guarded([&] { *out = new h2g_ctx(device, (cudaStream_t)stream); });
+  return guarded([&] {
+    // The planner and batch builders allocate and free large host vectors every product; keep them on
+    // the heap (no per-product mmap / munmap and page-fault storms once glibc's thresholds adapt)
+    static std::once_flag malloc_once;
+    std::call_once(malloc_once, [] {
+      mallopt(M_MMAP_THRESHOLD, 512 << 20);
+      mallopt(M_TRIM_THRESHOLD, 1 << 30);
+    });
+    *out = new h2g_ctx(device, (cudaStream_t)stream);
+  });
 }
 
 int h2g_ctx_destroy(h2g_ctx* ctx) {
