@@ -108,6 +108,13 @@ int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, i
 /* re-compression of g onto `coarse` (phase 2) */
 int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
                 h2g_h2** z);
+/* same, and the dense blocks of z that are dense blocks of g are copied, while phase 2 runs, into
+   near_host at their offsets of z's packed nearfield layout; h2g_h2_download with near_data ==
+   near_host then moves only the remaining blocks. near_host (pinned for overlap) holds near_len
+   doubles (no prefetch when that is less than z's nearfield) and must stay valid until that
+   download returns. */
+int h2g_coarsen_prefetch(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
+                         double* near_host, long long near_len, h2g_h2** z);
 /* orthogonalise + coarsen onto the own block tree */
 int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z);
 /* Interpolation H^2 matrix of a point-kernel problem with the couplings and nearfield blocks

@@ -56,6 +56,7 @@ SIGNATURES = {
     "h2g_blocks_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, I64P, U8P]),
     "h2g_multiply": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
     "h2g_coarsen": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
+    "h2g_coarsen_prefetch": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, F64P, C.c_longlong, C.POINTER(P)]),
     "h2g_recompress": (C.c_int, [P, P, C.c_double, C.c_int, C.POINTER(P)]),
     "h2g_last_error": (C.c_char_p, []),
 }

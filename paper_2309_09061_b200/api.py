@@ -12,7 +12,10 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import _native as N
+import os as _os
 from .device import Context, DeviceH2, default_context
 from .errors import InvalidInputError
 from .h2 import H2Matrix
@@ -95,6 +98,9 @@ def multiply_coarsen(x, y, tol: float, *, coarse: BlockTree | None = None, max_r
     return z.download() if hx else z
 
 
+_NO_PREFETCH = _os.environ.get("H2G_NO_PREFETCH", "") not in ("", "0")  # A/B switch for the e2e tools
+
+
 def multiply_coarsen_packed(xp: dict, x_tree: BlockTree, yp: dict | None = None, y_tree: BlockTree | None = None,
                             tol: float = 0.0, *, coarse: BlockTree | None = None, max_rank: int | None = None,
                             out: dict | None = None, ctx: Context | None = None) -> dict:
@@ -108,5 +114,16 @@ def multiply_coarsen_packed(xp: dict, x_tree: BlockTree, yp: dict | None = None,
     dx = DeviceH2.upload_packed(xp, x_tree, ctx, asynchronous=True)
     dy = dx if yp is None else DeviceH2.upload_packed(yp, y_tree if y_tree is not None else x_tree, ctx,
                                                       asynchronous=True)
-    z = multiply_coarsen(dx, dy, tol, coarse=coarse, max_rank=max_rank, ctx=ctx)
+    g = multiply(dx, dy, tol, max_rank=max_rank, ctx=ctx)
+    coarse = coarse if coarse is not None else dx.block_tree
+    nh = None if out is None else out.get("near_data")
+    h = N.P()
+    if nh is not None and not _NO_PREFETCH and nh.dtype == np.float64 and nh.flags.c_contiguous and nh.ndim == 1:
+        # Z's dense blocks shared with G stream into out["near_data"] while phase 2 runs
+        N.check(ctx.lib.h2g_coarsen_prefetch(ctx.h, g.h, ctx.blocks(coarse), float(tol), _mr(max_rank), 1,
+                                             nh.ctypes.data_as(N.F64P), nh.size, C.byref(h)))
+    else:
+        N.check(ctx.lib.h2g_coarsen(ctx.h, g.h, ctx.blocks(coarse), float(tol), _mr(max_rank), 1, C.byref(h)))
+    z = DeviceH2(ctx, h, coarse, coarse.rows, coarse.cols)
+    del g
     return z.download_packed(out)

@@ -350,6 +350,19 @@ struct Gather {
     items.push_back(total);
     total += n;
   }
+  // as run(), but only the ranges `runs` of the packed layout are copied to the host
+  void run_runs(Ctx& C, Arena& ar, double* host, const std::vector<std::pair<long long, long long>>& runs) {
+    if (total == 0 || items.empty()) return;
+    double* d = ar.alloc(total);
+    for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(d + items[i]);
+    long long* di = C.push(items);
+    C.flush();
+    cuda_check(launch_gather(di, (int)(items.size() / 3), C.st), "gather");
+    for (auto& r : runs)
+      cuda_check(cudaMemcpyAsync(host + r.first, d + r.first, (r.second - r.first) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, C.st),
+                 "download");
+  }
   void run(Ctx& C, Arena& ar, double* host) {
     if (total == 0) return;
     double* d = ar.alloc(total);
@@ -392,6 +405,9 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_
     Gather gr, gc, gcp, gn;
     pack_basis(*h.rb, rb_rank, rb_loff, rb_xoff, gr);
     pack_basis(*h.cb, cb_rank, cb_loff, cb_xoff, gc);
+    // blocks prefetched into this very host buffer during coarsen are skipped (their bytes are there)
+    const bool pre = h.near_host && h.near_host == near_data && h.near_host_ready;
+    std::vector<std::pair<long long, long long>> runs;  // non-prefetched dense ranges [lo, hi)
     for (int b = 0; b < B.nb; ++b) {
       coup_off[b] = -1;
       near_off[b] = -1;
@@ -401,14 +417,28 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_
         coup_off[b] = gcp.total;
         gcp.add(h.coup[b], (long long)h.rb->rank[t] * h.cb->rank[s]);
       } else {
+        const long long sz = (long long)B.rows->size(t) * B.cols->size(s);
         near_off[b] = gn.total;
-        gn.add(h.near[b], (long long)B.rows->size(t) * B.cols->size(s));
+        if (pre && h.near_on_host[b]) {
+          gn.total += sz;  // already on the host
+        } else {
+          if (pre) {
+            if (!runs.empty() && runs.back().second == gn.total) runs.back().second += sz;
+            else runs.emplace_back(gn.total, gn.total + sz);
+          }
+          gn.add(h.near[b], sz);
+        }
       }
     }
     gr.run(C, ar, rb_data);
     gc.run(C, ar, cb_data);
     gcp.run(C, ar, coup_data);
-    gn.run(C, ar, near_data);
+    if (pre) {
+      gn.run_runs(C, ar, near_data, runs);
+      cuda_check(cudaStreamWaitEvent(C.st, h.near_host_ready, 0), "wait prefetch");
+    } else {
+      gn.run(C, ar, near_data);
+    }
     C.sync();
   });
 }
@@ -476,8 +506,13 @@ int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, i
 
 int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
                 h2g_h2** z) {
+  return h2g_coarsen_prefetch(ctx, g, coarse, tol, max_rank, scale_blocks, nullptr, 0, z);
+}
+
+int h2g_coarsen_prefetch(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
+                         double* near_host, long long near_len, h2g_h2** z) {
   return guarded([&] {
-    auto Z = coarsen(ctx->c, *g->h, coarse->b, tol, max_rank, scale_blocks != 0);
+    auto Z = coarsen(ctx->c, *g->h, coarse->b, tol, max_rank, scale_blocks != 0, near_host, near_len);
     Z->keep.push_back(coarse->rows);
     Z->keep.push_back(coarse->cols);
     Z->keep.push_back(g->h->bt);

@@ -136,8 +136,14 @@ struct H2 {
   std::vector<ArenaPtr> owned;
   ArenaPtr near_owner;  // arena holding the nearfield blocks (shared by a coarsened result)
   cudaEvent_t near_ready = nullptr;  // asynchronous upload: the nearfield copy completes at this event
+  // nearfield prefetch to the host (coarsen with a host buffer): blocks already copied, the target
+  // buffer and the event that completes the copy
+  std::vector<char> near_on_host;
+  double* near_host = nullptr;
+  cudaEvent_t near_host_ready = nullptr;
   ~H2() {
     if (near_ready) cudaEventDestroy(near_ready);
+    if (near_host_ready) cudaEventDestroy(near_host_ready);
   }
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
   std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
@@ -426,6 +432,8 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
 PTree product_tree(BView bx, BView by);
 std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt);
 std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling);
+std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
+                            bool scale, double* near_host, long long near_cap);
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale);
 void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool accumulate);

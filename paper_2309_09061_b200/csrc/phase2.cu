@@ -739,10 +739,86 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, d
 // Phase-2 driver (reference coarsening.py:408-422).
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale) {
+  return coarsen(C, g, coarse, tol, max_rank, scale, nullptr, 0);
+}
+
+// Z's dense blocks that are G's dense blocks (shared in project_final) are final already: with a
+// host buffer for Z's packed nearfield, copy them there now on the copy stream, overlapping the
+// whole of phase 2; h2g_h2_download then only moves the rest.
+struct NearPrefetch {
+  std::vector<char> mask;
+  ArenaPtr arena;
+  cudaEvent_t ev = nullptr;
+};
+
+static NearPrefetch prefetch_near(Ctx& C, const H2& g, const Blocks& cbk, double* near_host, long long near_cap) {
+  NearPrefetch P;
+  const Blocks& pt = *g.bt;
+  P.mask.assign(cbk.nb, 0);
+  std::vector<long long> items;
+  std::vector<long long> zoff(cbk.nb, -1), zlen(cbk.nb, 0);
+  long long off = 0, npf = 0;
+  for (int b = 0; b < cbk.nb; ++b) {
+    if (!cbk.leaf(b) || cbk.adm[b]) continue;
+    const int t = cbk.row[b], r = cbk.col[b];
+    const long long sz = (long long)cbk.rows->size(t) * cbk.cols->size(r);
+    zoff[b] = off;
+    zlen[b] = sz;
+    const int pb = pt.find(t, r);
+    if (pb >= 0 && pt.near_leaf(pb) && sz > 0) {
+      P.mask[b] = 1;
+      items.push_back((long long)g.near[pb]);
+      items.push_back(sz);
+      items.push_back(off);  // patched to the staging address below
+      ++npf;
+    }
+    off += sz;
+  }
+  if (!npf || off > near_cap) {
+    P.mask.clear();
+    return P;
+  }
+  if (!C.up_stream) cuda_check(cudaStreamCreateWithFlags(&C.up_stream, cudaStreamNonBlocking), "stream");
+  P.arena = std::make_shared<Arena>(C.up_stream);
+  double* stage = P.arena->alloc(off);
+  for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(stage + items[i]);
+  long long* di = C.push(items);
+  C.flush();
+  cudaEvent_t e;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(e, C.st), "event");  // G complete and the item list copied
+  cuda_check(cudaStreamWaitEvent(C.up_stream, e, 0), "wait");
+  cudaEventDestroy(e);
+  cuda_check(launch_gather(di, (int)npf, C.up_stream), "gather(prefetch)");
+  ++C.launches;
+  for (int b = 0; b < cbk.nb;) {  // one copy per run of consecutive prefetched blocks
+    if (!P.mask[b]) { ++b; continue; }
+    const long long lo = zoff[b];
+    long long hi = lo;
+    int e2 = b;
+    for (; e2 < cbk.nb; ++e2) {
+      if (zoff[e2] < 0) continue;  // not a dense block: does not break the run
+      if (!P.mask[e2]) break;
+      hi = zoff[e2] + zlen[e2];
+    }
+    cuda_check(cudaMemcpyAsync(near_host + lo, stage + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                               C.up_stream),
+               "prefetch download");
+    b = e2;
+  }
+  cuda_check(cudaEventCreateWithFlags(&P.ev, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(P.ev, C.up_stream), "event");
+  return P;
+}
+
+std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
+                            bool scale, double* near_host, long long near_cap) {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   wait_near(C, g);
+  NearPrefetch pf;
+  if (near_host && g.near_owner) pf = prefetch_near(C, g, *coarse, near_host, near_cap);
   // structure of both passes on host threads while the block norms run on the GPU
   const BView gv{g.bt.get(), false}, gvt{g.bt.get(), true};
   const BView cvw{coarse.get(), false}, cvt{coarse.get(), true};
@@ -795,6 +871,12 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   e2 = e1;
   StageTag tagp(C, "p2.project");
   auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar);
+  if (pf.ev) {
+    Z->near_on_host = std::move(pf.mask);
+    Z->near_host = near_host;
+    Z->near_host_ready = pf.ev;
+    Z->owned.push_back(pf.arena);
+  }
   Z->owned.push_back(ar2);
   Z->own_rows = g.own_rows;
   Z->own_cols = g.own_cols;

@@ -185,6 +185,20 @@ def test_packed_host_buffer_path():
     v = np.random.default_rng(3).standard_normal(x.shape[1])
     from paper_2309_09061_b200.h2 import h2_matvec_host
     assert rel(h2_matvec_host(z2, v), h2_matvec_host(z, v)) <= 1e-13
+    # preallocated output: Z's dense blocks shared with G are prefetched into out["near_data"]
+    # during phase 2 (h2g_coarsen_prefetch); the result must be bit-identical, every entry written
+    keys = [k for k in zp if not k.startswith("bt.")]
+    for pad in (7, 0):
+        out = {k: torch.full((zp[k].size + pad,), float("nan") if k.endswith("data") else -7,
+                             dtype=torch.float64 if k.endswith("data") else torch.int64).pin_memory().numpy()
+               for k in keys}
+        z3 = P.multiply_coarsen_packed(xp, x.block_tree, yp, y.block_tree, eps, out=out)
+        for k in keys:
+            assert np.array_equal(z3[k], zp[k]), k
+    # a nearfield buffer too small for Z: no prefetch, a fresh array is returned
+    out = {"near_data": np.zeros(max(0, zp["near_data"].size - 1))}
+    z4 = P.multiply_coarsen_packed(xp, x.block_tree, yp, y.block_tree, eps, out=out)
+    assert np.array_equal(z4["near_data"], zp["near_data"])
 
 
 @pytest.mark.parametrize("name", ["rand_s0_tol1e-3", "c1"])
