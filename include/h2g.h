@@ -38,6 +38,16 @@ typedef struct h2g_h2 h2g_h2;
 int h2g_ctx_create(int device, void* stream, h2g_ctx** out);
 int h2g_ctx_destroy(h2g_ctx* ctx);
 int h2g_ctx_set_timing(h2g_ctx* ctx, int on);
+/* Multi-GPU (one process per GPU): the ranks sharing each product.  Every rank holds the whole of
+   X and Y; multiply / coarsen split the row (and column) cluster trees into subtrees at the first
+   level with >= size clusters (h2g_tree_partition), compute their own subtrees' clusters and blocks
+   plus the replicated top levels, and exchange the results with `fn`, an in-place all-gather of a
+   device buffer: segment i = bytes [off[i], off[i+1]) is valid on rank i on entry and on every rank
+   on return; issued on `stream`; channel 0 / 1 = the row / column pass (concurrent host threads;
+   use one communicator each).  Returns 0 on success.  size 1 (default): single GPU. */
+typedef int (*h2g_allgather_fn)(void* user, int channel, void* dbuf, const long long* off, int nseg,
+                                void* stream);
+int h2g_ctx_set_comm(h2g_ctx* ctx, int rank, int size, h2g_allgather_fn fn, void* user);
 /* ms per stage of the last multiply / coarsen: setup, t1_row, t1_col, t1_mat, t2_row, t2_col, t2_mat
    (the reference harness's stage split, bench.py:195-237) */
 int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);
@@ -59,6 +69,9 @@ int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path);
 int h2g_tree_create(h2g_ctx* ctx, int n, const long long* start, const long long* stop,
                     const long long* child_ptr, const long long* child_idx, h2g_tree** out);
 void h2g_tree_destroy(h2g_tree* t);
+/* Host-only: owner rank (or -1 = replicated top level) of every cluster for nparts ranks, and the
+   partition level (-1: no level has nparts clusters, everything replicated). */
+int h2g_tree_partition(h2g_tree* t, int nparts, long long* owner, int* level);
 
 /* block tree (reference BlockTree, trees.py:176-227): nb blocks in preorder */
 int h2g_blocks_create(h2g_ctx* ctx, h2g_tree* rows, h2g_tree* cols, int nb, const long long* row,

@@ -38,6 +38,8 @@ SIGNATURES = {
     "h2g_ctx_kernel_stats": (C.c_int, [P, F64P, C.c_int]),
     "h2g_ctx_trace_begin": (C.c_int, [P]),
     "h2g_ctx_trace_dump": (C.c_int, [P, C.c_char_p]),
+    "h2g_ctx_set_comm": (C.c_int, [P, C.c_int, C.c_int, C.c_void_p, P]),
+    "h2g_tree_partition": (C.c_int, [P, C.c_int, I64P, C.POINTER(C.c_int)]),
     "h2g_tree_create": (C.c_int, [P, C.c_int, I64P, I64P, I64P, I64P, C.POINTER(P)]),
     "h2g_tree_destroy": (None, [P]),
     "h2g_blocks_create": (C.c_int, [P, P, P, C.c_int, I64P, I64P, I64P, I64P, U8P, C.POINTER(P)]),

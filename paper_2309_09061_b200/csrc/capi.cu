@@ -72,6 +72,18 @@ int h2g_ctx_set_timing(h2g_ctx* ctx, int on) {
   return 0;
 }
 
+int h2g_ctx_set_comm(h2g_ctx* ctx, int rank, int size, h2g_allgather_fn fn, void* user) {
+  return guarded([&] {
+    if (size < 1 || rank < 0 || rank >= size) throw InvalidInput("rank outside [0, size)");
+    if (size > 1 && !fn) throw InvalidInput("a partitioned product needs an all-gather function");
+    ctx->c.comm = Comm{rank, size, (AllgatherFn)fn, user};
+    if (ctx->c.side_) {
+      ctx->c.side_->comm = ctx->c.comm;
+      ctx->c.side_->channel = 1;
+    }
+  });
+}
+
 int h2g_ctx_stage_times(h2g_ctx* ctx, double* o) {
   const StageTimes& t = ctx->c.times;
   o[0] = t.setup; o[1] = t.t1_row; o[2] = t.t1_col; o[3] = t.t1_mat;
@@ -170,6 +182,15 @@ int h2g_tree_create(h2g_ctx*, int n, const long long* start, const long long* st
 }
 
 void h2g_tree_destroy(h2g_tree* t) { delete t; }
+
+int h2g_tree_partition(h2g_tree* t, int nparts, long long* owner, int* level) {
+  return guarded([&] {
+    if (nparts < 1) throw InvalidInput("number of parts must be >= 1");
+    const Part p = make_part(*t->t, nparts, 0);
+    *level = p.level;
+    for (int i = 0; i < t->t->n; ++i) owner[i] = p.on() ? p.owner[i] : -1;
+  });
+}
 
 int h2g_blocks_create(h2g_ctx*, h2g_tree* rows, h2g_tree* cols, int nb, const long long* row,
                       const long long* col, const long long* cptr, const long long* cidx,

@@ -200,6 +200,8 @@ Ctx& Ctx::side() {
   side_->trace_base = trace_base;
   side_->trace_host0 = trace_host0;
   side_->trace_out = trace_out;
+  side_->comm = comm;
+  side_->channel = 1;
   // the side stream starts after everything queued so far on the main stream
   cudaEvent_t e;
   cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");

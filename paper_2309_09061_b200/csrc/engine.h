@@ -171,6 +171,20 @@ struct HView {
   }
 };
 
+// ------------------------------------------------------------------ multi-GPU
+// In-place variable all-gather over the ranks of one product: dbuf holds nseg = P segments
+// [off[i], off[i+1]) bytes; on entry segment `rank` is valid, on return every segment is.  Issued on
+// `stream` (the device buffer is stream-ordered); returns 0 on success.  Supplied by the host
+// (torch.distributed over NCCL in production, gloo with host staging in tests); `channel` 0 / 1 keeps
+// the concurrent row / column passes on separate communicators.
+typedef int (*AllgatherFn)(void* user, int channel, void* dbuf, const long long* off, int nseg, void* stream);
+struct Comm {
+  int rank = 0, size = 1;
+  AllgatherFn fn = nullptr;
+  void* user = nullptr;
+  bool on() const { return size > 1 && fn != nullptr; }
+};
+
 // ------------------------------------------------------------------ context: stream + staging
 struct StageTimes {
   float setup = 0, t1_row = 0, t1_col = 0, t1_mat = 0, t2_row = 0, t2_col = 0, t2_mat = 0;
@@ -231,6 +245,8 @@ struct Ctx {
   void sub_end(int cls, cudaEvent_t a) { if (trace) prof_end(cls, a, 0.0, 0.0); }
   void drain_prof();
 
+  Comm comm;        // ranks sharing this product (size 1: single GPU)
+  int channel = 0;  // communicator of this context's host thread (side context: 1)
   std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
   cudaStream_t up_stream = nullptr;  // structure uploads from the planner thread
   char* up_host = nullptr;
@@ -414,6 +430,33 @@ struct PTree {  // product block tree with the classified triples per node
   } dev;
 };
 void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby);
+
+// ------------------------------------------------------------------ row-subtree partition (shard.cu)
+// Ownership of the clusters of one tree among P ranks: the subtrees rooted at the first level with
+// at least P clusters (level log2 P on the balanced BASELINE trees) are dealt out in contiguous runs;
+// clusters above that level are replicated (owner -1) and computed by every rank.
+struct Part {
+  int P = 1, me = 0, level = -1;
+  std::vector<int> owner;
+  bool on() const { return level >= 0; }
+  bool mine(int t) const { return !on() || owner[t] < 0 || owner[t] == me; }
+  bool top(int t) const { return !on() || owner[t] < 0; }
+  std::vector<int> filter(const std::vector<int>& L) const;  // the clusters of L this rank computes
+};
+Part make_part(const Tree& tr, int P, int me);
+inline Part make_part(const Tree& tr, const Comm& c) {
+  return c.on() ? make_part(tr, c.size, c.rank) : Part{};
+}
+// One exchanged array: `len` doubles produced by rank `owner`; on the owner *dst is the source, on
+// every other rank *dst is set to the received copy (allocated from the arena passed to exchange()).
+struct XItem {
+  int owner;
+  long long len;
+  double** dst;
+};
+void exchange(Ctx& C, Arena& ar, const std::vector<XItem>& items);
+// Integer per-cluster values (ranks): v[t] for the listed clusters is taken from owner[t].
+void exchange_ints(Ctx& C, const Part& part, const std::vector<int>& ids, std::vector<int>& v);
 
 // ------------------------------------------------------------------ stages
 std::shared_ptr<Tree> make_tree(int n, const long long* start, const long long* stop, const long long* cptr,

@@ -61,6 +61,55 @@ void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<i
   }
 }
 
+// Multi-GPU: after the partitioned levels (>= part.level) every rank receives the other ranks'
+// results -- ranks, Q_t (leaf basis or the stacked transfers), basis_change and the projections
+// A_ts -- so the replicated top levels and the later stages see the full induced basis.
+static void exchange_induced(Ctx& C, Arena& out, const Part& part, HView x, HView y,
+                             const std::vector<std::vector<int>>& mids, Induced& R) {
+  const Tree& tr = x.rows();
+  const Basis& VX = x.rb();
+  const Basis& VY = y.rb();
+  Basis& q = *R.q;
+  std::vector<int> ids;
+  for (int l = part.level; l <= tr.depth; ++l)
+    for (int t : tr.by_level[l]) ids.push_back(t);
+  StageTag tag(C, "p1.exchange");
+  exchange_ints(C, part, ids, q.rank);
+  std::vector<XItem> items;
+  std::vector<double*> qp(tr.n, nullptr);
+  for (int t : ids) {
+    const int o = part.owner[t], k = q.rank[t];
+    int m = tr.size(t);
+    if (!tr.leaf(t)) {
+      m = 0;
+      for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
+    }
+    if (o == part.me) qp[t] = tr.leaf(t) ? q.leaf[t] : q.xfer[tr.kid(t, 0)];
+    else R.bc[t] = Mat{nullptr, k, VX.rank[t]};
+    items.push_back(XItem{o, (long long)m * k, &qp[t]});
+    items.push_back(XItem{o, (long long)k * VX.rank[t], &R.bc[t].p});
+    for (int b : mids[t]) {
+      const int ky = VY.rank[x.col(b)];
+      if (o != part.me) R.proj[b] = Mat{nullptr, k, ky};
+      items.push_back(XItem{o, (long long)k * ky, &R.proj[b].p});
+    }
+  }
+  exchange(C, out, items);
+  for (int t : ids) {
+    if (part.owner[t] == part.me) continue;
+    if (tr.leaf(t)) {
+      q.leaf[t] = qp[t];
+    } else {
+      int off = 0;
+      for (int i = 0; i < tr.nkids(t); ++i) {
+        const int c = tr.kid(t, i);
+        q.xfer[c] = qp[t] + (long long)off * q.rank[t];
+        off += q.rank[c];
+      }
+    }
+  }
+}
+
 // Fig. 3: bottom-up compression of the induced row basis (reference induced.py:76-184).
 Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, PRef P, double tol,
                      int max_rank, bool scale, double level_decay) {
@@ -87,9 +136,10 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
   q.xfer.assign(tr.n, nullptr);
   R.bc.assign(tr.n, Mat{});
 
+  const Part part = make_part(tr, C.comm);  // multi-GPU: this rank's subtrees (all of tr when P = 1)
   std::vector<int> leaf_blocks;
   for (int t = 0; t < tr.n; ++t)
-    if (tr.leaf(t))
+    if (tr.leaf(t) && part.mine(t))
       for (int b : mids[t]) leaf_blocks.push_back(b);
   R.proj.assign(B.nb, Mat{});
   {
@@ -100,8 +150,10 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
   std::vector<Mat> blk(B.nb);
   std::vector<Mat> vx(tr.n);
   std::vector<Mat> rfb(B.nb);
+  std::vector<int> Lp;
   for (int lev = tr.depth; lev >= 0; --lev) {
-    const std::vector<int>& L = tr.by_level[lev];
+    if (part.on()) Lp = part.filter(tr.by_level[lev]);
+    const std::vector<int>& L = part.on() ? Lp : tr.by_level[lev];
     StageTag tag(C, "p1.L" + std::to_string(lev));
     GBatch g1, g2;
     std::vector<Mat>& rf = rfb;
@@ -244,6 +296,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       }
     }
     g4.run(C);
+    if (part.on() && lev == part.level) exchange_induced(C, out, part, x, y, mids, R);
   }
   return R;
 }
@@ -274,9 +327,12 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   const Basis& W = *qc.q;
   G->coup.assign(B.nb, nullptr);
   G->near.assign(B.nb, nullptr);
+  // multi-GPU: this rank assembles the product blocks of its row subtrees (and the replicated top)
+  const Part part = make_part(rows, C.comm);
   std::vector<Mat> cp(B.nb);
   for (int b = 0; b < B.nb; ++b) {
     const int t = B.row[b], r = B.col[b];
+    if (!part.mine(t)) continue;
     if (B.near_leaf(b)) {
       G->near[b] = ar->alloc((size_t)rows.size(t) * cols.size(r));
     } else {
@@ -290,7 +346,14 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
   {
     HostTimer hx(C, "asm_xv1");
-    xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
+    if (part.on()) {
+      std::vector<int> want;
+      for (int b : pt.need_xv)
+        if (part.mine(x.row(b))) want.push_back(b);
+      xv_compute(C, sc, x, y, P, want, qr.xv);
+    } else {
+      xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
+    }
   }
   {
     HostTimer hx(C, "asm_xv2");
@@ -302,6 +365,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     GBatch g;
     for (int bts : pt.rf_blocks) {  // (planner thread: distinct X blocks of kind-a triples)
       const int t = x.row(bts), s = x.col(bts);
+      if (!part.mine(t)) continue;
       // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
       Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
       g.out(m, false);
@@ -404,6 +468,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     double fl = 0.0;
     for (int b = 0; b < B.nb; ++b) {
       const int t = B.row[b], r = B.col[b];
+      if (!part.mine(t)) continue;
       const bool dense = B.near_leaf(b);
       const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
       GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
@@ -479,6 +544,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       for (int i = 0; i < B.nkids(b); ++i) {
         const int ch = B.kid(b, i);
         const int t2 = B.row[ch], r2 = B.col[ch];
+        if (!part.mine(t2)) continue;
         Mat E, F;
         if (t2 != t) E = Q.xferm(t2);
         if (r2 != r) F = W.xferm(r2);
@@ -496,6 +562,18 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
     g1.run(C);
     g2.run(C);
+  }
+  if (part.on()) {  // every rank continues with the whole of G (couplings and nearfield)
+    StageTag tagx(C, "p1.exchange");
+    std::vector<XItem> items;
+    for (int b = 0; b < B.nb; ++b) {
+      if (!B.leaf(b)) continue;
+      const int t = B.row[b], r = B.col[b];
+      if (part.top(t)) continue;
+      if (B.adm[b]) items.push_back(XItem{part.owner[t], (long long)Q.rank[t] * W.rank[r], &G->coup[b]});
+      else items.push_back(XItem{part.owner[t], (long long)rows.size(t) * cols.size(r), &G->near[b]});
+    }
+    exchange(C, *ar, items);
   }
   return G;  // scratch is released stream-ordered (cudaFreeAsync) after the queued work
 

@@ -285,17 +285,30 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   S.r.assign(tr.n, Mat{});
   S.z.assign(tr.n, Mat{});
   S.reps.assign(pt.nb, CTRef{});
+  // multi-GPU: this rank's subtrees of tr. The replicated top levels may not merge representations
+  // of partitioned children (those stay on their rank); the BASELINE trees never do -- no product
+  // block above the partition level is covered -- and otherwise the pass runs replicated.
+  Part part = make_part(tr, C.comm);
+  if (part.on())
+    for (int l = 0; l < part.level && part.on(); ++l)
+      for (int t : tr.by_level[l])
+        if (!sub_cov[t].empty()) {
+          part = Part{};
+          break;
+        }
   CT mpool, singles, acc, nxt, tg[8];  // per-level scratch trees (capacity reused)
   std::vector<int> mroot(pt.nb, -1);
   Arena sc(C.st);
   double* d_msc = sc.alloc(std::max(1, pt.nb));  // sigma_1 of merged reps, per block
 
   // top-down condensation weights Z_t (coarsening.py:231-245)
+  std::vector<int> Lp;
   for (int lev = 0; lev <= tr.depth; ++lev) {
     StageTag tag(C, "p2.Z.L" + std::to_string(lev));
     GBatch ge;
     QrBatch qb;
-    for (int t : tr.by_level[lev]) {
+    if (part.on()) Lp = part.filter(tr.by_level[lev]);
+    for (int t : part.on() ? Lp : tr.by_level[lev]) {
       const int k = v1.rank[t];
       QrItem it{};
       it.s0 = qb.sl.begin();
@@ -328,7 +341,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
 
   std::vector<Mat> lm(pt.nb);  // R_t S_b for admissible leaves used inside representations
   for (int lev = tr.depth; lev >= 0; --lev) {
-    const std::vector<int>& L = tr.by_level[lev];
+    if (part.on()) Lp = part.filter(tr.by_level[lev]);
+    const std::vector<int>& L = part.on() ? Lp : tr.by_level[lev];
     const size_t nl = L.size();
     StageTag tag(C, "p2.B.L" + std::to_string(lev));
     HostTimer htv(C, "p2_vz_plan");
@@ -597,6 +611,43 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       for (int b : sub_cov[t]) all(b);
     }
     gq.run(C);
+    if (part.on() && lev == part.level) {
+      // every rank receives the partitioned levels' ranks, Q_t and R_t (the representations stay
+      // with their rank: only its own rows' final projection reads them)
+      StageTag tagx(C, "p2.exchange");
+      std::vector<int> ids;
+      for (int l = part.level; l <= tr.depth; ++l)
+        for (int t : tr.by_level[l]) ids.push_back(t);
+      exchange_ints(C, part, ids, q.rank);
+      std::vector<XItem> items;
+      std::vector<double*> qp(tr.n, nullptr);
+      for (int t : ids) {
+        const int o = part.owner[t], k = q.rank[t];
+        int m = tr.size(t);
+        if (!tr.leaf(t)) {
+          m = 0;
+          for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
+        }
+        if (o == part.me) qp[t] = tr.leaf(t) ? q.leaf[t] : q.xfer[tr.kid(t, 0)];
+        else S.r[t] = Mat{nullptr, k, v1.rank[t]};
+        items.push_back(XItem{o, (long long)m * k, &qp[t]});
+        items.push_back(XItem{o, (long long)k * v1.rank[t], &S.r[t].p});
+      }
+      exchange(C, out, items);
+      for (int t : ids) {
+        if (part.owner[t] == part.me) continue;
+        if (tr.leaf(t)) {
+          q.leaf[t] = qp[t];
+        } else {
+          int off = 0;
+          for (int i = 0; i < tr.nkids(t); ++i) {
+            const int c = tr.kid(t, i);
+            q.xfer[c] = qp[t] + (long long)off * q.rank[t];
+            off += q.rank[c];
+          }
+        }
+      }
+    }
   }
   return S;
 }
@@ -642,9 +693,11 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     return chain[ckey(r, c)];
   };
   std::vector<int> lv;
+  // multi-GPU: the coarse blocks of this rank's row subtrees, then an all-gather of Z
+  const Part part = make_part(*cb.rows, C.comm);
   // collect the needed chains
   for (int b = 0; b < cb.nb; ++b) {
-    if (!cb.adm_leaf(b)) continue;
+    if (!cb.adm_leaf(b) || !part.mine(cb.row[b])) continue;
     const int pb = pt.find(cb.row[b], cb.col[b]);
     if (pt.adm_leaf(pb)) continue;
     const CTRef rr = rs.reps[pb];
@@ -664,10 +717,21 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     gw.run(C);
   }
   GBatch g1;
+  std::vector<XItem> items;
   for (int b = 0; b < cb.nb; ++b) {
     if (!cb.leaf(b)) continue;
     const int t = cb.row[b], r = cb.col[b];
     const int pb = pt.find(t, r);
+    const bool shared = !cb.adm[b] && pt.near_leaf(pb) && !g.T && g.h->near_owner;
+    if (!part.mine(t) && !shared) {  // received below
+      if (cb.adm[b]) items.push_back(XItem{part.owner[t], (long long)qr.rank[t] * qc.rank[r], &Z->coup[b]});
+      else items.push_back(XItem{part.owner[t], (long long)cb.rows->size(t) * ctree.size(r), &Z->near[b]});
+      continue;
+    }
+    if (!part.top(t) && !shared) {
+      if (cb.adm[b]) items.push_back(XItem{part.owner[t], (long long)qr.rank[t] * qc.rank[r], &Z->coup[b]});
+      else items.push_back(XItem{part.owner[t], (long long)cb.rows->size(t) * ctree.size(r), &Z->near[b]});
+    }
     if (cb.adm[b]) {
       Mat S{ar->alloc((size_t)qr.rank[t] * qc.rank[r]), qr.rank[t], qc.rank[r]};
       Z->coup[b] = S.p;
@@ -686,7 +750,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
           else g1.t3(M.ref(), X, chain_ref(r, c).ref(), M.c, qc.rank[c]);
         }
       }
-    } else if (pt.near_leaf(pb) && !g.T && g.h->near_owner) {
+    } else if (shared) {
       // the reference copies G's dense block (coarsening.py:397-398); device matrices are immutable,
       // so Z shares it (its arena stays alive with Z) instead of copying
       Z->near[b] = g.h->near[pb];
@@ -701,6 +765,10 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     }
   }
   g1.run(C);
+  if (part.on()) {
+    StageTag tagx(C, "p2.exchange");
+    exchange(C, *ar, items);
+  }
   return Z;
 }
 
@@ -712,9 +780,12 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, d
   NormBatch nbn, nbc;
   std::vector<int> ids;
   HView v{&g, false};
+  // multi-GPU: the blocks read by this rank's row or column passes
+  const Part pr = make_part(*B.rows, C.comm), pc = make_part(*B.cols, C.comm);
   cuda_check(cudaMemsetAsync(d_nn, 0, sizeof(double) * B.nb, C.st), "memset");
   for (int b = 0; b < B.nb; ++b) {
     if (!B.leaf(b)) continue;
+    if (!pr.mine(B.row[b]) && !pc.mine(B.col[b])) continue;
     const bool coupling = B.adm[b];
     const int t = B.row[b], s = B.col[b];
     const int m = coupling ? g.rb->rank[t] : B.rows->size(t);

@@ -1,0 +1,100 @@
+"""Multi-GPU partition of the product through the C ABI: P ranks over gloo (host-staged
+all-gathers) sharing the box's one GPU, each computing its row/column subtrees; Z on every rank must
+meet the single-GPU golden bars (ranks equal to the reference's, probe errors <= 10 eps) and equal the
+single-rank product.  (NCCL refuses two ranks on one device; the collective is the only difference of
+the NCCL path, see paper_2309_09061_b200/shard.py.)"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, names, q):
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        sys.path.insert(0, HERE)
+        sys.path.insert(0, os.path.dirname(HERE))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2309_09061_b200 as P
+        from helpers import load, rel
+        from test_gpu_parity import _inputs, _probe_tol
+        from paper_2309_09061_b200.device import Context, DeviceH2
+        from paper_2309_09061_b200.h2 import h2_matvec_host
+        from paper_2309_09061_b200.shard import Sharding
+        ctx = Context(0)
+        sh = Sharding(ctx)
+        res = {}
+        for name in names:
+            d = load(name)
+            x, y, eps = _inputs(d)  # (inputs prepared unpartitioned on the default context)
+            dx = DeviceH2.upload(x, ctx)
+            dy = dx if y is x else DeviceH2.upload(y, ctx)
+            g = P.multiply(dx, dy, eps, ctx=ctx)
+            gh = g.download()
+            z = P.coarsen(g, dx.block_tree, eps, ctx=ctx).download()
+            tol = _probe_tol(eps)
+            r = {
+                "induced_row": list(gh.row_basis.rank) == list(d["rank.induced_row"]),
+                "induced_col": list(gh.col_basis.rank) == list(d["rank.induced_col"]),
+                "final_row": list(z.row_basis.rank) == list(d["rank.final_row"]),
+                "final_col": list(z.col_basis.rank) == list(d["rank.final_col"]),
+                "gv": max(rel(h2_matvec_host(gh, v), d["probe.gv"][i]) for i, v in enumerate(d["probe.v"])),
+                "zv": max(rel(h2_matvec_host(z, v), d["probe.zv"][i]) for i, v in enumerate(d["probe.v"])),
+                "tol": tol,
+            }
+            zs = P.coarsen(P.multiply(x, y, eps), x.block_tree, eps)  # single rank, default context
+            r["vs_single"] = max(rel(h2_matvec_host(z, v), h2_matvec_host(zs, v)) for v in d["probe.v"])
+            res[name] = r
+        q.put((rank, res, sh.calls, sh.bytes))
+        dist.destroy_process_group()
+    except BaseException as e:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}, 0, 0))
+        raise SystemExit(1) from e
+
+
+def _run(world, names):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, res, calls, nbytes = q.get(timeout=600)
+        assert "error" not in res, res.get("error")
+        out[rank] = (res, calls, nbytes)
+    for p in procs:
+        p.join(60)
+    return out
+
+
+@pytest.mark.parametrize("world,names", [(2, ["rand_s0_tol1e-3", "rand_s2_2d", "c1", "c2"]), (3, ["c1", "rand_s1_tol0"])])
+def test_partitioned_product_meets_golden_bars(world, names):
+    out = _run(world, names)
+    for rank, (res, calls, nbytes) in out.items():
+        assert calls > 0 and nbytes > 0  # the results really travelled between the ranks
+        for name, r in res.items():
+            for k in ("induced_row", "induced_col", "final_row", "final_col"):
+                assert r[k], (rank, name, k)
+            assert r["gv"] <= r["tol"], (rank, name, r)
+            assert r["zv"] <= r["tol"], (rank, name, r)
+            assert r["vs_single"] <= 1e-12, (rank, name, r)
