@@ -12,8 +12,11 @@ recompressed at eps on the GPU before timing.  Metric: DOF/s = n / product time.
 
 --impl reference times the CPU oracle (a NumPy restatement of h2mul, oracle/) with all host
 threads on a bounded sample (the same generator at a reduced n) -- the reference arm.
-Multi-GPU (N > 1): independent replicas, one product per rank (weak scaling); the sharded
-product is future work.
+Multi-GPU (N > 1, one process per GPU under torchrun): by default ONE product per step computed
+jointly by all ranks -- the row (and column) cluster trees split into subtrees at level log2 N,
+results all-gathered over NCCL (paper_2309_09061_b200/shard.py, csrc/shard.cu) -- so value =
+n / (max-over-ranks step time), strong scaling.  --parallelism replicas runs N independent
+products instead (weak scaling, value = N n / time).
 """
 
 from __future__ import annotations
@@ -40,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=8192)
+    ap.add_argument("--parallelism", default="shard", choices=["shard", "replicas"])
     ap.add_argument("--profile-json", default=None, help="write per-stage / per-kernel detail here")
     return ap.parse_args()
 
@@ -205,9 +209,17 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # H2G_BENCH_BACKEND=gloo: functional check of the N > 1 path with ranks sharing the GPUs there
+    # are (host-staged all-gathers; its timings are not a measurement)
+    backend = os.environ.get("H2G_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2309_09061_b200 as P
     from paper_2309_09061_b200.device import Context, DeviceH2
     from paper_2309_09061_b200.problems import CONFIGS
@@ -228,6 +240,11 @@ def main():
     t_prep = time.perf_counter() - t0
     coarse = dx.block_tree
     stream = ctx.stream
+    shard = world > 1 and args.parallelism == "shard"
+    if shard:  # from here on every product on ctx is partitioned across the ranks
+        from paper_2309_09061_b200.shard import Sharding
+        sharding = Sharding(ctx)
+    units = n if shard else world * n  # DOF of the products one step completes, all ranks together
 
     def step():
         g = P.multiply(dx, dy, eps, ctx=ctx)
@@ -240,6 +257,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ctx.counters(reset=True)
+    xc0 = (sharding.calls, sharding.bytes) if shard else (0, 0)
     clocks = ClockSampler(local)
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -254,8 +272,14 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     cnt = ctx.counters(reset=True)
+    xchg = None
+    if shard:
+        xchg = {"allgathers_per_step": (sharding.calls - xc0[0]) / args.steps,
+                "bytes_per_step": (sharding.bytes - xc0[1]) / args.steps, "backend": backend,
+                "partition": "row/column cluster trees split at the first level with >= N clusters; "
+                             "top levels replicated"}
     ms = reduce_max(e0.elapsed_time(e1) / args.steps, torch.device("cuda", local))
-    value = world * n / (ms / 1e3)
+    value = units / (ms / 1e3)
 
     # stage split (reference harness stage names) and per-kernel-class accounting, untimed step
     ctx.set_timing(True)
@@ -375,14 +399,15 @@ def main():
         line = {
             "metric": "h2_product_dof_per_s", "value": value, "unit": "DOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded points per BASELINE generator; interpolation inputs recompressed on GPU)",
             "config": {"workload": f"{args.config} product X*Y -> Z (multiply + coarsen onto X's tree)",
                        "n": n, "geometry": spec["geometry"], "kernel_x": spec["kernel_x"],
                        "kernel_y": spec["kernel_y"], "leaf": spec["leaf"], "eta": spec["eta"],
-                       "order": spec["order"], "eps": eps, "parallelism": f"replicas x{world}",
+                       "order": spec["order"], "eps": eps,
+                       "parallelism": f"row-subtree partition x{world}" if shard else f"replicas x{world}",
                        "l2": f"inputs larger than L2 (X packed {dx.packed_bytes() / 1e6:.0f} MB)"},
-            "e2e": {"value": world * n / e2e_s, "unit": "DOF/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": units / e2e_s, "unit": "DOF/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds": e2e_s},
             "gpu_launches": cnt["launches"] // args.steps * args.steps,
             "host_syncs_per_step": cnt["syncs"] / args.steps,
@@ -394,6 +419,7 @@ def main():
             "accuracy": {"eps2_power_iteration": eps2, "steps": 20, "seed": 0, "eps": eps,
                          "estimator": "reference bench.py:147-174 on GPU matvecs"},
             "matvec": matvec,
+            "exchange": xchg,
             "setup_s": {"build_inputs": t_build, "upload_recompress": t_prep},
         }
         if args.profile_json:
