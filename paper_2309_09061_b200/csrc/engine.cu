@@ -295,12 +295,14 @@ void GBatch::run(Ctx& C) {
   ++C.launches;
   outs.clear();
   terms.clear();
+  tiles.clear();
+  tiles_ready = false;
   k2max = 0;
 }
 
-void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
-  HostTimer ht(C, "gbatch_run");
-  std::vector<GTile> tiles;
+void GBatch::prepare_tiles() {
+  tiles.clear();
+  tiles.reserve(outs.size());
   for (int i = 0; i < (int)outs.size(); ++i) {
     const GOut& o = outs[i];
     if (o.m <= 0 || o.n <= 0) continue;
@@ -308,6 +310,12 @@ void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
   }
+  tiles_ready = true;
+}
+
+void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
+  HostTimer ht(C, "gbatch_run");
+  if (!tiles_ready) prepare_tiles();
   if (!tiles.empty()) {
     GOut* d_o = C.push(outs);
     GTile* d_l = C.push(tiles);

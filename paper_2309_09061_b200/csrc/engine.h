@@ -319,6 +319,9 @@ struct GBatch {
   void run(Ctx& C);
   // launch with a device-resident term array (terms generated on the GPU); `outs` index into it
   void run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint);
+  std::vector<GTile> tiles;  // prepare_tiles(): the 64x64 output tiles, built ahead (any thread)
+  bool tiles_ready = false;
+  void prepare_tiles();
   bool empty() const { return outs.empty(); }
 };
 

@@ -341,6 +341,57 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       if (B.adm_leaf(b)) G->coup[b] = cp[b].p;
     }
   }
+  // the grouped launch's output list (one GOut per product block, its 64x64 tiles) is pure
+  // structure: built on a helper thread while this one issues the xv / row-factor work and tables
+  const bool prof = C.prof;
+  auto outs_fut = std::async(std::launch::async, [&, prof] {
+    GBatch g;
+    int k2max = 0;
+    for (int k : y.cb().rank) k2max = std::max(k2max, k);
+    for (int k : x.cb().rank) k2max = std::max(k2max, k);
+    if (k2max > 256) throw StructureErr("gsum: 3-factor middle dimension above 256");
+    g.k2max = std::max(k2max, 64);  // group sums T (64 x ka) / U (kb x 64) share the Ts buffer
+    g.outs.reserve(B.nb);
+    double fl = 0.0;
+    const Tree& mid = x.cols();
+    for (int b = 0; b < B.nb; ++b) {
+      const int t = B.row[b], r = B.col[b];
+      if (!part.mine(t)) continue;
+      const bool dense = B.near_leaf(b);
+      const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
+      GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
+      // grouped kind-a / kind-b terms (asm_expand_kernel emits nf = 4 / 5 under the same rule)
+      const int ka = y.cb().rank[r], kb = x.rb().rank[t];
+      if (ka <= 64) {
+        o.ka = ka;
+        o.da = dense ? y.cb().leafm(r).tref() : qc.bc[r].tref();
+      }
+      if (kb <= 64) {
+        o.kb = kb;
+        o.ab = dense ? x.rb().leafm(t).ref() : qr.bc[t].ref();
+      }
+      g.outs.push_back(o);
+      if (prof)
+        for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+          const int s = pt.ts[i];
+          const double m = tgt.r, n = tgt.c;
+          if (pt.tk[i] == 'c') fl += 2 * m * n * mid.size(s);
+          else if (pt.tk[i] == 'a') {
+            const double k = y.rb().rank[s], k2 = y.cb().rank[r];
+            fl += 2 * m * k * k2 + 2 * m * k2 * n;
+          } else {
+            const double k = x.rb().rank[t], k2 = x.cb().rank[s];
+            fl += 2 * m * k * k2 + 2 * m * k2 * n;
+          }
+        }
+    }
+    g.prepare_tiles();
+    return std::make_pair(std::move(g), fl);
+  });
+  struct JoinOuts {  // never leave the helper running past an exception
+    std::future<std::pair<GBatch, double>>& f;
+    ~JoinOuts() { if (f.valid()) f.wait(); }
+  } join_outs{outs_fut};
   // memoised leaf products needed by dense targets, and row factors of admissible X blocks
   HostTimer ht1(C, "assemble_xv_rf");
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
@@ -459,44 +510,9 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
     htt.~HostTimer();
     new (&htt) HostTimer(C, "asm_outs");
-    GBatch g;
-    int k2max = 0;
-    for (int k : y.cb().rank) k2max = std::max(k2max, k);
-    for (int k : x.cb().rank) k2max = std::max(k2max, k);
-    if (k2max > 256) throw StructureErr("gsum: 3-factor middle dimension above 256");
-    g.k2max = std::max(k2max, 64);  // group sums T (64 x ka) / U (kb x 64) share the Ts buffer
-    double fl = 0.0;
-    for (int b = 0; b < B.nb; ++b) {
-      const int t = B.row[b], r = B.col[b];
-      if (!part.mine(t)) continue;
-      const bool dense = B.near_leaf(b);
-      const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
-      GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
-      // grouped kind-a / kind-b terms (asm_expand_kernel emits nf = 4 / 5 under the same rule)
-      const int ka = y.cb().rank[r], kb = x.rb().rank[t];
-      if (ka <= 64) {
-        o.ka = ka;
-        o.da = dense ? y.cb().leafm(r).tref() : qc.bc[r].tref();
-      }
-      if (kb <= 64) {
-        o.kb = kb;
-        o.ab = dense ? x.rb().leafm(t).ref() : qr.bc[t].ref();
-      }
-      g.outs.push_back(o);
-      if (C.prof)
-        for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
-          const int s = pt.ts[i];
-          const double m = tgt.r, n = tgt.c;
-          if (pt.tk[i] == 'c') fl += 2 * m * n * mid.size(s);
-          else if (pt.tk[i] == 'a') {
-            const double k = y.rb().rank[s], k2 = y.cb().rank[r];
-            fl += 2 * m * k * k2 + 2 * m * k2 * n;
-          } else {
-            const double k = x.rb().rank[t], k2 = x.cb().rank[s];
-            fl += 2 * m * k * k2 + 2 * m * k2 * n;
-          }
-        }
-    }
+    auto gf = outs_fut.get();
+    GBatch& g = gf.first;
+    const double fl = gf.second;
     static const bool dbg_asm = getenv("H2G_DEBUG_ASM") != nullptr;
     if (dbg_asm) {  // output-shape census of the assembly launch (algorithmic vs 64x64-tile work)
       auto up = [](double v, double q) { return std::ceil(v / q) * q; };

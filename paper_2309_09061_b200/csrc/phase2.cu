@@ -655,6 +655,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
 // Final projection (reference coarsening.py:354-405).
 static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs,
                                          std::shared_ptr<const Blocks> coarse, ArenaPtr ar) {
+  HostTimer htp(C, "p2_project_plan");
   const BView pv = g.bv();
   const BView cv{coarse.get(), false};
   validate_coarse(pv, cv);
@@ -716,6 +717,8 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     }
     gw.run(C);
   }
+  htp.~HostTimer();
+  new (&htp) HostTimer(C, "p2_project_blocks");
   GBatch g1;
   std::vector<XItem> items;
   for (int b = 0; b < cb.nb; ++b) {

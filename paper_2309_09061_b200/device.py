@@ -278,6 +278,19 @@ class DeviceH2:
         cur.wait_stream(self.ctx.stream)
         return out
 
+    def save(self, path):
+        """Write this matrix to a binary packed file (packed.save_packed; device gather + one copy
+        per family, no host H2Matrix objects)."""
+        from .packed import save_packed
+        save_packed(path, self.download_packed(), self.block_tree)
+
+    @classmethod
+    def load(cls, path, ctx: Context | None = None) -> "DeviceH2":
+        """Upload a binary packed file (packed.save_packed / save_h2) to the device."""
+        from .packed import load_packed
+        d, bt = load_packed(path)
+        return cls.upload_packed(d, bt, ctx)
+
     def packed_bytes(self) -> int:
         """Bytes of the packed float64 payload (bases + couplings + nearfield)."""
         s = self.sizes()

@@ -21,7 +21,10 @@ import numpy as np
 from .h2 import ClusterBasis, H2Matrix
 from .trees import BlockTree, ClusterTree
 
-__all__ = ["pack_h2", "unpack_h2", "pack_tree", "unpack_tree"]
+__all__ = ["pack_h2", "unpack_h2", "pack_tree", "unpack_tree", "pack_structure", "unpack_structure",
+           "save_h2", "load_h2", "save_packed", "load_packed", "FORMAT"]
+
+FORMAT = "h2g-packed-1"  # on-disk: one .npz (uncompressed) holding the packed layout below
 
 
 def pack_tree(tree, p, out):
@@ -79,16 +82,33 @@ def _unpack_basis(d, p, tree) -> ClusterBasis:
     return ClusterBasis(tree, rank, leaf, xfer)
 
 
-def pack_h2(g: H2Matrix, prefix: str = "") -> dict:
-    out = {}
+def pack_structure(bt: BlockTree, prefix: str = "", out: dict | None = None) -> dict:
+    """Cluster trees + block tree of the packed layout (rows., cols., bt. keys)."""
+    out = {} if out is None else out
     p = prefix
-    bt = g.block_tree
     pack_tree(bt.rows, p + "rows.", out)
     pack_tree(bt.cols, p + "cols.", out)
     f = bt.flat()
     out[p + "bt.row"], out[p + "bt.col"] = f["row"], f["col"]
     out[p + "bt.child_ptr"], out[p + "bt.child_idx"] = f["child_ptr"], f["child_idx"]
     out[p + "bt.adm"] = np.asarray(bt.admissible, dtype=np.uint8)
+    return out
+
+
+def unpack_structure(d, prefix: str = "", rows=None, cols=None) -> BlockTree:
+    p = prefix
+    rows = rows if rows is not None else unpack_tree(d, p + "rows.")
+    cols = cols if cols is not None else unpack_tree(d, p + "cols.")
+    ptr, idx = np.asarray(d[p + "bt.child_ptr"]), np.asarray(d[p + "bt.child_idx"])
+    kids = [tuple(int(c) for c in idx[ptr[i]:ptr[i + 1]]) for i in range(len(ptr) - 1)]
+    return BlockTree(rows, cols, d[p + "bt.row"], d[p + "bt.col"], kids, np.asarray(d[p + "bt.adm"]).astype(bool))
+
+
+def pack_h2(g: H2Matrix, prefix: str = "") -> dict:
+    out = {}
+    p = prefix
+    bt = g.block_tree
+    pack_structure(bt, p, out)
     _pack_basis(g.row_basis, p + "rb.", out)
     _pack_basis(g.col_basis, p + "cb.", out)
     for name, store in (("coup", g.coupling), ("near", g.nearfield)):
@@ -105,12 +125,8 @@ def pack_h2(g: H2Matrix, prefix: str = "") -> dict:
 
 def unpack_h2(d, prefix: str = "", rows=None, cols=None) -> H2Matrix:
     p = prefix
-    rows = rows if rows is not None else unpack_tree(d, p + "rows.")
-    cols = cols if cols is not None else unpack_tree(d, p + "cols.")
-    ptr, idx = np.asarray(d[p + "bt.child_ptr"]), np.asarray(d[p + "bt.child_idx"])
-    kids = [tuple(int(c) for c in idx[ptr[i]:ptr[i + 1]]) for i in range(len(ptr) - 1)]
-    bt = BlockTree(rows, cols, d[p + "bt.row"], d[p + "bt.col"], kids,
-                   np.asarray(d[p + "bt.adm"]).astype(bool))
+    bt = unpack_structure(d, p, rows, cols)
+    rows, cols = bt.rows, bt.cols
     rb = _unpack_basis(d, p + "rb.", rows)
     cb = _unpack_basis(d, p + "cb.", cols)
     coup, near = {}, {}
@@ -126,3 +142,35 @@ def unpack_h2(d, prefix: str = "", rows=None, cols=None) -> H2Matrix:
                 n = rows.size(t) * cols.size(s)
                 near[b] = ndat[noff[b]:noff[b] + n].reshape(rows.size(t), cols.size(s))
     return H2Matrix(bt, rb, cb, coup, near)
+
+
+def save_packed(path, packed: dict, block_tree: BlockTree | None = None):
+    """Write a packed-layout dict (e.g. DeviceH2.download_packed()) to one binary .npz; the
+    structure keys come from `block_tree` when the dict lacks them.  Replaces the reference's
+    JSON serialisation (h2mul/h2.py:314-397) for matrices of GB size."""
+    d = dict(packed)
+    if "bt.row" not in d:
+        if block_tree is None:
+            raise ValueError("packed dict without structure: pass its block_tree")
+        pack_structure(block_tree, "", d)
+    np.savez(path, __format__=np.array([FORMAT]), **d)
+
+
+def load_packed(path):
+    """(packed dict, BlockTree) of a file written by save_packed / save_h2."""
+    with np.load(path) as z:
+        if "__format__" not in z.files or str(z["__format__"][0]) != FORMAT:
+            raise ValueError(f"{path}: not an {FORMAT} file")
+        d = {k: z[k] for k in z.files if k != "__format__"}
+    return d, unpack_structure(d)
+
+
+def save_h2(path, g: H2Matrix):
+    """Host H2Matrix -> binary packed file (h2mul.h2_to_json's role, h2.py:362-381)."""
+    save_packed(path, pack_h2(g))
+
+
+def load_h2(path) -> H2Matrix:
+    """Binary packed file -> host H2Matrix (h2mul.h2_from_json's role, h2.py:384-397)."""
+    d, bt = load_packed(path)
+    return unpack_h2(d, rows=bt.rows, cols=bt.cols)

@@ -259,3 +259,17 @@ def test_gpu_input_builder_matches_host(name, n):
     d = load(name)
     x = P.recompress(dxr, spec["eps"])
     assert list(x.download().row_basis.rank) == list(d["rank.x_row"])
+
+
+def test_device_save_load_roundtrip(tmp_path):
+    """DeviceH2.save / DeviceH2.load through the binary packed file: bit-identical Z."""
+    P = _P()
+    d = load("rand_s2_2d")
+    x, y, eps = _inputs(d)
+    dx = P.DeviceH2.upload(x)
+    z = P.coarsen(P.multiply(dx, P.DeviceH2.upload(y), eps), dx.block_tree, eps)
+    path = tmp_path / "z.npz"
+    z.save(path)
+    z2 = P.DeviceH2.load(path)
+    a, b = z.download_packed(), z2.download_packed()
+    assert set(a) == set(b) and all(np.array_equal(a[k], b[k]) for k in a)

@@ -61,3 +61,23 @@ def test_interpolation_is_accurate_small():
     r = np.abs(pts[:, None] - pts[None, :])
     ref = np.where(r > 0, -np.log(np.where(r > 0, r, 1.0)), 0.0) * w * w
     assert np.linalg.norm(dense - ref, 2) / np.linalg.norm(ref, 2) < 1e-3
+
+
+def test_binary_packed_file_roundtrip(tmp_path):
+    """save_h2 / load_h2 (the binary replacement of h2_to_json / h2_from_json, h2.py:314-397)."""
+    from paper_2309_09061_b200.packed import load_h2, load_packed, save_h2, FORMAT
+    d = load("rand_s0_tol1e-3")
+    g = unpack_h2(d, "x/")
+    path = tmp_path / "x.npz"
+    save_h2(path, g)
+    g2 = load_h2(path)
+    assert g2.block_tree.row == g.block_tree.row and g2.block_tree.col == g.block_tree.col
+    assert list(g2.row_basis.rank) == list(g.row_basis.rank)
+    v = np.random.default_rng(0).standard_normal(g.shape[1])
+    assert np.array_equal(h2_matvec_host(g2, v), h2_matvec_host(g, v))
+    p1, p2 = pack_h2(g), load_packed(path)[0]
+    assert set(p1) == set(p2) and all(np.array_equal(p1[k], p2[k]) for k in p1)
+    bad = tmp_path / "bad.npz"
+    np.savez(bad, x=np.zeros(1))
+    with pytest.raises(ValueError, match=FORMAT):
+        load_h2(bad)
