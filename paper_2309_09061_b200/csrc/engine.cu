@@ -54,10 +54,10 @@ void* Arena::alloc_bytes(size_t nb) {
 
 double* Arena::alloc(size_t n) { return (double*)alloc_bytes(n * sizeof(double)); }
 
-Ctx::Ctx(int dev, cudaStream_t s) : device(dev), st(s) {
+Ctx::Ctx(int dev, cudaStream_t s, int priority) : device(dev), st(s) {
   cuda_check(cudaSetDevice(dev), "cudaSetDevice");
   if (!st) {
-    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, priority), "stream");
     own_stream = true;
   }
   // keep freed stream-ordered allocations in the pool between products (the default threshold of 0
@@ -191,8 +191,29 @@ void Ctx::flush() {
   }
 }
 
+Ctx& Ctx::aux() {
+  if (!aux_) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    aux_.reset(new Ctx(device, nullptr, least));
+  }
+  aux_->timing = timing;
+  aux_->prof = prof;
+  aux_->trace = trace;
+  aux_->trace_tid = 2;
+  aux_->trace_base = trace_base;
+  aux_->trace_host0 = trace_host0;
+  aux_->trace_out = trace_out;
+  aux_->channel = 2;  // no collectives
+  return *aux_;
+}
+
 Ctx& Ctx::side() {
-  if (!side_) side_.reset(new Ctx(device, nullptr));
+  if (!side_) {
+    int prio = 0;
+    cudaStreamGetPriority(st, &prio);  // as urgent as the main stream
+    side_.reset(new Ctx(device, nullptr, prio));
+  }
   side_->timing = timing;
   side_->prof = prof;
   side_->trace = trace;

@@ -251,9 +251,11 @@ struct Ctx {
   cudaStream_t up_stream = nullptr;  // structure uploads from the planner thread
   char* up_host = nullptr;
   size_t up_cap = 0;
-  Ctx(int dev, cudaStream_t s);
+  std::unique_ptr<Ctx> aux_;   // low-priority stream: work ahead of the critical path (dense targets)
+  Ctx(int dev, cudaStream_t s, int priority = 0);
   ~Ctx();
   Ctx& side();
+  Ctx& aux();
   void join_side(Ctx& S);  // main stream waits for the side stream's queued work
   void* stage(const void* src, size_t bytes);  // returns device pointer (copied at the next flush())
   void flush();  // enqueue the host->device copy of everything staged since the last flush
@@ -425,6 +427,15 @@ struct PTree {  // product block tree with the classified triples per node
   // (kinds a / b) and the triple arrays already copied to the device
   std::vector<int> need_xv, need_wy;
   std::vector<int> rf_blocks;  // distinct admissible-leaf X blocks of kind-a triples on non-dense targets
+  // dense targets assembled ahead (assemble_dense_early): they depend on the inputs only, so they
+  // run on the auxiliary stream while the induced bases are computed
+  struct Early {
+    bool on = false;
+    ArenaPtr near;             // the dense target blocks (become G's nearfield)
+    std::vector<double*> blk;  // per product block: its dense target (this rank's rows) or null
+    ArenaPtr scratch;          // memoised leaf products and the expanded terms
+    cudaEvent_t done = nullptr;
+  } early;
   struct Dev {
     int *tnode = nullptr, *ts = nullptr, *tbx = nullptr, *tby = nullptr;
     char* tk = nullptr;
@@ -477,6 +488,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
                      int max_rank, bool scale, double level_decay);
 PTree product_tree(BView bx, BView by);
 std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt);
+void assemble_dense_early(Ctx& A, HView x, HView y, PRef P, PTree& pt, cudaEvent_t inputs_ready, const Comm& comm);
 std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling);
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,
                             bool scale, double* near_host, long long near_cap);

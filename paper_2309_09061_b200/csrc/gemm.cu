@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restric
   };
   for (int ti = o.t0; ti < o.t1; ++ti) {
     const GTerm t = terms[ti];
+    if (t.nf == 0) continue;  // no-op (triple assembled by another launch)
     if (grp && t.nf != grp) flush();
     if (t.nf == 1) {
 #pragma unroll

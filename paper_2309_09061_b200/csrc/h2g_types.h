@@ -160,6 +160,8 @@ struct AsmTables {
   const int* kwy_col;    // rank of W_Y per column cluster
   const int* size_mid;   // middle cluster sizes
   int grouped;           // emit nf = 4 / 5 group terms where the shared factor has rank <= 64
+  int only;              // 0: every triple; 1: dense targets only; 2: coupling targets only
+                         // (the other triples become nf = 0 no-op terms; their tables are not read)
 };
 
 }  // namespace h2g

@@ -1637,7 +1637,11 @@ __global__ void asm_expand_kernel(AsmTables T, int ntrip, GTerm* __restrict__ te
   g.alpha = 1.0;
   g.pad_ = 0;
   g.d = MatRef{nullptr, 0, 0};
-  if (k == 'a' && T.grouped && T.kwy_col[r] <= 64) {  // T += (xv | row factor) S_Y; flushed * D_r
+  if ((T.only == 1 && !dense) || (T.only == 2 && dense)) {  // handled by another launch
+    g.nf = 0;
+    g.k = g.k2 = 0;
+    g.a = g.b = g.d;
+  } else if (k == 'a' && T.grouped && T.kwy_col[r] <= 64) {  // T += (xv | row factor) S_Y; flushed * D_r
     g.nf = 4;
     g.k = T.ky_mid[s];
     g.k2 = 0;

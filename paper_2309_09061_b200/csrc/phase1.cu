@@ -308,6 +308,134 @@ static void emit_push(GBatch& g, const Mat* E, const Mat& S, const Mat* F) {
   else g.t1(S.ref());
 }
 
+// Dense targets of the product (inadmissible T^XY leaves) take only input factors -- kind a:
+// (X|ts V_Y,s) S_Y W_Y,r^T, kind b: V_X,t S_X (Y|sr^T W_X,s)^T, kind c: N_X N_Y (induced.py:
+// 286-307) -- so they are assembled as soon as T^XY exists, on the low-priority auxiliary stream,
+// while the induced bases (the level-serial critical path) run.  assemble() then adds the push-down.
+void assemble_dense_early(Ctx& A, HView x, HView y, PRef P, PTree& pt, cudaEvent_t inputs_ready, const Comm& comm) {
+  const Blocks& B = *pt.bt;
+  const Tree& rows = *B.rows;
+  const Tree& cols = *B.cols;
+  const Part part = make_part(rows, comm);
+  PTree::Early& E = pt.early;
+  E.near = std::make_shared<Arena>(A.st);
+  E.near->cross_stream = true;  // read and written by the main stream later
+  E.scratch = std::make_shared<Arena>(A.st);
+  E.blk.assign(B.nb, nullptr);
+  for (int b = 0; b < B.nb; ++b)
+    if (B.near_leaf(b) && part.mine(B.row[b]))
+      E.blk[b] = E.near->alloc((size_t)rows.size(B.row[b]) * cols.size(B.col[b]));
+  if (inputs_ready) cuda_check(cudaStreamWaitEvent(A.st, inputs_ready, 0), "wait inputs");
+  wait_near(A, *x.h);
+  wait_near(A, *y.h);
+  if (pt.dev.ready) cuda_check(cudaStreamWaitEvent(A.st, pt.dev.ready, 0), "wait upload");
+  // memoised leaf products of the dense targets (induced.py:245-258)
+  std::vector<Mat> xv, wy;
+  HView yT{y.h, !y.T}, xT{x.h, !x.T};
+  {
+    std::vector<int> want;
+    for (int b : pt.need_xv)
+      if (part.mine(x.row(b))) want.push_back(b);
+    xv_compute(A, *E.scratch, x, y, P, want, xv);
+  }
+  xv_compute(A, *E.scratch, yT, xT, PRef{P.P, !P.T}, pt.need_wy, wy);
+  const Blocks& BX = *x.h->bt;
+  const Blocks& BY = *y.h->bt;
+  const Tree& mid = x.cols();
+  const int ntrip = (int)pt.ts.size();
+  std::vector<unsigned char> ndense(B.nb), xadm(BX.nb);
+  for (int b = 0; b < B.nb; ++b) ndense[b] = B.near_leaf(b) ? 1 : 0;
+  const MatRef z{nullptr, 0, 0};
+  std::vector<MatRef> xcoup(BX.nb, z), xnear(BX.nb, z), xvr(BX.nb, z);
+  for (int b = 0; b < BX.nb; ++b) {
+    xadm[b] = BX.adm_leaf(b) ? 1 : 0;
+    if (BX.adm_leaf(b)) xcoup[b] = x.coup(b);
+    if (BX.near_leaf(b)) xnear[b] = x.near(b);
+    if (b < (int)xv.size()) xvr[b] = xv[b].ref();
+  }
+  std::vector<MatRef> ycoup(BY.nb, z), ynear(BY.nb, z), wyl(BY.nb, z);
+  for (int b = 0; b < BY.nb; ++b) {
+    if (BY.adm_leaf(b)) ycoup[b] = y.coup(b);
+    if (BY.near_leaf(b)) ynear[b] = y.near(b);
+    if (b < (int)wy.size()) wyl[b] = wy[b].ref();
+  }
+  std::vector<MatRef> vxleaf(rows.n, z), wyleaf(cols.n, z);
+  for (int t = 0; t < rows.n; ++t)
+    if (rows.leaf(t)) vxleaf[t] = x.rb().leafm(t).ref();
+  for (int r = 0; r < cols.n; ++r)
+    if (cols.leaf(r)) wyleaf[r] = y.cb().leafm(r).ref();
+  std::vector<int> size_mid(mid.n);
+  for (int s = 0; s < mid.n; ++s) size_mid[s] = mid.size(s);
+  AsmTables T{};
+  T.tnode = pt.dev.tnode;
+  T.ts = pt.dev.ts;
+  T.tk = pt.dev.tk;
+  T.tbx = pt.dev.tbx;
+  T.tby = pt.dev.tby;
+  T.node_row = A.push(B.row);
+  T.node_col = A.push(B.col);
+  T.node_dense = A.push(ndense);
+  T.xcoup = A.push(xcoup);
+  T.xnear = A.push(xnear);
+  T.xadm = A.push(xadm);
+  T.xv = A.push(xvr);
+  T.ycoup = A.push(ycoup);
+  T.ynear = A.push(ynear);
+  T.wyl = A.push(wyl);
+  T.vxleaf = A.push(vxleaf);
+  T.wyleaf = A.push(wyleaf);
+  T.kx_row = A.push(x.rb().rank);
+  T.kwx_mid = A.push(x.cb().rank);
+  T.ky_mid = A.push(y.rb().rank);
+  T.kwy_col = A.push(y.cb().rank);
+  T.size_mid = A.push(size_mid);
+  T.grouped = 1;
+  T.only = 1;  // coupling targets need the induced bases: assemble() does them
+  GTerm* d_terms = (GTerm*)E.scratch->alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
+  A.flush();
+  cuda_check(launch_asm_expand(T, ntrip, d_terms, A.st), "asm_expand(dense)");
+  ++A.launches;
+  GBatch g;
+  int k2max = 0;
+  for (int k : y.cb().rank) k2max = std::max(k2max, k);
+  for (int k : x.cb().rank) k2max = std::max(k2max, k);
+  if (k2max > 256) throw StructureErr("gsum: 3-factor middle dimension above 256");
+  g.k2max = std::max(k2max, 64);
+  double fl = 0.0;
+  for (int b = 0; b < B.nb; ++b) {
+    if (!E.blk[b]) continue;
+    const int t = B.row[b], r = B.col[b];
+    const Mat tgt{E.blk[b], rows.size(t), cols.size(r)};
+    GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
+    const int ka = y.cb().rank[r], kb = x.rb().rank[t];
+    if (ka <= 64) {
+      o.ka = ka;
+      o.da = y.cb().leafm(r).tref();
+    }
+    if (kb <= 64) {
+      o.kb = kb;
+      o.ab = x.rb().leafm(t).ref();
+    }
+    g.outs.push_back(o);
+    if (A.prof)
+      for (int i = pt.tptr[b]; i < pt.tptr[b + 1]; ++i) {
+        const int s = pt.ts[i];
+        const double m = tgt.r, n = tgt.c;
+        if (pt.tk[i] == 'c') fl += 2 * m * n * mid.size(s);
+        else if (pt.tk[i] == 'a') fl += 2 * m * y.rb().rank[s] * ka + 2 * m * ka * n;
+        else fl += 2 * m * kb * x.cb().rank[s] + 2 * m * x.cb().rank[s] * n;
+      }
+  }
+  {
+    StageTag tag(A, "p1.dense");
+    g.run_device_terms(A, d_terms, fl);
+  }
+  cuda_check(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(E.done, A.st), "event");
+  A.flush();
+  E.on = true;
+}
+
 // Product over T^XY in the induced bases + push-down (reference induced.py:220-355).
 std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt) {
   HostTimer ht(C, "assemble_total");
@@ -318,6 +446,11 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   auto ar = std::make_shared<Arena>(C.st);
   G->owned.push_back(ar);
   G->near_owner = ar;
+  const bool early = pt.early.on;  // dense targets already queued on the auxiliary stream
+  if (early) {
+    G->owned.push_back(pt.early.near);
+    G->near_owner = pt.early.near;
+  }
   Arena sc(C.st);
   const Blocks& B = *pt.bt;
   const Tree& rows = *B.rows;
@@ -334,7 +467,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     const int t = B.row[b], r = B.col[b];
     if (!part.mine(t)) continue;
     if (B.near_leaf(b)) {
-      G->near[b] = ar->alloc((size_t)rows.size(t) * cols.size(r));
+      G->near[b] = early ? pt.early.blk[b] : ar->alloc((size_t)rows.size(t) * cols.size(r));
     } else {
       Arena& a = B.adm_leaf(b) ? *ar : sc;
       cp[b] = Mat{a.alloc((size_t)Q.rank[t] * W.rank[r]), Q.rank[t], W.rank[r]};
@@ -358,6 +491,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       const int t = B.row[b], r = B.col[b];
       if (!part.mine(t)) continue;
       const bool dense = B.near_leaf(b);
+      if (dense && early) continue;
       const Mat tgt = dense ? Mat{G->near[b], rows.size(t), cols.size(r)} : cp[b];
       GOut o{tgt.p, tgt.c, tgt.r, tgt.c, 0, pt.tptr[b], pt.tptr[b + 1]};
       // grouped kind-a / kind-b terms (asm_expand_kernel emits nf = 4 / 5 under the same rule)
@@ -395,7 +529,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   // memoised leaf products needed by dense targets, and row factors of admissible X blocks
   HostTimer ht1(C, "assemble_xv_rf");
   HView yT{y.h, !y.T}, xT{x.h, !x.T};
-  {
+  if (!early) {
     HostTimer hx(C, "asm_xv1");
     if (part.on()) {
       std::vector<int> want;
@@ -406,7 +540,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       xv_compute(C, sc, x, y, P, pt.need_xv, qr.xv);
     }
   }
-  {
+  if (!early) {
     HostTimer hx(C, "asm_xv2");
     xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, pt.need_wy, qc.xv);
   }
@@ -464,7 +598,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     HostTimer htt(C, "asm_tables");
     std::vector<int> size_mid(mid.n);
     for (int s = 0; s < mid.n; ++s) size_mid[s] = mid.size(s);
-    AsmTables T;
+    AsmTables T{};
     T.tnode = pt.dev.tnode;
     T.ts = pt.dev.ts;
     T.tk = pt.dev.tk;
@@ -495,19 +629,12 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     T.kwy_col = C.push(y.cb().rank);
     T.size_mid = C.push(size_mid);
     T.grouped = 1;
+    T.only = early ? 2 : 0;
     GTerm* d_terms = (GTerm*)sc.alloc_bytes(sizeof(GTerm) * std::max(1, ntrip));
     C.flush();
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
     C.sub_end(S_MISC, sw);
     ++C.launches;
-    if (pt.dev.block) {  // the triple arrays are consumed: release them in stream order
-      cudaFreeAsync(pt.dev.block, C.st);
-      pt.dev.block = nullptr;
-    }
-    if (pt.dev.ready) {
-      cudaEventDestroy(pt.dev.ready);
-      pt.dev.ready = nullptr;
-    }
     htt.~HostTimer();
     new (&htt) HostTimer(C, "asm_outs");
     auto gf = outs_fut.get();
@@ -547,6 +674,21 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
                 alg[d] * 1e-9, pad[d] * 1e-9);
     }
     g.run_device_terms(C, d_terms, fl);
+  }
+  // the dense targets (queued ahead) receive the push-down: wait for them; the triple arrays are
+  // consumed by both expansions, release them in stream order
+  if (early) {
+    cuda_check(cudaStreamWaitEvent(C.st, pt.early.done, 0), "wait dense targets");
+    cudaEventDestroy(pt.early.done);
+    pt.early.done = nullptr;
+  }
+  if (pt.dev.block) {
+    cudaFreeAsync(pt.dev.block, C.st);
+    pt.dev.block = nullptr;
+  }
+  if (pt.dev.ready) {
+    cudaEventDestroy(pt.dev.ready);
+    pt.dev.ready = nullptr;
   }
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
   HostTimer ht3(C, "assemble_pushdown");
@@ -614,16 +756,35 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr, e4 = nullptr;
   record(C, e0);
   // T^XY is pure structure: build it on a host thread while the GPU computes weights and bases
-  auto pt_future = std::async(std::launch::async, [&x, &y, &C] {
-    PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
-    ptree_prepare(pt, C, *x.bt, y.bt->nb);
-    return pt;
-  });
   auto keep = std::make_shared<Arena>(C.st);
   Arena sc(C.st);
   HView X{&x, false}, Y{&y, false}, XT{&x, true}, YT{&y, true};
   StageTag tag0(C, "p1.weights");
   MatStore P = basis_product(C, sc, *x.cb, *y.rb);
+  // T^XY is pure structure: build it on a host thread while the GPU computes weights and bases;
+  // the same thread then queues the dense targets (inputs only) on the low-priority stream
+  const bool ahead = !serial_passes();
+  cudaEvent_t p_ready = nullptr;
+  Ctx* A = nullptr;
+  if (ahead) {
+    A = &C.aux();
+    cuda_check(cudaEventCreateWithFlags(&p_ready, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(p_ready, C.st), "event");
+  }
+  auto pt_future = std::async(std::launch::async, [&x, &y, &C, &P, A, p_ready, X, Y] {
+    PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+    ptree_prepare(pt, C, *x.bt, y.bt->nb);
+    if (A) assemble_dense_early(*A, X, Y, PRef{&P, false}, pt, p_ready, C.comm);
+    return pt;
+  });
+  struct PtJoin {  // never leave the planner running past an exception
+    std::future<PTree>& f;
+    cudaEvent_t e;
+    ~PtJoin() {
+      if (f.valid()) f.wait();
+      if (e) cudaEventDestroy(e);
+    }
+  } pt_join{pt_future, p_ready};
   record(C, e1);
   // the row and column bases are independent until the assembly: run them concurrently, the
   // column pass on a side stream driven by a second host thread
@@ -678,6 +839,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   }
   StageTag taga(C, "p1.asm");
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
+  if (A) C.join_side(*A);  // counters / profile of the auxiliary stream's work
   record(C, e4);
   G->owned.push_back(keep);
   G->owned.push_back(keep2);

@@ -30,7 +30,9 @@ class Context:
         self.lib = N.load()
         self.device = device
         # the native context runs on a torch-owned stream so torch CUDA events can time it
-        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        # high priority: the engine queues work ahead on a low-priority stream (dense-target assembly)
+        # that must not hold back the level-serial critical path
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device, priority=-5)
         h = N.P()
         N.check(self.lib.h2g_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
         self.h = h
