@@ -15,6 +15,8 @@ import numpy as np
 from .errors import CudaError, InvalidInputError, StructureError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libh2g.so")
+# H2G_LIB: an alternative build of the same library (A/B timing of engine changes, tools/ab.sh)
+LIB_PATH = os.environ.get("H2G_LIB", LIB_PATH)
 
 _lib = None
 

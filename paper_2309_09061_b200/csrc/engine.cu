@@ -651,7 +651,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     const int k1 = std::min(it.m, it.kx);
     const int n = it.m - k1;
     it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
-    if (svd_finish_smem(it.m, it.kx, true) > kSmemLimit) fin_rsmem = false;
+    if (svd_finish_smem(it.m, it.kx, true, false) > kSmemLimit) fin_rsmem = false;
     if (tile_path(n)) {
       const long long per = 128LL * tpc;
       it.nchunk = (int)std::max<long long>(1, (it.N + per - 1) / per);
@@ -688,10 +688,14 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   if (sm_prep > kSmemLimit) throw StructureErr("svd: protected basis too large for shared memory");
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
+  // the finish stage keeps R in shared memory when it fits (first choice), V beside it when that fits too
+  bool fin_vsmem = true;
+  for (const SvdItem& it : live)
+    if (svd_finish_smem(it.m, it.kx, fin_rsmem, true) > kSmemLimit) fin_vsmem = false;
   for (size_t i = 0; i < live.size(); ++i) {
     const SvdItem& it = live[i];
     const int n = it.m - std::min(it.m, it.kx);
-    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem));
+    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem, fin_vsmem));
     if (sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
     if (tile_path(n)) continue;
     sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
@@ -747,7 +751,8 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   int fin_nmax = 0;
   for (auto& it : live) fin_nmax = std::max(fin_nmax, it.m - std::min(it.m, it.kx));
   C.flush();
-  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, fin_nmax, C.st), "svd_finish");
+  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, fin_vsmem, fin_nmax, C.st),
+             "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);

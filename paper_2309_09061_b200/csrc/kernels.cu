@@ -521,19 +521,25 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
   const int np = (nr + 1) & ~1;
   const int npairs = np / 2, m1 = np - 1;
   const double tol2 = kEps * kEps * (double)n;
-  const int q = threadIdx.x >> 3, ol = lane & 7;
+  const int q0 = threadIdx.x >> 3, ol = lane & 7, nq = blockDim.x >> 3;
   const unsigned omask = 0xffu << (lane & 24);
-  const bool act = q < npairs;
-  // circle method positions of this octet's pair, advanced by one per step (no divisions)
-  int xa = q, xb = q == 0 ? 0 : m1 - q;
-  if (xb >= m1) xb -= m1;
+  // circle method positions of this octet's pairs (q0 and q0 + nq: n <= 192 with 64 octets),
+  // advanced by one per step (no divisions)
+  int xa0 = q0 < m1 ? q0 : 0, xb0 = q0 == 0 ? 0 : (q0 < m1 ? m1 - q0 : 0);
+  if (xb0 >= m1) xb0 -= m1;
+  int xa1 = q0 + nq < m1 ? q0 + nq : 0, xb1 = q0 + nq < m1 ? m1 - q0 - nq : 0;
+  if (xb1 >= m1) xb1 -= m1;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int step = 0; step < m1; ++step) {
-      const int a = (q == 0) ? 0 : 1 + xa;
-      const int b = 1 + xb;
-      if (act && a < nr && b < nr) {
+     constexpr int kReps = NPL > 16 ? 2 : 1;  // n <= 128: one pair per octet suffices
+#pragma unroll
+     for (int r = 0; r < kReps; ++r) {
+      const int q = q0 + r * nq;
+      const int a = (q == 0) ? 0 : 1 + (r ? xa1 : xa0);
+      const int b = 1 + (r ? xb1 : xb0);
+      if (q < npairs && a < nr && b < nr) {
         double* ra = W + a * n;
         double* rb = W + b * n;
         double x[NPL], y[NPL];
@@ -576,8 +582,11 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
           if (ol == 0) *flag = 1;
         }
       }
-      if (++xa == m1) xa = 0;
-      if (++xb == m1) xb = 0;
+     }
+      if (++xa0 == m1) xa0 = 0;
+      if (++xb0 == m1) xb0 = 0;
+      if (++xa1 == m1) xa1 = 0;
+      if (++xb1 == m1) xb1 = 0;
       __syncthreads();
     }
     const int any = *flag;
@@ -860,12 +869,13 @@ __device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, d
   return n;
 }
 
-// NPLO: octet-Jacobi entries per lane (8: n <= 64, 16: n <= 128), 0: half-warp loop (n > 128)
+// NPLO: octet-Jacobi entries per lane (8: n <= 64, 16: n <= 128, 24: n <= 192), 0: half-warp loop
 static constexpr int NT = 512;
 // RS: R in shared memory (compile-time, so every access to it is an LDS/STS rather than a generic
 // load), else R is worked on in place in global memory (items too large for shared memory).
 template <int NPLO, bool RS>
-__global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items) {
+__global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
+                                                                             int vsm) {
   extern __shared__ double smem[];
   __shared__ int flag;
   __shared__ int s_k2;
@@ -875,9 +885,7 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
   const long long N = it.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ldv = kx | 1;
-  double* V = smem;                          // m x ldv (reflectors from the tsqr stage)
-  double* tv = V + (long long)m * ldv;       // kx + 1
-  double* sig = tv + kx + 1;                 // n
+  double* sig = smem;                        // n
   int* ord = (int*)(sig + n);                // n ints
   double* cn = sig + n + (n / 2 + 1);        // QRCP column norms (n), reference norms (n), reflector (n)
   double* cn0 = cn + n;
@@ -885,8 +893,12 @@ __global__ void __launch_bounds__(NT, NPLO == 16 ? 1 : 2) svd_finish_kernel(cons
   int* perm = (int*)(vh + n);                // n ints
   int* iperm = perm + n;                     // n ints
   double* R = RS ? vh + n + n + 1 : it.rbuf;
+  // V (m x ldv, reflectors of the protected basis) and tv (kx + 1): staged in shared memory after
+  // the rest when they fit (vsm), else read where the tsqr stage left them
+  double* V = vsm ? (RS ? R + (long long)n * n : vh + n + n + 1) : it.vws;
+  double* tv = V + (long long)m * ldv;
   __shared__ int ired[NT / 32 + 2];
-  if (kx > 0) {
+  if (kx > 0 && vsm) {
     for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
     for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
   }
@@ -1709,6 +1721,8 @@ static void init_attributes() {
     opt_in((const void*)svd_finish_kernel<0, true>);
     opt_in((const void*)svd_finish_kernel<8, true>);
     opt_in((const void*)svd_finish_kernel<16, true>);
+    opt_in((const void*)svd_finish_kernel<24, true>);
+    opt_in((const void*)svd_finish_kernel<24, false>);
     opt_in((const void*)svd_finish_kernel<0, false>);
     opt_in((const void*)svd_finish_kernel<8, false>);
     opt_in((const void*)svd_finish_kernel<16, false>);
@@ -1763,10 +1777,10 @@ size_t merge_smem(int n, bool rsmem) {
   return sizeof(double) * ((size_t)kPanel * (n | 1) + 68 + (rsmem ? (size_t)n * n : 0));
 }
 
-size_t svd_finish_smem(int m, int kx, bool rsmem) {
+size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem) {
   const int k1 = m < kx ? m : kx;
   const int n = m - k1;
-  return sizeof(double) * ((size_t)m * (kx | 1) + kx + 1 + n + (n / 2 + 1) + 4 * (size_t)n + 1 +
+  return sizeof(double) * ((vsmem ? (size_t)m * (kx | 1) + kx + 1 : 0) + n + (n / 2 + 1) + 4 * (size_t)n + 1 +
                            (rsmem ? (size_t)n * n : 0));
 }
 
@@ -1778,17 +1792,21 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
   return cudaGetLastError();
 }
 
-cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, int nmax, cudaStream_t st) {
+cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, bool vsmem, int nmax,
+                              cudaStream_t st) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
+  const int v = vsmem ? 1 : 0;
   if (rsmem) {
-    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items);
-    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items);
-    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items);
+    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, v);
+    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items, v);
+    else if (nmax <= 192) svd_finish_kernel<24, true><<<nitems, NT, smem, st>>>(items, v);
+    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items, v);
   } else {
-    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items);
-    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items);
-    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items);
+    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items, v);
+    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items, v);
+    else if (nmax <= 192) svd_finish_kernel<24, false><<<nitems, NT, smem, st>>>(items, v);
+    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items, v);
   }
   return cudaGetLastError();
 }

@@ -150,6 +150,7 @@ struct PtrClusterHash {
 };
 
 static void resolve_jobs(Ctx& C, Arena& sc, Jobs& J, const Basis& w) {
+  HostTimer ht(C, "p2_jobs");
   std::unordered_map<std::pair<const double*, int>, Mat, PtrClusterHash> inter;
   inter.reserve(J.v.size());
   std::vector<std::vector<std::pair<const Jobs::J*, int>>> waves;
@@ -462,6 +463,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     if (dbg_jobs)
       fprintf(stderr, "level %d: %zu merged reps, %zu nodes, %zu jobs, path pool %zu\n", lev, mblocks.size(),
               mpool.cl.size(), J.v.size(), J.pool.size());
+    htm.~HostTimer();
+    new (&htm) HostTimer(C, "p2_merge_resolve");
     resolve_jobs(C, sc, J, w1);
     }
 

@@ -13,7 +13,8 @@ dxr, dyr, spec = build_config_device(cfg, n=n, ctx=ctx)
 dx = P.recompress(dxr, spec["eps"], ctx=ctx)
 dy = dx if dyr is dxr else P.recompress(dyr, spec["eps"], ctx=ctx)
 eps = spec["eps"]
-z = P.coarsen(P.multiply(dx, dy, eps, ctx=ctx), dx.block_tree, eps, ctx=ctx)
+for _ in range(int(os.environ.get("WARMUP", "3"))):  # steady state (host allocations, pools)
+    z = P.coarsen(P.multiply(dx, dy, eps, ctx=ctx), dx.block_tree, eps, ctx=ctx)
 ctx.synchronize()
 ctx.set_timing(True)
 g = P.multiply(dx, dy, eps, ctx=ctx)
