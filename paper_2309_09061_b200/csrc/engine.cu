@@ -555,7 +555,7 @@ void NormBatch::run_async(Ctx& C) {
       mid.push_back(it);
       continue;
     }
-    const bool rowside = (it.m <= it.N) || (it.m <= 160);
+    const bool rowside = it.m <= it.N;
     const long long g = rowside ? it.m : it.N;
     if (norm_smem(it.m, it.N, true) <= kSmemLimit) {
       smem = std::max(smem, norm_smem(it.m, it.N, true));

@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
 }
 
 // ---------------------------------------------------------------------------------------------
-// norm_kernel: sigma_1 of hstack(segs) (m x N).  Gram on the row side (m <= N or m <= 160),
+// norm_kernel: sigma_1 of hstack(segs) (m x N).  Gram on the row side (m <= N),
 // else on the column side; tridiagonalise; Sturm multisection for lambda_max.
 // ---------------------------------------------------------------------------------------------
 
@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
     if (threadIdx.x == 0) *it.out = 0.0;
     return;
   }
-  const bool rowside = (m <= N) || (m <= 160);
+  const bool rowside = m <= N;  // Gram on the smaller side
   const int g = rowside ? m : (int)N;
   double* G = it.gbuf ? it.gbuf : smem;                  // g x g (global scratch for large items)
   double* Pn = it.gbuf ? smem : G + (long long)g * g;    // 32 x max(m, N) panel
@@ -1812,7 +1812,7 @@ cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, boo
 }
 
 size_t norm_smem(int m, long long N, bool gram_in_smem) {
-  const bool rowside = (m <= N) || (m <= 160);
+  const bool rowside = m <= N;  // Gram on the smaller side
   const int g = rowside ? m : (int)N;
   const int w = rowside ? m : (int)N;
   return sizeof(double) * ((gram_in_smem ? (size_t)g * g : 0) + (size_t)kPanel * w + 4 * (size_t)g);
