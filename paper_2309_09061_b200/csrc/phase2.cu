@@ -655,13 +655,67 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   return S;
 }
 
-// Final projection (reference coarsening.py:354-405).
-static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs,
-                                         std::shared_ptr<const Blocks> coarse, ArenaPtr ar) {
-  HostTimer htp(C, "p2_project_plan");
+// Final projection (reference coarsening.py:354-405), in two parts: the structure (product block
+// of every coarse leaf, representation leaves of the covered admissible blocks, the transfer chains
+// to materialise) needs only the row pass and is planned while the column pass still runs; the
+// products need both.
+struct ProjLeaf {
+  int c;
+  bool adm;
+  Mat M;
+};
+struct ProjPlan {
+  std::vector<int> pb;          // per coarse block: the product block (leaves only)
+  std::vector<int> lptr;        // per coarse block: its representation leaves [lptr[b], lptr[b+1])
+  std::vector<ProjLeaf> leaves;
+  std::vector<std::vector<std::pair<int, int>>> waves;  // chains (r, c) of depth >= 2, by depth
+};
+
+static ProjPlan plan_project(HView g, const CState& rs, const Blocks& cb) {
   const BView pv = g.bv();
-  const BView cv{coarse.get(), false};
-  validate_coarse(pv, cv);
+  validate_coarse(pv, BView{&cb, false});
+  const Blocks& pt = *g.h->bt;
+  const Tree& ctree = *cb.cols;
+  // multi-GPU: the coarse blocks of this rank's row subtrees
+  ProjPlan P;
+  P.pb.assign(cb.nb, -1);
+  P.lptr.assign(cb.nb + 1, 0);
+  std::unordered_map<long long, char> seen;
+  seen.reserve(1024);
+  std::function<void(int, int)> need = [&](int r, int c) {
+    if (ctree.parent[c] == r || c == r) return;
+    const long long key = (long long)r * ctree.n + c;
+    if (seen.count(key)) return;
+    seen[key] = 1;
+    need(r, ctree.parent[c]);
+    int d = 0;
+    for (int u = c; u != r; u = ctree.parent[u]) ++d;
+    if ((int)P.waves.size() <= d) P.waves.resize(d + 1);
+    P.waves[d].push_back(std::make_pair(r, c));
+  };
+  std::vector<int> lv;
+  for (int b = 0; b < cb.nb; ++b) {
+    P.lptr[b + 1] = P.lptr[b];
+    if (!cb.leaf(b)) continue;
+    const int pb = pt.find(cb.row[b], cb.col[b]);
+    P.pb[b] = pb;
+    if (!cb.adm[b] || pt.adm_leaf(pb)) continue;
+    const CTRef rr = rs.reps[pb];
+    if (!rr.t) continue;  // (a partitioned rank holds only its own rows' representations)
+    lv.clear();
+    rr.t->leaves(rr.root, lv);
+    for (int u : lv) {
+      P.leaves.push_back(ProjLeaf{rr.t->cl[u], rr.t->adm[u] != 0, rr.t->mat[u]});
+      need(cb.col[b], rr.t->cl[u]);
+    }
+    P.lptr[b + 1] = (int)P.leaves.size();
+  }
+  return P;
+}
+
+static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs,
+                                         std::shared_ptr<const Blocks> coarse, ArenaPtr ar, const ProjPlan& plan) {
+  HostTimer htp(C, "p2_project_plan");
   auto Z = std::make_shared<H2>();
   Z->bt = coarse;
   Z->rb = rs.q;
@@ -680,37 +734,15 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   std::unordered_map<long long, Mat> chain;
   chain.reserve(1024);
   auto ckey = [&](int r, int c) { return (long long)r * ctree.n + c; };
-  std::vector<std::vector<std::pair<int, int>>> waves;
-  std::function<void(int, int)> need = [&](int r, int c) {
-    if (ctree.parent[c] == r || c == r) return;
-    const long long key = ckey(r, c);
-    if (chain.count(key)) return;
-    need(r, ctree.parent[c]);
-    int d = 0;
-    for (int u = c; u != r; u = ctree.parent[u]) ++d;
-    chain[key] = Mat{sc.alloc((size_t)qc.rank[c] * qc.rank[r]), qc.rank[c], qc.rank[r]};
-    if ((int)waves.size() <= d) waves.resize(d + 1);
-    waves[d].push_back(std::make_pair(r, c));
-  };
+  for (auto& wave : plan.waves)
+    for (auto& key : wave)
+      chain[ckey(key.first, key.second)] =
+          Mat{sc.alloc((size_t)qc.rank[key.second] * qc.rank[key.first]), qc.rank[key.second], qc.rank[key.first]};
   auto chain_ref = [&](int r, int c) -> Mat {
     if (ctree.parent[c] == r) return qc.xferm(c);
     return chain[ckey(r, c)];
   };
-  std::vector<int> lv;
-  // multi-GPU: the coarse blocks of this rank's row subtrees, then an all-gather of Z
-  const Part part = make_part(*cb.rows, C.comm);
-  // collect the needed chains
-  for (int b = 0; b < cb.nb; ++b) {
-    if (!cb.adm_leaf(b) || !part.mine(cb.row[b])) continue;
-    const int pb = pt.find(cb.row[b], cb.col[b]);
-    if (pt.adm_leaf(pb)) continue;
-    const CTRef rr = rs.reps[pb];
-    if (!rr.t) throw StructureErr("missing representation of a covered product block");
-    lv.clear();
-    rr.t->leaves(rr.root, lv);
-    for (int u : lv) need(cb.col[b], rr.t->cl[u]);
-  }
-  for (auto& wave : waves) {
+  for (auto& wave : plan.waves) {
     GBatch gw;
     for (auto& key : wave) {
       const int r = key.first, c = key.second;
@@ -720,6 +752,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     }
     gw.run(C);
   }
+  const Part part = make_part(*cb.rows, C.comm);
   htp.~HostTimer();
   new (&htp) HostTimer(C, "p2_project_blocks");
   GBatch g1;
@@ -727,7 +760,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
   for (int b = 0; b < cb.nb; ++b) {
     if (!cb.leaf(b)) continue;
     const int t = cb.row[b], r = cb.col[b];
-    const int pb = pt.find(t, r);
+    const int pb = plan.pb[b];
     const bool shared = !cb.adm[b] && pt.near_leaf(pb) && !g.T && g.h->near_owner;
     if (!part.mine(t) && !shared) {  // received below
       if (cb.adm[b]) items.push_back(XItem{part.owner[t], (long long)qr.rank[t] * qc.rank[r], &Z->coup[b]});
@@ -745,15 +778,14 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
       if (pt.adm_leaf(pb)) {
         g1.t3(rs.r[t].ref(), g.coup(pb), cs.r[r].tref(), rs.r[t].c, cs.r[r].c);
       } else {
-        const CT& rep = *rs.reps[pb].t;
-        lv.clear();
-        rep.leaves(rs.reps[pb].root, lv);
-        for (int u : lv) {  // lift (coarsening.py:374-382)
-          const int c = rep.cl[u];
-          const Mat& M = rep.mat[u];
-          const MatRef X = rep.adm[u] ? cs.r[c].tref() : qc.leafm(c).ref();
-          if (c == r) g1.t2(M.ref(), X, M.c);
-          else g1.t3(M.ref(), X, chain_ref(r, c).ref(), M.c, qc.rank[c]);
+        if (plan.lptr[b] == plan.lptr[b + 1] && !rs.reps[pb].t)
+          throw StructureErr("missing representation of a covered product block");
+        for (int li = plan.lptr[b]; li < plan.lptr[b + 1]; ++li) {  // lift (coarsening.py:374-382)
+          const ProjLeaf& L = plan.leaves[li];
+          const int c = L.c;
+          const MatRef X = L.adm ? cs.r[c].tref() : qc.leafm(c).ref();
+          if (c == r) g1.t2(L.M.ref(), X, L.M.c);
+          else g1.t3(L.M.ref(), X, chain_ref(r, c).ref(), L.M.c, qc.rank[c]);
         }
       }
     } else if (shared) {
@@ -914,11 +946,13 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   // row and column coarse bases are independent until the final projection: concurrent passes
   auto ar2 = std::make_shared<Arena>(C.st);
   CState rs, cs;
+  ProjPlan plan;
   if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
     rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
                      prep_r.get());
     cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
                      prep_c.get());
+    plan = plan_project(HView{&g, false}, rs, *coarse);
   } else {
     Ctx& S = C.side();
     ar2->st = S.st;
@@ -936,6 +970,8 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     try {
       rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
                        prep_r.get());
+      HostTimer htpp(C, "p2_project_structure");
+      plan = plan_project(HView{&g, false}, rs, *coarse);  // while the column pass runs
     } catch (...) {
       th.join();
       throw;
@@ -947,7 +983,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   if (C.timing) { e1 = C.event(); cudaEventRecord(e1, C.st); }
   e2 = e1;
   StageTag tagp(C, "p2.project");
-  auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar);
+  auto Z = project_final(C, HView{&g, false}, rs, cs, coarse, ar, plan);
   if (pf.ev) {
     Z->near_on_host = std::move(pf.mask);
     Z->near_host = near_host;
