@@ -350,8 +350,8 @@ def main():
             traffic = json.load(fh).get("dram_bytes_per_launch")
     roofline = {"bound": "fp64", "kernel": "gsum_mma_kernel", "achieved": achieved, "peak": peak_fp64,
                 "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": traffic,
-                "traffic_note": "dram read+write of the assembly launch (grid 46288) from one ncu --set full "
-                                "capture, profiles/r01_gsum_ncu.json",
+                "traffic_note": "dram read+write of the dense-target assembly launch (gsum_mma_kernel<1>, the "
+                                "longest GEMM launch) from one ncu --set full capture, profiles/r01_gsum_ncu.json",
                 "flops_note": "reference-ledger flops of the terms (per-triple shapes); the grouped assembly "
                               "executes fewer",
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in MEASURED_PEAKS.json)",

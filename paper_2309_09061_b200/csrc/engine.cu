@@ -342,7 +342,7 @@ void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
     GTile* d_l = C.push(tiles);
     cudaEvent_t ev = C.prof_begin();
     C.flush();
-    cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+    cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st, tag), "gsum");
     C.prof_end(K_GSUM, ev, flops_hint, 0.0);
     ++C.launches;
   }

@@ -23,7 +23,7 @@ struct CudaFailure : std::runtime_error { using std::runtime_error::runtime_erro
 void cuda_check(cudaError_t e, const char* what);
 
 // ------------------------------------------------------------------ kernels (kernels.cu)
-cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
+cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t, int tag = 0);
 cudaError_t launch_qr_chunks(const QrItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
                              cudaStream_t);
 cudaError_t launch_tsqr_merge(const MergeWork*, int nwork, size_t smem, bool rsmem, cudaStream_t);
@@ -321,6 +321,7 @@ struct GBatch {
   void run(Ctx& C);
   // launch with a device-resident term array (terms generated on the GPU); `outs` index into it
   void run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint);
+  int tag = 0;               // kernel symbol (1: dense-target assembly, selectable in profilers)
   std::vector<GTile> tiles;  // prepare_tiles(): the 64x64 output tiles, built ahead (any thread)
   bool tiles_ready = false;
   void prepare_tiles();

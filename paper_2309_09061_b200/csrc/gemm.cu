@@ -136,6 +136,9 @@ __device__ __forceinline__ void acc_to_smem(const Acc& a, double* S, int ld, int
       }
 }
 
+// Tag: 0 = every batch, 1 = the dense-target assembly (same code; its own symbol so profilers can
+// select that launch by name)
+template <int Tag>
 __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restrict__ outs,
                                                          const GTerm* __restrict__ terms,
                                                          const GTile* __restrict__ tiles, int k2max) {
@@ -224,17 +227,19 @@ size_t gsum_mma_smem(int k2max) {
 }
 
 cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
-                            cudaStream_t st) {
+                            cudaStream_t st, int tag) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, (const void*)gsum_mma_kernel);
-    cudaFuncSetAttribute((const void*)gsum_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024 - (int)fa.sharedSizeBytes);
-    cudaFuncSetAttribute((const void*)gsum_mma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    for (const void* fn : {(const void*)gsum_mma_kernel<0>, (const void*)gsum_mma_kernel<1>}) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, fn);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
   });
   if (ntiles == 0) return cudaSuccess;
-  gsum_mma_kernel<<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
+  if (tag == 1) gsum_mma_kernel<1><<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
+  else gsum_mma_kernel<0><<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
   return cudaGetLastError();
 }
 

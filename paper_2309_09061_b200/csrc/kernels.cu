@@ -1733,11 +1733,11 @@ static void init_attributes() {
 }
 
 cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
-                            cudaStream_t st);
+                            cudaStream_t st, int tag);
 
 cudaError_t launch_gsum(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
-                        cudaStream_t st) {
-  return launch_gsum_mma(outs, terms, tiles, ntiles, k2max, st);
+                       cudaStream_t st, int tag) {
+  return launch_gsum_mma(outs, terms, tiles, ntiles, k2max, st, tag);
 }
 
 size_t qr_smem(int n, bool rsmem) {

@@ -428,6 +428,7 @@ void assemble_dense_early(Ctx& A, HView x, HView y, PRef P, PTree& pt, cudaEvent
   }
   {
     StageTag tag(A, "p1.dense");
+    g.tag = 1;  // gsum_mma_kernel<1>: the dense-target launch, selectable by name in ncu
     g.run_device_terms(A, d_terms, fl);
   }
   cuda_check(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming), "event");
