@@ -751,7 +751,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   int fin_nmax = 0;
   for (auto& it : live) fin_nmax = std::max(fin_nmax, it.m - std::min(it.m, it.kx));
   C.flush();
-  cuda_check(launch_svd_finish(d_items, (int)live.size(), sm_fin, fin_rsmem, fin_vsmem, fin_nmax, C.st),
+  cuda_check(launch_svd_finish(d_items, d_s, (int)live.size(), sm_fin, fin_rsmem, fin_vsmem, fin_nmax, C.st),
              "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;

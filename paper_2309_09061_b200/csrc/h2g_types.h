@@ -89,7 +89,7 @@ struct SvdItem {
   double* rbuf;     // nchunk x (n x n) partial R factors, n = m - min(m, kx)
   double* vws;      // m x kx Householder vectors of V + kx coefficients
   int* sweeps_out;  // optional diagnostic: Jacobi sweeps used, n, live rows, k2
-  int pad2_;
+  int zskip;        // 1: segments whose device divisor is exactly 0 are absent (their widths leave N)
   double* q2;       // tile path with kx > 0: explicit Q_V (m x m), written by svd_prep_kernel
 };
 

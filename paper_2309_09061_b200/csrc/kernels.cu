@@ -875,6 +875,7 @@ static constexpr int NT = 512;
 // load), else R is worked on in place in global memory (items too large for shared memory).
 template <int NPLO, bool RS>
 __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
+                                                                             const Seg* __restrict__ segs,
                                                                              int vsm) {
   extern __shared__ double smem[];
   __shared__ int flag;
@@ -882,7 +883,12 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
   __shared__ double jred[NT / 32 + 2];
   const SvdItem it = items[blockIdx.x];
   const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
-  const long long N = it.N;
+  long long N = it.N;
+  if (it.zskip)  // blocks of exactly zero norm are not columns of the reference's stack (induced.py:121-125)
+    for (int q = it.s0; q < it.s1; ++q) {
+      const Seg sg = segs[q];
+      if (sg.sdiv && *sg.sdiv == 0.0) N -= sg.w;
+    }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ldv = kx | 1;
   double* sig = smem;                        // n
@@ -1792,21 +1798,21 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
   return cudaGetLastError();
 }
 
-cudaError_t launch_svd_finish(const SvdItem* items, int nitems, size_t smem, bool rsmem, bool vsmem, int nmax,
-                              cudaStream_t st) {
+cudaError_t launch_svd_finish(const SvdItem* items, const Seg* segs, int nitems, size_t smem, bool rsmem, bool vsmem,
+                              int nmax, cudaStream_t st) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
   const int v = vsmem ? 1 : 0;
   if (rsmem) {
-    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, v);
-    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items, v);
-    else if (nmax <= 192) svd_finish_kernel<24, true><<<nitems, NT, smem, st>>>(items, v);
-    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items, v);
+    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, segs, v);
+    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items, segs, v);
+    else if (nmax <= 192) svd_finish_kernel<24, true><<<nitems, NT, smem, st>>>(items, segs, v);
+    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items, segs, v);
   } else {
-    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items, v);
-    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items, v);
-    else if (nmax <= 192) svd_finish_kernel<24, false><<<nitems, NT, smem, st>>>(items, v);
-    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items, v);
+    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items, segs, v);
+    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items, segs, v);
+    else if (nmax <= 192) svd_finish_kernel<24, false><<<nitems, NT, smem, st>>>(items, segs, v);
+    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items, segs, v);
   }
   return cudaGetLastError();
 }

@@ -151,6 +151,8 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
   std::vector<Mat> vx(tr.n);
   std::vector<Mat> rfb(B.nb);
   std::vector<int> Lp;
+  double* d_nrm = sc.alloc(std::max(1, B.nb));  // sigma_1 per block (0: absent from the SVD stacks)
+  cuda_check(cudaMemsetAsync(d_nrm, 0, sizeof(double) * std::max(1, B.nb), C.st), "memset");
   for (int lev = tr.depth; lev >= 0; --lev) {
     if (part.on()) Lp = part.filter(tr.by_level[lev]);
     const std::vector<int>& L = part.on() ? Lp : tr.by_level[lev];
@@ -212,11 +214,11 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
     }
     g2.run(C);
 
-    // block norms for block-relative scaling (induced.py:121-125); exact zero norms are skipped
-    std::vector<double> nrm(B.nb, 1.0);
+    // block norms for block-relative scaling (induced.py:121-125), left on the device: they divide
+    // the SVD segments there, and the SVD drops the columns of exact-zero blocks (SvdItem::zskip)
+    // -- no host synchronisation for them
     if (scale) {
       NormBatch nbat;
-      std::vector<int> ids;
       for (int t : L)
         for (int b : mids[t]) {
           NormItem it{};
@@ -225,11 +227,11 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
           it.s1 = nbat.sl.begin();
           it.m = blk[b].r;
           it.N = blk[b].c;
+          it.out = d_nrm + b;
           nbat.items.push_back(it);
-          ids.push_back(b);
         }
-      auto v = nbat.run(C, sc);
-      for (size_t i = 0; i < ids.size(); ++i) nrm[ids[i]] = v[i];
+      nbat.scratch = &sc;
+      nbat.run_async(C);
     }
 
     // weighted stack w_i = blk_i Z_s^T / ||blk_i|| and the protected truncated SVD (induced.py:115-146)
@@ -243,13 +245,12 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       it.s0 = sv.sl.begin();
       long long N = 0;
       for (int b : mids[t]) {
-        if (scale && nrm[b] == 0.0) continue;
         const Mat& Z = zy[x.col(b)];
         if (Z.r == 0 || m == 0) continue;
         Mat w{sc.alloc((size_t)m * Z.r), m, Z.r};
         g3.out(w, false);
-        g3.t2(blk[b].ref(), Z.tref(), Z.c, scale ? 1.0 / nrm[b] : 1.0);
-        sv.sl.add(w.ref(), Z.r);
+        g3.t2(blk[b].ref(), Z.tref(), Z.c);
+        sv.sl.add(w.ref(), Z.r, 1.0, scale ? d_nrm + b : nullptr);  // w_i = blk_i Z_s^T / ||blk_i||
         N += Z.r;
       }
       it.s1 = sv.sl.begin();
@@ -257,6 +258,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       it.kx = kx;
       it.N = N;
       it.v = vx[t].ref();
+      it.zskip = scale ? 1 : 0;
       it.tol = tol * std::pow(level_decay, (double)lev);
       it.cap = max_rank < 0 ? -1 : std::max(0, max_rank - k1);
       const long long kcap = std::min<long long>(m, k1 + N);
