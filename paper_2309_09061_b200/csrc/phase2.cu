@@ -266,7 +266,8 @@ static CPrep prep_rows(BView pv, BView coarse) {
 
 // Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
 static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
-                          const std::vector<double>& cn, const double* d_nn, const CPrep& prep) {
+                          const std::vector<double>& cn, const double* d_nn, const CPrep& prep,
+                          cudaEvent_t nn_ready = nullptr) {
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   const BView pv = g.bv();
   const Blocks& pt = *g.h->bt;
@@ -340,6 +341,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     qb.run(C, sc);
   }
 
+  // the nearfield norms (SVD segment divisors at the leaves) come from the auxiliary stream
+  if (nn_ready) cuda_check(cudaStreamWaitEvent(C.st, nn_ready, 0), "wait nearfield norms");
   std::vector<Mat> lm(pt.nb);  // R_t S_b for admissible leaves used inside representations
   for (int lev = tr.depth; lev >= 0; --lev) {
     if (part.on()) Lp = part.filter(tr.by_level[lev]);
@@ -813,7 +816,10 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
 // sigma_1 of every coupling (synchronously: their exact zeros skip rows of the Z stacks) and every
 // nearfield block of g (asynchronously into a device array: they only scale SVD segments)
 // (coarsening.py:342-351)
-static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn) {
+// The coupling norms are needed first (top-down Z), the nearfield norms only at the leaf SVDs: with
+// an auxiliary context the latter run there, under the Z levels, and `nn_ready` completes them.
+static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn, Ctx* A = nullptr,
+                      cudaEvent_t* nn_ready = nullptr) {
   const Blocks& B = *g.bt;
   NormBatch nbn, nbc;
   std::vector<int> ids;
@@ -839,7 +845,19 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, d
     nb.items.push_back(it);
     if (coupling) ids.push_back(b);
   }
-  nbn.run_async(C);
+  if (A) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(e, C.st), "event");  // G final, d_nn zero-filled
+    cuda_check(cudaStreamWaitEvent(A->st, e, 0), "wait");
+    cudaEventDestroy(e);
+    nbn.run_async(*A);
+    A->flush();
+    cuda_check(cudaEventCreateWithFlags(nn_ready, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(*nn_ready, A->st), "event");
+  } else {
+    nbn.run_async(C);
+  }
   cn.assign(B.nb, 0.0);
   auto vals = nbc.run(C, sc);
   for (size_t i = 0; i < ids.size(); ++i) cn[ids[i]] = vals[i];
@@ -935,10 +953,16 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   auto prep_c = std::async(std::launch::async, [gvt, cvt] { return prep_rows(gvt, cvt); });
   Arena sc(C.st);
   std::vector<double> cn;
+  cudaEvent_t nn_ready = nullptr;
+  struct EvGuard {
+    cudaEvent_t& e;
+    ~EvGuard() { if (e) cudaEventDestroy(e); }
+  } nn_guard{nn_ready};
   double* d_nn = sc.alloc(std::max(1, g.bt->nb));
   if (scale) {
     StageTag tag(C, "p2.norms");
-    all_norms(C, sc, g, cn, d_nn);
+    if (!serial_passes()) all_norms(C, sc, g, cn, d_nn, &C.aux(), &nn_ready);
+    else all_norms(C, sc, g, cn, d_nn);
   }
   prep_r.wait();
   prep_c.wait();
@@ -961,7 +985,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     std::thread th([&] {
       try {
         cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
-                         prep_c.get());
+                         prep_c.get(), nn_ready);
         S.sync();
       } catch (...) {
         err = std::current_exception();
@@ -969,7 +993,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     });
     try {
       rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
-                       prep_r.get());
+                       prep_r.get(), nn_ready);
       HostTimer htpp(C, "p2_project_structure");
       plan = plan_project(HView{&g, false}, rs, *coarse);  // while the column pass runs
     } catch (...) {
@@ -991,6 +1015,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     Z->owned.push_back(pf.arena);
   }
   Z->owned.push_back(ar2);
+  if (nn_ready) C.join_side(C.aux());  // counters / profile of the auxiliary stream's norms
   Z->own_rows = g.own_rows;
   Z->own_cols = g.own_cols;
   if (C.timing) {
