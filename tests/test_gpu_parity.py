@@ -273,3 +273,61 @@ def test_device_save_load_roundtrip(tmp_path):
     z2 = P.DeviceH2.load(path)
     a, b = z.download_packed(), z2.download_packed()
     assert set(a) == set(b) and all(np.array_equal(a[k], b[k]) for k in a)
+
+
+def _expand(basis, t):
+    from paper_2309_09061_b200.h2 import expand_basis
+    return expand_basis(basis, t)
+
+
+@pytest.mark.parametrize("seed,tol", [(30, 0.1), (31, 1e-3), (32, 0.0)])
+def test_induced_and_final_bases_are_isometric(seed, tol):
+    """Q_t^T Q_t = I for every cluster of the induced (phase 1) and final (phase 2) bases
+    (reference test_induced.py:97-104, test_coarsening.py:153-166)."""
+    P = _P()
+    x, y = _oracle_pair(seed)
+    g = P.multiply(x, y, tol)
+    z = P.coarsen(g, x.block_tree, tol)
+    for basis in (g.row_basis, g.col_basis, z.row_basis, z.col_basis):
+        for t in range(basis.tree.nnodes):
+            q = _expand(basis, t)
+            assert np.linalg.norm(q.T @ q - np.eye(q.shape[1])) <= 1e-11
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_induced_bases_protect_the_input_bases(seed):
+    """span V_X,t is inside the induced row basis Q_t, span W_Y,r inside the column basis
+    (reference test_induced.py:85-94: Q_t basis_change_t = V_X,t)."""
+    P = _P()
+    x, y = _oracle_pair(seed + 20)
+    g = P.multiply(x, y, 0.3)
+    for q_basis, v_basis in ((g.row_basis, x.row_basis), (g.col_basis, y.col_basis)):
+        for t in range(q_basis.tree.nnodes):
+            q, v = _expand(q_basis, t), _expand(v_basis, t)
+            assert np.linalg.norm(v - q @ (q.T @ v)) <= 1e-12 * (1 + np.linalg.norm(v))
+
+
+def test_block_relative_error_per_coarse_leaf():
+    """Coarsening onto a coarser admissibility: every coarse admissible leaf within 10 eps of the
+    product block (reference test_coarsening.py:190-206)."""
+    P = _P()
+    from paper_2309_09061_b200.h2 import to_dense
+    from paper_2309_09061_b200.trees import build_block_tree
+    eps = 1e-4
+    x, y = _oracle_pair(13)
+    g = P.multiply(x, y, eps)
+    coarse = build_block_tree(g.block_tree.rows, g.block_tree.cols, 1.0)
+    z = P.coarsen(g, coarse, eps)
+    ref, got = to_dense(g), to_dense(z)
+    rows, cols = coarse.rows, coarse.cols
+    checked = 0
+    for b in range(coarse.nblocks):
+        if coarse.children[b] or not coarse.admissible[b]:
+            continue
+        t, r = coarse.row[b], coarse.col[b]
+        sr = slice(int(rows.start[t]), int(rows.stop[t]))
+        sc = slice(int(cols.start[r]), int(cols.stop[r]))
+        blk_ref, blk_got = ref[sr, sc], got[sr, sc]
+        assert np.linalg.norm(blk_got - blk_ref, 2) <= 10 * eps * np.linalg.norm(blk_ref, 2) + 1e-13
+        checked += 1
+    assert checked > 0
