@@ -98,3 +98,42 @@ def test_partitioned_product_meets_golden_bars(world, names):
             assert r["gv"] <= r["tol"], (rank, name, r)
             assert r["zv"] <= r["tol"], (rank, name, r)
             assert r["vs_single"] <= 1e-12, (rank, name, r)
+
+
+def _nccl_worker(port, q):
+    try:
+        import ctypes as C
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        sys.path.insert(0, os.path.dirname(HERE))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        from paper_2309_09061_b200.device import Context
+        from paper_2309_09061_b200.shard import Sharding
+        ctx = Context(0)
+        sh = Sharding(ctx)  # one rank: the engine never calls it, so call the trampoline directly
+        buf = torch.arange(4096, dtype=torch.uint8, device="cuda")
+        ref = buf.clone()
+        off = (C.c_longlong * 2)(0, 4096)
+        rc = sh._allgather(None, 1, buf.data_ptr(), off, 1, ctx.stream.cuda_stream)
+        torch.cuda.synchronize()
+        q.put((rc, bool(torch.equal(buf, ref)), sh.calls, sh.backend))
+        dist.destroy_process_group()
+    except BaseException:
+        import traceback
+        q.put(("error", traceback.format_exc(), 0, ""))
+
+
+def test_nccl_allgather_trampoline_world1():
+    """The NCCL branch of the engine's all-gather callback (broadcasts on the engine's stream via
+    ExternalStream + __cuda_array_interface__) runs cleanly; world size 1 is all one GPU allows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(60)
+    assert res[0] == 0, res
+    assert res[1] and res[2] == 1 and res[3] == "nccl"
