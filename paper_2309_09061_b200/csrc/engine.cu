@@ -1158,7 +1158,9 @@ void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
   }
   const int nbx = BX.nb;
   std::vector<char> seenx(nbx, 0), seeny(nby, 0), seenf(nbx, 0);
+  const Part part = make_part(*B.rows, C.comm);  // multi-GPU: only this rank's product rows
   for (int b = 0; b < B.nb; ++b) {
+    if (!part.mine(B.row[b])) continue;
     if (!B.near_leaf(b)) {
       for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
         const int bts = P.tbx[i];
