@@ -283,9 +283,16 @@ struct HostTimer {
   const char* name;
   std::chrono::steady_clock::time_point t0;
   HostTimer(Ctx& c, const char* n) : C(c), name(n), t0(std::chrono::steady_clock::now()) {}
-  ~HostTimer() {
-    if (C.timing)
+  ~HostTimer() { stop(); }
+  void stop() {  // book the running section (no-op once stopped)
+    if (name && C.timing)
       C.htime[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    name = nullptr;
+  }
+  void next(const char* n) {  // book the running section and start the next one
+    stop();
+    name = n;
+    t0 = std::chrono::steady_clock::now();
   }
 };
 

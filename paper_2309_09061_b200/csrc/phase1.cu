@@ -638,8 +638,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     cuda_check(launch_asm_expand(T, ntrip, d_terms, C.st), "asm_expand");
     C.sub_end(S_MISC, sw);
     ++C.launches;
-    htt.~HostTimer();
-    new (&htt) HostTimer(C, "asm_outs");
+    htt.next("asm_outs");
     auto gf = outs_fut.get();
     GBatch& g = gf.first;
     const double fl = gf.second;

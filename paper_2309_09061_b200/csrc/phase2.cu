@@ -385,8 +385,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     }
     g1.run(C);
     g2.run(C);
-    htv.~HostTimer();
-    new (&htv) HostTimer(C, "p2_dummy");
+    htv.stop();
 
     // merged representations of subdivided covered blocks (coarsening.py:260-279); all column
     // trees of the level live in pooled flat trees (no per-block allocations)
@@ -466,8 +465,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     if (dbg_jobs)
       fprintf(stderr, "level %d: %zu merged reps, %zu nodes, %zu jobs, path pool %zu\n", lev, mblocks.size(),
               mpool.cl.size(), J.v.size(), J.pool.size());
-    htm.~HostTimer();
-    new (&htm) HostTimer(C, "p2_merge_resolve");
+    htm.next("p2_merge_resolve");
     resolve_jobs(C, sc, J, w1);
     }
 
@@ -756,8 +754,7 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     gw.run(C);
   }
   const Part part = make_part(*cb.rows, C.comm);
-  htp.~HostTimer();
-  new (&htp) HostTimer(C, "p2_project_blocks");
+  htp.next("p2_project_blocks");
   GBatch g1;
   std::vector<XItem> items;
   for (int b = 0; b < cb.nb; ++b) {
