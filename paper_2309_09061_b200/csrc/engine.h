@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <future>
 #include <cstdlib>
 #include <map>
 #include <memory>
@@ -148,6 +149,9 @@ struct H2 {
   }
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
   std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
+  // phase-2 block-norm batches of this matrix (product output): built on a host thread while the
+  // assembly runs on the GPU, consumed by coarsen (declared last: joined before the rest goes)
+  std::shared_future<std::shared_ptr<struct NormPrep>> norm_prep;
 };
 
 // Transposable view of an H^2 matrix (reference H2Matrix.transposed, h2.py:169-173).
@@ -367,6 +371,15 @@ struct NormBatch {
   Arena* scratch = nullptr;  // for Gram matrices of large items (else a local arena)
 };
 
+// Spectral-norm batches of every leaf block of an H^2 matrix (reference coarsening.py:342-351):
+// nearfield norms (device-resident divisors) and coupling norms (read back), pure host structure.
+struct NormPrep {
+  NormBatch nbn, nbc;
+  std::vector<int> ids;   // block of each coupling item
+  std::vector<int> nids;  // block of each nearfield item (its output slot in the divisor array)
+};
+std::shared_ptr<NormPrep> build_norm_prep(const H2& g, const Comm& comm);
+
 struct SvdBatch {
   SegList sl;
   std::vector<SvdItem> items;
@@ -496,7 +509,9 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
 Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, PRef P, double tol,
                      int max_rank, bool scale, double level_decay);
 PTree product_tree(BView bx, BView by);
-std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt);
+std::vector<Mat> row_factors(Ctx& C, Arena& sc, HView x, HView y, const Induced& qr, PRef P, const PTree& pt);
+std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt,
+                             const std::vector<Mat>* rf_pre = nullptr);
 void assemble_dense_early(Ctx& A, HView x, HView y, PRef P, PTree& pt, cudaEvent_t inputs_ready, const Comm& comm);
 std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling);
 std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, double tol, int max_rank,

@@ -362,6 +362,10 @@ __global__ void qr_out_kernel(const QrItem* __restrict__ items) {
 // Rotation of the row pair (a, b) with Gram entries al = |a|^2, be = |b|^2, ga = a.b:
 // t = sign(d) 2ga / (|d| + hypot(d, 2ga)), d = be - al (the smaller root of t^2 + 2 zeta t - 1,
 // zeta = d / 2ga; Rutishauser), c = 1 / sqrt(1 + t^2), s = c t.  One sqrt, one division, one rsqrt.
+// Row stride of R in the finish kernel's shared memory: >= n and == 4 (mod 16) -- even (double2
+// rows) and 8 banks between consecutive rows.
+__host__ __device__ inline int fin_ld(int n) { return n + (20 - n % 16) % 16; }
+
 __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga, double& c, double& sn) {
   const double d = be - al, g2 = 2.0 * ga;
   const double ad = fabs(d), ag = fabs(g2);
@@ -385,7 +389,7 @@ __device__ __forceinline__ void jacobi_rotation(double al, double be, double ga,
 
 // NPL > 0: rows of length n <= 16 NPL held in registers per half-warp (unrolled); NPL = 0: loops.
 template <int NPL>
-__device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
+__device__ int jacobi_rows(double* W, int nr, int n, int ld, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   // Rows whose norm is below eps * (largest row norm) can never pass the truncation threshold
   // (thr >= max(rows, cols) eps sigma_1); rotating against them moves the other row by less than
@@ -395,7 +399,7 @@ __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
     double mx = 0.0;
     for (int i = warp; i < nr; i += nw) {
       double s = 0.0;
-      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * n + j], W[(long long)i * n + j], s);
+      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * ld + j], W[(long long)i * ld + j], s);
       s = warp_sum(s);
       mx = fmax(mx, s);
     }
@@ -430,8 +434,8 @@ __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
         const int a = (q == 0) ? 0 : 1 + xa;
         const int b = 1 + xb;
         if (a >= nr || b >= nr) continue;  // bye (odd nr): uniform per half-warp
-        double* ra = W + (long long)a * n;
-        double* rb = W + (long long)b * n;
+        double* ra = W + (long long)a * ld;
+        double* rb = W + (long long)b * ld;
         double al = 0.0, be = 0.0, ga = 0.0;
         double xav[NPL > 0 ? NPL : 1], xbv[NPL > 0 ? NPL : 1];
         if (NPL > 0) {
@@ -497,14 +501,22 @@ __device__ int jacobi_rows(double* W, int nr, int n, int* flag, double* red) {
 // ceil(n / 8) entries per lane.  Against the half-warp version it halves the lanes per pair, so
 // every step is one round and the three butterflies cost 3 levels per 4 pairs instead of 4 levels
 // per 2 -- the step is then bound by the FP64 pipe rather than by shuffles and issue overhead.
-template <int NPL>
-__device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red) {
+// V2 (R in shared memory, ld even and the padding columns zero): lane ol of an octet owns the
+// double2 pairs (2 ol, 2 ol + 1) + 16 k, so each octet's LDS.128 / STS.128 covers 128 contiguous
+// bytes -- one conflict-free quarter-warp wavefront whatever the two rows are (the scalar mapping
+// ol + 8 k put two rows' 64-byte windows in one half-warp, two-way conflicts for most pairs).
+// Stop after a sweep whose rotations all had |cos angle| = |gamma| / sqrt(alpha beta) <= 1e-9:
+// cyclic Jacobi converges quadratically, so the rows are then orthogonal to ~1e-18 and the
+// confirming sweep (which would find nothing above the sqrt(n) eps threshold) is skipped.
+static constexpr double kQuad = 1e-18;
+template <int NPL, bool V2>
+__device__ int jacobi_rows_oct(double* W, int nr, int n, int ld, int* flag, double* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   {
     double mx = 0.0;
     for (int i = warp; i < nr; i += nw) {
       double s = 0.0;
-      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * n + j], W[(long long)i * n + j], s);
+      for (int j = lane; j < n; j += 32) s = fma(W[(long long)i * ld + j], W[(long long)i * ld + j], s);
       s = warp_sum(s);
       mx = fmax(mx, s);
     }
@@ -530,7 +542,7 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
   int xa1 = q0 + nq < m1 ? q0 + nq : 0, xb1 = q0 + nq < m1 ? m1 - q0 - nq : 0;
   if (xb1 >= m1) xb1 -= m1;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
+    if (threadIdx.x == 0) flag[0] = flag[1] = 0;
     __syncthreads();
     for (int step = 0; step < m1; ++step) {
      constexpr int kReps = NPL > 16 ? 2 : 1;  // n <= 128: one pair per octet suffices
@@ -540,14 +552,28 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
       const int a = (q == 0) ? 0 : 1 + (r ? xa1 : xa0);
       const int b = 1 + (r ? xb1 : xb0);
       if (q < npairs && a < nr && b < nr) {
-        double* ra = W + a * n;
-        double* rb = W + b * n;
+        double* ra = W + a * ld;
+        double* rb = W + b * ld;
         double x[NPL], y[NPL];
+        if (V2) {
 #pragma unroll
-        for (int k = 0; k < NPL; ++k) {
-          const int j = ol + 8 * k;
-          x[k] = j < n ? ra[j] : 0.0;
-          y[k] = j < n ? rb[j] : 0.0;
+          for (int k = 0; k < NPL; k += 2) {
+            const int j = 2 * ol + 8 * k;
+            double2 u = make_double2(0.0, 0.0), v = make_double2(0.0, 0.0);
+            if (j < n) {
+              u = *reinterpret_cast<const double2*>(ra + j);
+              v = *reinterpret_cast<const double2*>(rb + j);
+            }
+            x[k] = u.x; x[k + 1] = u.y;
+            y[k] = v.x; y[k + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < NPL; ++k) {
+            const int j = ol + 8 * k;
+            x[k] = j < n ? ra[j] : 0.0;
+            y[k] = j < n ? rb[j] : 0.0;
+          }
         }
         double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
 #pragma unroll
@@ -571,15 +597,29 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
         if (ga != 0.0 && al > frozen && be > frozen && ga * ga > tol2 * al * be) {
           double c, sn;
           jacobi_rotation(al, be, ga, c, sn);
+          if (V2) {
 #pragma unroll
-          for (int k = 0; k < NPL; ++k) {
-            const int j = ol + 8 * k;
-            if (j < n) {
-              ra[j] = c * x[k] - sn * y[k];
-              rb[j] = sn * x[k] + c * y[k];
+            for (int k = 0; k < NPL; k += 2) {
+              const int j = 2 * ol + 8 * k;
+              if (j < n) {
+                *reinterpret_cast<double2*>(ra + j) = make_double2(c * x[k] - sn * y[k], c * x[k + 1] - sn * y[k + 1]);
+                *reinterpret_cast<double2*>(rb + j) = make_double2(sn * x[k] + c * y[k], sn * x[k + 1] + c * y[k + 1]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) {
+              const int j = ol + 8 * k;
+              if (j < n) {
+                ra[j] = c * x[k] - sn * y[k];
+                rb[j] = sn * x[k] + c * y[k];
+              }
             }
           }
-          if (ol == 0) *flag = 1;
+          if (ol == 0) {
+            flag[0] = 1;
+            if (ga * ga > kQuad * al * be) flag[1] = 1;
+          }
         }
       }
      }
@@ -589,9 +629,9 @@ __device__ int jacobi_rows_oct(double* W, int nr, int n, int* flag, double* red)
       if (++xb1 == m1) xb1 = 0;
       __syncthreads();
     }
-    const int any = *flag;
+    const int any = flag[0], large = flag[1];
     __syncthreads();
-    if (!any) return sweep + 1;
+    if (!any || !large) return sweep + 1;
   }
   return 40;
 }
@@ -741,132 +781,140 @@ __global__ void __launch_bounds__(kThreads, 3) svd_tsqr_kernel(const SvdItem* __
 // is kept.  perm[c] = original column of column c.  Used as the Jacobi preconditioner
 // (Drmac-Veselic): W Pi = Q1 R1, and the rows of R1 are graded by the pivoting, so one-sided Jacobi
 // on them needs a few sweeps instead of ~15.  Left singular vectors of W^T = Pi x those of R1^T.
-__device__ int qrcp_rows_precondition(double* W, int n, int* perm, double* cn, double* cn0, double* vh,
-                                      double* red, int* ired) {
+// Truncation-aware deflation (stop_scale > 0): the threshold is thr = max(tol, big eps sigma_1) >=
+// thr_lo = max(tol, big eps |r_00|) (|r_00| = largest column norm <= sigma_1).  Once the trailing
+// block's Frobenius norm is <= kDeflate thr_lo, dropping its rows moves every singular value by at
+// most kDeflate^2 thr / 2 relative to thr (sigma_i(A)^2 - sigma_i(B)^2 in [0, ||C||^2] for A =
+// [B; C]) -- below the FP64 SVD's own absolute error eps sigma_1 (sigma_1 / thr <= 1e7 on every
+// config), so no truncation decision changes, and the kept rows' Jacobi runs on fewer rows.
+static constexpr double kDeflate = 1e-5;
+
+__device__ __forceinline__ void argmax_pair(double& best, int& bi, unsigned mask, int width) {
+  // (value, index) maximum over `width` lanes, ties to the smaller index
+  for (int o = width >> 1; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(mask, best, o);
+    const int oi = __shfl_xor_sync(mask, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+}
+
+// One barrier per pivot step.  Columns never move: the pivot p of step j is recorded (pst[p] = j)
+// and its entries stay untouched until the loop ends (every warp reads them to form the same
+// reflector redundantly), then row j of it becomes beta and the rows below zero.  The rows of R1
+// are therefore the rows of (R1 in pivoted column order) with the columns back in original order --
+// row-Jacobi is invariant under column permutations, so perm = identity.  Thread groups of four own
+// columns (rows split by residue mod 4) and publish per-warp argmax partials of the updated column
+// norms into a double-buffered slot for the next step.
+__device__ int qrcp_rows_precondition(double* W, int n, int ld, int* perm, double* cn, double* cn0, double* beta_s,
+                                      int* pst, double* red, int* ired, double tol = 0.0, double big_eps = 0.0) {
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  double cn0_first = 0.0;
+  const int grp = tid >> 2, sub = tid & 3, ngrp = nt >> 2;
+  const unsigned qmask = 0xfu << (lane & ~3);
   for (int c = tid; c < n; c += nt) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s = fma(W[(long long)i * n + c], W[(long long)i * n + c], s);
+    for (int i = 0; i < n; ++i) s = fma(W[(long long)i * ld + c], W[(long long)i * ld + c], s);
     cn[c] = cn0[c] = s;
     perm[c] = c;
+    pst[c] = -1;
   }
   __syncthreads();
-  for (int j = 0; j < n; ++j) {
+  // argmax partials of step 0 (buffer 0)
+  {
     double best = -1.0;
-    int bi = j;
-    for (int c = j + tid; c < n; c += nt)
-      if (cn[c] > best) { best = cn[c]; bi = c; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
+    int bi = n;
+    if (sub == 0)
+      for (int c = grp; c < n; c += ngrp)
+        if (cn[c] > best) { best = cn[c]; bi = c; }
+    argmax_pair(best, bi, 0xffffffffu, 32);
     if (lane == 0) { red[warp] = best; ired[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double b = -1.0;
-      int p = j;
-      for (int w = 0; w < nw; ++w)
-        if (red[w] > b || (red[w] == b && ired[w] < p)) { b = red[w]; p = ired[w]; }
-      ired[nw] = p;
+  }
+  __syncthreads();
+  double stop2 = 0.0;
+  int j = 0;
+  for (; j < n; ++j) {
+    const int buf = (j & 1) * nw, nbuf = ((j + 1) & 1) * nw;
+    // every warp reduces the partials itself (no second barrier)
+    double best = lane < nw ? red[buf + lane] : -1.0;
+    int p = lane < nw ? ired[buf + lane] : n;
+    argmax_pair(best, p, 0xffffffffu, 32);
+    const double bst = cn[p];
+    if (j == 0) {
+      const double thr_lo = fmax(tol, big_eps * sqrt(bst));
+      stop2 = fmax(kEps * kEps * bst * 0.25, kDeflate * kDeflate * thr_lo * thr_lo);
+    } else if ((double)(n - j) * bst <= stop2) {
+      break;
     }
-    __syncthreads();
-    const int p = ired[nw];
-    {
-      // Early stop: once the trailing block (rows j.., columns j..) has Frobenius norm^2
-      // <= (n - j) max cn <= eps^2 r_00^2 / 4, its rows sit below the Jacobi freeze level
-      // (eps x largest row norm; row 0 of R1 has norm >= |r_00|): they would never be rotated and
-      // can never pass the truncation threshold, so they are left unreduced and excluded.
-      const double bst = cn[p];
-      if (j == 0) cn0_first = bst;
-      else if ((double)(n - j) * bst * 4.0 <= kEps * kEps * cn0_first) return j;
+    // reflector of column p, rows j.. (LAPACK dlarfg sign convention), formed by every warp
+    double ss = 0.0;
+    for (int i = j + 1 + lane; i < n; i += 32) ss = fma(W[(long long)i * ld + p], W[(long long)i * ld + p], ss);
+    ss = warp_sum(ss);
+    const double alpha = W[(long long)j * ld + p];
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) * __drcp_rn(beta);
+      scale = __drcp_rn(alpha - beta);
     }
-    if (p != j) {
-      for (int i = tid; i < n; i += nt) {
-        const double a = W[(long long)i * n + j];
-        W[(long long)i * n + j] = W[(long long)i * n + p];
-        W[(long long)i * n + p] = a;
-      }
-      if (tid == 0) {
-        double t = cn[j]; cn[j] = cn[p]; cn[p] = t;
-        t = cn0[j]; cn0[j] = cn0[p]; cn0[p] = t;
-        const int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
-      }
-      __syncthreads();
-    }
-    if (warp == 0) {  // reflector for column j, rows j..n-1
-      double ss = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) ss = fma(W[(long long)i * n + j], W[(long long)i * n + j], ss);
-      ss = warp_sum(ss);
-      const double alpha = W[(long long)j * n + j];
-      double tau = 0.0, scale = 0.0;
-      if (ss != 0.0) {
-        const double nrm = sqrt(alpha * alpha + ss);
-        const double beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) * __drcp_rn(beta);
-        scale = __drcp_rn(alpha - beta);
-      }
-      for (int i = j + 1 + lane; i < n; i += 32) {
-        vh[i] = W[(long long)i * n + j] * scale;
-        W[(long long)i * n + j] = 0.0;
-      }
-      if (lane == 0) {
-        if (ss != 0.0) W[(long long)j * n + j] = alpha >= 0.0 ? -sqrt(alpha * alpha + ss) : sqrt(alpha * alpha + ss);
-        red[nw + 1] = tau;
-      }
-    }
-    __syncthreads();
-    const double tau = red[nw + 1];
-    // trailing update: four threads per column (rows split by residue mod 4, quad shuffles),
-    // so the dependent chain per column is a quarter of the remaining rows
-    {
-      const int sub = tid & 3;
-      const unsigned qmask = 0xfu << (lane & ~3);
-      for (int cb = j + 1; cb < n; cb += nt / 4) {
-        const int c = cb + (tid >> 2);
-        const bool act = c < n;
-        double tw = 0.0;
-        if (tau != 0.0) {
-          double w0 = 0.0, w1 = 0.0;
-          if (act) {
-            int i = j + 1 + sub;
-            for (; i + 4 < n; i += 8) {
-              w0 = fma(vh[i], W[(long long)i * n + c], w0);
-              w1 = fma(vh[i + 4], W[(long long)(i + 4) * n + c], w1);
-            }
-            if (i < n) w0 = fma(vh[i], W[(long long)i * n + c], w0);
-          }
-          double wv = w0 + w1;
-          wv += __shfl_xor_sync(qmask, wv, 1);
-          wv += __shfl_xor_sync(qmask, wv, 2);
-          if (act) {
-            tw = tau * (wv + W[(long long)j * n + c]);
-            for (int i2 = j + 1 + sub; i2 < n; i2 += 4) W[(long long)i2 * n + c] -= tw * vh[i2];
-          }
-          __syncwarp(qmask);  // row j of column c read by all four before the update below
-          if (act && sub == 0) W[(long long)j * n + c] -= tw;
-          __syncwarp(qmask);
+    if (tid == 0) beta_s[j] = beta;
+    // trailing update of the remaining columns: v = [1; W(j+1:, p) scale]
+    double cbest = -1.0;
+    int cbi = n;
+    for (int cb = 0; cb < n; cb += ngrp) {
+      const int c = cb + grp;
+      const bool act = c < n && c != p && pst[c] < 0;
+      if (act && tau != 0.0) {
+        double w0 = 0.0, w1 = 0.0;
+        int i = j + 1 + sub;
+        for (; i + 4 < n; i += 8) {
+          w0 = fma(W[(long long)i * ld + p], W[(long long)i * ld + c], w0);
+          w1 = fma(W[(long long)(i + 4) * ld + p], W[(long long)(i + 4) * ld + c], w1);
         }
-        if (act) {
-          const double rj = W[(long long)j * n + c];
-          const bool recompute = cn[c] - rj * rj <= 1e-2 * cn0[c];
-          __syncwarp(qmask);
-          if (sub == 0) cn[c] -= rj * rj;
-          if (recompute) {  // cancellation: recompute the trailing norm exactly
-            double s2 = 0.0;
-            for (int i2 = j + 1 + sub; i2 < n; i2 += 4) s2 = fma(W[(long long)i2 * n + c], W[(long long)i2 * n + c], s2);
-            s2 += __shfl_xor_sync(qmask, s2, 1);
-            s2 += __shfl_xor_sync(qmask, s2, 2);
-            if (sub == 0) cn[c] = cn0[c] = s2;
-          }
+        if (i < n) w0 = fma(W[(long long)i * ld + p], W[(long long)i * ld + c], w0);
+        double wv = w0 + w1;
+        wv += __shfl_xor_sync(qmask, wv, 1);
+        wv += __shfl_xor_sync(qmask, wv, 2);
+        const double rj0 = W[(long long)j * ld + c];
+        const double tw = tau * fma(wv, scale, rj0);
+        const double tws = tw * scale;
+        for (int i2 = j + 1 + sub; i2 < n; i2 += 4) W[(long long)i2 * ld + c] -= tws * W[(long long)i2 * ld + p];
+        __syncwarp(qmask);  // row j of column c read by all four before it changes
+        if (sub == 0) W[(long long)j * ld + c] = rj0 - tw;
+        __syncwarp(qmask);
+      } else if (c == p && sub == 0) {
+        pst[c] = j;
+      }
+      if (act) {
+        const double rj = W[(long long)j * ld + c];
+        const bool recompute = cn[c] - rj * rj <= 1e-2 * cn0[c];
+        __syncwarp(qmask);
+        double nc = cn[c] - rj * rj;
+        if (recompute) {  // cancellation: recompute the trailing norm exactly
+          double s2 = 0.0;
+          for (int i2 = j + 1 + sub; i2 < n; i2 += 4) s2 = fma(W[(long long)i2 * ld + c], W[(long long)i2 * ld + c], s2);
+          s2 += __shfl_xor_sync(qmask, s2, 1);
+          s2 += __shfl_xor_sync(qmask, s2, 2);
+          nc = s2;
+          if (sub == 0) cn0[c] = s2;
         }
+        if (sub == 0) cn[c] = nc;
+        if (nc > cbest) { cbest = nc; cbi = c; }
       }
     }
+    if (sub != 0) { cbest = -1.0; cbi = n; }
+    argmax_pair(cbest, cbi, 0xffffffffu, 32);
+    if (lane == 0) { red[nbuf + warp] = cbest; ired[nbuf + warp] = cbi; }
     __syncthreads();
   }
-  return n;
+  // pivot columns: beta on their step's row, zeros below
+  for (int c = grp; c < n; c += ngrp) {
+    const int sj = pst[c];
+    if (sj < 0) continue;
+    if (sub == 0) W[(long long)sj * ld + c] = beta_s[sj];
+    for (int i = sj + 1 + sub; i < n; i += 4) W[(long long)i * ld + c] = 0.0;
+  }
+  __syncthreads();
+  return j;
 }
 
 // NPLO: octet-Jacobi entries per lane (8: n <= 64, 16: n <= 128, 24: n <= 192), 0: half-warp loop
@@ -877,10 +925,10 @@ template <int NPLO, bool RS>
 __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
                                                                              const Seg* __restrict__ segs,
                                                                              int vsm) {
-  extern __shared__ double smem[];
-  __shared__ int flag;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int flag[2];
   __shared__ int s_k2;
-  __shared__ double jred[NT / 32 + 2];
+  __shared__ double jred[2 * (NT / 32) + 2];
   const SvdItem it = items[blockIdx.x];
   const int m = it.m, kx = it.kx, k1 = min(m, kx), n = svd_n(it);
   long long N = it.N;
@@ -898,12 +946,16 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
   double* vh = cn0 + n;
   int* perm = (int*)(vh + n);                // n ints
   int* iperm = perm + n;                     // n ints
-  double* R = RS ? vh + n + n + 1 : it.rbuf;
+  // R in shared memory: 16-byte aligned rows of stride ld = fin_ld(n) (padding columns zero), so the
+  // octet Jacobi moves double2 and the QRCP trailing update's 4 x 4 (rows x columns) half-warp
+  // accesses fall in distinct banks; in global memory (the merge output) the stride stays n
+  const int ld = RS ? fin_ld(n) : n;
+  double* R = RS ? smem + (((int)(vh + 2 * n + 1 - smem) + 1) & ~1) : it.rbuf;
   // V (m x ldv, reflectors of the protected basis) and tv (kx + 1): staged in shared memory after
   // the rest when they fit (vsm), else read where the tsqr stage left them
-  double* V = vsm ? (RS ? R + (long long)n * n : vh + n + n + 1) : it.vws;
+  double* V = vsm ? (RS ? R + (long long)n * ld : vh + n + n + 1) : it.vws;
   double* tv = V + (long long)m * ldv;
-  __shared__ int ired[NT / 32 + 2];
+  __shared__ int ired[2 * (NT / 32) + 2];
   if (kx > 0 && vsm) {
     for (int e = threadIdx.x; e < m * ldv; e += blockDim.x) V[e] = it.vws[e];
     for (int e = threadIdx.x; e < kx; e += blockDim.x) tv[e] = it.vws[m * ldv + e];
@@ -912,17 +964,22 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
   long long tk[5] = {clock64(), 0, 0, 0, 0};  // phase timestamps (diagnostic output only)
   if (n > 0 && N > 0) {
     if (RS)
-      for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) R[e] = it.rbuf[e];
+      for (long long e = threadIdx.x; e < (long long)n * ld; e += blockDim.x) {
+        const int i = (int)(e / ld), j = (int)(e % ld);
+        R[e] = j < n ? it.rbuf[(long long)i * n + j] : 0.0;
+      }
     __syncthreads();
     tk[1] = clock64();
     // B = R^T Q_B^T: left singular vectors of B = those of R^T.  QRCP preconditioning R Pi = Q1 R1,
     // then the left singular vectors of R^T are Pi x the normalised rows of R1 after row Jacobi.
-    const int nr = qrcp_rows_precondition(R, n, perm, cn, cn0, vh, jred, ired);
+    const long long bigc = (long long)n > N ? (long long)n : N;
+    const int nr = qrcp_rows_precondition(R, n, ld, perm, cn, cn0, vh, iperm, jred, ired, it.tol, (double)bigc * kEps);
     for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
     __syncthreads();
     tk[2] = clock64();
-    const int sw = (NPLO > 0 && n <= 8 * NPLO) ? jacobi_rows_oct<(NPLO > 0 ? NPLO : 1)>(R, nr, n, &flag, jred)
-                                                : jacobi_rows<0>(R, nr, n, &flag, jred);
+    const int sw = (NPLO > 0 && n <= 8 * NPLO)
+                       ? jacobi_rows_oct<(NPLO > 0 ? NPLO : 2), RS>(R, nr, n, ld, flag, jred)
+                       : jacobi_rows<0>(R, nr, n, ld, flag, jred);
     tk[3] = clock64();
     if (it.sweeps_out && threadIdx.x == 0) {
       it.sweeps_out[0] = sw;
@@ -931,7 +988,7 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
     }
     for (int i = warp; i < n; i += nw) {
       double s = 0.0;
-      for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * n + j], R[(long long)i * n + j], s);
+      for (int j = lane; j < n; j += 32) s = fma(R[(long long)i * ld + j], R[(long long)i * ld + j], s);
       s = warp_sum(s);
       if (lane == 0) sig[i] = sqrt(s);
     }
@@ -976,7 +1033,7 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
         val = qrow[j];
       } else {
         const int src = ord[j - k1];
-        const double* rr = R + (long long)src * n;
+        const double* rr = R + (long long)src * ld;
         double s0 = 0.0, s1 = 0.0;
         int l = 0;
         for (; l + 1 < n; l += 2) {
@@ -996,7 +1053,7 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
       val = (i == j) ? 1.0 : 0.0;
     } else {
       const int src = ord[j - k1];
-      val = (i < k1) ? 0.0 : R[(long long)src * n + iperm[i - k1]] / sig[src];
+      val = (i < k1) ? 0.0 : R[(long long)src * ld + iperm[i - k1]] / sig[src];
     }
     Q[e] = val;
   }
@@ -1786,8 +1843,8 @@ size_t merge_smem(int n, bool rsmem) {
 size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem) {
   const int k1 = m < kx ? m : kx;
   const int n = m - k1;
-  return sizeof(double) * ((vsmem ? (size_t)m * (kx | 1) + kx + 1 : 0) + n + (n / 2 + 1) + 4 * (size_t)n + 1 +
-                           (rsmem ? (size_t)n * n : 0));
+  return sizeof(double) * ((vsmem ? (size_t)m * (kx | 1) + kx + 1 : 0) + n + (n / 2 + 1) + 4 * (size_t)n + 2 +
+                           (rsmem ? (size_t)n * fin_ld(n) : 0));
 }
 
 cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork* work, int nwork, size_t smem,

@@ -439,9 +439,32 @@ void assemble_dense_early(Ctx& A, HView x, HView y, PRef P, PTree& pt, cudaEvent
   E.on = true;
 }
 
+// Row factors of the admissible X blocks of kind-a triples: bc_t S_X P_s (induced.py:260-265).
+// They need only the row basis, so multiply() issues them as soon as the row pass is done, in the
+// shadow of the column pass.
+std::vector<Mat> row_factors(Ctx& C, Arena& sc, HView x, HView y, const Induced& qr, PRef P, const PTree& pt) {
+  HostTimer hx(C, "asm_rf");
+  const Basis& Q = *qr.q;
+  const Part part = make_part(*pt.bt->rows, C.comm);
+  std::vector<Mat> rf(x.h->bt->nb);
+  GBatch g;
+  for (int bts : pt.rf_blocks) {  // (planner thread: distinct X blocks of kind-a triples)
+    const int t = x.row(bts), s = x.col(bts);
+    if (!part.mine(t)) continue;
+    Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
+    g.out(m, false);
+    g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
+    rf[bts] = m;
+  }
+  g.run(C);
+  return rf;
+}
+
 // Product over T^XY in the induced bases + push-down (reference induced.py:220-355).
-std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt) {
+std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc, PRef P, PTree& pt,
+                             const std::vector<Mat>* rf_pre) {
   HostTimer ht(C, "assemble_total");
+  HostTimer htpro(C, "asm_prologue");
   auto G = std::make_shared<H2>();
   G->bt = pt.bt;
   G->rb = qr.q;
@@ -477,6 +500,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       if (B.adm_leaf(b)) G->coup[b] = cp[b].p;
     }
   }
+  htpro.stop();
   // the grouped launch's output list (one GOut per product block, its 64x64 tiles) is pure
   // structure: built on a helper thread while this one issues the xv / row-factor work and tables
   const bool prof = C.prof;
@@ -547,21 +571,9 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     HostTimer hx(C, "asm_xv2");
     xv_compute(C, sc, yT, xT, PRef{P.P, !P.T}, pt.need_wy, qc.xv);
   }
-  std::vector<Mat> rf(x.h->bt->nb);
-  {
-    HostTimer hx(C, "asm_rf");
-    GBatch g;
-    for (int bts : pt.rf_blocks) {  // (planner thread: distinct X blocks of kind-a triples)
-      const int t = x.row(bts), s = x.col(bts);
-      if (!part.mine(t)) continue;
-      // row_factor for an admissible X block: bc_t S_X P_s (induced.py:260-265)
-      Mat m{sc.alloc((size_t)Q.rank[t] * y.rb().rank[s]), Q.rank[t], y.rb().rank[s]};
-      g.out(m, false);
-      g.t3(qr.bc[t].ref(), x.coup(bts), P.at(s), qr.bc[t].c, P.rows(s));
-      rf[bts] = m;
-    }
-    g.run(C);
-  }
+  std::vector<Mat> rf_local;
+  if (!rf_pre) rf_local = row_factors(C, sc, x, y, qr, P, pt);
+  const std::vector<Mat>& rf = rf_pre ? *rf_pre : rf_local;
   // all terminal triples (induced.py:286-307), one output per product block; the terms are
   // expanded on the GPU from the triple list and per-block operand tables (asm_expand_kernel)
   {
@@ -735,6 +747,13 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
     exchange(C, *ar, items);
   }
+  // phase 2's block-norm batches are pure structure of G: build them on a host thread now, while
+  // the assembly and push-down run on the GPU (coarsen picks them up)
+  {
+    const H2* gp = G.get();
+    const Comm comm = C.comm;
+    G->norm_prep = std::async(std::launch::async, [gp, comm] { return build_norm_prep(*gp, comm); }).share();
+  }
   return G;  // scratch is released stream-ordered (cudaFreeAsync) after the queued work
 
 }
@@ -792,6 +811,9 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   // column pass on a side stream driven by a second host thread
   auto keep2 = std::make_shared<Arena>(C.st);
   Induced qr, qc;
+  PTree pt;
+  std::vector<Mat> rf;
+  bool have_rf = false;
   // each pass first forms its own total weights (weights.py:60-101): Z_Y for the rows, Z_X^T for
   // the columns
   auto row_pass = [&](Ctx& c, Arena& out, Arena& scr) {
@@ -824,23 +846,31 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     });
     try {
       qr = row_pass(C, *keep, sc);
+      // the row factors need only the row basis: issue them while the column pass finishes
+      // (only when the planner thread is done already -- it also queues the dense targets)
+      static const bool early_rf = getenv("H2G_NO_EARLY_RF") == nullptr;
+      if (early_rf && pt_future.wait_for(std::chrono::seconds(0)) == std::future_status::ready) {
+        pt = pt_future.get();
+        rf = row_factors(C, sc, X, Y, qr, PRef{&P, false}, pt);
+        have_rf = true;
+      }
     } catch (...) {
       th.join();
       throw;
     }
+    HostTimer hj(C, "p1_join");
     th.join();
     if (err) std::rethrow_exception(err);
     C.join_side(S);
   }
   record(C, e2);
   e3 = e2;
-  PTree pt;
-  {
+  if (!have_rf) {
     HostTimer ht(C, "product_tree_wait");
     pt = pt_future.get();
   }
   StageTag taga(C, "p1.asm");
-  auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt);
+  auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt, have_rf ? &rf : nullptr);
   if (A) C.join_side(*A);  // counters / profile of the auxiliary stream's work
   record(C, e4);
   G->owned.push_back(keep);

@@ -815,15 +815,12 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
 // (coarsening.py:342-351)
 // The coupling norms are needed first (top-down Z), the nearfield norms only at the leaf SVDs: with
 // an auxiliary context the latter run there, under the Z levels, and `nn_ready` completes them.
-static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn, Ctx* A = nullptr,
-                      cudaEvent_t* nn_ready = nullptr) {
+std::shared_ptr<NormPrep> build_norm_prep(const H2& g, const Comm& comm) {
   const Blocks& B = *g.bt;
-  NormBatch nbn, nbc;
-  std::vector<int> ids;
+  auto np = std::make_shared<NormPrep>();
   HView v{&g, false};
   // multi-GPU: the blocks read by this rank's row or column passes
-  const Part pr = make_part(*B.rows, C.comm), pc = make_part(*B.cols, C.comm);
-  cuda_check(cudaMemsetAsync(d_nn, 0, sizeof(double) * B.nb, C.st), "memset");
+  const Part pr = make_part(*B.rows, comm), pc = make_part(*B.cols, comm);
   for (int b = 0; b < B.nb; ++b) {
     if (!B.leaf(b)) continue;
     if (!pr.mine(B.row[b]) && !pc.mine(B.col[b])) continue;
@@ -831,17 +828,31 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, d
     const int t = B.row[b], s = B.col[b];
     const int m = coupling ? g.rb->rank[t] : B.rows->size(t);
     const int n = coupling ? g.cb->rank[s] : B.cols->size(s);
-    NormBatch& nb = coupling ? nbc : nbn;
+    NormBatch& nb = coupling ? np->nbc : np->nbn;
     NormItem it{};
     it.s0 = nb.sl.begin();
     nb.sl.add(coupling ? v.coup(b) : v.near(b), n);
     it.s1 = nb.sl.begin();
     it.m = m;
     it.N = n;
-    if (!coupling) it.out = d_nn + b;
     nb.items.push_back(it);
-    if (coupling) ids.push_back(b);
+    (coupling ? np->ids : np->nids).push_back(b);
   }
+  return np;
+}
+
+static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn, Ctx* A = nullptr,
+                      cudaEvent_t* nn_ready = nullptr) {
+  const Blocks& B = *g.bt;
+  HostTimer ht(C, "p2_norm_build");
+  std::shared_ptr<NormPrep> np;
+  if (g.norm_prep.valid()) np = g.norm_prep.get();  // built while the assembly ran
+  if (!np) np = build_norm_prep(g, C.comm);
+  NormBatch nbn = np->nbn, nbc = np->nbc;  // copies: the prepared batches stay reusable
+  for (size_t i = 0; i < nbn.items.size(); ++i) nbn.items[i].out = d_nn + np->nids[i];
+  const std::vector<int>& ids = np->ids;
+  cuda_check(cudaMemsetAsync(d_nn, 0, sizeof(double) * B.nb, C.st), "memset");
+  ht.next("p2_norm_launch");
   if (A) {
     cudaEvent_t e;
     cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -940,9 +951,11 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  HostTimer htpre(C, "p2_pre");
   wait_near(C, g);
   NearPrefetch pf;
   if (near_host && g.near_owner) pf = prefetch_near(C, g, *coarse, near_host, near_cap);
+  htpre.stop();
   // structure of both passes on host threads while the block norms run on the GPU
   const BView gv{g.bt.get(), false}, gvt{g.bt.get(), true};
   const BView cvw{coarse.get(), false}, cvt{coarse.get(), true};
