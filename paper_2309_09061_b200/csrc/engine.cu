@@ -376,6 +376,14 @@ static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>&
 
 // Register-tile TSQR (tileqr.cu) handles R factors up to 128 columns; H2G_NO_TILE=1 forces the
 // panel kernels (A/B comparisons).
+// Wide SVD inputs without a protected basis go through the double-double Gram (gram.cu) when the
+// Gram fits the Cholesky CTA's shared memory (H2G_NO_GRAM=1: Householder TSQR, for A/B).
+static constexpr long long kGramCols = 512;  // columns per Gram CTA
+static bool gram_path(int kx, int n, long long N) {
+  static const bool off = getenv("H2G_NO_GRAM") != nullptr;
+  return !off && kx == 0 && n > 0 && N > 0 && gram_chol_smem(n) <= (size_t)kSmemLimit;
+}
+
 static bool tile_path(int n) {
   static const bool off = getenv("H2G_NO_TILE") != nullptr;
   return !off && n <= 128;
@@ -636,7 +644,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<long long> tile_lines;
   for (auto& it : items) {
     const int n = it.m - std::min(it.m, it.kx);
-    if (it.m > 0 && n > 0 && tile_path(n)) tile_lines.push_back(it.N);
+    if (it.m > 0 && n > 0 && tile_path(n) && !gram_path(it.kx, n, it.N)) tile_lines.push_back(it.N);
   }
   const int tpc = tiles_per_cta(tile_lines);
   std::vector<TileItem> titems;
@@ -644,6 +652,10 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<std::tuple<double*, int, int, int>> tparts;
   std::vector<int> prep_ids;
   int tnmax = 0;
+  std::vector<GramWork> gwork;
+  std::vector<int> gids;
+  int gmax = 0;
+  int* g_nr = (int*)scratch.alloc_bytes(items.size() * sizeof(int));
   for (size_t i = 0; i < items.size(); ++i) {
     SvdItem& it = items[i];
     it.rank_out = d_rank + i;
@@ -652,6 +664,25 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     const int n = it.m - k1;
     it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
     if (svd_finish_smem(it.m, it.kx, true, false) > kSmemLimit) fin_rsmem = false;
+    if (gram_path(it.kx, n, it.N)) {
+      // double-double Gram + pivoted Cholesky (gram.cu) instead of the Householder TSQR
+      const int ncc = (int)std::max<long long>(1, (it.N + kGramCols - 1) / kGramCols);
+      it.nchunk = ncc * gram_reps(n);  // partial slices summed by the Cholesky CTA
+      it.gpart = scratch.alloc((size_t)it.nchunk * 2 * n * n);
+      it.rbuf = scratch.alloc((size_t)n * n);
+      it.pre_nr = g_nr + gids.size();
+      const int li = (int)live.size(), nt = (n + 63) / 64;
+      for (int c = 0; c < ncc; ++c)
+        for (int ti = 0; ti < nt; ++ti)
+          for (int tj = ti; tj < nt; ++tj) {
+            GramWork w{li, ti, tj, c, (long long)c * kGramCols, std::min<long long>(it.N, (long long)(c + 1) * kGramCols)};
+            gwork.push_back(w);
+          }
+      gids.push_back(li);
+      gmax = std::max(gmax, n);
+      live.push_back(it);
+      continue;
+    }
     if (tile_path(n)) {
       const long long per = 128LL * tpc;
       it.nchunk = (int)std::max<long long>(1, (it.N + per - 1) / per);
@@ -697,7 +728,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     const int n = it.m - std::min(it.m, it.kx);
     sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem, fin_vsmem));
     if (sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
-    if (tile_path(n)) continue;
+    if (it.pre_nr || tile_path(n)) continue;
     sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
     sm_merge = std::max(sm_merge, merge_smem(n, rsmem));
     if (sm_tsqr > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
@@ -725,6 +756,13 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     }
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
+  if (!gids.empty()) {
+    GramWork* d_gw = C.push(gwork);
+    int* d_gids = C.push(gids);
+    C.flush();
+    cuda_check(launch_gram(d_items, d_s, d_gw, (int)gwork.size(), d_gids, (int)gids.size(), gmax, C.st), "gram");
+    C.launches += 2;
+  }
   if (!work.empty()) {
     C.flush();
     cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");

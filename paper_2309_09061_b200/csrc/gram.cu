@@ -1,0 +1,376 @@
+// Wide truncated SVD inputs without a protected basis (phase-2 C_t = [V_t Z_t^T | N / ||N|| ...],
+// reference coarsening.py:294-326, and the orthogonalisations of h2.py:79-113): the n x n triangular
+// factor the one-sided Jacobi needs is formed from the Gram matrix G = C C^T in double-double
+// arithmetic instead of a Householder TSQR of C^T.
+//
+//   gram_dd_partial_kernel  one CTA per (item, column chunk, 64 x 64 tile of G's upper triangle):
+//                           G_tile += sum over the chunk's columns of c_i c_j, each product exact
+//                           (two_prod) and accumulated as a double-double -- no sequential chain,
+//                           every item and chunk independent
+//   gram_chol_kernel        one CTA per item: sums the chunk partials (fixed order), then a
+//                           pivoted Cholesky of G in double-double (pivot = largest remaining
+//                           diagonal = QRCP's largest trailing column norm), one barrier per step.
+//                           Row j of the factor is written as doubles at the original column
+//                           positions (no physical pivoting: the row-Jacobi that follows is
+//                           invariant under column permutations).
+//
+// Why this is as accurate as the Householder path: the double-double Gram carries ~1e-32 relative
+// error against ||C||^2, and so does its Cholesky factor R (R^T R = G + E, ||E|| ~ 1e-32
+// sigma_1^2), hence sigma_i(R)^2 = sigma_i(C)^2 + O(1e-32 sigma_1^2) -- far below the FP64 SVD's
+// own eps sigma_1 for every singular value the truncation can keep (sigma_1 / thr <= 1e7).  The
+// factor is rounded to doubles once (backward error eps ||R||, the same as Householder's).  The
+// pivoted Cholesky stops under the same rule as the QRCP preconditioner (trailing mass below
+// kDeflate thr_lo), so the rows it drops cannot change a truncation decision.
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "h2g_types.h"
+
+namespace h2g {
+
+namespace {
+
+constexpr int kGT = 64;    // Gram tile
+constexpr int kGP = 32;    // panel columns
+constexpr int kGThr = 256;
+constexpr int kGSeg = 64;  // staged segment descriptors per Gram CTA
+constexpr int kCThr = 512;
+constexpr double kEpsG = 2.220446049250313e-16;
+constexpr double kDeflateG = 1e-5;
+
+struct dd {
+  double hi, lo;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {
+  const double s = a + b;
+  return dd{s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  double s, e;
+  two_sum(a.hi, b.hi, s, e);
+  e += a.lo + b.lo;
+  return fast_two_sum(s, e);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return dd{-a.hi, -a.lo}; }
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  const double p = a.hi * b.hi;
+  double e = fma(a.hi, b.hi, -p);
+  e = fma(a.hi, b.lo, e);
+  e = fma(a.lo, b.hi, e);
+  return fast_two_sum(p, e);
+}
+__device__ __forceinline__ dd dd_recip(dd b) {  // 1 / b, two Newton-style corrections
+  const double q1 = 1.0 / b.hi;
+  // r = 1 - b q1
+  dd r = dd_add(dd{1.0, 0.0}, dd_neg(dd_mul(b, dd{q1, 0.0})));
+  const double q2 = r.hi * q1;
+  dd q = fast_two_sum(q1, q2);
+  r = dd_add(dd{1.0, 0.0}, dd_neg(dd_mul(b, q)));
+  return dd_add(q, dd{r.hi * q1, 0.0});
+}
+__device__ __forceinline__ dd dd_sqrt(dd a) {  // a > 0
+  const double x = sqrt(a.hi);
+  const double p = x * x;
+  const double pe = fma(x, x, -p);
+  const dd r = dd_add(a, dd{-p, -pe});
+  return fast_two_sum(x, r.hi / (2.0 * x));
+}
+
+__device__ __forceinline__ double gseg_scale(const Seg& sg) {
+  if (!sg.sdiv) return sg.scale;
+  const double d = *sg.sdiv;
+  return d > 0.0 ? sg.scale / d : sg.scale;
+}
+
+__device__ __forceinline__ int gfind_seg(const Seg* __restrict__ segs, int s0, int s1, long long line) {
+  int lo = s0, hi = s1 - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].off <= line) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ long long pidx(int i, int j, int m) {  // packed upper triangle, i <= j
+  return (long long)i * (2 * m - i + 1) / 2 + (j - i);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const SvdItem* __restrict__ items,
+                                                                const Seg* __restrict__ segs,
+                                                                const GramWork* __restrict__ work) {
+  __shared__ __align__(16) double Pa[kGP][kGT + 2];
+  __shared__ __align__(16) double Pb[kGP][kGT + 2];
+  __shared__ long long s_off[kGSeg];
+  __shared__ const double* s_p[kGSeg];
+  __shared__ int s_rs[kGSeg], s_cs[kGSeg];
+  __shared__ double s_sc[kGSeg];
+  __shared__ int s_first, s_n;
+  const GramWork w = work[blockIdx.x];
+  const SvdItem it = items[w.item];
+  const int m = it.m;
+  const int ia = w.ti * kGT, jb = w.tj * kGT;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kGThr / 32;
+  // active 4 x 4 blocks of this tile only (upper triangle on a diagonal tile), replicated over
+  // interleaved panel columns when the set is small
+  const bool diag = w.ti == w.tj;
+  const int nbi = (min(kGT, m - ia) + 3) / 4, nbj = (min(kGT, m - jb) + 3) / 4;
+  const int nblk = diag ? nbi * (nbi + 1) / 2 : nbi * nbj;
+  const int reps = gram_reps(m), span = (nblk + 31) / 32 * 32;
+  const int rep = tid / span, blk = tid % span;
+  const bool act = rep < reps && blk < nblk;
+  int bi = 0, bj = 0;
+  if (diag) {
+    int rem = blk;
+    while (bi < nbi && rem >= nbi - bi) { rem -= nbi - bi; ++bi; }
+    bj = bi + rem;
+  } else {
+    bi = blk / nbj;
+    bj = blk % nbj;
+  }
+  double hi[16], lo[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0.0;
+  // the chunk's segment descriptors, staged once (two binary searches)
+  if (tid == 0) {
+    const int a = gfind_seg(segs, it.s0, it.s1, w.c0);
+    const int b = gfind_seg(segs, it.s0, it.s1, w.c1 - 1);
+    s_first = a;
+    s_n = b - a + 1;
+  }
+  __syncthreads();
+  const int sfirst = s_first, ns = s_n;
+  const bool staged = ns <= kGSeg;
+  if (staged)
+    for (int q = tid; q < ns; q += kGThr) {
+      const Seg sg = segs[sfirst + q];
+      s_off[q] = sg.off;
+      s_p[q] = sg.a.p;
+      s_rs[q] = sg.a.rs;
+      s_cs[q] = sg.a.cs;
+      s_sc[q] = gseg_scale(sg);
+    }
+  for (long long c0 = w.c0; c0 < w.c1; c0 += kGP) {
+    __syncthreads();  // previous panel consumed (and the descriptors staged)
+    {
+      // lane = panel column (row-major sources: consecutive lanes read consecutive addresses),
+      // warps over the tile's rows
+      const long long c = c0 + lane;
+      const double* col = nullptr;
+      long long rs = 0;
+      double sc = 0.0;
+      if (c < w.c1) {
+        if (staged) {
+          int lo2 = 0, hi2 = ns - 1;
+          while (lo2 < hi2) {
+            const int mid = (lo2 + hi2 + 1) >> 1;
+            if (s_off[mid] <= c) lo2 = mid; else hi2 = mid - 1;
+          }
+          col = s_p[lo2] + (c - s_off[lo2]) * s_cs[lo2];
+          rs = s_rs[lo2];
+          sc = s_sc[lo2];
+        } else {
+          const Seg sg = segs[gfind_seg(segs, it.s0, it.s1, c)];
+          col = sg.a.p + (c - sg.off) * sg.a.cs;
+          rs = sg.a.rs;
+          sc = gseg_scale(sg);
+        }
+      }
+      for (int r = warp; r < kGT; r += nw) {
+        const int ra = ia + r, rb = jb + r;
+        Pa[lane][r] = (col && ra < m) ? sc * col[(long long)ra * rs] : 0.0;
+        if (w.ti != w.tj) Pb[lane][r] = (col && rb < m) ? sc * col[(long long)rb * rs] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll 2
+      for (int p = rep; p < kGP; p += reps) {
+        const double2 a01 = *reinterpret_cast<const double2*>(&Pa[p][4 * bi]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&Pa[p][4 * bi + 2]);
+        const double* pb = w.ti != w.tj ? &Pb[p][0] : &Pa[p][0];
+        const double2 b01 = *reinterpret_cast<const double2*>(pb + 4 * bj);
+        const double2 b23 = *reinterpret_cast<const double2*>(pb + 4 * bj + 2);
+        const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int q = 4 * u + v;
+            const double pr = a[u] * b[v];
+            const double pe = fma(a[u], b[v], -pr);
+            double s, e;
+            two_sum(hi[q], pr, s, e);
+            hi[q] = s;
+            lo[q] += e + pe;
+          }
+      }
+    }
+  }
+  if (!act) return;
+  double* gh = it.gpart + (size_t)(w.chunk * reps + rep) * 2 * m * m;
+  double* gl = gh + (size_t)m * m;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = ia + 4 * bi + u, j = jb + 4 * bj + v;
+      if (i < m && j < m && i <= j) {
+        const dd r = fast_two_sum(hi[4 * u + v], lo[4 * u + v]);
+        gh[(size_t)i * m + j] = r.hi;
+        gl[(size_t)i * m + j] = r.lo;
+      }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void argmax_pair_g(double& best, int& bi, int width) {
+  for (int o = width >> 1; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+}
+
+__global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const SvdItem* __restrict__ items,
+                                                             const int* __restrict__ ids) {
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ double red[2 * (kCThr / 32)];
+  __shared__ int ired[2 * (kCThr / 32)];
+  const SvdItem it = items[ids[blockIdx.x]];
+  const int m = it.m;
+  const long long np = (long long)m * (m + 1) / 2;
+  double* Gh = gsm;
+  double* Gl = Gh + np;
+  unsigned char* done = reinterpret_cast<unsigned char*>(Gl + np);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, nt = blockDim.x;
+  double* R = it.rbuf;  // m x m, row-major
+  // 1. sum the chunk partials in a fixed order
+  for (int i = warp; i < m; i += nw)
+    for (int j = i + lane; j < m; j += 32) {
+      dd acc{0.0, 0.0};
+      for (int ch = 0; ch < it.nchunk; ++ch) {
+        const double* gh = it.gpart + (size_t)ch * 2 * m * m;
+        acc = dd_add(acc, dd{gh[(size_t)i * m + j], gh[(size_t)m * m + (size_t)i * m + j]});
+      }
+      const long long e = pidx(i, j, m);
+      Gh[e] = acc.hi;
+      Gl[e] = acc.lo;
+    }
+  for (int c = tid; c < m; c += nt) done[c] = 0;
+  __syncthreads();
+  // argmax partials of the diagonal (buffer 0)
+  {
+    double best = -1.0;
+    int bi = m;
+    for (int i = warp; i < m; i += nw) {
+      if (lane == 0) {
+        const double d = Gh[pidx(i, i, m)];
+        if (d > best || (d == best && i < bi)) { best = d; bi = i; }
+      }
+    }
+    argmax_pair_g(best, bi, 32);
+    if (lane == 0) { red[warp] = best; ired[warp] = bi; }
+  }
+  __syncthreads();
+  const long long bigc = (long long)m > it.N ? (long long)m : it.N;
+  double stop2 = 0.0;
+  int j = 0;
+  for (; j < m; ++j) {
+    const int buf = (j & 1) * nw, nbuf = ((j + 1) & 1) * nw;
+    double best = lane < nw ? red[buf + lane] : -1.0;
+    int p = lane < nw ? ired[buf + lane] : m;
+    argmax_pair_g(best, p, 32);
+    if (p >= m) break;
+    const dd gpp{Gh[pidx(p, p, m)], Gl[pidx(p, p, m)]};
+    const double bst = gpp.hi + gpp.lo;
+    if (!(bst > 0.0)) break;
+    if (j == 0) {
+      const double thr_lo = fmax(it.tol, (double)bigc * kEpsG * sqrt(bst));
+      stop2 = fmax(kEpsG * kEpsG * bst * 0.25, kDeflateG * kDeflateG * thr_lo * thr_lo);
+    } else if ((double)(m - j) * bst <= stop2) {
+      break;
+    }
+    // done[p] is read this step only behind explicit `== p` tests (short-circuit), so it is set now
+    if (tid == 0) done[p] = 1;
+    const dd inv = dd_recip(gpp);
+    // row j of the factor: r_c = G_pc / r_pp at the original column positions
+    if (warp == (j % nw)) {
+      const dd rpp = dd_sqrt(gpp);
+      const dd irpp = dd_recip(rpp);
+      for (int c = lane; c < m; c += 32) {
+        double v;
+        if (c == p) {
+          v = rpp.hi + rpp.lo;
+        } else if (done[c]) {
+          v = 0.0;
+        } else {
+          const long long e = c < p ? pidx(c, p, m) : pidx(p, c, m);
+          const dd r = dd_mul(dd{Gh[e], Gl[e]}, irpp);
+          v = r.hi + r.lo;
+        }
+        R[(size_t)j * m + c] = v;
+      }
+    }
+    // Schur complement of the remaining rows / columns; diagonal argmax partials for step j + 1
+    double cbest = -1.0;
+    int cbi = m;
+    for (int a = warp; a < m; a += nw) {
+      if (a == p || done[a]) continue;
+      const long long ea = a < p ? pidx(a, p, m) : pidx(p, a, m);
+      const dd gpa = dd_mul(dd{Gh[ea], Gl[ea]}, inv);
+      for (int b = a + lane; b < m; b += 32) {
+        if (b == p || done[b]) continue;
+        const long long eb = b < p ? pidx(b, p, m) : pidx(p, b, m);
+        const dd t = dd_mul(gpa, dd{Gh[eb], Gl[eb]});
+        const long long e = pidx(a, b, m);
+        const dd nv = dd_add(dd{Gh[e], Gl[e]}, dd_neg(t));
+        Gh[e] = nv.hi;
+        Gl[e] = nv.lo;
+        if (b == a) {
+          const double d = nv.hi + nv.lo;
+          if (d > cbest || (d == cbest && a < cbi)) { cbest = d; cbi = a; }
+        }
+      }
+    }
+    argmax_pair_g(cbest, cbi, 32);
+    if (lane == 0) { red[nbuf + warp] = cbest; ired[nbuf + warp] = cbi; }
+    __syncthreads();  // Schur complement, partials and done[p] complete
+  }
+  // rows below the numerical rank: zero (they are deflated, see kDeflateG)
+  for (long long e = (long long)j * m + tid; e < (long long)m * m; e += nt) R[e] = 0.0;
+  if (tid == 0) *it.pre_nr = j;
+}
+
+size_t gram_chol_smem(int m) {
+  const size_t np = (size_t)m * (m + 1) / 2;
+  return sizeof(double) * 2 * np + (size_t)m + 16;
+}
+
+cudaError_t launch_gram(const SvdItem* items, const Seg* segs, const GramWork* work, int nwork, const int* ids,
+                        int nids, int mmax, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)gram_chol_kernel);
+    cudaFuncSetAttribute((const void*)gram_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - (int)fa.sharedSizeBytes);
+  });
+  if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, 0, st>>>(items, segs, work);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || nids == 0) return e;
+  gram_chol_kernel<<<nids, mmax <= 64 ? 256 : kCThr, gram_chol_smem(mmax), st>>>(items, ids);
+  return cudaGetLastError();
+}
+
+}  // namespace h2g

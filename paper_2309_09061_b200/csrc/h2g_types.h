@@ -91,6 +91,23 @@ struct SvdItem {
   int* sweeps_out;  // optional diagnostic: Jacobi sweeps used, n, live rows, k2
   int zskip;        // 1: segments whose device divisor is exactly 0 are absent (their widths leave N)
   double* q2;       // tile path with kx > 0: explicit Q_V (m x m), written by svd_prep_kernel
+  double* gpart;    // Gram path (kx = 0): nchunk x {hi, lo} x (m x m) partial double-double Grams
+  int* pre_nr;      // Gram path: rows of the pivoted-Cholesky factor in rbuf (the finish skips QRCP)
+};
+
+// Gram CTAs of a small item (m <= 64, one 64 x 64 tile) run `reps` replicas of its 4 x 4 block set
+// over interleaved panel columns, each replica writing its own partial slice.
+__host__ __device__ inline int gram_reps(int m) {
+  if (m > 64) return 1;
+  const int nb = (m + 3) / 4, nblk = nb * (nb + 1) / 2, span = (nblk + 31) / 32 * 32;
+  const int r = 256 / span;
+  return r > 1 ? r : 1;
+}
+
+// One CTA of the double-double Gram (gram.cu): columns [c0, c1) of item `item`, G tile (ti, tj).
+struct GramWork {
+  int item, ti, tj, chunk;
+  long long c0, c1;
 };
 
 // Register-tile TSQR (tileqr.cu): one item = one stacked operand reduced to an n x n R factor

@@ -973,7 +973,14 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
     // B = R^T Q_B^T: left singular vectors of B = those of R^T.  QRCP preconditioning R Pi = Q1 R1,
     // then the left singular vectors of R^T are Pi x the normalised rows of R1 after row Jacobi.
     const long long bigc = (long long)n > N ? (long long)n : N;
-    const int nr = qrcp_rows_precondition(R, n, ld, perm, cn, cn0, vh, iperm, jred, ired, it.tol, (double)bigc * kEps);
+    int nr;
+    if (it.pre_nr) {  // Gram path: R is already the pivoted (double-double) Cholesky factor
+      nr = *it.pre_nr;
+      for (int c = threadIdx.x; c < n; c += blockDim.x) perm[c] = c;
+      __syncthreads();
+    } else {
+      nr = qrcp_rows_precondition(R, n, ld, perm, cn, cn0, vh, iperm, jred, ired, it.tol, (double)bigc * kEps);
+    }
     for (int c = threadIdx.x; c < n; c += blockDim.x) iperm[perm[c]] = c;
     __syncthreads();
     tk[2] = clock64();
