@@ -384,6 +384,48 @@ static bool gram_path(int kx, int n, long long N) {
   return !off && kx == 0 && n > 0 && N > 0 && gram_chol_smem(n) <= (size_t)kSmemLimit;
 }
 
+// Items of one double-double Gram launch pair (gram.cu), shared by the SVD and QR batches.
+struct GramBatch {
+  std::vector<GramItem> items;
+  std::vector<GramWork> work;
+  int mmax = 0;
+  // lines of hstack(segs[s0:s1]) (hcols) or vstack (rows), m-dimensional; factor into rbuf, rows into *nr
+  void add(Arena& scratch, int s0, int s1, int m, long long N, int hcols, double tol, double* rbuf, int* nr) {
+    const int ncc = (int)std::max<long long>(1, (N + kGramCols - 1) / kGramCols);
+    GramItem g{};
+    g.s0 = s0;
+    g.s1 = s1;
+    g.m = m;
+    g.nslice = ncc * gram_reps(m);  // partial slices summed by the Cholesky CTA
+    g.N = N;
+    g.hcols = hcols;
+    g.tol = tol;
+    g.gpart = scratch.alloc((size_t)g.nslice * 2 * m * m);
+    g.rbuf = rbuf;
+    g.nr = nr;
+    const int gi = (int)items.size(), nt = (m + 63) / 64;
+    for (int c = 0; c < ncc; ++c)
+      for (int ti = 0; ti < nt; ++ti)
+        for (int tj = ti; tj < nt; ++tj)
+          work.push_back(GramWork{gi, ti, tj, c, (long long)c * kGramCols, std::min<long long>(N, (long long)(c + 1) * kGramCols)});
+    items.push_back(g);
+    mmax = std::max(mmax, m);
+  }
+  void launch(Ctx& C, const Seg* d_segs) {
+    if (items.empty()) return;
+    GramItem* d_it = C.push(items);
+    GramWork* d_w = C.push(work);
+    C.flush();
+    cuda_check(launch_gram(d_it, d_segs, d_w, (int)work.size(), (int)items.size(), mmax, C.st), "gram");
+    C.launches += 2;
+  }
+};
+
+static bool gram_qr_path(int n, long long M) {
+  static const bool off = getenv("H2G_NO_GRAM_QR") != nullptr;
+  return !off && gram_path(0, n, M);
+}
+
 static bool tile_path(int n) {
   static const bool off = getenv("H2G_NO_TILE") != nullptr;
   return !off && n <= 128;
@@ -453,14 +495,26 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   bool rsmem = true;
   std::vector<long long> tile_lines;
   for (auto& it : items)
-    if (it.n > 0 && it.M > 0 && tile_path(it.n)) tile_lines.push_back(it.M);
+    if (it.n > 0 && it.M > 0 && tile_path(it.n) && !gram_qr_path(it.n, it.M)) tile_lines.push_back(it.M);
   const int tpc = tiles_per_cta(tile_lines);
   std::vector<TileItem> titems;
   std::vector<TileWork> twork;
   std::vector<std::tuple<double*, int, int, int>> tparts;
   int tnmax = 0;
+  GramBatch gb;
+  int* g_nr = nullptr;
   for (auto& it : items) {
     if (it.n == 0 || it.M == 0) continue;
+    if (gram_qr_path(it.n, it.M)) {
+      // R-only QR as the pivoted double-double Cholesky factor of the stack's Gram: every consumer
+      // of these factors (weights.py:37-101, coarsening.py:231-245) uses only R^T R
+      if (!g_nr) g_nr = (int*)scratch.alloc_bytes(items.size() * sizeof(int));
+      it.rbuf = scratch.alloc((size_t)it.n * it.n);
+      it.full = 1;
+      gb.add(scratch, it.s0, it.s1, it.n, it.M, 0, 0.0, it.rbuf, g_nr + gb.items.size());
+      live.push_back(it);
+      continue;
+    }
     if (tile_path(it.n)) {
       const long long per = 128LL * tpc;
       it.nchunk = (int)((it.M + per - 1) / per);
@@ -502,7 +556,7 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
   for (size_t i = 0; i < live.size(); ++i) {
-    if (tile_path(live[i].n)) continue;
+    if (live[i].full || tile_path(live[i].n)) continue;
     sm_chunk = std::max(sm_chunk, qr_smem(live[i].n, rsmem));
     sm_merge = std::max(sm_merge, merge_smem(live[i].n, rsmem));
     for (int c = 0; c < live[i].nchunk; ++c) work.push_back(SvdWork{(int)i, c, 0, 0});
@@ -520,6 +574,7 @@ void QrBatch::run(Ctx& C, Arena& scratch) {
   SvdWork* d_work = C.push(work);
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
+  gb.launch(C, d_s);
   if (!work.empty()) {
     C.flush();
     cuda_check(launch_qr_chunks(d_items, d_s, d_work, (int)work.size(), sm_chunk, rsmem, C.st), "qr_chunks");
@@ -652,9 +707,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<std::tuple<double*, int, int, int>> tparts;
   std::vector<int> prep_ids;
   int tnmax = 0;
-  std::vector<GramWork> gwork;
-  std::vector<int> gids;
-  int gmax = 0;
+  GramBatch gb;
   int* g_nr = (int*)scratch.alloc_bytes(items.size() * sizeof(int));
   for (size_t i = 0; i < items.size(); ++i) {
     SvdItem& it = items[i];
@@ -666,20 +719,9 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     if (svd_finish_smem(it.m, it.kx, true, false) > kSmemLimit) fin_rsmem = false;
     if (gram_path(it.kx, n, it.N)) {
       // double-double Gram + pivoted Cholesky (gram.cu) instead of the Householder TSQR
-      const int ncc = (int)std::max<long long>(1, (it.N + kGramCols - 1) / kGramCols);
-      it.nchunk = ncc * gram_reps(n);  // partial slices summed by the Cholesky CTA
-      it.gpart = scratch.alloc((size_t)it.nchunk * 2 * n * n);
       it.rbuf = scratch.alloc((size_t)n * n);
-      it.pre_nr = g_nr + gids.size();
-      const int li = (int)live.size(), nt = (n + 63) / 64;
-      for (int c = 0; c < ncc; ++c)
-        for (int ti = 0; ti < nt; ++ti)
-          for (int tj = ti; tj < nt; ++tj) {
-            GramWork w{li, ti, tj, c, (long long)c * kGramCols, std::min<long long>(it.N, (long long)(c + 1) * kGramCols)};
-            gwork.push_back(w);
-          }
-      gids.push_back(li);
-      gmax = std::max(gmax, n);
+      it.pre_nr = g_nr + gb.items.size();
+      gb.add(scratch, it.s0, it.s1, n, it.N, 1, it.tol, it.rbuf, it.pre_nr);
       live.push_back(it);
       continue;
     }
@@ -756,13 +798,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     }
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
-  if (!gids.empty()) {
-    GramWork* d_gw = C.push(gwork);
-    int* d_gids = C.push(gids);
-    C.flush();
-    cuda_check(launch_gram(d_items, d_s, d_gw, (int)gwork.size(), d_gids, (int)gids.size(), gmax, C.st), "gram");
-    C.launches += 2;
-  }
+  gb.launch(C, d_s);
   if (!work.empty()) {
     C.flush();
     cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");

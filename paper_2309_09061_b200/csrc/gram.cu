@@ -105,7 +105,7 @@ __device__ __forceinline__ long long pidx(int i, int j, int m) {  // packed uppe
 }  // namespace
 
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const SvdItem* __restrict__ items,
+__global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* __restrict__ items,
                                                                 const Seg* __restrict__ segs,
                                                                 const GramWork* __restrict__ work) {
   __shared__ __align__(16) double Pa[kGP][kGT + 2];
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const SvdItem* _
   __shared__ double s_sc[kGSeg];
   __shared__ int s_first, s_n;
   const GramWork w = work[blockIdx.x];
-  const SvdItem it = items[w.item];
+  const GramItem it = items[w.item];
   const int m = it.m;
   const int ia = w.ti * kGT, jb = w.tj * kGT;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kGThr / 32;
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const SvdItem* _
       const Seg sg = segs[sfirst + q];
       s_off[q] = sg.off;
       s_p[q] = sg.a.p;
-      s_rs[q] = sg.a.rs;
-      s_cs[q] = sg.a.cs;
+      s_rs[q] = it.hcols ? sg.a.rs : sg.a.cs;  // element stride along a line
+      s_cs[q] = it.hcols ? sg.a.cs : sg.a.rs;  // line stride
       s_sc[q] = gseg_scale(sg);
     }
   for (long long c0 = w.c0; c0 < w.c1; c0 += kGP) {
@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const SvdItem* _
           sc = s_sc[lo2];
         } else {
           const Seg sg = segs[gfind_seg(segs, it.s0, it.s1, c)];
-          col = sg.a.p + (c - sg.off) * sg.a.cs;
-          rs = sg.a.rs;
+          col = sg.a.p + (c - sg.off) * (it.hcols ? sg.a.cs : sg.a.rs);
+          rs = it.hcols ? sg.a.rs : sg.a.cs;
           sc = gseg_scale(sg);
         }
       }
@@ -242,12 +242,11 @@ __device__ __forceinline__ void argmax_pair_g(double& best, int& bi, int width) 
   }
 }
 
-__global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const SvdItem* __restrict__ items,
-                                                             const int* __restrict__ ids) {
+__global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __restrict__ items) {
   extern __shared__ __align__(16) double gsm[];
   __shared__ double red[2 * (kCThr / 32)];
   __shared__ int ired[2 * (kCThr / 32)];
-  const SvdItem it = items[ids[blockIdx.x]];
+  const GramItem it = items[blockIdx.x];
   const int m = it.m;
   const long long np = (long long)m * (m + 1) / 2;
   double* Gh = gsm;
@@ -259,7 +258,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const SvdItem* __re
   for (int i = warp; i < m; i += nw)
     for (int j = i + lane; j < m; j += 32) {
       dd acc{0.0, 0.0};
-      for (int ch = 0; ch < it.nchunk; ++ch) {
+      for (int ch = 0; ch < it.nslice; ++ch) {
         const double* gh = it.gpart + (size_t)ch * 2 * m * m;
         acc = dd_add(acc, dd{gh[(size_t)i * m + j], gh[(size_t)m * m + (size_t)i * m + j]});
       }
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const SvdItem* __re
   }
   // rows below the numerical rank: zero (they are deflated, see kDeflateG)
   for (long long e = (long long)j * m + tid; e < (long long)m * m; e += nt) R[e] = 0.0;
-  if (tid == 0) *it.pre_nr = j;
+  if (tid == 0) *it.nr = j;
 }
 
 size_t gram_chol_smem(int m) {
@@ -357,8 +356,8 @@ size_t gram_chol_smem(int m) {
   return sizeof(double) * 2 * np + (size_t)m + 16;
 }
 
-cudaError_t launch_gram(const SvdItem* items, const Seg* segs, const GramWork* work, int nwork, const int* ids,
-                        int nids, int mmax, cudaStream_t st) {
+cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
+                        int mmax, cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncAttributes fa;
@@ -368,8 +367,8 @@ cudaError_t launch_gram(const SvdItem* items, const Seg* segs, const GramWork* w
   });
   if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, 0, st>>>(items, segs, work);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || nids == 0) return e;
-  gram_chol_kernel<<<nids, mmax <= 64 ? 256 : kCThr, gram_chol_smem(mmax), st>>>(items, ids);
+  if (e != cudaSuccess || nitems == 0) return e;
+  gram_chol_kernel<<<nitems, mmax <= 64 ? 256 : kCThr, gram_chol_smem(mmax), st>>>(items);
   return cudaGetLastError();
 }
 

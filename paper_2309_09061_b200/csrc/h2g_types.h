@@ -60,6 +60,8 @@ struct QrItem {
   long long M;
   double* out;
   double* rbuf;  // nchunk x (n x n) partial R factors
+  int full;      // 1: rbuf holds a pivoted (Gram) factor, copied whole (not only its upper triangle)
+  int pad_;
 };
 
 // Tree merge of two partial R factors: rbuf[a] <- R([rbuf[a]; rbuf[b]]) (n x n each).
@@ -103,6 +105,18 @@ __host__ __device__ inline int gram_reps(int m) {
   const int r = 256 / span;
   return r > 1 ? r : 1;
 }
+
+// Double-double Gram + pivoted Cholesky item (gram.cu): the lines of hstack(segs) (hcols = 1: the
+// columns of an m-row wide matrix) or of vstack(segs) (hcols = 0: the rows of an N x m stack).
+struct GramItem {
+  int s0, s1, m, nslice;  // nslice partial slices (column chunks x replicas)
+  long long N;            // lines
+  int hcols, pad_;
+  double tol;             // truncation tolerance of the SVD that follows (0: factorisation only)
+  double* gpart;          // nslice x {hi, lo} x (m x m)
+  double* rbuf;           // m x m factor (rows = pivot steps, columns in original order)
+  int* nr;                // rows of the factor
+};
 
 // One CTA of the double-double Gram (gram.cu): columns [c0, c1) of item `item`, G tile (ti, tj).
 struct GramWork {

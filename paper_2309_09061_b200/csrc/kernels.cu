@@ -349,7 +349,7 @@ __global__ void qr_out_kernel(const QrItem* __restrict__ items) {
   const long long rows = it.M < n ? it.M : n;
   for (long long e = threadIdx.x; e < rows * n; e += blockDim.x) {
     const long long i = e / n, j = e % n;
-    it.out[e] = j >= i ? it.rbuf[i * n + j] : 0.0;
+    it.out[e] = (it.full || j >= i) ? it.rbuf[i * n + j] : 0.0;
   }
 }
 
