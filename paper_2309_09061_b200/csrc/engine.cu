@@ -421,6 +421,13 @@ struct GramBatch {
   }
 };
 
+// Protected-basis items (phase 1) through the Gram as well: opt-in (H2G_GRAM_PROT=1) -- measured
+// neutral on c2 / c4 (the projection GEMM costs what the TSQR and QRCP saved).
+static bool gram_prot_path(int n) {
+  static const bool on = getenv("H2G_GRAM_PROT") != nullptr;
+  return on && gram_path(0, n, 1);
+}
+
 static bool gram_qr_path(int n, long long M) {
   static const bool off = getenv("H2G_NO_GRAM_QR") != nullptr;
   return !off && gram_path(0, n, M);
@@ -699,7 +706,8 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<long long> tile_lines;
   for (auto& it : items) {
     const int n = it.m - std::min(it.m, it.kx);
-    if (it.m > 0 && n > 0 && tile_path(n) && !gram_path(it.kx, n, it.N)) tile_lines.push_back(it.N);
+    if (it.m > 0 && n > 0 && tile_path(n) && !gram_path(it.kx, n, it.N) && !(it.kx > 0 && it.N > 0 && gram_prot_path(n)))
+      tile_lines.push_back(it.N);
   }
   const int tpc = tiles_per_cta(tile_lines);
   std::vector<TileItem> titems;
@@ -708,6 +716,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   std::vector<int> prep_ids;
   int tnmax = 0;
   GramBatch gb;
+  GBatch gproj;  // projections of protected-basis items onto Q_V[:, k1:]
   int* g_nr = (int*)scratch.alloc_bytes(items.size() * sizeof(int));
   for (size_t i = 0; i < items.size(); ++i) {
     SvdItem& it = items[i];
@@ -717,6 +726,29 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     const int n = it.m - k1;
     it.vws = it.kx > 0 ? scratch.alloc((size_t)it.m * (it.kx | 1) + it.kx) : nullptr;
     if (svd_finish_smem(it.m, it.kx, true, false) > kSmemLimit) fin_rsmem = false;
+    if (it.kx > 0 && n > 0 && it.N > 0 && gram_prot_path(n)) {
+      // protected basis: B = Q_V[:, k1:]^T A (double, as the reference forms Q_full^T hstack(w),
+      // induced.py:127-137) per segment, then the same double-double Gram of B; svd_prep_kernel
+      // supplies the explicit Q_V and the finish forms Q_t = Q_V [[I, 0], [0, U]]
+      it.q2 = scratch.alloc((size_t)it.m * it.m);
+      prep_ids.push_back((int)live.size());
+      const size_t full = svd_prep_smem(it.m, it.kx, true);
+      sm_prep = std::max(sm_prep, full <= kSmemLimit ? full : svd_prep_smem(it.m, it.kx, false));
+      it.rbuf = scratch.alloc((size_t)n * n);
+      it.pre_nr = g_nr + gb.items.size();
+      const int s0n = (int)sl.segs.size();
+      for (int q = it.s0; q < it.s1; ++q) {
+        Seg sg = sl.segs[q];
+        const Mat b{scratch.alloc((size_t)n * sg.w), n, sg.w};
+        gproj.out(b, false);
+        gproj.t2(MatRef{it.q2 + k1, 1, it.m}, sg.a, it.m);
+        sg.a = b.ref();  // scale and device divisor apply to B's columns as to A's
+        sl.segs.push_back(sg);
+      }
+      gb.add(scratch, s0n, (int)sl.segs.size(), n, it.N, 1, it.tol, it.rbuf, it.pre_nr);
+      live.push_back(it);
+      continue;
+    }
     if (gram_path(it.kx, n, it.N)) {
       // double-double Gram + pivoted Cholesky (gram.cu) instead of the Householder TSQR
       it.rbuf = scratch.alloc((size_t)n * n);
@@ -798,16 +830,17 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     }
   cudaEvent_t ev = C.prof_begin();
   cudaEvent_t sv = C.sub_begin();
+  if (!prep_ids.empty()) {  // explicit Q_V first: the Gram projections and the tile path read it
+    int* d_ids = C.push(prep_ids);
+    C.flush();
+    cuda_check(launch_svd_prep(d_items, d_ids, (int)prep_ids.size(), sm_prep, C.st), "svd_prep");
+    ++C.launches;
+  }
+  if (!gproj.outs.empty()) gproj.run(C);
   gb.launch(C, d_s);
   if (!work.empty()) {
     C.flush();
     cuda_check(launch_svd_tsqr(d_items, d_s, d_work, (int)work.size(), sm_tsqr, rsmem, C.st), "svd_tsqr");
-    ++C.launches;
-  }
-  if (!prep_ids.empty()) {
-    int* d_ids = C.push(prep_ids);
-    C.flush();
-    cuda_check(launch_svd_prep(d_items, d_ids, (int)prep_ids.size(), sm_prep, C.st), "svd_prep");
     ++C.launches;
   }
   const TileItem* d_ti = nullptr;
