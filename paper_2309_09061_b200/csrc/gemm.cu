@@ -85,10 +85,14 @@ __device__ __forceinline__ void store_chunk(const double (&ra)[kPerA], const dou
   }
 }
 
-__device__ __forceinline__ void mma_chunk(Acc& acc, const double* As, const double* Bs, int kc) {
+// mt / nt: valid rows / columns of the tile; a warp whose 16 x 32 quadrant lies wholly outside
+// skips its DMMAs (its accumulators stay zero and are never stored) -- partial edge tiles of
+// k x k outputs (e.g. 78 x 78 in 64 x 64 tiles) otherwise spend the tensor pipe on padding.
+__device__ __forceinline__ void mma_chunk(Acc& acc, const double* As, const double* Bs, int kc, int mt, int nt) {
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int wr = warp_row0(), wc = warp_col0();
+  if (wr >= mt || wc >= nt) return;
   for (int kk = 0; kk < kc; kk += 4) {
     double a[kRT], b[kCT];
 #pragma unroll
@@ -114,7 +118,7 @@ __device__ void tile_gemm(Acc& acc, const MatRef& A, int ai0, int mt, const MatR
     store_chunk(ra, rb, As, Bs);
     __syncthreads();
     if (kk + kKC < k) fetch_chunk(ra, rb, A, ai0, mt, B, bj0, nt, kk + kKC, min(kKC, k - kk - kKC), alpha);
-    mma_chunk(acc, As, Bs, (kc + 3) & ~3);
+    mma_chunk(acc, As, Bs, (kc + 3) & ~3, mt, nt);
   }
 }
 
