@@ -331,3 +331,18 @@ def test_block_relative_error_per_coarse_leaf():
         assert np.linalg.norm(blk_got - blk_ref, 2) <= 10 * eps * np.linalg.norm(blk_ref, 2) + 1e-13
         checked += 1
     assert checked > 0
+
+
+@pytest.mark.parametrize("env", [{"H2G_NO_GRAM": "1", "H2G_NO_GRAM_QR": "1"},  # Householder TSQR everywhere
+                                 {"H2G_GRAM_PROT": "1"}])                        # Gram for protected SVDs too
+def test_alternative_factorisation_paths(env):
+    """The factorisation paths selected by environment switches (read once per process) keep every
+    golden gate: the Householder TSQR + QRCP path that the double-double Gram path replaced by
+    default, and the opt-in Gram path for the protected-basis SVDs of phase 1."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_parity.py"),
+           "-k", "test_golden_parity", "-m", "gpu"]
+    r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
