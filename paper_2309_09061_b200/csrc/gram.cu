@@ -67,7 +67,7 @@ __device__ __forceinline__ dd dd_mul(dd a, dd b) {
   return fast_two_sum(p, e);
 }
 __device__ __forceinline__ dd dd_recip(dd b) {  // 1 / b, two Newton-style corrections
-  const double q1 = 1.0 / b.hi;
+  const double q1 = __drcp_rn(b.hi);
   // r = 1 - b q1
   dd r = dd_add(dd{1.0, 0.0}, dd_neg(dd_mul(b, dd{q1, 0.0})));
   const double q2 = r.hi * q1;
@@ -80,7 +80,7 @@ __device__ __forceinline__ dd dd_sqrt(dd a) {  // a > 0
   const double p = x * x;
   const double pe = fma(x, x, -p);
   const dd r = dd_add(a, dd{-p, -pe});
-  return fast_two_sum(x, r.hi / (2.0 * x));
+  return fast_two_sum(x, r.hi * (0.5 * __drcp_rn(x)));
 }
 
 __device__ __forceinline__ double gseg_scale(const Seg& sg) {
@@ -251,9 +251,13 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
   const long long np = (long long)m * (m + 1) / 2;
   double* Gh = gsm;
   double* Gl = Gh + np;
-  unsigned char* done = reinterpret_cast<unsigned char*>(Gl + np);
+  int* roff = reinterpret_cast<int*>(Gl + np);  // packed offset of (i, i)
+  unsigned char* done = reinterpret_cast<unsigned char*>(roff + m);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, nt = blockDim.x;
   double* R = it.rbuf;  // m x m, row-major
+  for (int i = tid; i < m; i += blockDim.x) roff[i] = (int)pidx(i, i, m);
+  __syncthreads();
+#define PX(i, j) (roff[(i)] + ((j) - (i)))
   // 1. sum the chunk partials in a fixed order
   for (int i = warp; i < m; i += nw)
     for (int j = i + lane; j < m; j += 32) {
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
         const double* gh = it.gpart + (size_t)ch * 2 * m * m;
         acc = dd_add(acc, dd{gh[(size_t)i * m + j], gh[(size_t)m * m + (size_t)i * m + j]});
       }
-      const long long e = pidx(i, j, m);
+      const long long e = PX(i, j);
       Gh[e] = acc.hi;
       Gl[e] = acc.lo;
     }
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
     int bi = m;
     for (int i = warp; i < m; i += nw) {
       if (lane == 0) {
-        const double d = Gh[pidx(i, i, m)];
+        const double d = Gh[PX(i, i)];
         if (d > best || (d == best && i < bi)) { best = d; bi = i; }
       }
     }
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
     int p = lane < nw ? ired[buf + lane] : m;
     argmax_pair_g(best, p, 32);
     if (p >= m) break;
-    const dd gpp{Gh[pidx(p, p, m)], Gl[pidx(p, p, m)]};
+    const dd gpp{Gh[PX(p, p)], Gl[PX(p, p)]};
     const double bst = gpp.hi + gpp.lo;
     if (!(bst > 0.0)) break;
     if (j == 0) {
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
         } else if (done[c]) {
           v = 0.0;
         } else {
-          const long long e = c < p ? pidx(c, p, m) : pidx(p, c, m);
+          const long long e = c < p ? PX(c, p) : PX(p, c);
           const dd r = dd_mul(dd{Gh[e], Gl[e]}, irpp);
           v = r.hi + r.lo;
         }
@@ -324,21 +328,56 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
     // Schur complement of the remaining rows / columns; diagonal argmax partials for step j + 1
     double cbest = -1.0;
     int cbi = m;
-    for (int a = warp; a < m; a += nw) {
-      if (a == p || done[a]) continue;
-      const long long ea = a < p ? pidx(a, p, m) : pidx(p, a, m);
-      const dd gpa = dd_mul(dd{Gh[ea], Gl[ea]}, inv);
-      for (int b = a + lane; b < m; b += 32) {
-        if (b == p || done[b]) continue;
-        const long long eb = b < p ? pidx(b, p, m) : pidx(p, b, m);
-        const dd t = dd_mul(gpa, dd{Gh[eb], Gl[eb]});
-        const long long e = pidx(a, b, m);
-        const dd nv = dd_add(dd{Gh[e], Gl[e]}, dd_neg(t));
-        Gh[e] = nv.hi;
-        Gl[e] = nv.lo;
-        if (b == a) {
-          const double d = nv.hi + nv.lo;
-          if (d > cbest || (d == cbest && a < cbi)) { cbest = d; cbi = a; }
+    // two rows per warp iteration: their double-double chains are independent and interleave
+    for (int a0 = warp; a0 < m; a0 += 2 * nw) {
+      const int a1 = a0 + nw;
+      const bool v0 = a0 != p && !done[a0];
+      const bool v1 = a1 < m && a1 != p && !done[a1];
+      dd g0{0.0, 0.0}, g1{0.0, 0.0};
+      if (v0) {
+        const long long e = a0 < p ? PX(a0, p) : PX(p, a0);
+        g0 = dd_mul(dd{Gh[e], Gl[e]}, inv);
+      }
+      if (v1) {
+        const long long e = a1 < p ? PX(a1, p) : PX(p, a1);
+        g1 = dd_mul(dd{Gh[e], Gl[e]}, inv);
+      }
+      if (!v0 && !v1) continue;
+      for (int k = lane; a0 + k < m; k += 32) {
+        const int b0 = a0 + k, b1 = a1 + k;
+        const bool w0 = v0 && b0 != p && !done[b0];
+        const bool w1 = v1 && b1 < m && b1 != p && !done[b1];
+        dd x0{0.0, 0.0}, y0{0.0, 0.0}, x1{0.0, 0.0}, y1{0.0, 0.0};
+        long long e0 = 0, e1 = 0;
+        if (w0) {
+          const long long eb = b0 < p ? PX(b0, p) : PX(p, b0);
+          e0 = PX(a0, b0);
+          x0 = dd{Gh[eb], Gl[eb]};
+          y0 = dd{Gh[e0], Gl[e0]};
+        }
+        if (w1) {
+          const long long eb = b1 < p ? PX(b1, p) : PX(p, b1);
+          e1 = PX(a1, b1);
+          x1 = dd{Gh[eb], Gl[eb]};
+          y1 = dd{Gh[e1], Gl[e1]};
+        }
+        const dd n0 = dd_add(y0, dd_neg(dd_mul(g0, x0)));
+        const dd n1 = dd_add(y1, dd_neg(dd_mul(g1, x1)));
+        if (w0) {
+          Gh[e0] = n0.hi;
+          Gl[e0] = n0.lo;
+          if (k == 0) {
+            const double d = n0.hi + n0.lo;
+            if (d > cbest || (d == cbest && a0 < cbi)) { cbest = d; cbi = a0; }
+          }
+        }
+        if (w1) {
+          Gh[e1] = n1.hi;
+          Gl[e1] = n1.lo;
+          if (k == 0) {
+            const double d = n1.hi + n1.lo;
+            if (d > cbest || (d == cbest && a1 < cbi)) { cbest = d; cbi = a1; }
+          }
         }
       }
     }
@@ -349,11 +388,12 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
   // rows below the numerical rank: zero (they are deflated, see kDeflateG)
   for (long long e = (long long)j * m + tid; e < (long long)m * m; e += nt) R[e] = 0.0;
   if (tid == 0) *it.nr = j;
+#undef PX
 }
 
 size_t gram_chol_smem(int m) {
   const size_t np = (size_t)m * (m + 1) / 2;
-  return sizeof(double) * 2 * np + (size_t)m + 16;
+  return sizeof(double) * 2 * np + sizeof(int) * (size_t)m + (size_t)m + 16;
 }
 
 cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
