@@ -689,17 +689,17 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     }
     g.run_device_terms(C, d_terms, fl);
   }
-  // the dense targets (queued ahead) receive the push-down: wait for them; the triple arrays are
-  // consumed by both expansions, release them in stream order
-  if (early) {
+  // the dense targets (queued ahead) receive the push-down's expansions: the main stream waits for
+  // them just before the first expansion launch (the coupling pushes of the upper levels do not
+  // touch them); the triple arrays are consumed by both expansions, release them in stream order
+  bool dense_wait = early;
+  auto wait_dense = [&] {
+    if (!dense_wait) return;
     cuda_check(cudaStreamWaitEvent(C.st, pt.early.done, 0), "wait dense targets");
     cudaEventDestroy(pt.early.done);
     pt.early.done = nullptr;
-  }
-  if (pt.dev.block) {
-    cudaFreeAsync(pt.dev.block, C.st);
-    pt.dev.block = nullptr;
-  }
+    dense_wait = false;
+  };
   if (pt.dev.ready) {
     cudaEventDestroy(pt.dev.ready);
     pt.dev.ready = nullptr;
@@ -733,7 +733,13 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       }
     }
     g1.run(C);
+    if (!g2.outs.empty()) wait_dense();
     g2.run(C);
+  }
+  wait_dense();
+  if (pt.dev.block) {  // after the main stream has waited for the dense targets' expansion
+    cudaFreeAsync(pt.dev.block, C.st);
+    pt.dev.block = nullptr;
   }
   if (part.on()) {  // every rank continues with the whole of G (couplings and nearfield)
     StageTag tagx(C, "p1.exchange");
