@@ -1238,48 +1238,93 @@ PTree product_tree(BView bx, BView by) {
 // Planner-thread epilogue: distinct dense-target operand blocks, and the triple arrays copied to the
 // device on a private stream (overlapping the GPU's basis construction).
 void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
+  static const bool dbg = getenv("H2G_DEBUG_PLANNER") != nullptr;
+  const auto tp0 = std::chrono::steady_clock::now();
+  auto tms = [tp0] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count(); };
   const Blocks& B = *P.bt;
   const int nt = (int)P.ts.size();
   // order each node's triples c, a, b (stable): the assembly sums kind-a terms into one T and
-  // kind-b terms into one U before applying their shared factor (GOut ka / kb)
+  // kind-b terms into one U before applying their shared factor (GOut ka / kb).  Nodes are
+  // independent: block ranges of about equal triple counts go to host threads.
+  const int nthr = (int)std::min<long long>(8, std::max<long long>(1, nt / 65536));
+  std::vector<int> cut(nthr + 1, B.nb);
+  cut[0] = 0;
+  for (int k = 1, b = 0; k < nthr; ++k) {
+    const long long target = (long long)nt * k / nthr;
+    while (b < B.nb && P.tptr[b] < target) ++b;
+    cut[k] = b;
+  }
+  auto par = [&](auto&& fn) {  // fn(b0, b1) over the block ranges
+    std::vector<std::thread> th;
+    for (int k = 1; k < nthr; ++k) th.emplace_back(fn, cut[k], cut[k + 1]);
+    fn(cut[0], cut[1]);
+    for (auto& t : th) t.join();
+  };
   {
-    std::vector<int> ts2(nt), tbx2(nt), tby2(nt);
-    std::vector<char> tk2(nt);
-    for (int b = 0; b < B.nb; ++b) {
-      int o = P.tptr[b];
-      for (const char kind : {'c', 'a', 'b'})
-        for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i)
-          if (P.tk[i] == kind) {
-            ts2[o] = P.ts[i];
-            tbx2[o] = P.tbx[i];
-            tby2[o] = P.tby[i];
-            tk2[o] = kind;
-            ++o;
-          }
-      if (o != P.tptr[b + 1]) throw StructureErr("product tree: unknown triple kind");
-    }
-    P.ts.swap(ts2);
-    P.tbx.swap(tbx2);
-    P.tby.swap(tby2);
-    P.tk.swap(tk2);
-  }
-  const int nbx = BX.nb;
-  std::vector<char> seenx(nbx, 0), seeny(nby, 0), seenf(nbx, 0);
-  const Part part = make_part(*B.rows, C.comm);  // multi-GPU: only this rank's product rows
-  for (int b = 0; b < B.nb; ++b) {
-    if (!part.mine(B.row[b])) continue;
-    if (!B.near_leaf(b)) {
-      for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
-        const int bts = P.tbx[i];
-        if (P.tk[i] == 'a' && BX.adm_leaf(bts) && !seenf[bts]) { seenf[bts] = 1; P.rf_blocks.push_back(bts); }
+    std::atomic<int> bad{0};
+    par([&](int b0, int b1) {  // in place, one node at a time through a small local buffer
+      std::vector<int> ts2, tbx2, tby2;
+      std::vector<char> tk2;
+      for (int b = b0; b < b1; ++b) {
+        const int i0 = P.tptr[b], i1 = P.tptr[b + 1], cnt = i1 - i0;
+        ts2.resize(cnt); tbx2.resize(cnt); tby2.resize(cnt); tk2.resize(cnt);
+        int o = 0;
+        for (const char kind : {'c', 'a', 'b'})
+          for (int i = i0; i < i1; ++i)
+            if (P.tk[i] == kind) {
+              ts2[o] = P.ts[i];
+              tbx2[o] = P.tbx[i];
+              tby2[o] = P.tby[i];
+              tk2[o] = kind;
+              ++o;
+            }
+        if (o != cnt) { bad = 1; continue; }
+        std::copy(ts2.begin(), ts2.end(), P.ts.begin() + i0);
+        std::copy(tbx2.begin(), tbx2.end(), P.tbx.begin() + i0);
+        std::copy(tby2.begin(), tby2.end(), P.tby.begin() + i0);
+        std::copy(tk2.begin(), tk2.end(), P.tk.begin() + i0);
       }
-      continue;
-    }
-    for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
-      if (P.tk[i] == 'a' && !seenx[P.tbx[i]]) { seenx[P.tbx[i]] = 1; P.need_xv.push_back(P.tbx[i]); }
-      if (P.tk[i] == 'b' && !seeny[P.tby[i]]) { seeny[P.tby[i]] = 1; P.need_wy.push_back(P.tby[i]); }
+    });
+    if (bad) throw StructureErr("product tree: unknown triple kind");
+  }
+  const double t_re = tms();
+  const int nbx = BX.nb;
+  const Part part = make_part(*B.rows, C.comm);  // multi-GPU: only this rank's product rows
+  // per range: first appearances within the range; merged in range order (= global first
+  // appearance, the serial order)
+  std::vector<std::vector<int>> lx(nthr), ly(nthr), lf(nthr);
+  {
+    std::vector<std::thread> th;
+    auto run = [&](int k) {
+      std::vector<char> sx(nbx, 0), sy(nby, 0), sf(nbx, 0);
+      for (int b = cut[k]; b < cut[k + 1]; ++b) {
+        if (!part.mine(B.row[b])) continue;
+        if (!B.near_leaf(b)) {
+          for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
+            const int bts = P.tbx[i];
+            if (P.tk[i] == 'a' && BX.adm_leaf(bts) && !sf[bts]) { sf[bts] = 1; lf[k].push_back(bts); }
+          }
+          continue;
+        }
+        for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) {
+          if (P.tk[i] == 'a' && !sx[P.tbx[i]]) { sx[P.tbx[i]] = 1; lx[k].push_back(P.tbx[i]); }
+          if (P.tk[i] == 'b' && !sy[P.tby[i]]) { sy[P.tby[i]] = 1; ly[k].push_back(P.tby[i]); }
+        }
+      }
+    };
+    for (int k = 1; k < nthr; ++k) th.emplace_back(run, k);
+    run(0);
+    for (auto& t : th) t.join();
+  }
+  {
+    std::vector<char> seenx(nbx, 0), seeny(nby, 0), seenf(nbx, 0);
+    for (int k = 0; k < nthr; ++k) {
+      for (int v : lf[k]) if (!seenf[v]) { seenf[v] = 1; P.rf_blocks.push_back(v); }
+      for (int v : lx[k]) if (!seenx[v]) { seenx[v] = 1; P.need_xv.push_back(v); }
+      for (int v : ly[k]) if (!seeny[v]) { seeny[v] = 1; P.need_wy.push_back(v); }
     }
   }
+  const double t_dd = tms();
   if (nt == 0) return;
   const size_t n4 = (size_t)nt * 4, pad = 256;
   const size_t bytes = 4 * ((n4 + pad - 1) / pad * pad) + nt + pad;
@@ -1290,15 +1335,20 @@ void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
     C.up_cap = bytes * 2;
     cuda_check(cudaMallocHost(&C.up_host, C.up_cap), "cudaMallocHost");
   }
+  const double t_sy = tms();
   const size_t stride = (n4 + pad - 1) / pad * pad;
   char* h = C.up_host;
   int* htnode = (int*)h;
-  for (int b = 0; b < B.nb; ++b)
-    for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) htnode[i] = b;
-  memcpy(h + stride, P.ts.data(), n4);
-  memcpy(h + 2 * stride, P.tbx.data(), n4);
-  memcpy(h + 3 * stride, P.tby.data(), n4);
-  memcpy(h + 4 * stride, P.tk.data(), nt);
+  par([&](int b0, int b1) {  // staging into the pinned buffer, by block ranges
+    if (b0 >= b1) return;
+    const int i0 = P.tptr[b0], i1 = P.tptr[b1];
+    for (int b = b0; b < b1; ++b)
+      for (int i = P.tptr[b]; i < P.tptr[b + 1]; ++i) htnode[i] = b;
+    memcpy(h + stride + 4 * (size_t)i0, P.ts.data() + i0, 4 * (size_t)(i1 - i0));
+    memcpy(h + 2 * stride + 4 * (size_t)i0, P.tbx.data() + i0, 4 * (size_t)(i1 - i0));
+    memcpy(h + 3 * stride + 4 * (size_t)i0, P.tby.data() + i0, 4 * (size_t)(i1 - i0));
+    memcpy(h + 4 * stride + i0, P.tk.data() + i0, (size_t)(i1 - i0));
+  });
   cuda_check(cudaMallocAsync(&P.dev.block, bytes, C.up_stream), "cudaMallocAsync");
   cuda_check(cudaMemcpyAsync(P.dev.block, h, bytes, cudaMemcpyHostToDevice, C.up_stream), "upload");
   char* d = (char*)P.dev.block;
@@ -1309,6 +1359,9 @@ void ptree_prepare(PTree& P, Ctx& C, const Blocks& BX, int nby) {
   P.dev.tk = d + 4 * stride;
   cuda_check(cudaEventCreateWithFlags(&P.dev.ready, cudaEventDisableTiming), "event");
   cuda_check(cudaEventRecord(P.dev.ready, C.up_stream), "event");
+  if (dbg)
+    fprintf(stderr, "ptree_prepare: %d triples, reorder %.2f, dedupe %.2f, sync/alloc %.2f, staged+queued %.2f ms\n", nt,
+            t_re, t_dd, t_sy, tms());
 }
 
 // ============================================================================ setup stages

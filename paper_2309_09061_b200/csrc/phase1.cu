@@ -798,10 +798,20 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     cuda_check(cudaEventCreateWithFlags(&p_ready, cudaEventDisableTiming), "event");
     cuda_check(cudaEventRecord(p_ready, C.st), "event");
   }
-  auto pt_future = std::async(std::launch::async, [&x, &y, &C, &P, A, p_ready, X, Y] {
+  static const bool dbg_plan = getenv("H2G_DEBUG_PLANNER") != nullptr;
+  const auto t_mul0 = std::chrono::steady_clock::now();
+  auto ms_since = [t_mul0] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_mul0).count();
+  };
+  auto pt_future = std::async(std::launch::async, [&x, &y, &C, &P, A, p_ready, X, Y, ms_since] {
     PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+    const double t1 = ms_since();
     ptree_prepare(pt, C, *x.bt, y.bt->nb);
+    const double t2 = ms_since();
     if (A) assemble_dense_early(*A, X, Y, PRef{&P, false}, pt, p_ready, C.comm);
+    if (dbg_plan)
+      fprintf(stderr, "planner: product tree %.2f ms, prepared %.2f ms, dense targets queued %.2f ms\n", t1, t2,
+              ms_since());
     return pt;
   });
   struct PtJoin {  // never leave the planner running past an exception
@@ -871,6 +881,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   }
   record(C, e2);
   e3 = e2;
+  if (dbg_plan) fprintf(stderr, "main: induced passes issued and joined %.2f ms\n", ms_since());
   if (!have_rf) {
     HostTimer ht(C, "product_tree_wait");
     pt = pt_future.get();
