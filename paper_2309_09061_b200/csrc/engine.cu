@@ -1440,7 +1440,11 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
   std::vector<Mat> Tb(nb);
   GBatch g;
   NormBatch nbatch;
-  std::vector<int> order;
+  // sigma_1 of every T_b stays on the device as its segment's divisor (no host round trip); an
+  // exactly-zero T_b (sigma_1 = 0, skipped by the reference, weights.py:86-89) contributes zero rows,
+  // which leave the stack's Gram -- all its factor's consumers see -- unchanged
+  double* d_nrm = scaling ? ar.alloc(std::max(1, nb)) : nullptr;
+  if (scaling) cuda_check(cudaMemsetAsync(d_nrm, 0, sizeof(double) * std::max(1, nb), C.st), "memset");
   for (int t = 0; t < tr.n; ++t)
     for (int b : adm_of[t]) {
       const Mat& R = rw[h.col(b)];
@@ -1455,15 +1459,14 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
         it.s1 = nbatch.sl.begin();
         it.m = Tb[b].r;
         it.N = kr;
+        it.out = d_nrm + b;
         nbatch.items.push_back(it);
-        order.push_back(b);
       }
     }
   g.run(C);
-  std::vector<double> nrm(nb, 1.0);
   if (scaling) {
-    auto v = nbatch.run(C, ar);
-    for (size_t i = 0; i < order.size(); ++i) nrm[order[i]] = v[i];
+    nbatch.scratch = &ar;
+    nbatch.run_async(C);
   }
   MatStore Z(tr.n);
   for (int lev = 0; lev <= tr.depth; ++lev) {
@@ -1484,8 +1487,7 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
         M += ze.r;
       }
       for (int b : adm_of[s]) {
-        if (scaling && nrm[b] == 0.0) continue;
-        q.sl.add(Tb[b].ref(), Tb[b].r, scaling ? 1.0 / nrm[b] : 1.0);
+        q.sl.add(Tb[b].ref(), Tb[b].r, 1.0, scaling ? d_nrm + b : nullptr);
         M += Tb[b].r;
       }
       it.s1 = q.sl.begin();

@@ -266,7 +266,7 @@ static CPrep prep_rows(BView pv, BView coarse) {
 
 // Fig. 5: adaptive coarse row basis (reference coarsening.py:187-332).
 static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol, int max_rank, bool scale,
-                          const std::vector<double>& cn, const double* d_nn, const CPrep& prep,
+                          const double* d_cn, const double* d_nn, const CPrep& prep,
                           cudaEvent_t nn_ready = nullptr) {
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   const BView pv = g.bv();
@@ -325,9 +325,10 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
         M += ze.r;
       }
       for (int b : row_adm[t]) {
-        if (scale && cn[b] == 0.0) continue;
+        // S_tr^T / ||S_tr||_2 with the norm as a device divisor; an exactly-zero coupling (skipped
+        // by coarsening.py:239-241) adds zero rows, which leave the stack's Gram unchanged
         const int kc = w1.rank[pv.col(b)];
-        qb.sl.add(trn(g.coup(b)), kc, scale ? 1.0 / cn[b] : 1.0);
+        qb.sl.add(trn(g.coup(b)), kc, 1.0, scale ? d_cn + b : nullptr);
         M += kc;
       }
       it.s1 = qb.sl.begin();
@@ -841,7 +842,7 @@ std::shared_ptr<NormPrep> build_norm_prep(const H2& g, const Comm& comm) {
   return np;
 }
 
-static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, double* d_nn, Ctx* A = nullptr,
+static void all_norms(Ctx& C, Arena& sc, const H2& g, double* d_cn, double* d_nn, Ctx* A = nullptr,
                       cudaEvent_t* nn_ready = nullptr) {
   const Blocks& B = *g.bt;
   HostTimer ht(C, "p2_norm_build");
@@ -866,9 +867,12 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, std::vector<double>& cn, d
   } else {
     nbn.run_async(C);
   }
-  cn.assign(B.nb, 0.0);
-  auto vals = nbc.run(C, sc);
-  for (size_t i = 0; i < ids.size(); ++i) cn[ids[i]] = vals[i];
+  // coupling norms stay on the device too (no host round trip); the passes' streams fork from the
+  // main stream after this launch
+  cuda_check(cudaMemsetAsync(d_cn, 0, sizeof(double) * std::max(1, B.nb), C.st), "memset");
+  for (size_t i = 0; i < nbc.items.size(); ++i) nbc.items[i].out = d_cn + ids[i];
+  nbc.scratch = &sc;
+  nbc.run_async(C);
 }
 
 // Phase-2 driver (reference coarsening.py:408-422).
@@ -962,17 +966,17 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   auto prep_r = std::async(std::launch::async, [gv, cvw] { return prep_rows(gv, cvw); });
   auto prep_c = std::async(std::launch::async, [gvt, cvt] { return prep_rows(gvt, cvt); });
   Arena sc(C.st);
-  std::vector<double> cn;
   cudaEvent_t nn_ready = nullptr;
   struct EvGuard {
     cudaEvent_t& e;
     ~EvGuard() { if (e) cudaEventDestroy(e); }
   } nn_guard{nn_ready};
   double* d_nn = sc.alloc(std::max(1, g.bt->nb));
+  double* d_cn = sc.alloc(std::max(1, g.bt->nb));
   if (scale) {
     StageTag tag(C, "p2.norms");
-    if (!serial_passes()) all_norms(C, sc, g, cn, d_nn, &C.aux(), &nn_ready);
-    else all_norms(C, sc, g, cn, d_nn);
+    if (!serial_passes()) all_norms(C, sc, g, d_cn, d_nn, &C.aux(), &nn_ready);
+    else all_norms(C, sc, g, d_cn, d_nn);
   }
   prep_r.wait();
   prep_c.wait();
@@ -982,9 +986,9 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   CState rs, cs;
   ProjPlan plan;
   if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
-    rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
+    rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, d_cn, d_nn,
                      prep_r.get());
-    cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
+    cs = coarse_rows(C, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, d_cn, d_nn,
                      prep_c.get());
     plan = plan_project(HView{&g, false}, rs, *coarse);
   } else {
@@ -994,7 +998,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     std::exception_ptr err;
     std::thread th([&] {
       try {
-        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, cn, d_nn,
+        cs = coarse_rows(S, *ar2, HView{&g, true}, BView{coarse.get(), true}, tol, max_rank, scale, d_cn, d_nn,
                          prep_c.get(), nn_ready);
         S.sync();
       } catch (...) {
@@ -1002,7 +1006,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
       }
     });
     try {
-      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, cn, d_nn,
+      rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, d_cn, d_nn,
                        prep_r.get(), nn_ready);
       HostTimer htpp(C, "p2_project_structure");
       plan = plan_project(HView{&g, false}, rs, *coarse);  // while the column pass runs
