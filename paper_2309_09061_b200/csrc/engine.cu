@@ -378,7 +378,11 @@ static void run_merges(Ctx& C, const std::vector<std::tuple<double*, int, int>>&
 // panel kernels (A/B comparisons).
 // Wide SVD inputs without a protected basis go through the double-double Gram (gram.cu) when the
 // Gram fits the Cholesky CTA's shared memory (H2G_NO_GRAM=1: Householder TSQR, for A/B).
-static constexpr long long kGramCols = 512;  // columns per Gram CTA
+// columns per Gram CTA (H2G_GRAM_COLS overrides, for tuning)
+static long long gram_cols() {
+  static const long long v = getenv("H2G_GRAM_COLS") ? std::max(32LL, atoll(getenv("H2G_GRAM_COLS"))) : 512;
+  return v;
+}
 static bool gram_path(int kx, int n, long long N) {
   static const bool off = getenv("H2G_NO_GRAM") != nullptr;
   return !off && kx == 0 && n > 0 && N > 0 && gram_chol_smem(n) <= (size_t)kSmemLimit;
@@ -391,7 +395,7 @@ struct GramBatch {
   int mmax = 0;
   // lines of hstack(segs[s0:s1]) (hcols) or vstack (rows), m-dimensional; factor into rbuf, rows into *nr
   void add(Arena& scratch, int s0, int s1, int m, long long N, int hcols, double tol, double* rbuf, int* nr) {
-    const int ncc = (int)std::max<long long>(1, (N + kGramCols - 1) / kGramCols);
+    const int ncc = (int)std::max<long long>(1, (N + gram_cols() - 1) / gram_cols());
     GramItem g{};
     g.s0 = s0;
     g.s1 = s1;
@@ -407,7 +411,7 @@ struct GramBatch {
     for (int c = 0; c < ncc; ++c)
       for (int ti = 0; ti < nt; ++ti)
         for (int tj = ti; tj < nt; ++tj)
-          work.push_back(GramWork{gi, ti, tj, c, (long long)c * kGramCols, std::min<long long>(N, (long long)(c + 1) * kGramCols)});
+          work.push_back(GramWork{gi, ti, tj, c, (long long)c * gram_cols(), std::min<long long>(N, (long long)(c + 1) * gram_cols())});
     items.push_back(g);
     mmax = std::max(mmax, m);
   }
