@@ -1,17 +1,20 @@
 """Benchmark: the adaptive H^2 x H^2 product (multiply + coarsen) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--n N] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--n N] [--impl ours|reference]
 
-One step = one full product Z = X*Y on the BASELINE config (default configs[1] = c2: n=16384 2-D
-uniform points, -log kernel, leaf 64, eta 1, Chebyshev order 4, eps 1e-6), i.e. phase 1
-(basis products + weights + induced bases + assembly over T^XY) followed by phase 2
-(re-compression onto X's block tree) -- the stages the reference harness times
-(bench.py:195-237 of h2mul; its t_total excludes only the weights, which we include).
-Inputs are built by the reference's interpolation recipe (synthetic seeded points) and
-recompressed at eps on the GPU before timing.  Metric: DOF/s = n / product time.
+One step = one full product Z = X*Y on the largest BASELINE config that fits one B200 (default
+configs[3] = c4: n = 262,144 Fibonacci-sphere points, X from 1/r and Y from exp(-r)/r, leaf 128,
+eta 2, Chebyshev order 4 (rank 64), eps 1e-6), i.e. phase 1 (basis products + weights + induced
+bases + assembly over T^XY) followed by phase 2 (re-compression onto X's block tree) -- the
+stages the reference harness times (bench.py:195-237 of h2mul; its t_total excludes only the
+weights, which we include).  Inputs are built on the GPU by the reference's interpolation recipe
+(synthetic seeded points) and recompressed at eps before timing.  Metric: DOF/s = n / product time.
 
---impl reference times the CPU oracle (a NumPy restatement of h2mul, oracle/) with all host
-threads on a bounded sample (the same generator at a reduced n) -- the reference arm.
+--impl reference times the reference's CPU path (the oracle port, oracle/h2_oracle.py: the
+reference is pure Python, so nothing compiles into oracle/_ref; the port was measured to cost the
+same as h2mul itself) with 1 BLAS thread -- the reference protocol pins it (cli.py:12-15) --
+on a bounded sample: the same generator at a reduced n (--cpu-sample-n, default per config),
+because 25 full-size c4 CPU products (~18 min each) cannot fit the driver's window.
 Multi-GPU (N > 1, one process per GPU under torchrun): by default ONE product per step computed
 jointly by all ranks -- the row (and column) cluster trees split into subtrees at level log2 N,
 results all-gathered over NCCL (paper_2309_09061_b200/shard.py, csrc/shard.cu) -- so value =
@@ -38,11 +41,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-n", type=int, default=8192)
+    ap.add_argument("--cpu-sample-n", type=int, default=None,
+                    help="n of the CPU (reference-arm / cpu_baseline) sample; default per config")
     ap.add_argument("--parallelism", default="shard", choices=["shard", "replicas"])
     ap.add_argument("--profile-json", default=None, help="write per-stage / per-kernel detail here")
     return ap.parse_args()
@@ -141,47 +145,86 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# CPU sample sizes: about 10-15 s of single-thread CPU work per product (c2 at 8,192: ~7 s;
+# c4 at 4,096: ~12 s), the same generator as the GPU line
+CPU_SAMPLE_N = {"c1": 2048, "c2": 8192, "c3": 8192, "c4": 4096, "c5": 4096}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def build_inputs(cfg, n):
     from paper_2309_09061_b200.problems import build_config
     xr, yr, spec = build_config(cfg, n=n)
     return xr, yr, spec
 
 
-def cpu_oracle_run(cfg, n, threads):
-    """Time the CPU oracle on the config's generator at size n; returns (seconds, detail)."""
+def _blas_threads(threads):
     os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
     try:
         from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=threads)
     except Exception:  # pragma: no cover
-        threadpool_limits = None
+        return None
+
+
+def cpu_oracle_prepare(cfg, n):
+    """CPU oracle inputs at size n: the config's generator, recompressed at eps (untimed)."""
     import oracle as O
     from paper_2309_09061_b200.packed import pack_h2
     xr, yr, spec = build_inputs(cfg, n)
-    ctxm = threadpool_limits(limits=threads) if threadpool_limits else None
+    x = O.o_recompress(O.o_from_packed(pack_h2(xr)), spec["eps"])
+    y = x if yr is xr else O.o_recompress(O.o_from_packed(pack_h2(yr)), spec["eps"])
+    return x, y, spec["eps"]
+
+
+def cpu_oracle_time(x, y, eps):
+    """One full CPU product (weights + phase 1 + phase 2); returns (seconds, stage detail)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    final, induced, tm, _ = O.o_run_stages(x, y, x.bt, eps)
+    return time.perf_counter() - t0, tm   # includes the weights (t_setup), like our timed step
+
+
+def cpu_oracle_run(cfg, n, threads):
+    """Time the CPU oracle on the config's generator at size n; returns (seconds, detail)."""
+    lim = _blas_threads(threads)
     try:
-        x = O.o_recompress(O.o_from_packed(pack_h2(xr)), spec["eps"])
-        y = x if yr is xr else O.o_recompress(O.o_from_packed(pack_h2(yr)), spec["eps"])
-        t0 = time.perf_counter()
-        final, induced, tm, _ = O.o_run_stages(x, y, x.bt, spec["eps"])
-        wall = time.perf_counter() - t0   # includes the weights (t_setup), like our timed step
+        x, y, eps = cpu_oracle_prepare(cfg, n)
+        return cpu_oracle_time(x, y, eps)
     finally:
-        if ctxm is not None:
-            ctxm.__exit__(None, None, None)
-    return wall, tm
+        if lim is not None:
+            lim.__exit__(None, None, None)
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the CPU oracle with all host threads, bounded sample per step."""
+    """Reference arm: the reference's CPU path (oracle port) at 1 BLAS thread as the reference
+    protocol pins it (cli.py:12-15), bounded sample per step (same generator, reduced n)."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    n = args.cpu_sample_n
-    for _ in range(args.warmup):
-        cpu_oracle_run(args.config, n, threads)
-    times = []
-    for _ in range(args.steps):
-        t, _ = cpu_oracle_run(args.config, n, threads)
-        times.append(t)
+    threads = 1
+    n = args.cpu_sample_n or CPU_SAMPLE_N[args.config]
+    lim = _blas_threads(threads)
+    try:
+        x, y, eps = cpu_oracle_prepare(args.config, n)
+        for _ in range(args.warmup):
+            cpu_oracle_time(x, y, eps)
+        times = []
+        for _ in range(args.steps):
+            t, _ = cpu_oracle_time(x, y, eps)
+            times.append(t)
+    finally:
+        if lim is not None:
+            lim.__exit__(None, None, None)
     ms = 1e3 * sum(times) / len(times)
     value = n / (ms / 1e3)
     from paper_2309_09061_b200.problems import CONFIGS
@@ -191,11 +234,16 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded points, BASELINE generator)",
-        "config": {"workload": f"{args.config} product X*Y -> Z (multiply + coarsen), sample n={n}",
-                   "n": n, "leaf": spec["leaf"], "eta": spec["eta"], "order": spec["order"], "eps": spec["eps"]},
+        "config": {"workload": f"{args.config} product X*Y -> Z (multiply + coarsen onto X's tree)",
+                   "n": spec["n"], "geometry": spec["geometry"], "kernel_x": spec["kernel_x"],
+                   "kernel_y": spec["kernel_y"], "leaf": spec["leaf"], "eta": spec["eta"],
+                   "order": spec["order"], "eps": spec["eps"], "sample_n": n},
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.config} generator at n={n} (full product incl. weights), "
-                                   f"oracle/h2_oracle.py NumPy restatement, BLAS threads={threads}"},
+                         "cpu": cpu_model(),
+                         "sample": f"{args.config} generator at reduced n={n} (the full n={spec['n']} "
+                                   f"product takes minutes per step on one core), full product incl. "
+                                   f"weights, oracle/h2_oracle.py NumPy restatement of h2mul, 1 BLAS thread "
+                                   f"(reference cli.py:12-15)"},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,14 +276,18 @@ def main():
     n = args.n or spec["n"]
     eps = spec["eps"]
     ctx = Context(local)
+    from paper_2309_09061_b200.problems import build_config_device
     t0 = time.perf_counter()
-    xr, yr, spec = build_inputs(args.config, n)
+    # raw interpolation inputs built on the GPU (structure and the small interpolation bases on the
+    # host, couplings / nearfield evaluated by h2g_h2_build_kernel; pinned to the reference's raw
+    # inputs by tests/test_gpu_fullsize.py)
+    dxr, dyr, spec = build_config_device(args.config, n=n, ctx=ctx)
+    ctx.synchronize()
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    dxr = DeviceH2.upload(xr, ctx)
     dx = P.recompress(dxr, eps, ctx=ctx)
-    dy = dx if yr is xr else P.recompress(DeviceH2.upload(yr, ctx), eps, ctx=ctx)
-    del dxr
+    dy = dx if dyr is dxr else P.recompress(dyr, eps, ctx=ctx)
+    del dxr, dyr
     ctx.synchronize()
     t_prep = time.perf_counter() - t0
     coarse = dx.block_tree
@@ -257,18 +309,26 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ctx.counters(reset=True)
+    ctx.memory(reset=True)
     xc0 = (sharding.calls, sharding.bytes) if shard else (0, 0)
     clocks = ClockSampler(local)
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
+    # ncu --profile-from-start off captures exactly the launches between cudaProfilerStart / Stop, on
+    # every engine thread and stream (NVTX ranges are per host thread and would miss the column
+    # passes and the planner-queued launches)
+    torch.cuda.profiler.start()
+    torch.cuda.nvtx.range_push("timed")
     e0.record(stream)
     for _ in range(args.steps):
         z = step()
     e1.record(stream)
     torch.cuda.nvtx.range_pop()
     e1.synchronize()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    mem = ctx.memory()
     torch.cuda.synchronize()
     clk = clocks.stop()
     cnt = ctx.counters(reset=True)
@@ -289,13 +349,19 @@ def main():
     st1 = ctx.stage_times()
     z = P.coarsen(g, coarse, eps, ctx=ctx)
     st2 = ctx.stage_times()
+    g_ranks = g.ranks()
     ks = ctx.kernel_stats(reset=True)
     hts = ctx.host_times(reset=True)
     ctx.set_profile(False)
     ctx.set_timing(False)
-    stages = {k: st1[k] for k in ("t_setup", "t1_row", "t1_col", "t1_mat")}
-    stages.update({k: st2[k] for k in ("t2_row", "t2_col", "t2_mat")})
-    zr, zc = z.download().row_basis.rank, None
+    stages = {k: st1[k] for k in ("t_setup", "t_setup_col", "t1_row", "t1_col", "t1_span", "t1_mat")}
+    stages.update({k: st2[k] for k in ("t2_norms", "t2_row", "t2_col", "t2_span", "t2_mat")})
+    stages["note"] = ("device seconds of one product in the reference harness's split (bench.py:195-237); "
+                      "row and column passes of each phase run concurrently on two streams, t*_row / t*_col "
+                      "are each pass's own span and t*_span their joint span; t_setup = basis product + the "
+                      "row pass's weights (t_setup_col: the column pass's, concurrent); t2_row includes "
+                      "t2_norms as in the reference")
+    zr = [int(r) for r in z.ranks()[0]]
 
     # end to end through the C-ABI boundary on HOST buffers: X (and Y) in the packed layout in
     # pinned host memory -> h2g_h2_upload -> multiply -> coarsen -> h2g_h2_download into pinned
@@ -366,6 +432,8 @@ def main():
     # accuracy of the full-size product: the reference's 20-step power-iteration estimate of
     # |XY - Z|_2 / |XY|_2 (bench.py:147-174), every matvec on the GPU
     eps2 = P.estimate_relative_spectral_error(dx, dy, z, steps=20, seed=0)
+    eps2_induced = P.estimate_relative_spectral_error(dx, dy, g, steps=20, seed=0)
+    del g
     # H^2 matvec: HBM bound, every stored entry of Z read once per product
     vz = torch.randn(n, dtype=torch.float64, device=torch.device("cuda", local))
     for _ in range(3):
@@ -388,10 +456,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_n = args.cpu_sample_n
+        cpu_n = args.cpu_sample_n or CPU_SAMPLE_N[args.config]
         wall, tm = cpu_oracle_run(args.config, cpu_n, 1)
-        cpu = {"value": cpu_n / wall, "unit": "DOF/s", "cores": 1, "kind": "port",
-               "sample": f"{args.config} generator at n={cpu_n}, full product incl. weights "
+        cpu = {"value": cpu_n / wall, "unit": "DOF/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
+               "sample": f"{args.config} generator at reduced n={cpu_n}, full product incl. weights "
                          f"({wall:.1f} s), oracle/h2_oracle.py (NumPy restatement of h2mul), 1 BLAS thread",
                "stages_s": tm}
 
@@ -415,8 +483,13 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "stages_s": stages,
-            "ranks": {"final_max": int(max(zr)), "final_mean": float(sum(zr) / len(zr))},
-            "accuracy": {"eps2_power_iteration": eps2, "steps": 20, "seed": 0, "eps": eps,
+            "ranks": {"final_max": int(max(zr)), "final_mean": float(sum(zr) / len(zr)),
+                      "induced_max": int(max(g_ranks[0])), "induced_mean": float(g_ranks[0].mean())},
+            "memory": {"engine_used_high_gb": mem["used_high"] / 1e9,
+                       "engine_reserved_high_gb": mem["reserved_high"] / 1e9,
+                       "note": "high-water marks of the engine's cudaMallocAsync arenas over the timed steps"},
+            "accuracy": {"eps2_power_iteration": eps2, "eps2_induced": eps2_induced, "steps": 20, "seed": 0,
+                         "eps": eps,
                          "estimator": "reference bench.py:147-174 on GPU matvecs"},
             "matvec": matvec,
             "exchange": xchg,

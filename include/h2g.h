@@ -51,6 +51,13 @@ int h2g_ctx_set_comm(h2g_ctx* ctx, int rank, int size, h2g_allgather_fn fn, void
 /* ms per stage of the last multiply / coarsen: setup, t1_row, t1_col, t1_mat, t2_row, t2_col, t2_mat
    (the reference harness's stage split, bench.py:195-237) */
 int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);
+/* out[0..n) = {setup, t1_row, t1_col, t1_mat, t2_row, t2_col, t2_mat, setup_col, t1_span, t2_span,
+   t2_norms} ms (bench.py:195-237 split; the row / column passes of a phase run concurrently, each
+   t*_row / t*_col is its own stream span, t*_span the joint span) */
+int h2g_ctx_stage_times_ext(h2g_ctx* ctx, double* out, int n);
+/* device memory of the engine's arenas (the device's default cudaMallocAsync pool), bytes:
+   out4 = {used high-water, used now, reserved high-water, reserved now}; reset: restart the marks */
+int h2g_ctx_mem(h2g_ctx* ctx, long long* out4, int reset);
 /* kernel launches and host synchronisations since the last reset: out2 = {launches, syncs} */
 int h2g_ctx_counters(h2g_ctx* ctx, long long* out2, int reset);
 int h2g_ctx_synchronize(h2g_ctx* ctx);
@@ -102,6 +109,8 @@ int h2g_h2_upload_async(h2g_ctx* ctx, h2g_blocks* bt,
 void h2g_h2_destroy(h2g_h2* h);
 /* out8 = {nblocks, row-tree nodes, col-tree nodes, rb_len, cb_len, coup_len, near_len, block child_idx len} */
 int h2g_h2_sizes(h2g_h2* h, long long* out8);
+/* per-cluster ranks of the row and column bases (ClusterBasis.rank, h2.py:32-72); no device work */
+int h2g_h2_ranks(h2g_h2* h, long long* row_rank, long long* col_rank);
 int h2g_h2_structure(h2g_h2* h, long long* row, long long* col, long long* child_ptr, long long* child_idx,
                      unsigned char* adm);
 int h2g_h2_download(h2g_ctx* ctx, h2g_h2* h, long long* rb_rank, long long* rb_leaf_off,

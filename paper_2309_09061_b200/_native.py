@@ -33,6 +33,8 @@ SIGNATURES = {
     "h2g_ctx_destroy": (C.c_int, [P]),
     "h2g_ctx_set_timing": (C.c_int, [P, C.c_int]),
     "h2g_ctx_stage_times": (C.c_int, [P, F64P]),
+    "h2g_ctx_stage_times_ext": (C.c_int, [P, F64P, C.c_int]),
+    "h2g_ctx_mem": (C.c_int, [P, I64P, C.c_int]),
     "h2g_ctx_counters": (C.c_int, [P, I64P, C.c_int]),
     "h2g_ctx_synchronize": (C.c_int, [P]),
     "h2g_ctx_host_times": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int]),
@@ -54,6 +56,7 @@ SIGNATURES = {
                                 C.POINTER(P)]),
     "h2g_h2_destroy": (None, [P]),
     "h2g_h2_sizes": (C.c_int, [P, I64P]),
+    "h2g_h2_ranks": (C.c_int, [P, I64P, I64P]),
     "h2g_h2_structure": (C.c_int, [P, I64P, I64P, I64P, I64P, U8P]),
     "h2g_h2_download": (C.c_int, [P, P, I64P, I64P, I64P, F64P, I64P, I64P, I64P, F64P, I64P, F64P, I64P, F64P]),
     "h2g_product_tree": (C.c_int, [P, P, C.POINTER(P), I64P]),

@@ -91,6 +91,32 @@ int h2g_ctx_stage_times(h2g_ctx* ctx, double* o) {
   return 0;
 }
 
+int h2g_ctx_stage_times_ext(h2g_ctx* ctx, double* o, int n) {
+  const StageTimes& t = ctx->c.times;
+  const double v[11] = {t.setup, t.t1_row, t.t1_col, t.t1_mat, t.t2_row, t.t2_col, t.t2_mat,
+                        t.setup_col, t.t1_span, t.t2_span, t.t2_norms};
+  for (int i = 0; i < n && i < 11; ++i) o[i] = v[i];
+  return 0;
+}
+
+int h2g_ctx_mem(h2g_ctx* ctx, long long* o, int reset) {
+  return guarded([&] {
+    cudaMemPool_t pool;
+    cuda_check(cudaDeviceGetDefaultMemPool(&pool, ctx->c.device), "default pool");
+    unsigned long long v[4] = {0, 0, 0, 0};
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v[0]);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v[1]);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &v[2]);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v[3]);
+    for (int i = 0; i < 4; ++i) o[i] = (long long)v[i];
+    if (reset) {
+      unsigned long long z = 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &z);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &z);
+    }
+  });
+}
+
 int h2g_ctx_counters(h2g_ctx* ctx, long long* o, int reset) {
   o[0] = ctx->c.launches;
   o[1] = ctx->c.syncs;
@@ -343,6 +369,14 @@ int h2g_h2_sizes(h2g_h2* hh, long long* o) {
     o[5] = cl;
     o[6] = nl;
     o[7] = (long long)B.cidx.size();
+  });
+}
+
+int h2g_h2_ranks(h2g_h2* hh, long long* rr, long long* cr) {
+  return guarded([&] {
+    const H2& h = *hh->h;
+    for (size_t i = 0; i < h.rb->rank.size(); ++i) rr[i] = h.rb->rank[i];
+    for (size_t i = 0; i < h.cb->rank.size(); ++i) cr[i] = h.cb->rank[i];
   });
 }
 

@@ -194,9 +194,17 @@ struct Comm {
 };
 
 // ------------------------------------------------------------------ context: stream + staging
+// Device times (ms) in the reference harness's stage split (bench.py:195-237).  The row and column
+// passes of each phase run concurrently on two streams: t1_row / t1_col (t2_row / t2_col) are each
+// pass's own span on its stream, the *_span fields the joint span; setup = basis product + the row
+// pass's total weights, setup_col = the column pass's weights (concurrent with setup's weights);
+// t2_norms = the block norms (part of t2_row, as in the reference).
 struct StageTimes {
   float setup = 0, t1_row = 0, t1_col = 0, t1_mat = 0, t2_row = 0, t2_col = 0, t2_mat = 0;
+  float setup_col = 0, t1_span = 0, t2_span = 0, t2_norms = 0;
 };
+// event on the context's stream when timing (null otherwise)
+inline cudaEvent_t mark_event(struct Ctx& c);
 
 // Per-kernel-class accounting for the roofline (profile mode only; never inside a timed step).
 enum KClass { K_GSUM = 0, K_QR = 1, K_SVD = 2, K_NORM = 3, K_GATHER = 4, K_MV = 5, K_NCLASS = 6 };
@@ -283,6 +291,18 @@ struct Ctx {
   void ensure_read(size_t bytes);
   cudaEvent_t event();
 };
+
+inline cudaEvent_t mark_event(Ctx& c) {
+  if (!c.timing) return nullptr;
+  cudaEvent_t e = c.event();
+  cudaEventRecord(e, c.st);
+  return e;
+}
+inline float event_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  if (a && b) cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
 
 // Scoped host timer, active when the context is in timing mode.
 struct HostTimer {

@@ -832,15 +832,24 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   bool have_rf = false;
   // each pass first forms its own total weights (weights.py:60-101): Z_Y for the rows, Z_X^T for
   // the columns
+  cudaEvent_t ev_r[3] = {}, ev_c[3] = {};  // begin / weights done / end of each pass (timing mode)
   auto row_pass = [&](Ctx& c, Arena& out, Arena& scr) {
+    ev_r[0] = mark_event(c);
     MatStore rwy = basis_weights(c, scr, *y.cb);
     MatStore zy = total_weights(c, scr, Y, rwy, scaling);
-    return induced_rows(c, out, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+    ev_r[1] = mark_event(c);
+    Induced r = induced_rows(c, out, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
+    ev_r[2] = mark_event(c);
+    return r;
   };
   auto col_pass = [&](Ctx& c, Arena& out, Arena& scr) {
+    ev_c[0] = mark_event(c);
     MatStore rwx = basis_weights(c, scr, *x.rb);
     MatStore zxt = total_weights(c, scr, XT, rwx, scaling);
-    return induced_rows(c, out, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+    ev_c[1] = mark_event(c);
+    Induced r = induced_rows(c, out, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
+    ev_c[2] = mark_event(c);
+    return r;
   };
   if (serial_passes()) {  // profiling aid: deterministic single-stream launch order
     qr = row_pass(C, *keep, sc);
@@ -896,9 +905,11 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   G->own_cols = y.own_cols;
   if (C.timing) {
     C.sync();
-    C.times.setup = elapsed(e0, e1);
-    C.times.t1_row = elapsed(e1, e2);
-    C.times.t1_col = elapsed(e2, e3);
+    C.times.setup = elapsed(e0, e1) + elapsed(ev_r[0], ev_r[1]);
+    C.times.setup_col = elapsed(ev_c[0], ev_c[1]);
+    C.times.t1_row = elapsed(ev_r[1], ev_r[2]);
+    C.times.t1_col = elapsed(ev_c[1], ev_c[2]);
+    C.times.t1_span = elapsed(e1, e2);
     C.times.t1_mat = elapsed(e3, e4);
   }
   return G;

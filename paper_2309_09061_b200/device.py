@@ -53,11 +53,24 @@ class Context:
     def set_timing(self, on: bool):
         N.check(self.lib.h2g_ctx_set_timing(self.h, 1 if on else 0))
 
+    STAGES = ("t_setup", "t1_row", "t1_col", "t1_mat", "t2_row", "t2_col", "t2_mat",
+              "t_setup_col", "t1_span", "t2_span", "t2_norms")
+
     def stage_times(self) -> dict:
-        out = np.zeros(7)
-        N.check(self.lib.h2g_ctx_stage_times(self.h, out.ctypes.data_as(N.F64P)))
-        keys = ["t_setup", "t1_row", "t1_col", "t1_mat", "t2_row", "t2_col", "t2_mat"]
-        return {k: float(v) / 1e3 for k, v in zip(keys, out)}
+        """Device seconds of the last multiply / coarsen in the reference harness's stage split
+        (bench.py:195-237).  Row and column passes of a phase run concurrently on two streams:
+        t1_row / t1_col (t2_row / t2_col) are each pass's own span, t1_span / t2_span the joint one."""
+        out = np.zeros(len(self.STAGES))
+        N.check(self.lib.h2g_ctx_stage_times_ext(self.h, out.ctypes.data_as(N.F64P), len(out)))
+        return {k: float(v) / 1e3 for k, v in zip(self.STAGES, out)}
+
+    def memory(self, reset: bool = False) -> dict:
+        """Bytes of the engine's device arenas (default cudaMallocAsync pool: high-water marks since
+        the last reset; torch's allocator statistics cannot see these)."""
+        out = np.zeros(4, np.int64)
+        N.check(self.lib.h2g_ctx_mem(self.h, out.ctypes.data_as(N.I64P), 1 if reset else 0))
+        return {"used_high": int(out[0]), "used": int(out[1]), "reserved_high": int(out[2]),
+                "reserved": int(out[3])}
 
     def counters(self, reset: bool = False) -> dict:
         out = np.zeros(2, np.int64)
@@ -182,6 +195,13 @@ class DeviceH2:
         out = np.zeros(8, np.int64)
         N.check(self.ctx.lib.h2g_h2_sizes(self.h, out.ctypes.data_as(N.I64P)))
         return out
+
+    def ranks(self) -> tuple[np.ndarray, np.ndarray]:
+        """Per-cluster ranks of the row and column bases (no device work, no download)."""
+        s = self.sizes()
+        rr, cr = np.zeros(int(s[1]), np.int64), np.zeros(int(s[2]), np.int64)
+        N.check(self.ctx.lib.h2g_h2_ranks(self.h, rr.ctypes.data_as(N.I64P), cr.ctypes.data_as(N.I64P)))
+        return rr, cr
 
     @property
     def block_tree(self) -> BlockTree:
