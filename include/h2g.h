@@ -153,6 +153,83 @@ int h2g_h2_build_kernel(h2g_ctx* ctx, h2g_blocks* bt, int kernel, int dim, const
    Replaces h2mul.h2_matvec / h2_matvec_adjoint (h2.py:224-267). */
 int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, double alpha, int accumulate);
 
+/* ---------------------------------------------------------------------------------------------
+   Stage-level entry points: the reference's stage functions one call at a time, as its harness
+   times them (bench.py:195-237) and as h2mul/__init__.py:11-32 exports them.  Results are opaque
+   handles owning their device memory; each can be inspected (shapes / download) or fed to the
+   next stage.  All calls run on the context's stream and return after the stage completes.
+   --------------------------------------------------------------------------------------------- */
+typedef struct h2g_basis h2g_basis;     /* ClusterBasis (h2.py:32-72) on the device */
+typedef struct h2g_mats h2g_mats;       /* per-cluster / per-block small matrices: BasisProduct.p
+                                           (h2.py:116-124), BasisWeights.r / TotalWeights.z
+                                           (weights.py:20-34), basis_change / block_projections
+                                           (induced.py:33-46), CoarsenState.r / .z (coarsening.py:36-50) */
+typedef struct h2g_induced h2g_induced; /* InducedBasisResult (induced.py:33-46) */
+typedef struct h2g_cstate h2g_cstate;   /* CoarsenState (coarsening.py:36-50) */
+
+/* which = 0: row basis, 1: column basis of g (a view; keeps g's memory alive) */
+int h2g_h2_basis(h2g_h2* g, int which, h2g_basis** out);
+/* a basis uploaded from the packed layout (rank / leaf_off / xfer_off / data), host arrays */
+int h2g_basis_upload(h2g_ctx* ctx, h2g_tree* tree, const long long* rank, const long long* leaf_off,
+                     const long long* xfer_off, const double* data, long long len, h2g_basis** out);
+/* out2 = {clusters, packed length}; then h2g_basis_download fills rank / leaf_off / xfer_off / data */
+int h2g_basis_sizes(h2g_basis* b, long long* out2);
+int h2g_basis_download(h2g_ctx* ctx, h2g_basis* b, long long* rank, long long* leaf_off, long long* xfer_off,
+                       double* data);
+void h2g_basis_destroy(h2g_basis* b);
+
+/* n matrices (rows[i] x cols[i], row-major at data + off[i]; off[i] < 0 or an empty shape: none) */
+int h2g_mats_upload(h2g_ctx* ctx, int n, const long long* rows, const long long* cols, const long long* off,
+                    const double* data, long long len, h2g_mats** out);
+/* *n = number of entries; rows / cols (may be NULL) receive the shapes (0 x 0 where absent) */
+int h2g_mats_shapes(h2g_mats* m, int* n, long long* rows, long long* cols);
+/* packed download: off[i] = offset of entry i in data (-1 if absent), row-major */
+int h2g_mats_download(h2g_ctx* ctx, h2g_mats* m, long long* off, double* data);
+void h2g_mats_destroy(h2g_mats* m);
+
+/* cluster_basis_product(wx, vy) (h2.py:127-145): P_s = W_X,s^T V_Y,s for every cluster s */
+int h2g_cluster_basis_product(h2g_ctx* ctx, h2g_basis* wx, h2g_basis* vy, h2g_mats** out);
+/* basis_weights(w) (weights.py:37-57): R_r with W_r = Q_r R_r (R factor only) */
+int h2g_basis_weights(h2g_ctx* ctx, h2g_basis* w, h2g_mats** out);
+/* total_weights(y or y^T, rw, scaling) (weights.py:60-101): transposed = 1 condenses the columns
+   of y^T (the reference's total_weights(x.transposed(), ...)) */
+int h2g_total_weights(h2g_ctx* ctx, h2g_h2* y, int transposed, h2g_mats* rw, int scaling, h2g_mats** out);
+/* compress_induced_row_basis(x, y, zy, pxy, tol, max_rank, scale_blocks, level_decay)
+   (induced.py:76-184); max_rank < 0: none */
+int h2g_compress_induced_row_basis(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, h2g_mats* zy, h2g_mats* pxy, double tol,
+                                   int max_rank, int scale_blocks, double level_decay, h2g_induced** out);
+/* compress_induced_col_basis(x, y, zx_adjoint, pxy, ...) (induced.py:187-200) */
+int h2g_compress_induced_col_basis(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, h2g_mats* zxt, h2g_mats* pxy, double tol,
+                                   int max_rank, int scale_blocks, double level_decay, h2g_induced** out);
+/* parts of an InducedBasisResult: q (isometric basis), basis_change (per cluster, Q_t^T V_t) and
+   block_projections (per block of X's block tree, or of Y^T's for a column basis, Q_t^T X|ts V_Y,s;
+   absent for admissible leaves); any output may be NULL */
+int h2g_induced_parts(h2g_induced* r, h2g_basis** q, h2g_mats** basis_change, h2g_mats** block_projections);
+/* an InducedBasisResult from given parts (e.g. computed elsewhere); col = 1 for a column basis */
+int h2g_induced_create(h2g_ctx* ctx, h2g_basis* q, h2g_mats* basis_change, h2g_mats* block_projections, int col,
+                       h2g_induced** out);
+void h2g_induced_destroy(h2g_induced* r);
+/* assemble_product(x, y, qrow, qcol, pxy) (induced.py:220-355); T^XY built inside (trees.py:314-359) */
+int h2g_assemble_product(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, h2g_induced* qrow, h2g_induced* qcol, h2g_mats* pxy,
+                         h2g_h2** out);
+/* _coupling_norms / _nearfield_norms (coarsening.py:342-351): spectral norms of g's admissible /
+   inadmissible leaves into DEVICE arrays indexed by block id (nblocks doubles each; other entries 0) */
+int h2g_block_norms(h2g_ctx* ctx, h2g_h2* g, double* coupling_norms, double* nearfield_norms);
+/* build_coarse_row_basis / build_coarse_col_basis (coarsening.py:187-339); norms: device arrays from
+   h2g_block_norms or NULL (computed when scale_blocks) */
+int h2g_build_coarse_row_basis(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank,
+                               int scale_blocks, const double* coupling_norms, const double* nearfield_norms,
+                               h2g_cstate** out);
+int h2g_build_coarse_col_basis(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank,
+                               int scale_blocks, const double* coupling_norms, const double* nearfield_norms,
+                               h2g_cstate** out);
+/* parts of a CoarsenState: q, r (Q_t^T V_t), z (condensation weights), number of stored reps */
+int h2g_cstate_parts(h2g_cstate* s, h2g_basis** q, h2g_mats** r, h2g_mats** z, long long* nreps);
+void h2g_cstate_destroy(h2g_cstate* s);
+/* project_final(g, rowstate, colstate, coarse) (coarsening.py:354-405) */
+int h2g_project_final(h2g_ctx* ctx, h2g_h2* g, h2g_cstate* rowstate, h2g_cstate* colstate, h2g_blocks* coarse,
+                      h2g_h2** out);
+
 const char* h2g_last_error(void);
 
 #ifdef __cplusplus

@@ -22,7 +22,7 @@ __all__ = [
     "o_qr_r", "o_full_qr", "o_tsvd", "o_norm2", "o_norms2",
     "o_basis_product", "o_basis_weights", "o_total_weights",
     "o_product_tree", "o_induced_rows", "o_induced_cols", "o_assemble",
-    "o_multiply", "o_coverage", "o_coarse_rows", "o_coarse_cols",
+    "o_multiply", "o_coverage", "o_coarse_rows", "o_coarse_cols", "o_coupling_norms", "o_nearfield_norms",
     "o_project_final", "o_coarsen", "o_orthogonalize", "o_recompress",
     "o_matvec", "o_matvec_t", "o_to_dense", "o_from_packed", "o_to_packed",
     "o_spectral_norm_est", "o_relative_spectral_error",

@@ -9,7 +9,13 @@ behind the C ABI in include/h2g.h.
 from .errors import CudaError, InvalidInputError, StructureError
 from .h2 import BasisProduct, ClusterBasis, H2Matrix, expand_basis, h2_matvec_host, storage_bytes, to_dense
 from .trees import (BlockTree, ClusterTree, ColumnTree, build_block_tree, build_cluster_tree,
-                    same_cluster_tree, sparsity_constant)
+                    build_product_block_tree, same_cluster_tree, sparsity_constant)
+
+# stage-level drop-ins (stages.py; reference h2mul/__init__.py:11-32), loaded with the native library
+_STAGES = ("cluster_basis_product", "basis_weights", "total_weights", "compress_induced_row_basis",
+           "compress_induced_col_basis", "assemble_product", "build_coarse_row_basis", "build_coarse_col_basis",
+           "project_final", "coupling_norms", "nearfield_norms", "block_norms", "InducedBasisResult",
+           "CoarsenState", "BasisWeights", "TotalWeights", "DeviceBasis", "DeviceMats")
 
 __version__ = "0.1.0"
 
@@ -22,6 +28,9 @@ def __getattr__(name):
     if name in ("estimate_relative_spectral_error", "h2_matvec", "h2_matvec_adjoint"):
         from . import errest
         return getattr(errest, name)
+    if name in _STAGES:
+        from . import stages
+        return getattr(stages, name)
     if name in ("Context", "DeviceH2", "default_context"):
         from . import device
         return getattr(device, name)

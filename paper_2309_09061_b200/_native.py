@@ -65,6 +65,33 @@ SIGNATURES = {
     "h2g_coarsen": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
     "h2g_coarsen_prefetch": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, F64P, C.c_longlong, C.POINTER(P)]),
     "h2g_recompress": (C.c_int, [P, P, C.c_double, C.c_int, C.POINTER(P)]),
+    # stage-level entry points (include/h2g.h)
+    "h2g_h2_basis": (C.c_int, [P, C.c_int, C.POINTER(P)]),
+    "h2g_basis_upload": (C.c_int, [P, P, I64P, I64P, I64P, F64P, C.c_longlong, C.POINTER(P)]),
+    "h2g_basis_sizes": (C.c_int, [P, I64P]),
+    "h2g_basis_download": (C.c_int, [P, P, I64P, I64P, I64P, F64P]),
+    "h2g_basis_destroy": (None, [P]),
+    "h2g_mats_upload": (C.c_int, [P, C.c_int, I64P, I64P, I64P, F64P, C.c_longlong, C.POINTER(P)]),
+    "h2g_mats_shapes": (C.c_int, [P, C.POINTER(C.c_int), I64P, I64P]),
+    "h2g_mats_download": (C.c_int, [P, P, I64P, F64P]),
+    "h2g_mats_destroy": (None, [P]),
+    "h2g_cluster_basis_product": (C.c_int, [P, P, P, C.POINTER(P)]),
+    "h2g_basis_weights": (C.c_int, [P, P, C.POINTER(P)]),
+    "h2g_total_weights": (C.c_int, [P, P, C.c_int, P, C.c_int, C.POINTER(P)]),
+    "h2g_compress_induced_row_basis": (C.c_int, [P, P, P, P, P, C.c_double, C.c_int, C.c_int, C.c_double,
+                                                 C.POINTER(P)]),
+    "h2g_compress_induced_col_basis": (C.c_int, [P, P, P, P, P, C.c_double, C.c_int, C.c_int, C.c_double,
+                                                 C.POINTER(P)]),
+    "h2g_induced_parts": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
+    "h2g_induced_create": (C.c_int, [P, P, P, P, C.c_int, C.POINTER(P)]),
+    "h2g_induced_destroy": (None, [P]),
+    "h2g_assemble_product": (C.c_int, [P, P, P, P, P, P, C.POINTER(P)]),
+    "h2g_block_norms": (C.c_int, [P, P, P, P]),
+    "h2g_build_coarse_row_basis": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, P, P, C.POINTER(P)]),
+    "h2g_build_coarse_col_basis": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, P, P, C.POINTER(P)]),
+    "h2g_cstate_parts": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P), I64P]),
+    "h2g_cstate_destroy": (None, [P]),
+    "h2g_project_final": (C.c_int, [P, P, P, P, P, C.POINTER(P)]),
     "h2g_last_error": (C.c_char_p, []),
 }
 

@@ -9,42 +9,9 @@
 
 using namespace h2g;
 
-struct h2g_ctx {
-  Ctx c;
-  h2g_ctx(int dev, cudaStream_t s) : c(dev, s) {}
-};
-struct h2g_tree {
-  std::shared_ptr<Tree> t;
-};
-struct h2g_blocks {
-  std::shared_ptr<Blocks> b;
-  std::shared_ptr<Tree> rows, cols;
-};
-struct h2g_h2 {
-  std::shared_ptr<H2> h;
-};
+#include "capi_handles.h"
 
-static thread_local std::string g_err;
-
-template <class F>
-static int guarded(F&& f) {
-  try {
-    f();
-    return 0;
-  } catch (const InvalidInput& e) {
-    g_err = e.what();
-    return 1;
-  } catch (const StructureErr& e) {
-    g_err = e.what();
-    return 2;
-  } catch (const CudaFailure& e) {
-    g_err = e.what();
-    return 3;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return 2;
-  }
-}
+thread_local std::string g_err;
 
 extern "C" {
 
@@ -233,7 +200,9 @@ int h2g_blocks_create(h2g_ctx*, h2g_tree* rows, h2g_tree* cols, int nb, const lo
 
 void h2g_blocks_destroy(h2g_blocks* b) { delete b; }
 
-static std::shared_ptr<Basis> upload_basis(Ctx& C, Arena& ar, const Tree* tree, const long long* rank,
+}  // extern "C"
+
+std::shared_ptr<Basis> upload_basis(Ctx& C, Arena& ar, const Tree* tree, const long long* rank,
                                            const long long* loff, const long long* xoff, const double* data,
                                            long long len) {
   auto B = std::make_shared<Basis>();
@@ -257,6 +226,8 @@ static std::shared_ptr<Basis> upload_basis(Ctx& C, Arena& ar, const Tree* tree, 
   }
   return B;
 }
+
+extern "C" {
 
 static int upload_impl(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, const long long* rb_loff,
                        const long long* rb_xoff, const double* rb_data, long long rb_len, const long long* cb_rank,
@@ -395,41 +366,9 @@ int h2g_h2_structure(h2g_h2* hh, long long* row, long long* col, long long* cptr
   });
 }
 
-struct Gather {
-  std::vector<long long> items;  // src, n, dst-offset (patched to absolute)
-  long long total = 0;
-  void add(const double* src, long long n) {
-    if (n <= 0) return;
-    items.push_back((long long)src);
-    items.push_back(n);
-    items.push_back(total);
-    total += n;
-  }
-  // as run(), but only the ranges `runs` of the packed layout are copied to the host
-  void run_runs(Ctx& C, Arena& ar, double* host, const std::vector<std::pair<long long, long long>>& runs) {
-    if (total == 0 || items.empty()) return;
-    double* d = ar.alloc(total);
-    for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(d + items[i]);
-    long long* di = C.push(items);
-    C.flush();
-    cuda_check(launch_gather(di, (int)(items.size() / 3), C.st), "gather");
-    for (auto& r : runs)
-      cuda_check(cudaMemcpyAsync(host + r.first, d + r.first, (r.second - r.first) * sizeof(double),
-                                 cudaMemcpyDeviceToHost, C.st),
-                 "download");
-  }
-  void run(Ctx& C, Arena& ar, double* host) {
-    if (total == 0) return;
-    double* d = ar.alloc(total);
-    for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(d + items[i]);
-    long long* di = C.push(items);
-    C.flush();
-    cuda_check(launch_gather(di, (int)(items.size() / 3), C.st), "gather");
-    cuda_check(cudaMemcpyAsync(host, d, total * sizeof(double), cudaMemcpyDeviceToHost, C.st), "download");
-  }
-};
+}  // extern "C"
 
-static void pack_basis(const Basis& B, long long* rank, long long* loff, long long* xoff, Gather& g) {
+void pack_basis(const Basis& B, long long* rank, long long* loff, long long* xoff, Gather& g) {
   const Tree& tr = *B.tree;
   for (int t = 0; t < tr.n; ++t) {
     rank[t] = B.rank[t];
@@ -447,6 +386,8 @@ static void pack_basis(const Basis& B, long long* rank, long long* loff, long lo
       g.add(B.xfer[t], (long long)B.rank[t] * B.rank[tr.parent[t]]);
     }
 }
+
+extern "C" {
 
 int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_loff, long long* rb_xoff,
                     double* rb_data, long long* cb_rank, long long* cb_loff, long long* cb_xoff, double* cb_data,

@@ -26,6 +26,18 @@ void cuda_check(cudaError_t e, const char* what) {
 // ============================================================================ infrastructure
 
 Arena::~Arena() {
+  if (cross_stream && free_st) {
+    for (cudaStream_t s : after) {
+      if (!s || s == free_st) continue;
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) continue;
+      cudaEventRecord(e, s);
+      cudaStreamWaitEvent(free_st, e, 0);
+      cudaEventDestroy(e);
+    }
+    for (void* p : chunks) cudaFreeAsync(p, free_st);
+    return;
+  }
   if (cross_stream) {
     cudaDeviceSynchronize();
     for (void* p : chunks) cudaFree(p);
@@ -251,6 +263,16 @@ void Ctx::join_side(Ctx& S) {
   }
   for (auto& kv : S.htime) htime["side." + kv.first] += kv.second;
   S.htime.clear();
+}
+
+void Ctx::order_free(Arena& a) {
+  a.cross_stream = true;
+  a.free_st = st;
+  a.after.clear();
+  a.after.push_back(a.st);
+  if (side_) a.after.push_back(side_->st);
+  if (aux_) a.after.push_back(aux_->st);
+  if (up_stream) a.after.push_back(up_stream);
 }
 
 cudaEvent_t Ctx::event() {

@@ -106,6 +106,10 @@ struct BView {
 struct Arena {  // bump allocator over cudaMalloc'd chunks, freed together
   cudaStream_t st = nullptr;
   bool cross_stream = false;  // used by other streams too: free after a device-wide sync
+  // cross-stream arenas with a free stream: freed stream-ordered on free_st after everything queued
+  // so far on the `after` streams (no device-wide synchronisation; see Ctx::order_free)
+  cudaStream_t free_st = nullptr;
+  std::vector<cudaStream_t> after;
   std::vector<void*> chunks;
   char* cur = nullptr;
   size_t left = 0;
@@ -290,6 +294,9 @@ struct Ctx {
   }
   void ensure_read(size_t bytes);
   cudaEvent_t event();
+  // a cross-stream arena of this context's product: free it on the main stream after the work
+  // queued on every stream of the context (main, side, auxiliary, uploads) at destruction time
+  void order_free(Arena& a);
 };
 
 inline cudaEvent_t mark_event(Ctx& c) {
@@ -552,5 +559,27 @@ std::shared_ptr<H2> build_kernel_h2(Ctx& C, std::shared_ptr<const Blocks> bt, in
                                     long long basis_len, const long long* node_off, const double* nodes,
                                     long long nodes_len);
 std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank);
+
+// ------------------------------------------------------------------ stage-level entry points
+// The reference's stage functions one call at a time (bench.py:195-237 times them individually):
+// results own their device arenas and can be inspected or fed to the next stage.
+struct InducedStage {  // InducedBasisResult (induced.py:33-46) of a row (T = false) or column pass
+  Induced ind;
+  ArenaPtr ar;
+  std::vector<ArenaPtr> keep;
+  bool T = false;
+};
+std::shared_ptr<InducedStage> induced_stage(Ctx& C, const H2& x, const H2& y, const MatStore& z, const MatStore& P,
+                                            bool col, double tol, int max_rank, bool scale, double level_decay);
+std::shared_ptr<H2> assemble_stage(Ctx& C, const H2& x, const H2& y, const InducedStage& qr, const InducedStage& qc,
+                                   const MatStore& P, std::vector<ArenaPtr> keep);
+struct CoarseStage;  // CoarsenState (coarsening.py:36-50), phase2.cu
+std::shared_ptr<CoarseStage> coarse_basis_stage(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, bool col,
+                                                double tol, int max_rank, bool scale, const double* d_cn,
+                                                const double* d_nn);
+void block_norms_stage(Ctx& C, const H2& g, double* d_cn, double* d_nn);
+std::shared_ptr<H2> project_final_stage(Ctx& C, const H2& g, const CoarseStage& rs, const CoarseStage& cs,
+                                        std::shared_ptr<const Blocks> coarse);
+std::shared_ptr<Basis> coarse_stage_basis(const CoarseStage& s, MatStore* r, MatStore* z, ArenaPtr* ar, int* nreps);
 
 }  // namespace h2g

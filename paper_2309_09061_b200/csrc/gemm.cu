@@ -7,7 +7,12 @@
 // shared memory, then T*D.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
+
+#ifndef GSUM_PIPE_MINB
+#define GSUM_PIPE_MINB 2
+#endif
 
 #include "h2g_types.h"
 
@@ -226,6 +231,269 @@ __global__ void __launch_bounds__(kThr, 2) gsum_mma_kernel(const GOut* __restric
       }
 }
 
+
+// ================================================================================================
+// gsum_pipe_kernel: the same contract, restructured for the FP64 tensor pipe's latency.
+//   * operands stream through a 3-stage shared-memory ring filled by cp.async (8-byte copies along
+//     the operand's contiguous dimension, zero-fill outside the tile), so two 16-wide k chunks are
+//     in flight while the third is multiplied -- no register prefetch, no spills;
+//   * the ring runs across the terms of a run (consecutive 2-factor terms into C, or the grouped
+//     nf = 4 / 5 terms into their intermediate), so the pipeline does not drain at term boundaries;
+//   * each operand keeps its memory order in shared memory ([i][k] for k-contiguous, [k][i] for
+//     i-contiguous views, strides == 4 mod 16 doubles: conflict-free DMMA fragment loads), so
+//     transposed views (column passes) load coalesced too;
+//   * intermediates (3-factor T, grouped T / U) are read by the fragment loads in place from Ts.
+// ================================================================================================
+namespace {
+
+constexpr int kPS = 3;                 // pipeline stages
+constexpr int kLdKc = kKC + 4;         // [i][k] stride (20)
+constexpr int kLdIc = kT + 4;          // [k][i] stride (68)
+constexpr int kStg = kT * kLdKc;       // doubles per operand stage (>= kKC * kLdIc)
+static_assert(kStg >= kKC * kLdIc, "stage size");
+
+struct StageMeta {
+  int aI, aK, bK, bJ;  // fragment strides of the staged (or direct) operands
+  int kc4;             // k steps of 4 in this chunk
+  int skipA, skipB;    // operand read directly from smem (offset in doubles into Ts), else -1
+  int pad_;
+  double alpha;
+};
+
+// One product of a run: acc += alpha * A[ai0 .. ai0+mr, 0:k] * B[0:k, bj0 .. bj0+nc]
+struct Job {
+  MatRef a, b;
+  int k;
+  double alpha;
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// Issue the copies of one chunk (k columns kk .. kk+kc of A's rows ai0.., rows kk.. of B's columns
+// bj0..) into one stage; `direct` operands (Ts) are not copied.
+__device__ __forceinline__ void issue_chunk(const Job& J, int ai0, int mr, int bj0, int nc, int kk, double* sA,
+                                            double* sB, bool dirA, bool dirB, StageMeta* meta,
+                                            int offA, int offB, int ldT) {
+  const int tid = threadIdx.x;
+  const int kc = min(kKC, J.k - kk);
+  const bool aK = J.a.cs == 1;  // A row-major (k contiguous)
+  const bool bN = J.b.cs == 1;  // B row-major (j contiguous)
+  if (!dirA) {
+    if (aK) {
+#pragma unroll
+      for (int q = 0; q < kT * kKC / kThr; ++q) {
+        const int e = tid + q * kThr, i = e / kKC, l = e % kKC;
+        const bool v = i < mr && l < kc;
+        cp_async8(sA + i * kLdKc + l, v ? J.a.p + (long long)(ai0 + i) * J.a.rs + (kk + l) : J.a.p, v);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kT * kKC / kThr; ++q) {
+        const int e = tid + q * kThr, l = e / kT, i = e % kT;
+        const bool v = i < mr && l < kc;
+        cp_async8(sA + l * kLdIc + i,
+                  v ? J.a.p + (long long)(ai0 + i) * J.a.rs + (long long)(kk + l) * J.a.cs : J.a.p, v);
+      }
+    }
+  }
+  if (!dirB) {
+    if (bN) {
+#pragma unroll
+      for (int q = 0; q < kT * kKC / kThr; ++q) {
+        const int e = tid + q * kThr, l = e / kT, j = e % kT;
+        const bool v = j < nc && l < kc;
+        cp_async8(sB + l * kLdIc + j, v ? J.b.p + (long long)(kk + l) * J.b.rs + (bj0 + j) : J.b.p, v);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kT * kKC / kThr; ++q) {
+        const int e = tid + q * kThr, j = e / kKC, l = e % kKC;
+        const bool v = j < nc && l < kc;
+        cp_async8(sB + j * kLdKc + l,
+                  v ? J.b.p + (long long)(kk + l) * J.b.rs + (long long)(bj0 + j) * J.b.cs : J.b.p, v);
+      }
+    }
+  }
+  if (tid == 0) {
+    StageMeta m;
+    if (dirA) { m.aI = ldT; m.aK = 1; m.skipA = offA + kk; } else { m.aI = aK ? kLdKc : 1; m.aK = aK ? 1 : kLdIc; m.skipA = -1; }
+    if (dirB) { m.bK = ldT; m.bJ = 1; m.skipB = offB + kk * ldT; } else { m.bK = bN ? kLdIc : 1; m.bJ = bN ? 1 : kLdKc; m.skipB = -1; }
+    m.kc4 = (kc + 3) >> 2;
+    m.pad_ = 0;
+    m.alpha = J.alpha;
+    *meta = m;
+  }
+}
+
+// One run of products into one accumulator, pipelined across all chunks of all its jobs.
+// getjob(j) returns job j (k = 0 jobs are skipped); rows ai0.. (mr valid) of every A, columns
+// bj0.. (nc valid) of every B; dirA / dirB: A / B read in place from Ts (+offA / +offB).
+template <class GetJob>
+__device__ void run_stream(Acc& acc, int njobs, GetJob getjob, int ai0, int mr, int bj0, int nc, bool dirA,
+                           bool dirB, int offA, int offB, double* ring, StageMeta* metas, const double* Ts,
+                           int ldT) {
+  // chunk count
+  int total = 0;
+  for (int j = 0; j < njobs; ++j) total += (getjob(j).k + kKC - 1) / kKC;
+  if (total == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = warp_row0(), wc = warp_col0();
+  const bool live = wr < mr && wc < nc;
+  // producer cursor
+  int pj = 0, pk = 0;
+  Job PJ = getjob(0);
+  while (PJ.k == 0) PJ = getjob(++pj);
+  auto produce = [&](int c) {
+    if (c < total) {
+      const int s = c % kPS;
+      issue_chunk(PJ, ai0, mr, bj0, nc, pk, ring + s * 2 * kStg, ring + s * 2 * kStg + kStg, dirA, dirB, metas + s,
+                  offA, offB, ldT);
+      pk += kKC;
+      if (pk >= PJ.k) {
+        pk = 0;
+        if (c + 1 < total) {
+          do { PJ = getjob(++pj); } while (PJ.k == 0);
+        }
+      }
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int c = 0; c < kPS - 1; ++c) produce(c);
+  for (int c = 0; c < total; ++c) {
+    cp_wait<kPS - 2>();
+    __syncthreads();
+    produce(c + kPS - 1);
+    const int s = c % kPS;
+    const StageMeta m = metas[s];
+    if (live) {
+      const double* sA = m.skipA >= 0 ? Ts + m.skipA : ring + s * 2 * kStg;
+      const double* sB = m.skipB >= 0 ? Ts + m.skipB : ring + s * 2 * kStg + kStg;
+      const bool scale = m.alpha != 1.0;
+      for (int q = 0; q < m.kc4; ++q) {
+        const int k = 4 * q + t4;
+        double a[kRT], b[kCT];
+#pragma unroll
+        for (int r = 0; r < kRT; ++r) a[r] = sA[(wr + r * 8 + g) * m.aI + k * m.aK];
+#pragma unroll
+        for (int cc = 0; cc < kCT; ++cc) b[cc] = sB[k * m.bK + (wc + cc * 8 + g) * m.bJ];
+        if (scale) {
+#pragma unroll
+          for (int r = 0; r < kRT; ++r) a[r] *= m.alpha;
+        }
+#pragma unroll
+        for (int r = 0; r < kRT; ++r)
+#pragma unroll
+          for (int cc = 0; cc < kCT; ++cc) dmma(acc.v[r][cc], a[r], b[cc]);
+      }
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();  // the ring (and metas) are reused by the next run
+}
+
+}  // namespace
+
+template <int Tag>
+__global__ void __launch_bounds__(kThr, GSUM_PIPE_MINB) gsum_pipe_kernel(const GOut* __restrict__ outs,
+                                                          const GTerm* __restrict__ terms,
+                                                          const GTile* __restrict__ tiles, int k2max) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ StageMeta metas[kPS];
+  double* ring = smem;                       // kPS x (A stage | B stage)
+  double* Ts = ring + kPS * 2 * kStg;        // 64 x ldT
+  const int ldT = k2max + 4;
+  const GTile tl = tiles[blockIdx.x];
+  const GOut o = outs[tl.out];
+  const int i0 = (tl.tij & 0xffff) * kT, j0 = (tl.tij >> 16) * kT;
+  const int mt = min(kT, o.m - i0), nt = min(kT, o.n - j0);
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = warp_row0(), wc = warp_col0();
+  if (k2max > 0)  // intermediates are read in place: keep their unwritten padding finite
+    for (int e = threadIdx.x; e < kT * ldT; e += kThr) Ts[e] = 0.0;
+  Acc acc, aux;
+  acc.zero();
+  auto single = [](Job J) { return [J](int) { return J; }; };
+  int ti = o.t0;
+  while (ti < o.t1) {
+    const GTerm t = terms[ti];
+    if (t.nf == 0) { ++ti; continue; }  // no-op (triple assembled by another launch)
+    // the run of consecutive terms with this nf (2, 4 and 5 accumulate into one target)
+    int te = ti + 1;
+    if (t.nf == 2 || t.nf == 4 || t.nf == 5)
+      while (te < o.t1 && (terms[te].nf == t.nf || terms[te].nf == 0)) ++te;
+    const int nrun = te - ti;
+    const GTerm* run = terms + ti;
+    auto getjob = [run](int j) {
+      const GTerm u = run[j];
+      return Job{u.a, u.b, u.nf == 0 ? 0 : u.k, u.alpha};
+    };
+    if (t.nf == 1) {
+#pragma unroll
+      for (int r = 0; r < kRT; ++r)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+            if (i < mt && j < nt) acc.v[r][c][h] += t.alpha * ld(t.a, i0 + i, j0 + j);
+          }
+    } else if (t.nf == 2) {
+      run_stream(acc, nrun, getjob, i0, mt, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT);
+    } else if (t.nf == 4) {  // T (mt x ka) = sum A B, then C += T * da
+      aux.zero();
+      run_stream(aux, nrun, getjob, i0, mt, 0, o.ka, false, false, 0, 0, ring, metas, Ts, ldT);
+      acc_to_smem(aux, Ts, ldT, kT, o.ka);
+      __syncthreads();
+      run_stream(acc, 1, single(Job{MatRef{Ts, ldT, 1}, o.da, o.ka, 1.0}), 0, mt, j0, nt, true, false, 0, 0, ring,
+                 metas, Ts, ldT);
+    } else if (t.nf == 5) {  // U (kb x nt) = sum A B, then C += ab * U
+      aux.zero();
+      run_stream(aux, nrun, getjob, 0, o.kb, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT);
+      acc_to_smem(aux, Ts, ldT, o.kb, kT);
+      __syncthreads();
+      run_stream(acc, 1, single(Job{o.ab, MatRef{Ts, ldT, 1}, o.kb, 1.0}), i0, mt, 0, nt, false, true, 0, 0, ring,
+                 metas, Ts, ldT);
+    } else {  // nf = 3: T = alpha A[i0.., :] B (mt x k2) in Ts, 64 columns at a time, then C += T D
+      for (int js = 0; js < t.k2; js += kT) {
+        aux.zero();
+        const int ns = min(kT, t.k2 - js);
+        run_stream(aux, 1, single(Job{t.a, MatRef{t.b.p + (long long)js * t.b.cs, t.b.rs, t.b.cs}, t.k, t.alpha}),
+                   i0, mt, 0, ns, false, false, 0, 0, ring, metas, Ts, ldT);
+        acc_to_smem(aux, Ts + js, ldT, kT, ns);
+      }
+      __syncthreads();
+      run_stream(acc, 1, single(Job{MatRef{Ts, ldT, 1}, t.d, t.k2, 1.0}), 0, mt, j0, nt, true, false, 0, 0, ring,
+                 metas, Ts, ldT);
+    }
+    ti = te;
+  }
+#pragma unroll
+  for (int r = 0; r < kRT; ++r)
+#pragma unroll
+    for (int c = 0; c < kCT; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+        if (i < mt && j < nt) {
+          double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+          *dst = (o.beta ? *dst : 0.0) + acc.v[r][c][h];
+        }
+      }
+}
+
+size_t gsum_pipe_smem(int k2max) {
+  return sizeof(double) * ((size_t)kPS * 2 * kStg + (k2max > 0 ? (size_t)kT * (k2max + 4) : 0));
+}
+
 size_t gsum_mma_smem(int k2max) {
   return sizeof(double) * ((size_t)kT * kLdA + (size_t)kKC * kLdB + (k2max > 0 ? (size_t)kT * (k2max + 4) : 0));
 }
@@ -234,14 +502,21 @@ cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* t
                             cudaStream_t st, int tag) {
   static std::once_flag once;
   std::call_once(once, [] {
-    for (const void* fn : {(const void*)gsum_mma_kernel<0>, (const void*)gsum_mma_kernel<1>}) {
+    for (const void* fn : {(const void*)gsum_mma_kernel<0>, (const void*)gsum_mma_kernel<1>,
+                           (const void*)gsum_pipe_kernel<0>, (const void*)gsum_pipe_kernel<1>}) {
       cudaFuncAttributes fa;
       cudaFuncGetAttributes(&fa, fn);
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
   });
+  static const bool v1 = getenv("H2G_GSUM_V1") != nullptr;  // previous kernel, for A/B
   if (ntiles == 0) return cudaSuccess;
+  if (!v1) {
+    if (tag == 1) gsum_pipe_kernel<1><<<ntiles, kThr, gsum_pipe_smem(k2max), st>>>(outs, terms, tiles, k2max);
+    else gsum_pipe_kernel<0><<<ntiles, kThr, gsum_pipe_smem(k2max), st>>>(outs, terms, tiles, k2max);
+    return cudaGetLastError();
+  }
   if (tag == 1) gsum_mma_kernel<1><<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
   else gsum_mma_kernel<0><<<ntiles, kThr, gsum_mma_smem(k2max), st>>>(outs, terms, tiles, k2max);
   return cudaGetLastError();

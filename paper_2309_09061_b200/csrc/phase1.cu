@@ -857,7 +857,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   } else {
     Ctx& S = C.side();
     keep2->st = S.st;
-    keep2->cross_stream = true;
+    C.order_free(*keep2);
     std::exception_ptr err;
     std::thread th([&] {
       try {
@@ -895,6 +895,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     HostTimer ht(C, "product_tree_wait");
     pt = pt_future.get();
   }
+  if (pt.early.near) C.order_free(*pt.early.near);
   StageTag taga(C, "p1.asm");
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt, have_rf ? &rf : nullptr);
   if (A) C.join_side(*A);  // counters / profile of the auxiliary stream's work
@@ -912,6 +913,56 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     C.times.t1_span = elapsed(e1, e2);
     C.times.t1_mat = elapsed(e3, e4);
   }
+  return G;
+}
+
+// ------------------------------------------------------------------ stage-level entry points
+// compress_induced_row_basis (induced.py:76-184) with z = Z_Y and P = P_XY, or
+// compress_induced_col_basis (induced.py:187-200: the row algorithm on Y^T X^T) with z = Z_X^T.
+std::shared_ptr<InducedStage> induced_stage(Ctx& C, const H2& x, const H2& y, const MatStore& z, const MatStore& P,
+                                            bool col, double tol, int max_rank, bool scale, double level_decay) {
+  if (!x.bt->cols->same(*y.bt->rows)) throw InvalidInput("x and y do not share the middle cluster tree");
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  wait_near(C, x);
+  wait_near(C, y);
+  auto out = std::make_shared<InducedStage>();
+  out->ar = std::make_shared<Arena>(C.st);
+  out->T = col;
+  if ((int)z.size() != x.bt->cols->n) throw InvalidInput("total weights do not match the middle cluster tree");
+  if ((int)P.size() != x.bt->cols->n) throw InvalidInput("basis product does not match the middle cluster tree");
+  if (!col)
+    out->ind = induced_rows(C, *out->ar, HView{&x, false}, HView{&y, false}, z, PRef{&P, false}, tol, max_rank, scale,
+                            level_decay);
+  else
+    out->ind = induced_rows(C, *out->ar, HView{&y, true}, HView{&x, true}, z, PRef{&P, true}, tol, max_rank, scale,
+                            level_decay);
+  C.sync();
+  return out;
+}
+
+// assemble_product (induced.py:220-355): T^XY built here (trees.py:314-359), every term on the GPU.
+std::shared_ptr<H2> assemble_stage(Ctx& C, const H2& x, const H2& y, const InducedStage& qr, const InducedStage& qc,
+                                   const MatStore& P, std::vector<ArenaPtr> keep) {
+  if (!x.bt->cols->same(*y.bt->rows)) throw InvalidInput("x and y do not share the middle cluster tree");
+  if (qr.T || !qc.T) throw InvalidInput("assemble_product needs an induced row basis and an induced column basis");
+  if (qr.ind.q->tree != x.bt->rows || qc.ind.q->tree != y.bt->cols)
+    throw InvalidInput("induced bases live on other cluster trees");
+  wait_near(C, x);
+  wait_near(C, y);
+  PTree pt = product_tree(BView{x.bt.get(), false}, BView{y.bt.get(), false});
+  ptree_prepare(pt, C, *x.bt, y.bt->nb);
+  // assemble() memoises the leaf products it needs in the Induced it is given (scratch memory):
+  // work on copies so the stage results stay reusable
+  Induced r = qr.ind, c = qc.ind;
+  auto G = assemble(C, HView{&x, false}, HView{&y, false}, r, c, PRef{&P, false}, pt, nullptr);
+  G->owned.push_back(qr.ar);
+  G->owned.push_back(qc.ar);
+  for (auto& a : qr.keep) G->owned.push_back(a);
+  for (auto& a : qc.keep) G->owned.push_back(a);
+  for (auto& a : keep) G->owned.push_back(a);
+  G->own_rows = x.own_rows;
+  G->own_cols = y.own_cols;
+  C.sync();
   return G;
 }
 

@@ -996,7 +996,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   } else {
     Ctx& S = C.side();
     ar2->st = S.st;
-    ar2->cross_stream = true;
+    C.order_free(*ar2);
     std::exception_ptr err;
     std::thread th([&] {
       try {
@@ -1157,6 +1157,83 @@ std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank) {
   }
   gb.run(C);
   return coarsen(C, o, g.bt, tol, max_rank, true);
+}
+
+// ------------------------------------------------------------------ stage-level entry points
+struct CoarseStage {
+  CState st;
+  ArenaPtr ar;
+  bool T = false;
+  const H2* g = nullptr;
+  std::shared_ptr<const Blocks> coarse;
+};
+
+void block_norms_stage(Ctx& C, const H2& g, double* d_cn, double* d_nn) {
+  wait_near(C, g);
+  Arena sc(C.st);
+  all_norms(C, sc, g, d_cn, d_nn);
+  C.sync();
+}
+
+// build_coarse_row_basis / build_coarse_col_basis (coarsening.py:187-339): one pass, on G (col =
+// false) or G^T with the transposed coarse tree (col = true).  Norms: given device arrays (per block
+// of G) or, with scale_blocks and none given, computed here (coarsening.py:342-351).
+std::shared_ptr<CoarseStage> coarse_basis_stage(Ctx& C, const H2& g, std::shared_ptr<const Blocks> coarse, bool col,
+                                                double tol, int max_rank, bool scale, const double* d_cn,
+                                                const double* d_nn) {
+  if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+  wait_near(C, g);
+  auto out = std::make_shared<CoarseStage>();
+  out->ar = std::make_shared<Arena>(C.st);
+  out->T = col;
+  out->g = &g;
+  out->coarse = coarse;
+  const BView gv{g.bt.get(), col}, cv{coarse.get(), col};
+  const CPrep prep = prep_rows(gv, cv);
+  Arena sc(C.st);
+  if (scale && (!d_cn || !d_nn)) {
+    double* cn = sc.alloc(std::max(1, g.bt->nb));
+    double* nn = sc.alloc(std::max(1, g.bt->nb));
+    all_norms(C, sc, g, cn, nn);
+    if (!d_cn) d_cn = cn;
+    if (!d_nn) d_nn = nn;
+  }
+  out->st = coarse_rows(C, *out->ar, HView{&g, col}, cv, tol, max_rank, scale, d_cn, d_nn, prep);
+  C.sync();
+  return out;
+}
+
+// project_final (coarsening.py:354-405) from the two pass states of the same G and coarse tree.
+std::shared_ptr<H2> project_final_stage(Ctx& C, const H2& g, const CoarseStage& rs, const CoarseStage& cs,
+                                        std::shared_ptr<const Blocks> coarse) {
+  if (rs.T || !cs.T) throw InvalidInput("project_final needs a row state and a column state");
+  if (rs.g != &g || cs.g != &g) throw InvalidInput("the coarsen states belong to another product");
+  if (rs.coarse.get() != coarse.get() || cs.coarse.get() != coarse.get())
+    throw InvalidInput("the coarsen states were built for another coarse block tree");
+  wait_near(C, g);
+  CState& r = const_cast<CState&>(rs.st);  // read only (states stay reusable)
+  CState& c = const_cast<CState&>(cs.st);
+  const ProjPlan plan = plan_project(HView{&g, false}, r, *coarse);
+  auto ar = std::make_shared<Arena>(C.st);
+  auto Z = project_final(C, HView{&g, false}, r, c, coarse, ar, plan);
+  Z->owned.push_back(rs.ar);
+  Z->owned.push_back(cs.ar);
+  Z->own_rows = g.own_rows;
+  Z->own_cols = g.own_cols;
+  C.sync();
+  return Z;
+}
+
+std::shared_ptr<Basis> coarse_stage_basis(const CoarseStage& s, MatStore* r, MatStore* z, ArenaPtr* ar, int* nreps) {
+  if (r) *r = s.st.r;
+  if (z) *z = s.st.z;
+  if (ar) *ar = s.ar;
+  if (nreps) {
+    int n = 0;
+    for (const auto& rep : s.st.reps) n += rep.t != nullptr;
+    *nreps = n;
+  }
+  return s.st.q;
 }
 
 }  // namespace h2g

@@ -270,6 +270,25 @@ class DeviceH2:
         """Host H2Matrix with the reference's container interface."""
         return unpack_h2(self.to_packed(), rows=self.rows, cols=self.cols)
 
+    # stage-level views (stages.py): bases as DeviceBasis, the transposed view for total_weights
+    @property
+    def row_basis(self):
+        from .stages import DeviceBasis
+        h = N.P()
+        N.check(self.ctx.lib.h2g_h2_basis(self.h, 0, C.byref(h)))
+        return DeviceBasis(self.ctx, h, self.rows, self)
+
+    @property
+    def col_basis(self):
+        from .stages import DeviceBasis
+        h = N.P()
+        N.check(self.ctx.lib.h2g_h2_basis(self.h, 1, C.byref(h)))
+        return DeviceBasis(self.ctx, h, self.cols, self)
+
+    def transposed(self):
+        from .stages import transposed
+        return transposed(self)
+
     @property
     def shape(self) -> tuple[int, int]:
         return (int(self.rows.stop[0] - self.rows.start[0]), int(self.cols.stop[0] - self.cols.start[0]))

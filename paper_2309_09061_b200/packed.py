@@ -66,6 +66,13 @@ def _pack_basis(basis, p, out):
     out[p + "data"] = data
 
 
+def pack_basis_arrays(basis):
+    """(rank, leaf_off, xfer_off, data) of one basis in the packed layout."""
+    out = {}
+    _pack_basis(basis, "", out)
+    return out["rank"], out["leaf_off"], out["xfer_off"], out["data"]
+
+
 def _unpack_basis(d, p, tree) -> ClusterBasis:
     rank = [int(v) for v in d[p + "rank"]]
     data = d[p + "data"]
