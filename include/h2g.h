@@ -48,6 +48,13 @@ int h2g_ctx_set_timing(h2g_ctx* ctx, int on);
 typedef int (*h2g_allgather_fn)(void* user, int channel, void* dbuf, const long long* off, int nseg,
                                 void* stream);
 int h2g_ctx_set_comm(h2g_ctx* ctx, int rank, int size, h2g_allgather_fn fn, void* user);
+/* Optional variable all-to-all for the partitioned product (replaces h2mul's nothing: SURVEY 8(e)
+   halo / transpose exchanges): rank i sends bytes [soff[j], soff[j+1]) of sbuf to rank j and
+   receives rank j's bytes into [roff[j], roff[j+1]) of rbuf, device buffers ordered on `stream`;
+   returns 0 on success.  Without it, those exchanges fall back to the all-gather. */
+typedef int (*h2g_alltoall_fn)(void* user, int channel, const void* sbuf, const long long* soff, void* rbuf,
+                               const long long* roff, int nseg, void* stream);
+int h2g_ctx_set_alltoall(h2g_ctx* ctx, h2g_alltoall_fn fn, void* user);
 /* ms per stage of the last multiply / coarsen: setup, t1_row, t1_col, t1_mat, t2_row, t2_col, t2_mat
    (the reference harness's stage split, bench.py:195-237) */
 int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);

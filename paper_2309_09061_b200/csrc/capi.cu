@@ -43,11 +43,20 @@ int h2g_ctx_set_comm(h2g_ctx* ctx, int rank, int size, h2g_allgather_fn fn, void
   return guarded([&] {
     if (size < 1 || rank < 0 || rank >= size) throw InvalidInput("rank outside [0, size)");
     if (size > 1 && !fn) throw InvalidInput("a partitioned product needs an all-gather function");
-    ctx->c.comm = Comm{rank, size, (AllgatherFn)fn, user};
+    const Comm prev = ctx->c.comm;
+    ctx->c.comm = Comm{rank, size, (AllgatherFn)fn, user, prev.a2a, prev.a2a_user};
     if (ctx->c.side_) {
       ctx->c.side_->comm = ctx->c.comm;
       ctx->c.side_->channel = 1;
     }
+  });
+}
+
+int h2g_ctx_set_alltoall(h2g_ctx* ctx, h2g_alltoall_fn fn, void* user) {
+  return guarded([&] {
+    ctx->c.comm.a2a = (AlltoallFn)fn;
+    ctx->c.comm.a2a_user = user;
+    if (ctx->c.side_) ctx->c.side_->comm = ctx->c.comm;
   });
 }
 

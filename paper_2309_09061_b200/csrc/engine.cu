@@ -95,6 +95,10 @@ Ctx::~Ctx() {
   for (auto e : evpool) cudaEventDestroy(e);
   cudaFreeHost(hstage);
   cudaFree(dstage);
+  for (auto& r : retired) {
+    cudaFreeHost(r.first);
+    cudaFree(r.second);
+  }
   if (hread) cudaFreeHost(hread);
   if (own_stream) cudaStreamDestroy(st);
 }
@@ -122,6 +126,11 @@ void Ctx::sync() {
   }
   stage_off = 0;
   stage_flushed = 0;
+  for (auto& r : retired) {  // staging buffers retired by an overflow: consumed now
+    cudaFreeHost(r.first);
+    cudaFree(r.second);
+  }
+  retired.clear();
   ++syncs;
   if (!pending.empty()) drain_prof();
 }
@@ -177,14 +186,16 @@ void Ctx::drain_prof() {
 void* Ctx::stage(const void* src, size_t bytes) {
   const size_t need = (bytes + 255) & ~size_t(255);
   if (stage_off + need > stage_cap) {
-    sync();  // flushes and drains: the whole buffer is free again
-    if (need > stage_cap) {
-      cudaFreeHost(hstage);
-      cudaFree(dstage);
-      stage_cap = std::max(need, stage_cap * 2);
-      cuda_check(cudaMallocHost(&hstage, stage_cap), "cudaMallocHost");
-      cuda_check(cudaMalloc(&dstage, stage_cap), "cudaMalloc stage");
-    }
+    // The buffer is full, but earlier pushes of the launch being prepared may still sit in it
+    // (their device pointers are already handed out): never recycle it here.  Flush it, retire it
+    // (freed at the next host sync, once the stream has consumed it) and continue in a new one.
+    flush();
+    retired.emplace_back(hstage, dstage);
+    stage_cap = std::max(need, stage_cap * 2);
+    cuda_check(cudaMallocHost(&hstage, stage_cap), "cudaMallocHost");
+    cuda_check(cudaMalloc(&dstage, stage_cap), "cudaMalloc stage");
+    stage_off = 0;
+    stage_flushed = 0;
   }
   char* h = hstage + stage_off;
   char* d = dstage + stage_off;
@@ -457,6 +468,14 @@ static bool gram_prot_path(int n) {
 static bool gram_qr_path(int n, long long M) {
   static const bool off = getenv("H2G_NO_GRAM_QR") != nullptr;
   return !off && gram_path(0, n, M);
+}
+
+// H2G_DEFER_OUT=1: the finish kernel writes U and Q_t = Q_V [[I, 0], [0, U]] is one batched GEMM
+// (explicit Q_V from svd_prep_kernel for every protected item).  Measured slower at c4 (the explicit
+// Q_V costs more than the in-kernel reflector application saves), so off by default.
+static bool defer_out() {
+  static const bool on = getenv("H2G_DEFER_OUT") != nullptr;
+  return on;
 }
 
 static bool tile_path(int n) {
@@ -788,6 +807,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
       it.nchunk = (int)std::max<long long>(1, (it.N + per - 1) / per);
       it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
       it.q2 = it.kx > 0 ? scratch.alloc((size_t)it.m * it.m) : nullptr;
+      if (it.q2 && n > 0 && defer_out()) it.u_out = scratch.alloc((size_t)n * n);
       if (it.kx > 0) {
         prep_ids.push_back((int)live.size());
         const size_t full = svd_prep_smem(it.m, it.kx, true);
@@ -813,6 +833,15 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
     it.nchunk = (int)std::max<long long>(1, (it.N + kChunkCols - 1) / kChunkCols);
     it.rbuf = n > 0 ? scratch.alloc((size_t)it.nchunk * n * n) : nullptr;
     if (svd_tsqr_smem(it.m, it.kx, true) > kSmemLimit || merge_smem(n, true) > kSmemLimit) rsmem = false;
+    if (it.kx > 0 && n > 0 && defer_out()) {
+      // explicit Q_V (svd_prep_kernel) so that the output is one GEMM instead of k1 sequential
+      // reflector applications per column inside the finish kernel
+      it.q2 = scratch.alloc((size_t)it.m * it.m);
+      it.u_out = scratch.alloc((size_t)n * n);
+      prep_ids.push_back((int)live.size());
+      const size_t full = svd_prep_smem(it.m, it.kx, true);
+      sm_prep = std::max(sm_prep, full <= kSmemLimit ? full : svd_prep_smem(it.m, it.kx, false));
+    }
     live.push_back(it);
   }
   if (live.empty()) return ranks;
@@ -890,6 +919,25 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   ++C.launches;
   C.prof_end(K_SVD, ev, fl, by);
   ranks = C.read(d_rank, items.size());
+  {  // deferred outputs: Q_t = [Q_V[:, :k1] | Q_V[:, k1:] U] (m x kt), one grouped GEMM
+    GBatch qo;
+    for (const SvdItem& it : live) {
+      if (!it.u_out) continue;
+      const int kt = ranks[it.rank_out - d_rank];
+      const int k1 = std::min(it.m, it.kx), n = it.m - k1, k2 = kt - k1;
+      if (k1 > 0) {
+        qo.out(Mat{it.q_out, it.m, k1}, false);
+        qo.outs.back().ldc = kt;
+        qo.t1(MatRef{it.q2, it.m, 1});
+      }
+      if (k2 > 0) {
+        qo.out(Mat{it.q_out + k1, it.m, k2}, false);
+        qo.outs.back().ldc = kt;
+        qo.t2(MatRef{it.q2 + k1, it.m, 1}, MatRef{it.u_out, n, 1}, n);
+      }
+    }
+    if (!qo.empty()) qo.run(C);
+  }
   if (dbg_sweeps) {
     std::vector<int> sw = C.read(d_sw, live.size() * 8);
     int mx = 0, mxn = 0;
@@ -1490,9 +1538,14 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
       }
     }
   g.run(C);
+  std::vector<double> nrm;
   if (scaling) {
     nbatch.scratch = &ar;
     nbatch.run_async(C);
+    // exactly-zero blocks are not rows of the reference's stack (weights.py:86-89): the factor's
+    // row count min(M, k) -- which sets the column counts (and so the eps * max(rows, cols) floor)
+    // of the SVD inputs built from these weights -- counts the nonzero blocks only
+    nrm = C.read(d_nrm, (size_t)std::max(1, nb));
   }
   MatStore Z(tr.n);
   for (int lev = 0; lev <= tr.depth; ++lev) {
@@ -1513,6 +1566,7 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
         M += ze.r;
       }
       for (int b : adm_of[s]) {
+        if (scaling && nrm[b] == 0.0) continue;
         q.sl.add(Tb[b].ref(), Tb[b].r, 1.0, scaling ? d_nrm + b : nullptr);
         M += Tb[b].r;
       }

@@ -190,10 +190,17 @@ struct HView {
 // (torch.distributed over NCCL in production, gloo with host staging in tests); `channel` 0 / 1 keeps
 // the concurrent row / column passes on separate communicators.
 typedef int (*AllgatherFn)(void* user, int channel, void* dbuf, const long long* off, int nseg, void* stream);
+// Variable all-to-all: rank i sends bytes [soff[j], soff[j+1]) of sbuf to rank j and receives rank j's
+// bytes into [roff[j], roff[j+1]) of rbuf (device buffers, stream-ordered).  Optional: without it the
+// engine falls back to all-gathers (every rank then receives every exchanged block).
+typedef int (*AlltoallFn)(void* user, int channel, const void* sbuf, const long long* soff, void* rbuf,
+                          const long long* roff, int nseg, void* stream);
 struct Comm {
   int rank = 0, size = 1;
   AllgatherFn fn = nullptr;
   void* user = nullptr;
+  AlltoallFn a2a = nullptr;
+  void* a2a_user = nullptr;
   bool on() const { return size > 1 && fn != nullptr; }
 };
 
@@ -226,6 +233,7 @@ struct Ctx {
   // pinned host staging and device staging for descriptors (reset at every host sync)
   char* hstage = nullptr;
   char* dstage = nullptr;
+  std::vector<std::pair<char*, char*>> retired;  // full staging buffers awaiting the next sync
   size_t stage_cap = 0, stage_off = 0, stage_flushed = 0;
   char* hread = nullptr;  // pinned read-back area
   size_t read_cap = 0;
@@ -521,6 +529,16 @@ struct XItem {
   double** dst;
 };
 void exchange(Ctx& C, Arena& ar, const std::vector<XItem>& items);
+// Point-to-point exchange: `len` doubles produced by rank `src` are needed by rank `dst` (src != dst);
+// every rank lists the same items in the same order.  On dst, *ptr is set to the received copy
+// (allocated from `ar`); on src, *ptr is the source.  One all-to-all (Comm::a2a), or an all-gather
+// when the host supplied none.
+struct PItem {
+  int src, dst;
+  long long len;
+  double** ptr;
+};
+void exchange_p2p(Ctx& C, Arena& ar, const std::vector<PItem>& items);
 // Integer per-cluster values (ranks): v[t] for the listed clusters is taken from owner[t].
 void exchange_ints(Ctx& C, const Part& part, const std::vector<int>& ids, std::vector<int>& v);
 

@@ -105,11 +105,26 @@ __device__ __forceinline__ long long pidx(int i, int j, int m) {  // packed uppe
 }  // namespace
 
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* __restrict__ items,
-                                                                const Seg* __restrict__ segs,
-                                                                const GramWork* __restrict__ work) {
-  __shared__ __align__(16) double Pa[kGP][kGT + 2];
-  __shared__ __align__(16) double Pb[kGP][kGT + 2];
+// Panels stream through a kGStages-deep shared-memory ring filled by cp.async (8-byte copies,
+// consecutive lanes = consecutive panel columns, zero-fill outside the tile / chunk): while a panel
+// is multiplied the next ones are in flight, so the FP64 pipe does not wait at the panel barrier
+// for the global loads.  Each thread scales the entries it copied (fl(sc * x), as the staged
+// values were formed before) once its copies have landed.
+constexpr int kGStages = 3;
+constexpr int kGLd = kGT + 2;
+__host__ __device__ constexpr size_t gram_partial_smem() {
+  return sizeof(double) * (size_t)kGStages * 2 * kGP * kGLd;
+}
+
+__device__ __forceinline__ void g_cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+
+__global__ void __launch_bounds__(kGThr, 2) gram_dd_partial_kernel(const GramItem* __restrict__ items,
+                                                                   const Seg* __restrict__ segs,
+                                                                   const GramWork* __restrict__ work) {
+  extern __shared__ __align__(16) double gring[];  // kGStages x {Pa, Pb} x [kGP][kGLd]
   __shared__ long long s_off[kGSeg];
   __shared__ const double* s_p[kGSeg];
   __shared__ int s_rs[kGSeg], s_cs[kGSeg];
@@ -120,8 +135,6 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* 
   const int m = it.m;
   const int ia = w.ti * kGT, jb = w.tj * kGT;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kGThr / 32;
-  // active 4 x 4 blocks of this tile only (upper triangle on a diagonal tile), replicated over
-  // interleaved panel columns when the set is small
   const bool diag = w.ti == w.tj;
   const int nbi = (min(kGT, m - ia) + 3) / 4, nbj = (min(kGT, m - jb) + 3) / 4;
   const int nblk = diag ? nbi * (nbi + 1) / 2 : nbi * nbj;
@@ -140,7 +153,6 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* 
   double hi[16], lo[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0.0;
-  // the chunk's segment descriptors, staged once (two binary searches)
   if (tid == 0) {
     const int a = gfind_seg(segs, it.s0, it.s1, w.c0);
     const int b = gfind_seg(segs, it.s0, it.s1, w.c1 - 1);
@@ -159,12 +171,17 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* 
       s_cs[q] = it.hcols ? sg.a.cs : sg.a.rs;  // line stride
       s_sc[q] = gseg_scale(sg);
     }
-  for (long long c0 = w.c0; c0 < w.c1; c0 += kGP) {
-    __syncthreads();  // previous panel consumed (and the descriptors staged)
-    {
-      // lane = panel column (row-major sources: consecutive lanes read consecutive addresses),
-      // warps over the tile's rows
-      const long long c = c0 + lane;
+  __syncthreads();
+  const long long npan = (w.c1 - w.c0 + kGP - 1) / kGP;
+  // this thread's copies: column `lane` of the panel, rows warp, warp + nw, ...
+  auto stage_a = [&](int s) { return gring + (size_t)s * 2 * kGP * kGLd; };
+  auto stage_b = [&](int s) { return gring + (size_t)s * 2 * kGP * kGLd + kGP * kGLd; };
+  static_assert(kGStages == 3, "scale registers");
+  double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0;  // scale of this thread's column per stage (registers)
+  auto issue = [&](long long p) {
+    if (p < npan) {
+      const int s = (int)(p % kGStages);
+      const long long c = w.c0 + p * kGP + lane;
       const double* col = nullptr;
       long long rs = 0;
       double sc = 0.0;
@@ -185,19 +202,47 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* 
           sc = gseg_scale(sg);
         }
       }
+      if (s == 0) sc0 = sc; else if (s == 1) sc1 = sc; else sc2 = sc;
+      double* Pa = stage_a(s);
+      double* Pb = stage_b(s);
+      const double* dummy = segs[it.s0].a.p;
       for (int r = warp; r < kGT; r += nw) {
         const int ra = ia + r, rb = jb + r;
-        Pa[lane][r] = (col && ra < m) ? sc * col[(long long)ra * rs] : 0.0;
-        if (w.ti != w.tj) Pb[lane][r] = (col && rb < m) ? sc * col[(long long)rb * rs] : 0.0;
+        const bool va = col && ra < m;
+        g_cp_async8(&Pa[lane * kGLd + r], va ? col + (long long)ra * rs : dummy, va);
+        if (!diag) {
+          const bool vb = col && rb < m;
+          g_cp_async8(&Pb[lane * kGLd + r], vb ? col + (long long)rb * rs : dummy, vb);
+        }
       }
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;");
+  };
+#pragma unroll
+  for (int p = 0; p < kGStages - 1; ++p) issue(p);
+  for (long long p = 0; p < npan; ++p) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 2));
+    {  // scale the entries this thread copied: fl(sc * x)
+      const int s = (int)(p % kGStages);
+      const double sc = s == 0 ? sc0 : (s == 1 ? sc1 : sc2);
+      double* Pa = stage_a(s);
+      double* Pb = stage_b(s);
+      for (int r = warp; r < kGT; r += nw) {
+        Pa[lane * kGLd + r] *= sc;
+        if (!diag) Pb[lane * kGLd + r] *= sc;
+      }
+    }
+    __syncthreads();  // panel p visible to all; every thread is past panel p - 1
+    issue(p + kGStages - 1);
     if (act) {
+      const int s = (int)(p % kGStages);
+      const double* Pa = stage_a(s);
+      const double* Pbb = diag ? Pa : stage_b(s);
 #pragma unroll 2
-      for (int p = rep; p < kGP; p += reps) {
-        const double2 a01 = *reinterpret_cast<const double2*>(&Pa[p][4 * bi]);
-        const double2 a23 = *reinterpret_cast<const double2*>(&Pa[p][4 * bi + 2]);
-        const double* pb = w.ti != w.tj ? &Pb[p][0] : &Pa[p][0];
+      for (int q0 = rep; q0 < kGP; q0 += reps) {
+        const double2 a01 = *reinterpret_cast<const double2*>(&Pa[q0 * kGLd + 4 * bi]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&Pa[q0 * kGLd + 4 * bi + 2]);
+        const double* pb = Pbb + q0 * kGLd;
         const double2 b01 = *reinterpret_cast<const double2*>(pb + 4 * bj);
         const double2 b23 = *reinterpret_cast<const double2*>(pb + 4 * bj + 2);
         const double a[4] = {a01.x, a01.y, a23.x, a23.y};
@@ -209,14 +254,15 @@ __global__ void __launch_bounds__(kGThr) gram_dd_partial_kernel(const GramItem* 
             const int q = 4 * u + v;
             const double pr = a[u] * b[v];
             const double pe = fma(a[u], b[v], -pr);
-            double s, e;
-            two_sum(hi[q], pr, s, e);
-            hi[q] = s;
+            double s2, e;
+            two_sum(hi[q], pr, s2, e);
+            hi[q] = s2;
             lo[q] += e + pe;
           }
       }
     }
   }
+  asm volatile("cp.async.wait_group 0;");
   if (!act) return;
   double* gh = it.gpart + (size_t)(w.chunk * reps + rep) * 2 * m * m;
   double* gl = gh + (size_t)m * m;
@@ -404,8 +450,10 @@ cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* 
     cudaFuncGetAttributes(&fa, (const void*)gram_chol_kernel);
     cudaFuncSetAttribute((const void*)gram_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024 - (int)fa.sharedSizeBytes);
+    cudaFuncSetAttribute((const void*)gram_dd_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)gram_partial_smem());
   });
-  if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, 0, st>>>(items, segs, work);
+  if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, gram_partial_smem(), st>>>(items, segs, work);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nitems == 0) return e;
   gram_chol_kernel<<<nitems, mmax <= 64 ? 256 : kCThr, gram_chol_smem(mmax), st>>>(items);

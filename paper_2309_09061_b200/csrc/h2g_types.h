@@ -95,6 +95,8 @@ struct SvdItem {
   double* q2;       // tile path with kx > 0: explicit Q_V (m x m), written by svd_prep_kernel
   double* gpart;    // Gram path (kx = 0): nchunk x {hi, lo} x (m x m) partial double-double Grams
   int* pre_nr;      // Gram path: rows of the pivoted-Cholesky factor in rbuf (the finish skips QRCP)
+  double* u_out;    // deferred output (kx > 0, n > 0, q2 set): the finish writes U (n x k2, ld n) and
+                    // the host forms Q_t = [Q_V[:, :k1] | Q_V[:, k1:] U] as one batched GEMM afterwards
 };
 
 // Gram CTAs of a small item (m <= 64, one 64 x 64 tile) run `reps` replicas of its 4 x 4 block set

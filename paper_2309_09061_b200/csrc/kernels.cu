@@ -1028,7 +1028,15 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
   __syncthreads();
   const int kt = k1 + k2;
   double* Q = it.q_out;  // m x kt
-  if (it.q2) {
+  if (it.u_out && k1 > 0 && n > 0) {
+    // deferred output: U = normalised rows of R1 in singular order, mapped back through the column
+    // pivoting; Q_t = Q_V [[I, 0], [0, U]] is one batched GEMM on the host's next launch
+    for (long long e = threadIdx.x; e < (long long)n * k2; e += blockDim.x) {
+      const int l = (int)(e / k2), j = (int)(e % k2);
+      const int src = ord[j];
+      it.u_out[(long long)l * n + j] = R[(long long)src * ld + iperm[l]] / sig[src];
+    }
+  } else if (it.q2) {
     // explicit Q_V from svd_prep_kernel: Q_t = [Q_V[:, :k1] | Q_V[:, k1:] U], U = normalised rows of
     // R1 (singular order) mapped back through the column pivoting -- one small product instead of
     // k1 sequential reflector applications per column

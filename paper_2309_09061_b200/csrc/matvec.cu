@@ -22,13 +22,37 @@ namespace {
 constexpr int kMvThreads = 256;
 
 // One warp per term (terms of an output are spread over the CTA's warps, no barriers between
-// them); lanes own rows (lane, lane + 32, ...) and stream k with four independent partial sums.
-// Row-contiguous blocks are re-read from L1 (a 64 x 64 block is 32 KB), column-contiguous ones
-// are coalesced.  Each warp accumulates into its own shared-memory row buffer; the buffers are
-// summed in warp order at the end, so the result does not depend on scheduling.
+// them).  Row-major blocks (k contiguous, the nearfield / coupling blocks of G and Z): 8 lanes per
+// row, 4 rows per warp step, each lane striding k by 8 -- every warp load covers four 64-byte row
+// segments (full sectors), partial sums joined by 3 butterflies.  Column-major views (transposed
+// blocks, adjoint): lanes own rows, so consecutive lanes read consecutive addresses.  Each warp
+// accumulates into its own shared-memory row buffer; the buffers are summed in warp order at the
+// end, so the result does not depend on scheduling.
 __device__ void mv_term_warp(const MvTerm& t, int m, double* acc) {
   const int lane = threadIdx.x & 31;
   const MatRef a = t.a;
+  if (a.cs == 1 && t.k >= 8) {
+    const int grp = lane >> 3, gl = lane & 7;
+    for (int i0 = 0; i0 < m; i0 += 4) {
+      const int i = i0 + grp;
+      double s0 = 0.0, s1 = 0.0;
+      if (i < m) {
+        const double* row = a.p + (long long)i * a.rs;
+        int j = gl;
+        for (; j + 8 < t.k; j += 16) {
+          s0 = fma(row[j], t.x[j], s0);
+          s1 = fma(row[j + 8], t.x[j + 8], s1);
+        }
+        if (j < t.k) s0 = fma(row[j], t.x[j], s0);
+      }
+      double s = s0 + s1;
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (gl == 0 && i < m) acc[i] += t.alpha * s;
+    }
+    return;
+  }
   for (int i = lane; i < m; i += 32) {
     const double* row = a.p + (long long)i * a.rs;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;

@@ -707,8 +707,14 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
   HostTimer ht3(C, "assemble_pushdown");
   StageTag tagp(C, "p1.push");
+  struct Expansion {
+    int ch;
+    Mat part;
+  };
+  static const bool exp3 = getenv("H2G_EXPAND_3F") != nullptr;  // previous one-launch form (A/B)
   for (int lev = 0; lev < B.depth; ++lev) {
     GBatch g1, g2;
+    std::vector<Expansion> exps;
     for (int b : B.by_level[lev]) {
       if (B.leaf(b)) continue;
       const int t = B.row[b], r = B.col[b];
@@ -724,8 +730,12 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
           Mat part{sc.alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
           g1.out(part, false);
           emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
-          g2.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
-          g2.t3(Q.leafm(t2).ref(), part.ref(), W.leafm(r2).tref(), Q.rank[t2], W.rank[r2]);
+          if (exp3) {
+            g2.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
+            g2.t3(Q.leafm(t2).ref(), part.ref(), W.leafm(r2).tref(), Q.rank[t2], W.rank[r2]);
+          } else {
+            exps.push_back(Expansion{ch, part});
+          }
         } else {
           g1.out(cp[ch], true);
           emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
@@ -733,8 +743,36 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       }
     }
     g1.run(C);
-    if (!g2.outs.empty()) wait_dense();
+    if (!g2.outs.empty() || !exps.empty()) wait_dense();
     g2.run(C);
+    // expansion into the inadmissible children, N += Q_leaf(t2) (part W_leaf(r2)^T) as two
+    // 2-factor launches: T = Q_leaf part once per target (a 3-factor term recomputes it for every
+    // 64-column tile of the target and pads its middle dimension to 64), then N += T W_leaf^T.
+    // Chunked so the intermediates stay within a bounded scratch (freed stream-ordered per chunk).
+    constexpr size_t kExpBudget = size_t(1) << 27;  // doubles (1 GiB) of intermediates per chunk
+    for (size_t e0 = 0; e0 < exps.size();) {
+      size_t need = 0, e1 = e0;
+      for (; e1 < exps.size(); ++e1) {
+        const int ch = exps[e1].ch;
+        const size_t sz = (size_t)rows.size(B.row[ch]) * W.rank[B.col[ch]];
+        if (e1 > e0 && need + sz > kExpBudget) break;
+        need += sz;
+      }
+      Arena ta(C.st);
+      GBatch ga, gb;
+      for (size_t e = e0; e < e1; ++e) {
+        const int ch = exps[e].ch;
+        const int t2 = B.row[ch], r2 = B.col[ch];
+        const Mat Tm{ta.alloc((size_t)rows.size(t2) * W.rank[r2]), rows.size(t2), W.rank[r2]};
+        ga.out(Tm, false);
+        ga.t2(Q.leafm(t2).ref(), exps[e].part.ref(), Q.rank[t2]);
+        gb.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
+        gb.t2(Tm.ref(), W.leafm(r2).tref(), W.rank[r2]);
+      }
+      ga.run(C);
+      gb.run(C);
+      e0 = e1;
+    }
   }
   wait_dense();
   if (pt.dev.block) {  // after the main stream has waited for the dense targets' expansion

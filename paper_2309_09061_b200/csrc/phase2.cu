@@ -303,7 +303,11 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   Arena sc(C.st);
   double* d_msc = sc.alloc(std::max(1, pt.nb));  // sigma_1 of merged reps, per block
 
-  // top-down condensation weights Z_t (coarsening.py:231-245)
+  // top-down condensation weights Z_t (coarsening.py:231-245).  Exactly-zero couplings are not
+  // rows of the reference's stack (coarsening.py:237-241): their norms are read back once so that
+  // the factor's row count min(M, k) -- the column count of the SVD inputs built from Z -- matches
+  std::vector<double> cn_host;
+  if (scale) cn_host = C.read(d_cn, (size_t)std::max(1, pt.nb));  // coupling norms: main-stream work
   std::vector<int> Lp;
   for (int lev = 0; lev <= tr.depth; ++lev) {
     StageTag tag(C, "p2.Z.L" + std::to_string(lev));
@@ -325,8 +329,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
         M += ze.r;
       }
       for (int b : row_adm[t]) {
-        // S_tr^T / ||S_tr||_2 with the norm as a device divisor; an exactly-zero coupling (skipped
-        // by coarsening.py:239-241) adds zero rows, which leave the stack's Gram unchanged
+        // S_tr^T / ||S_tr||_2 with the norm as a device divisor
+        if (scale && cn_host[b] == 0.0) continue;
         const int kc = w1.rank[pv.col(b)];
         qb.sl.add(trn(g.coup(b)), kc, 1.0, scale ? d_cn + b : nullptr);
         M += kc;
@@ -930,6 +934,15 @@ static NearPrefetch prefetch_near(Ctx& C, const H2& g, const Blocks& cbk, double
   cudaEventDestroy(e);
   cuda_check(launch_gather(di, (int)npf, C.up_stream), "gather(prefetch)");
   ++C.launches;
+  {  // the gather reads its descriptors from C's staging buffer, which C.sync() recycles: order the
+     // main stream after the gather so that no later host sync can hand the buffer out while the
+     // copy stream has not yet consumed it (the D2H copies below stay asynchronous)
+    cudaEvent_t g;
+    cuda_check(cudaEventCreateWithFlags(&g, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(g, C.up_stream), "event");
+    cuda_check(cudaStreamWaitEvent(C.st, g, 0), "wait");
+    cudaEventDestroy(g);
+  }
   for (int b = 0; b < cbk.nb;) {  // one copy per run of consecutive prefetched blocks
     if (!P.mask[b]) { ++b; continue; }
     const long long lo = zoff[b];

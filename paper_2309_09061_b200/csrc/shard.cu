@@ -84,6 +84,61 @@ void exchange(Ctx& C, Arena& ar, const std::vector<XItem>& items) {
     if (items[i].owner != me) *items[i].dst = pos[i];
 }
 
+void exchange_p2p(Ctx& C, Arena& ar, const std::vector<PItem>& items) {
+  if (!C.comm.on() || items.empty()) return;
+  const int P = C.comm.size, me = C.comm.rank;
+  if (!C.comm.a2a) {  // no all-to-all: every rank receives every item
+    std::vector<XItem> x;
+    x.reserve(items.size());
+    for (const PItem& it : items) x.push_back(XItem{it.src, it.len, it.ptr});
+    exchange(C, ar, x);
+    return;
+  }
+  std::vector<long long> soff(P + 1, 0), roff(P + 1, 0);
+  for (const PItem& it : items) {
+    if (it.src < 0 || it.src >= P || it.dst < 0 || it.dst >= P || it.src == it.dst)
+      throw StructureErr("exchange_p2p: item without a valid source and destination");
+    if (it.src == me) soff[it.dst + 1] += it.len;
+    if (it.dst == me) roff[it.src + 1] += it.len;
+  }
+  for (int i = 0; i < P; ++i) {
+    soff[i + 1] += soff[i];
+    roff[i + 1] += roff[i];
+  }
+  double* sbuf = soff[P] > 0 ? ar.alloc(soff[P]) : nullptr;
+  double* rbuf = roff[P] > 0 ? ar.alloc(roff[P]) : nullptr;
+  std::vector<long long> srun(soff.begin(), soff.end() - 1), rrun(roff.begin(), roff.end() - 1), g;
+  std::vector<std::pair<double**, double*>> recv;
+  for (const PItem& it : items) {
+    if (it.src == me && it.len > 0) {
+      if (!*it.ptr) throw StructureErr("exchange_p2p: item to send was not computed");
+      g.push_back((long long)*it.ptr);
+      g.push_back(it.len);
+      g.push_back((long long)(sbuf + srun[it.dst]));
+      srun[it.dst] += it.len;
+    }
+    if (it.dst == me) {
+      recv.emplace_back(it.ptr, rbuf + rrun[it.src]);
+      rrun[it.src] += it.len;
+    }
+  }
+  if (!g.empty()) {  // pack the outgoing blocks, grouped by destination
+    long long* di = C.push(g);
+    C.flush();
+    cuda_check(launch_gather(di, (int)(g.size() / 3), C.st), "gather(exchange_p2p)");
+    ++C.launches;
+  }
+  C.flush();
+  std::vector<long long> sb(P + 1), rb(P + 1);
+  for (int i = 0; i <= P; ++i) {
+    sb[i] = soff[i] * (long long)sizeof(double);
+    rb[i] = roff[i] * (long long)sizeof(double);
+  }
+  if (C.comm.a2a(C.comm.a2a_user, C.channel, sbuf, sb.data(), rbuf, rb.data(), P, C.st) != 0)
+    throw CudaFailure("all-to-all of the partitioned results failed");
+  for (auto& r : recv) *r.first = r.second;
+}
+
 void exchange_ints(Ctx& C, const Part& part, const std::vector<int>& ids, std::vector<int>& v) {
   if (!C.comm.on() || !part.on() || ids.empty()) return;
   const int P = C.comm.size, me = C.comm.rank;

@@ -6,7 +6,8 @@ import numpy as np
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CONFIG_CASES = ["c1", "c2", "c3", "c4", "c5"]
-RANDOM_CASES = ["rand_s0_tol1e-3", "rand_s1_tol0", "rand_s2_2d", "rand_s3_2d_tol0"]
+RANDOM_CASES = ["rand_s0_tol1e-3", "rand_s1_tol0", "rand_s2_2d", "rand_s3_2d_tol0", "rand_s5_zero_coup",
+                "rand_s6_zero_coup_tol0"]
 
 
 def load(name):
