@@ -63,8 +63,10 @@ int h2g_ctx_stage_times(h2g_ctx* ctx, double* out7);
    t*_row / t*_col is its own stream span, t*_span the joint span) */
 int h2g_ctx_stage_times_ext(h2g_ctx* ctx, double* out, int n);
 /* device memory of the engine's arenas (the device's default cudaMallocAsync pool), bytes:
-   out4 = {used high-water, used now, reserved high-water, reserved now}; reset: restart the marks */
-int h2g_ctx_mem(h2g_ctx* ctx, long long* out4, int reset);
+   out6 = {pool used high-water, used now, reserved high-water, reserved now, arena payload
+   high-water, payload now} (payload: bytes handed out by the process's arenas, without the 64 MB
+   chunk granularity); reset: restart the high-water marks */
+int h2g_ctx_mem(h2g_ctx* ctx, long long* out6, int reset);
 /* kernel launches and host synchronisations since the last reset: out2 = {launches, syncs} */
 int h2g_ctx_counters(h2g_ctx* ctx, long long* out2, int reset);
 int h2g_ctx_synchronize(h2g_ctx* ctx);

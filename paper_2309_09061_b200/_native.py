@@ -35,6 +35,7 @@ SIGNATURES = {
     "h2g_ctx_stage_times": (C.c_int, [P, F64P]),
     "h2g_ctx_stage_times_ext": (C.c_int, [P, F64P, C.c_int]),
     "h2g_ctx_mem": (C.c_int, [P, I64P, C.c_int]),
+    "h2g_ctx_set_alltoall": (C.c_int, [P, P, P]),
     "h2g_ctx_counters": (C.c_int, [P, I64P, C.c_int]),
     "h2g_ctx_synchronize": (C.c_int, [P]),
     "h2g_ctx_host_times": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int]),

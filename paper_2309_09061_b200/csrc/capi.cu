@@ -85,10 +85,13 @@ int h2g_ctx_mem(h2g_ctx* ctx, long long* o, int reset) {
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &v[2]);
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v[3]);
     for (int i = 0; i < 4; ++i) o[i] = (long long)v[i];
+    o[4] = g_arena_payload_high.load();
+    o[5] = g_arena_payload.load();
     if (reset) {
       unsigned long long z = 0;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &z);
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &z);
+      g_arena_payload_high = g_arena_payload.load();
     }
   });
 }
@@ -403,6 +406,7 @@ int h2g_h2_download(h2g_ctx* ctx, h2g_h2* hh, long long* rb_rank, long long* rb_
                     long long* coup_off, double* coup_data, long long* near_off, double* near_data) {
   return guarded([&] {
     Ctx& C = ctx->c;
+    gather_rows(C, *hh->h);  // a partitioned product: complete it first
     const H2& h = *hh->h;
     const Blocks& B = *h.bt;
     wait_near(C, h);
@@ -494,12 +498,15 @@ int h2g_h2_build_kernel(h2g_ctx* ctx, h2g_blocks* bt, int kernel, int dim, const
 int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, double alpha, int accumulate) {
   return guarded([&] {
     if (!x || !y) throw InvalidInput("matvec: null vector");
+    gather_rows(ctx->c, *g->h);  // a partitioned product: complete it first
     h2_matvec(ctx->c, HView{g->h.get(), trans != 0}, x, y, alpha, accumulate != 0);
   });
 }
 
 int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, int scaling, h2g_h2** g) {
   return guarded([&] {
+    need_whole(ctx->c, *x->h);
+    need_whole(ctx->c, *y->h);
     auto G = multiply(ctx->c, *x->h, *y->h, tol, max_rank, scaling != 0);
     G->keep.push_back(x->h->bt);
     G->keep.push_back(y->h->bt);
@@ -517,6 +524,7 @@ int h2g_coarsen(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max
 int h2g_coarsen_prefetch(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, int max_rank, int scale_blocks,
                          double* near_host, long long near_len, h2g_h2** z) {
   return guarded([&] {
+    need_rows_halo(ctx->c, *g->h);
     auto Z = coarsen(ctx->c, *g->h, coarse->b, tol, max_rank, scale_blocks != 0, near_host, near_len);
     Z->keep.push_back(coarse->rows);
     Z->keep.push_back(coarse->cols);
@@ -531,6 +539,7 @@ int h2g_coarsen_prefetch(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol
 int h2g_recompress(h2g_ctx* ctx, h2g_h2* x, double tol, int max_rank, h2g_h2** z) {
   return guarded([&] {
     if (tol < 0) throw InvalidInput("tolerance must be >= 0");
+    need_whole(ctx->c, *x->h);
     auto Z = recompress(ctx->c, *x->h, tol, max_rank);
     Z->keep.push_back(x->h->bt);
     Z->keep.push_back(x->h->own_rows);

@@ -155,6 +155,7 @@ int h2g_total_weights(h2g_ctx* ctx, h2g_h2* y, int transposed, h2g_mats* rw, int
     need(y, "y");
     need(rw, "rw");
     Ctx& C = ctx->c;
+    need_whole(C, *y->h);
     const H2& h = *y->h;
     const HView v{&h, transposed != 0};
     if ((int)rw->m.size() != v.cols().n) throw InvalidInput("basis weights do not match the column cluster tree");
@@ -173,6 +174,8 @@ static int induced_impl(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, h2g_mats* z, h2g_mat
     need(y, "y");
     need(z, "total weights");
     need(pxy, "pxy");
+    need_whole(ctx->c, *x->h);
+    need_whole(ctx->c, *y->h);
     auto s = induced_stage(ctx->c, *x->h, *y->h, z->m, pxy->m, col, tol, max_rank, scale != 0, level_decay);
     s->keep.insert(s->keep.end(), z->keep.begin(), z->keep.end());
     s->keep.insert(s->keep.end(), pxy->keep.begin(), pxy->keep.end());
@@ -237,6 +240,8 @@ int h2g_assemble_product(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, h2g_induced* qrow, 
     need(qcol, "qcol");
     need(pxy, "pxy");
     if ((int)pxy->m.size() != x->h->bt->cols->n) throw InvalidInput("pxy does not match the middle cluster tree");
+    need_whole(ctx->c, *x->h);
+    need_whole(ctx->c, *y->h);
     auto G = assemble_stage(ctx->c, *x->h, *y->h, *qrow->s, *qcol->s, pxy->m, pxy->keep);
     *out = new h2g_h2{G};
   });
@@ -246,6 +251,7 @@ int h2g_block_norms(h2g_ctx* ctx, h2g_h2* g, double* cn, double* nn) {
   return guarded([&] {
     need(g, "g");
     if (!cn || !nn) throw InvalidInput("norm arrays are required");
+    need_rows_halo(ctx->c, *g->h);
     block_norms_stage(ctx->c, *g->h, cn, nn);
   });
 }
@@ -255,6 +261,7 @@ static int coarse_impl(h2g_ctx* ctx, h2g_h2* g, h2g_blocks* coarse, double tol, 
   return guarded([&] {
     need(g, "g");
     need(coarse, "coarse");
+    need_rows_halo(ctx->c, *g->h);
     auto s = coarse_basis_stage(ctx->c, *g->h, coarse->b, col, tol, max_rank, scale != 0, cn, nn);
     *out = new h2g_cstate{s, g->h};
   });

@@ -25,17 +25,38 @@ void cuda_check(cudaError_t e, const char* what) {
 
 // ============================================================================ infrastructure
 
+// Process-wide payload of the arenas (bytes handed out, not the chunks behind them): the memory a
+// product actually needs, independent of the 64 MB chunk granularity (h2g_ctx_mem).
+std::atomic<long long> g_arena_payload{0}, g_arena_payload_high{0};
+
+// Destructors cannot throw: failed CUDA calls there are reported (and cleared, so that they do not
+// surface later as the "last error" of an unrelated launch) when H2G_DEBUG_API is set.
+static void dtor_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  static const bool dbg = getenv("H2G_DEBUG_API") != nullptr;
+  if (dbg) fprintf(stderr, "h2g: %s failed in a destructor: %s\n", what, cudaGetErrorString(e));
+  cudaGetLastError();
+}
+
+void mem_mark(const char* where) {
+  static const bool on = getenv("H2G_DEBUG_MEM") != nullptr;
+  if (on)
+    fprintf(stderr, "mem %-24s payload %9.1f MB  high %9.1f MB\n", where, g_arena_payload.load() / 1e6,
+            g_arena_payload_high.load() / 1e6);
+}
+
 Arena::~Arena() {
+  g_arena_payload -= (long long)bytes;
   if (cross_stream && free_st) {
     for (cudaStream_t s : after) {
       if (!s || s == free_st) continue;
       cudaEvent_t e;
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) continue;
-      cudaEventRecord(e, s);
-      cudaStreamWaitEvent(free_st, e, 0);
+      dtor_check(cudaEventRecord(e, s), "arena: event record on a user stream");
+      dtor_check(cudaStreamWaitEvent(free_st, e, 0), "arena: free stream wait");
       cudaEventDestroy(e);
     }
-    for (void* p : chunks) cudaFreeAsync(p, free_st);
+    for (void* p : chunks) dtor_check(cudaFreeAsync(p, free_st), "arena: cudaFreeAsync (cross-stream)");
     return;
   }
   if (cross_stream) {
@@ -43,7 +64,7 @@ Arena::~Arena() {
     for (void* p : chunks) cudaFree(p);
     return;
   }
-  for (void* p : chunks) cudaFreeAsync(p, st);
+  for (void* p : chunks) dtor_check(cudaFreeAsync(p, st), "arena: cudaFreeAsync");
 }
 
 void* Arena::alloc_bytes(size_t nb) {
@@ -56,6 +77,12 @@ void* Arena::alloc_bytes(size_t nb) {
     chunks.push_back(p);
     cur = (char*)p;
     left = chunk;
+  }
+  {
+    const long long now = (g_arena_payload += (long long)nb);
+    long long hw = g_arena_payload_high.load();
+    while (now > hw && !g_arena_payload_high.compare_exchange_weak(hw, now)) {
+    }
   }
   void* r = cur;
   cur += nb;
@@ -276,14 +303,34 @@ void Ctx::join_side(Ctx& S) {
   S.htime.clear();
 }
 
+void Ctx::gate_enter() {
+  if (!gate || !comm.on() || channel != 1) return;
+  std::unique_lock<std::mutex> lk(gate->m);
+  gate->cv.wait(lk, [this] { return gate->ch0_done; });
+  if (gate->ev0) cuda_check(cudaStreamWaitEvent(st, gate->ev0, 0), "gate wait");
+}
+
+void Ctx::gate_leave() {
+  if (!gate || channel != 0) return;
+  std::lock_guard<std::mutex> lk(gate->m);
+  if (gate->ch0_done) return;
+  if (comm.on()) {
+    cuda_check(cudaEventCreateWithFlags(&gate->ev0, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(gate->ev0, st), "event");
+  }
+  gate->ch0_done = true;
+  gate->cv.notify_all();
+}
+
+// Every use of a product's memory on the side, auxiliary or copy streams is joined into the main
+// stream before multiply / coarsen return (join_side, wait_near, the prefetch gather's event), so a
+// cross-stream arena is freed stream-ordered on the main stream alone -- no device-wide sync, and no
+// event on a stream that may be gone by then (the side / aux / copy streams die with their context;
+// the main stream is the caller's).
 void Ctx::order_free(Arena& a) {
   a.cross_stream = true;
   a.free_st = st;
   a.after.clear();
-  a.after.push_back(a.st);
-  if (side_) a.after.push_back(side_->st);
-  if (aux_) a.after.push_back(aux_->st);
-  if (up_stream) a.after.push_back(up_stream);
 }
 
 cudaEvent_t Ctx::event() {

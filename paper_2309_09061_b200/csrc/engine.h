@@ -2,8 +2,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <future>
+#include <mutex>
 #include <cstdlib>
 #include <map>
 #include <memory>
@@ -120,6 +123,9 @@ struct Arena {  // bump allocator over cudaMalloc'd chunks, freed together
   void* alloc_bytes(size_t nbytes);
 };
 using ArenaPtr = std::shared_ptr<Arena>;
+extern std::atomic<long long> g_arena_payload, g_arena_payload_high;
+// H2G_DEBUG_MEM=1: arena payload (now / high-water, MB) at the stage boundaries of a product
+void mem_mark(const char* where);
 
 struct Mat {
   double* p = nullptr;
@@ -140,6 +146,10 @@ struct Basis {  // leaf (size x k, ld k); xfer (k_c x k_parent, ld k_parent)
 
 struct H2 {
   std::shared_ptr<const Blocks> bt;
+  // partitioned product (multi-GPU): this rank holds the leaf blocks of its own block rows (plus the
+  // replicated top rows and, for G, the halo its column passes read); gather_rows() completes it
+  bool dist_rows = false;
+  bool dist_halo = false;  // a partitioned product G: also holds the blocks its column passes read
   std::shared_ptr<Basis> rb, cb;
   std::vector<double*> coup, near;
   std::vector<ArenaPtr> owned;
@@ -202,6 +212,21 @@ struct Comm {
   AlltoallFn a2a = nullptr;
   void* a2a_user = nullptr;
   bool on() const { return size > 1 && fn != nullptr; }
+};
+
+// Orders the collectives of the two concurrent passes of a partitioned product (row pass: channel 0,
+// column pass: channel 1, each on its own host thread, stream and communicator): channel 1 issues its
+// exchanges only after channel 0 has issued all of its own, and its stream waits for them, so every
+// rank issues -- and every GPU runs -- the collectives of the two communicators in the same order (no
+// cross-communicator circular wait).  Channel 0 never waits.
+struct PassGate {
+  std::mutex m;
+  std::condition_variable cv;
+  bool ch0_done = false;
+  cudaEvent_t ev0 = nullptr;  // channel 0's stream after its exchanges
+  ~PassGate() {
+    if (ev0) cudaEventDestroy(ev0);
+  }
 };
 
 // ------------------------------------------------------------------ context: stream + staging
@@ -274,6 +299,9 @@ struct Ctx {
   void drain_prof();
 
   Comm comm;        // ranks sharing this product (size 1: single GPU)
+  PassGate* gate = nullptr;  // set while two passes run concurrently (partitioned products)
+  void gate_enter();         // before this pass's partition-level exchanges
+  void gate_leave();         // after them (channel 0: releases channel 1; idempotent)
   int channel = 0;  // communicator of this context's host thread (side context: 1)
   std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
   cudaStream_t up_stream = nullptr;  // structure uploads from the planner thread
@@ -539,6 +567,14 @@ struct PItem {
   double** ptr;
 };
 void exchange_p2p(Ctx& C, Arena& ar, const std::vector<PItem>& items);
+// Complete a row-distributed matrix (H2::dist_rows) on every rank: all-gather of the leaf blocks of
+// the partitioned block rows (downloads and matvecs of a partitioned product call it).
+void gather_rows(Ctx& C, H2& h);
+// inputs of the partitioned stages: a product's factors must be whole (gathered if distributed);
+// coarsen reads its own rows plus the column halo (a partitioned product G has it, anything else
+// distributed is gathered)
+void need_whole(Ctx& C, H2& h);
+void need_rows_halo(Ctx& C, H2& h);
 // Integer per-cluster values (ranks): v[t] for the listed clusters is taken from owner[t].
 void exchange_ints(Ctx& C, const Part& part, const std::vector<int>& ids, std::vector<int>& v);
 

@@ -65,7 +65,7 @@ void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<i
 // results -- ranks, Q_t (leaf basis or the stacked transfers), basis_change and the projections
 // A_ts -- so the replicated top levels and the later stages see the full induced basis.
 static void exchange_induced(Ctx& C, Arena& out, const Part& part, HView x, HView y,
-                             const std::vector<std::vector<int>>& mids, Induced& R) {
+                             const std::vector<std::vector<int>>& mids, Induced& R, bool row_proj_local) {
   const Tree& tr = x.rows();
   const Basis& VX = x.rb();
   const Basis& VY = y.rb();
@@ -88,6 +88,12 @@ static void exchange_induced(Ctx& C, Arena& out, const Part& part, HView x, HVie
     else R.bc[t] = Mat{nullptr, k, VX.rank[t]};
     items.push_back(XItem{o, (long long)m * k, &qp[t]});
     items.push_back(XItem{o, (long long)k * VX.rank[t], &R.bc[t].p});
+    // projections A_ts: the assembly reads only its own rows' (and the replicated top's), and the
+    // top levels' ahat only those of the partition level's clusters -- the deeper rows stay local
+    // for the row pass (row_proj_local); the column pass's are read by every rank's assembly
+    // (product blocks of own rows reach columns of every rank), so they are all exchanged
+    static const bool proj_all = getenv("H2G_PROJ_ALL") != nullptr;  // A/B: exchange every projection
+    if (row_proj_local && !proj_all && tr.level[t] != part.level) continue;
     for (int b : mids[t]) {
       const int ky = VY.rank[x.col(b)];
       if (o != part.me) R.proj[b] = Mat{nullptr, k, ky};
@@ -298,7 +304,11 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       }
     }
     g4.run(C);
-    if (part.on() && lev == part.level) exchange_induced(C, out, part, x, y, mids, R);
+    if (part.on() && lev == part.level) {
+      C.gate_enter();
+      exchange_induced(C, out, part, x, y, mids, R, !x.T);  // row pass: x is X itself (not transposed)
+      C.gate_leave();
+    }
   }
   return R;
 }
@@ -705,6 +715,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     pt.dev.ready = nullptr;
   }
   // push-down of couplings on subdivided blocks, parents first (induced.py:328-344)
+  mem_mark("p1 before push-down");
   HostTimer ht3(C, "assemble_pushdown");
   StageTag tagp(C, "p1.push");
   struct Expansion {
@@ -779,17 +790,30 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     cudaFreeAsync(pt.dev.block, C.st);
     pt.dev.block = nullptr;
   }
-  if (part.on()) {  // every rank continues with the whole of G (couplings and nearfield)
+  if (part.on()) {
+    // G stays distributed by block rows: each rank keeps the blocks of its own rows (and the
+    // replicated top rows).  Phase 2's column pass of cluster r reads the blocks (t, r) of column r:
+    // each leaf block goes to its column's owner when that rank differs (the transpose halo, one
+    // all-to-all); blocks of replicated top columns below partitioned rows (none on the balanced
+    // BASELINE trees) are all-gathered.
     StageTag tagx(C, "p1.exchange");
-    std::vector<XItem> items;
+    const Part pcol = make_part(cols, C.comm);
+    std::vector<PItem> p2p;
+    std::vector<XItem> ag;
     for (int b = 0; b < B.nb; ++b) {
       if (!B.leaf(b)) continue;
       const int t = B.row[b], r = B.col[b];
       if (part.top(t)) continue;
-      if (B.adm[b]) items.push_back(XItem{part.owner[t], (long long)Q.rank[t] * W.rank[r], &G->coup[b]});
-      else items.push_back(XItem{part.owner[t], (long long)rows.size(t) * cols.size(r), &G->near[b]});
+      const long long len = B.adm[b] ? (long long)Q.rank[t] * W.rank[r] : (long long)rows.size(t) * cols.size(r);
+      double** dst = B.adm[b] ? &G->coup[b] : &G->near[b];
+      const int src = part.owner[t];
+      if (pcol.top(r)) ag.push_back(XItem{src, len, dst});
+      else if (pcol.owner[r] != src) p2p.push_back(PItem{src, pcol.owner[r], len, dst});
     }
-    exchange(C, *ar, items);
+    exchange_p2p(C, *ar, p2p);
+    exchange(C, *ar, ag);
+    G->dist_rows = true;
+    G->dist_halo = true;
   }
   // phase 2's block-norm batches are pure structure of G: build them on a host thread now, while
   // the assembly and push-down run on the GPU (coarsen picks them up)
@@ -896,6 +920,16 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     Ctx& S = C.side();
     keep2->st = S.st;
     C.order_free(*keep2);
+    PassGate gate;  // partitioned products: the column pass's collectives follow the row pass's
+    C.gate = &gate;
+    S.gate = &gate;
+    struct GateReset {
+      Ctx &a, &b;
+      ~GateReset() {
+        a.gate_leave();  // never leave the column pass waiting (row pass done or failed)
+        a.gate = b.gate = nullptr;
+      }
+    };
     std::exception_ptr err;
     std::thread th([&] {
       try {
@@ -907,8 +941,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
         err = std::current_exception();
       }
     });
+    GateReset gate_reset{C, S};
     try {
       qr = row_pass(C, *keep, sc);
+      C.gate_leave();
       // the row factors need only the row basis: issue them while the column pass finishes
       // (only when the planner thread is done already -- it also queues the dense targets)
       static const bool early_rf = getenv("H2G_NO_EARLY_RF") == nullptr;
@@ -918,6 +954,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
         have_rf = true;
       }
     } catch (...) {
+      C.gate_leave();
       th.join();
       throw;
     }
@@ -934,8 +971,10 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
     pt = pt_future.get();
   }
   if (pt.early.near) C.order_free(*pt.early.near);
+  mem_mark("p1 induced bases");
   StageTag taga(C, "p1.asm");
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt, have_rf ? &rf : nullptr);
+  mem_mark("p1 assembled");
   if (A) C.join_side(*A);  // counters / profile of the auxiliary stream's work
   record(C, e4);
   G->owned.push_back(keep);

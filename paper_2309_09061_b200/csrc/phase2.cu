@@ -623,6 +623,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     if (part.on() && lev == part.level) {
       // every rank receives the partitioned levels' ranks, Q_t and R_t (the representations stay
       // with their rank: only its own rows' final projection reads them)
+      C.gate_enter();
       StageTag tagx(C, "p2.exchange");
       std::vector<int> ids;
       for (int l = part.level; l <= tr.depth; ++l)
@@ -656,6 +657,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
           }
         }
       }
+      C.gate_leave();
     }
   }
   return S;
@@ -808,10 +810,10 @@ static std::shared_ptr<H2> project_final(Ctx& C, HView g, CState& rs, CState& cs
     }
   }
   g1.run(C);
-  if (part.on()) {
-    StageTag tagx(C, "p2.exchange");
-    exchange(C, *ar, items);
-  }
+  // multi-GPU: Z stays distributed by block rows (gather_rows completes it on demand: downloads,
+  // matvecs); the items listed above are what such a gather moves
+  if (part.on()) Z->dist_rows = true;
+  (void)items;
   return Z;
 }
 
@@ -992,6 +994,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     else all_norms(C, sc, g, d_cn, d_nn);
   }
   const cudaEvent_t ev_norms = mark_event(C);
+  mem_mark("p2 norms");
   prep_r.wait();
   prep_c.wait();
   auto ar = std::make_shared<Arena>(C.st);
@@ -1010,6 +1013,16 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     Ctx& S = C.side();
     ar2->st = S.st;
     C.order_free(*ar2);
+    PassGate gate;  // partitioned products: the column pass's collectives follow the row pass's
+    C.gate = &gate;
+    S.gate = &gate;
+    struct GateReset {
+      Ctx &a, &b;
+      ~GateReset() {
+        a.gate_leave();
+        a.gate = b.gate = nullptr;
+      }
+    } gate_reset{C, S};
     std::exception_ptr err;
     std::thread th([&] {
       try {
@@ -1026,10 +1039,12 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
       ev_r[0] = mark_event(C);
       rs = coarse_rows(C, *ar, HView{&g, false}, BView{coarse.get(), false}, tol, max_rank, scale, d_cn, d_nn,
                        prep_r.get(), nn_ready);
+      C.gate_leave();
       ev_r[1] = mark_event(C);
       HostTimer htpp(C, "p2_project_structure");
       plan = plan_project(HView{&g, false}, rs, *coarse);  // while the column pass runs
     } catch (...) {
+      C.gate_leave();
       th.join();
       throw;
     }
@@ -1037,6 +1052,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     if (err) std::rethrow_exception(err);
     C.join_side(S);
   }
+  mem_mark("p2 coarse bases");
   if (C.timing) { e1 = C.event(); cudaEventRecord(e1, C.st); }
   e2 = e1;
   StageTag tagp(C, "p2.project");

@@ -139,6 +139,31 @@ void exchange_p2p(Ctx& C, Arena& ar, const std::vector<PItem>& items) {
   for (auto& r : recv) *r.first = r.second;
 }
 
+void gather_rows(Ctx& C, H2& h) {
+  if (!h.dist_rows) return;
+  if (!C.comm.on()) throw InvalidInput("a partitioned matrix needs its communicator to be gathered");
+  const Blocks& B = *h.bt;
+  const Part part = make_part(*B.rows, C.comm);
+  std::vector<XItem> items;
+  for (int b = 0; b < B.nb; ++b) {
+    if (!B.leaf(b)) continue;
+    const int t = B.row[b], s = B.col[b];
+    if (part.top(t)) continue;
+    if (B.adm[b]) items.push_back(XItem{part.owner[t], (long long)h.rb->rank[t] * h.cb->rank[s], &h.coup[b]});
+    else items.push_back(XItem{part.owner[t], (long long)B.rows->size(t) * B.cols->size(s), &h.near[b]});
+  }
+  auto ar = std::make_shared<Arena>(C.st);
+  exchange(C, *ar, items);
+  h.owned.push_back(ar);
+  h.dist_rows = false;
+  h.dist_halo = false;
+}
+
+void need_whole(Ctx& C, H2& h) { gather_rows(C, h); }
+void need_rows_halo(Ctx& C, H2& h) {
+  if (h.dist_rows && !h.dist_halo) gather_rows(C, h);
+}
+
 void exchange_ints(Ctx& C, const Part& part, const std::vector<int>& ids, std::vector<int>& v) {
   if (!C.comm.on() || !part.on() || ids.empty()) return;
   const int P = C.comm.size, me = C.comm.rank;

@@ -67,10 +67,10 @@ class Context:
     def memory(self, reset: bool = False) -> dict:
         """Bytes of the engine's device arenas (default cudaMallocAsync pool: high-water marks since
         the last reset; torch's allocator statistics cannot see these)."""
-        out = np.zeros(4, np.int64)
+        out = np.zeros(6, np.int64)
         N.check(self.lib.h2g_ctx_mem(self.h, out.ctypes.data_as(N.I64P), 1 if reset else 0))
         return {"used_high": int(out[0]), "used": int(out[1]), "reserved_high": int(out[2]),
-                "reserved": int(out[3])}
+                "reserved": int(out[3]), "payload_high": int(out[4]), "payload": int(out[5])}
 
     def counters(self, reset: bool = False) -> dict:
         out = np.zeros(2, np.int64)

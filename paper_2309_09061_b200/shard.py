@@ -30,6 +30,8 @@ __all__ = ["Sharding", "allgather_segments", "tree_partition"]
 
 _ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_longlong), C.c_int,
                          C.c_void_p)
+_ALLTOALL = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_longlong), C.c_void_p,
+                        C.POINTER(C.c_longlong), C.c_int, C.c_void_p)
 
 
 class _DeviceBytes:
@@ -70,11 +72,16 @@ class Sharding:
         self.groups = [dist.new_group(ranks=ranks, backend=self.backend) for _ in range(2)]
         self.calls = 0
         self.bytes = 0
-        self._cb = _ALLGATHER(self._allgather)  # keep the trampoline alive
+        self._cb = _ALLGATHER(self._allgather)  # keep the trampolines alive
+        self._cb2 = _ALLTOALL(self._alltoall)
+        self.a2a_calls = 0
+        self.a2a_bytes = 0
         N.check(ctx.lib.h2g_ctx_set_comm(ctx.h, self.rank, self.size, C.cast(self._cb, C.c_void_p), None))
+        N.check(ctx.lib.h2g_ctx_set_alltoall(ctx.h, C.cast(self._cb2, C.c_void_p), None))
 
     def close(self):
         """Back to single-GPU products on this context."""
+        N.check(self.ctx.lib.h2g_ctx_set_alltoall(self.ctx.h, None, None))
         N.check(self.ctx.lib.h2g_ctx_set_comm(self.ctx.h, 0, 1, None, None))
 
     def _allgather(self, user, channel, dbuf, off, nseg, stream):
@@ -98,6 +105,41 @@ class Sharding:
                 allgather_segments(host, offs, group)
                 with torch.cuda.device(dev), torch.cuda.stream(ext):
                     buf.copy_(host)
+                ext.synchronize()
+            return 0
+        except BaseException:  # never unwind through the C frames
+            traceback.print_exc()
+            return 1
+
+
+    def _alltoall(self, user, channel, sbuf, soff, rbuf, roff, nseg, stream):
+        """Variable all-to-all of the engine's halo / transpose exchanges (one collective)."""
+        try:
+            import torch
+            import torch.distributed as dist
+            so = [int(soff[i]) for i in range(nseg + 1)]
+            ro = [int(roff[i]) for i in range(nseg + 1)]
+            self.a2a_calls += 1
+            self.a2a_bytes += so[-1]
+            dev = torch.device("cuda", self.ctx.device)
+            ssplit = [so[i + 1] - so[i] for i in range(nseg)]
+            rsplit = [ro[i + 1] - ro[i] for i in range(nseg)]
+            sb = torch.as_tensor(_DeviceBytes(sbuf or 0, so[-1]), device=dev) if so[-1] else \
+                torch.empty(0, dtype=torch.uint8, device=dev)
+            rb = torch.as_tensor(_DeviceBytes(rbuf or 0, ro[-1]), device=dev) if ro[-1] else \
+                torch.empty(0, dtype=torch.uint8, device=dev)
+            group = self.groups[channel]
+            ext = torch.cuda.ExternalStream(int(stream) if stream else 0, device=dev)
+            if self.backend == "nccl":
+                with torch.cuda.device(dev), torch.cuda.stream(ext):
+                    dist.all_to_all_single(rb, sb, rsplit, ssplit, group=group)
+            else:  # host staging
+                ext.synchronize()
+                hs = sb.cpu()
+                hr = torch.empty(ro[-1], dtype=torch.uint8)
+                dist.all_to_all_single(hr, hs, rsplit, ssplit, group=group)
+                with torch.cuda.device(dev), torch.cuda.stream(ext):
+                    rb.copy_(hr)
                 ext.synchronize()
             return 0
         except BaseException:  # never unwind through the C frames
