@@ -442,6 +442,8 @@ size_t gram_chol_smem(int m) {
   return sizeof(double) * 2 * np + sizeof(int) * (size_t)m + (size_t)m + 16;
 }
 
+cudaError_t launch_gram_chol(const GramItem* items, int nitems, int mmax, cudaStream_t st);
+
 cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
                         int mmax, cudaStream_t st) {
   static std::once_flag once;
@@ -456,6 +458,18 @@ cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* 
   if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, gram_partial_smem(), st>>>(items, segs, work);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nitems == 0) return e;
+  return launch_gram_chol(items, nitems, mmax, st);
+}
+
+cudaError_t launch_gram_chol(const GramItem* items, int nitems, int mmax, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)gram_chol_kernel);
+    cudaFuncSetAttribute((const void*)gram_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - (int)fa.sharedSizeBytes);
+  });
+  if (nitems == 0) return cudaSuccess;
   gram_chol_kernel<<<nitems, mmax <= 64 ? 256 : kCThr, gram_chol_smem(mmax), st>>>(items);
   return cudaGetLastError();
 }
