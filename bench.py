@@ -240,10 +240,11 @@ def run_reference(args, rank, world):
                    "order": spec["order"], "eps": spec["eps"], "sample_n": n},
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
                          "cpu": cpu_model(),
-                         "sample": f"{args.config} generator at reduced n={n} (the full n={spec['n']} "
-                                   f"product takes minutes per step on one core), full product incl. "
-                                   f"weights, oracle/h2_oracle.py NumPy restatement of h2mul, 1 BLAS thread "
-                                   f"(reference cli.py:12-15)"},
+                         "sample": (f"{args.config} generator at its full n={n}" if n == spec["n"] else
+                                    f"{args.config} generator at reduced n={n} (the full n={spec['n']} product "
+                                    f"takes minutes per step on one core)") +
+                                   ", full product incl. weights, oracle/h2_oracle.py NumPy restatement of h2mul, "
+                                   "1 BLAS thread (reference cli.py:12-15)"},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -402,22 +403,26 @@ def main():
     # roofline: dominant kernel class by device time in the profiled step
     peak_fp64 = fp64_peak_tflops()
     hbm, hbm_src = hbm_peak()
-    # dominant single kernel: gsum_mma_kernel (the "gsum" class is exactly that kernel; the other
-    # classes group several kernels, none of which individually exceeds it -- see the committed ncu
-    # launch list profiles/r01_launches_c2_summary.txt)
+    # dominant kernel: gsum_pipe_kernel -- the "gsum" class is exactly that kernel (both template
+    # instantiations: <1> is the dense-target assembly launch, <0> every other grouped GEMM); it is
+    # the largest kernel by device time in the committed ncu launch list of the timed region
+    # (profiles/r02_launches_c4_summary.txt: 33 % of kernel time), the other classes group several
     dom = "gsum"
     d = ks[dom]
     achieved = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
     total_flops = sum(v["flops"] for v in ks.values())
-    traffic = None
-    tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gsum_ncu.json")
+    traffic, traffic_note = None, None
+    tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gsum_ncu.json")
     if os.path.exists(tr_path):
         with open(tr_path) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
-    roofline = {"bound": "fp64", "kernel": "gsum_mma_kernel", "achieved": achieved, "peak": peak_fp64,
+            tr = json.load(fh)
+        traffic = tr.get("dram_bytes_per_launch")
+        traffic_note = (f"dram read+write of the dense-target assembly launch ({tr.get('kernel', '')}, grid "
+                        f"{tr.get('grid', '')}, the longest gsum launch of a c4 product) from one ncu --set full "
+                        f"capture, profiles/r02_gsum_ncu.json")
+    roofline = {"bound": "fp64", "kernel": "gsum_pipe_kernel", "achieved": achieved, "peak": peak_fp64,
                 "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": traffic,
-                "traffic_note": "dram read+write of the dense-target assembly launch (gsum_mma_kernel<1>, the "
-                                "longest GEMM launch) from one ncu --set full capture, profiles/r01_gsum_ncu.json",
+                "traffic_note": traffic_note,
                 "flops_note": "reference-ledger flops of the terms (per-triple shapes); the grouped assembly "
                               "executes fewer",
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (no FP64 entry in MEASURED_PEAKS.json)",
