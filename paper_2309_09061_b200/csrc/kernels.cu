@@ -924,7 +924,7 @@ static constexpr int NT = 512;
 template <int NPLO, bool RS>
 __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
                                                                              const Seg* __restrict__ segs,
-                                                                             int vsm) {
+                                                                             int vsm, long long smem_doubles) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int flag[2];
   __shared__ int s_k2;
@@ -1074,10 +1074,68 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
   }
   __syncthreads();
   if (k1 > 0) {
-    // Q = H_0 H_1 ... H_{k1-1} Y: reflectors in reverse order, one warp per column
-    for (int c = warp; c < kt; c += nw)
-      for (int j = k1 - 1; j >= 0; --j)
-        if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], Q, kt, c);
+    // Q = H_0 H_1 ... H_{k1-1} Y: reflectors in reverse order.  With R in shared memory its space is
+    // free now: Q is staged there in column blocks (column-major, each warp owning whole columns, so
+    // the k1 reflectors need no barrier), V beside it -- the global-memory version re-reads every
+    // column of Q (stride kt) for every reflector and thrashes L1 at m ~ 200.
+    int CB = 0;
+    const int ldq = m | 1;
+    double* Qs = nullptr;
+    const double* Vs = V;
+    const double* tvs = tv;
+    if (RS) {
+      const long long room_r = (long long)n * ld;  // R's region (doubles)
+      const long long avail = (long long)smem_doubles - (long long)(R - smem);
+      if (vsm) {  // V and tv are already in shared memory, after R
+        CB = (int)min((long long)kt, room_r / ldq);
+        Qs = R;
+      } else {
+        const long long vneed = (((long long)m * ldv + kx + 1) + 1) & ~1LL;
+        if (vneed + (long long)ldq < avail) {
+          double* Vd = R;
+          for (long long e = threadIdx.x; e < (long long)m * ldv + kx; e += blockDim.x) Vd[e] = it.vws[e];
+          Vs = Vd;
+          tvs = Vd + (long long)m * ldv;
+          Qs = Vd + vneed;
+          CB = (int)min((long long)kt, (avail - vneed) / ldq);
+        }
+      }
+    }
+    if (CB >= 4 || (CB > 0 && CB == kt)) {
+      __syncthreads();
+      for (int c0 = 0; c0 < kt; c0 += CB) {
+        const int cb = min(CB, kt - c0);
+        for (long long e = threadIdx.x; e < (long long)m * cb; e += blockDim.x) {
+          const int i = (int)(e / cb), c = (int)(e % cb);
+          Qs[(long long)c * ldq + i] = Q[(long long)i * kt + c0 + c];
+        }
+        __syncthreads();
+        for (int c = warp; c < cb; c += nw) {
+          double* qc = Qs + (long long)c * ldq;
+          for (int j = k1 - 1; j >= 0; --j) {
+            const double tau = tvs[j];
+            if (tau == 0.0) continue;
+            double part = 0.0;
+            for (int i = j + 1 + lane; i < m; i += 32) part = fma(Vs[(long long)i * ldv + j], qc[i], part);
+            const double wv = qc[j] + warp_sum(part);
+            __syncwarp();
+            if (lane == 0) qc[j] -= tau * wv;
+            for (int i = j + 1 + lane; i < m; i += 32) qc[i] -= tau * wv * Vs[(long long)i * ldv + j];
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        for (long long e = threadIdx.x; e < (long long)m * cb; e += blockDim.x) {
+          const int i = (int)(e / cb), c = (int)(e % cb);
+          Q[(long long)i * kt + c0 + c] = Qs[(long long)c * ldq + i];
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int c = warp; c < kt; c += nw)
+        for (int j = k1 - 1; j >= 0; --j)
+          if (tv[j] != 0.0) apply_reflector_col(V, ldv, m, j, tv[j], Q, kt, c);
+    }
   }
   }
   if (it.bc_out) {
@@ -1875,16 +1933,17 @@ cudaError_t launch_svd_finish(const SvdItem* items, const Seg* segs, int nitems,
   init_attributes();
   if (nitems == 0) return cudaSuccess;
   const int v = vsmem ? 1 : 0;
+  const long long sd = (long long)(smem / sizeof(double));
   if (rsmem) {
-    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, segs, v);
-    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items, segs, v);
-    else if (nmax <= 192) svd_finish_kernel<24, true><<<nitems, NT, smem, st>>>(items, segs, v);
-    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items, segs, v);
+    if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else if (nmax <= 128) svd_finish_kernel<16, true><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else if (nmax <= 192) svd_finish_kernel<24, true><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else svd_finish_kernel<0, true><<<nitems, NT, smem, st>>>(items, segs, v, sd);
   } else {
-    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items, segs, v);
-    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items, segs, v);
-    else if (nmax <= 192) svd_finish_kernel<24, false><<<nitems, NT, smem, st>>>(items, segs, v);
-    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items, segs, v);
+    if (nmax <= 64) svd_finish_kernel<8, false><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else if (nmax <= 128) svd_finish_kernel<16, false><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else if (nmax <= 192) svd_finish_kernel<24, false><<<nitems, NT, smem, st>>>(items, segs, v, sd);
+    else svd_finish_kernel<0, false><<<nitems, NT, smem, st>>>(items, segs, v, sd);
   }
   return cudaGetLastError();
 }

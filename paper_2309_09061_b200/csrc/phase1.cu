@@ -723,37 +723,78 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
     Mat part;
   };
   static const bool exp3 = getenv("H2G_EXPAND_3F") != nullptr;  // previous one-launch form (A/B)
+  static const bool push3 = getenv("H2G_PUSH_3F") != nullptr;  // previous 3-factor pushes (A/B)
+  constexpr size_t kPushBudget = size_t(1) << 27;  // doubles (1 GiB) of E_t2 S intermediates per chunk
   for (int lev = 0; lev < B.depth; ++lev) {
     GBatch g1, g2;
     std::vector<Expansion> exps;
-    for (int b : B.by_level[lev]) {
-      if (B.leaf(b)) continue;
-      const int t = B.row[b], r = B.col[b];
-      const Mat& S = cp[b];
-      for (int i = 0; i < B.nkids(b); ++i) {
-        const int ch = B.kid(b, i);
-        const int t2 = B.row[ch], r2 = B.col[ch];
-        if (!part.mine(t2)) continue;
-        Mat E, F;
-        if (t2 != t) E = Q.xferm(t2);
-        if (r2 != r) F = W.xferm(r2);
-        if (B.near_leaf(ch)) {
-          Mat part{sc.alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
-          g1.out(part, false);
-          emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
-          if (exp3) {
-            g2.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
-            g2.t3(Q.leafm(t2).ref(), part.ref(), W.leafm(r2).tref(), Q.rank[t2], W.rank[r2]);
-          } else {
-            exps.push_back(Expansion{ch, part});
+    // children (t2, r2) of a subdivided block b receive E_t2 S F_r2^T (induced.py:328-344): E_t2 S is
+    // shared by the children of one row child t2, so it is formed once per (b, t2) into scratch and the
+    // children take one 2-factor term each -- no 3-factor term recomputing it for every output tile
+    // and sibling.  Chunked over the parents to bound the scratch.
+    const std::vector<int>& lvl = B.by_level[lev];
+    for (size_t p0 = 0; p0 < lvl.size();) {
+      size_t need = 0, p1 = p0;
+      for (; p1 < lvl.size(); ++p1) {
+        const int b = lvl[p1];
+        if (B.leaf(b) || push3) continue;
+        size_t sz = 0;
+        for (int i = 0; i < B.nkids(b); ++i) {
+          const int ch = B.kid(b, i);
+          if (B.row[ch] != B.row[b]) sz += (size_t)Q.rank[B.row[ch]] * W.rank[B.col[b]];
+        }
+        if (p1 > p0 && need + sz > kPushBudget) break;
+        need += sz;
+      }
+      if (push3) p1 = lvl.size();
+      Arena ta(C.st);
+      GBatch ge;
+      for (size_t pi = p0; pi < p1; ++pi) {
+        const int b = lvl[pi];
+        if (B.leaf(b)) continue;
+        const int t = B.row[b], r = B.col[b];
+        const Mat& S = cp[b];
+        std::vector<std::pair<int, Mat>> es;  // (t2, E_t2 S) of this parent
+        for (int i = 0; i < B.nkids(b); ++i) {
+          const int ch = B.kid(b, i);
+          const int t2 = B.row[ch], r2 = B.col[ch];
+          if (!part.mine(t2)) continue;
+          Mat E, F;
+          if (t2 != t) E = Q.xferm(t2);
+          if (r2 != r) F = W.xferm(r2);
+          Mat src = S;  // E_t2 S, or S itself when the row cluster does not change
+          if (!push3 && t2 != t) {
+            auto it = std::find_if(es.begin(), es.end(), [t2](const std::pair<int, Mat>& e) { return e.first == t2; });
+            if (it == es.end()) {
+              Mat m2{ta.alloc((size_t)Q.rank[t2] * S.c), Q.rank[t2], S.c};
+              ge.out(m2, false);
+              ge.t2(E.ref(), S.ref(), E.c);
+              es.emplace_back(t2, m2);
+              it = es.end() - 1;
+            }
+            src = it->second;
           }
-        } else {
-          g1.out(cp[ch], true);
-          emit_push(g1, t2 != t ? &E : nullptr, S, r2 != r ? &F : nullptr);
+          const bool push_e = push3 && t2 != t;
+          if (B.near_leaf(ch)) {
+            Mat part{sc.alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
+            g1.out(part, false);
+            emit_push(g1, push_e ? &E : nullptr, src, r2 != r ? &F : nullptr);
+            if (exp3) {
+              g2.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
+              g2.t3(Q.leafm(t2).ref(), part.ref(), W.leafm(r2).tref(), Q.rank[t2], W.rank[r2]);
+            } else {
+              exps.push_back(Expansion{ch, part});
+            }
+          } else {
+            g1.out(cp[ch], true);
+            emit_push(g1, push_e ? &E : nullptr, src, r2 != r ? &F : nullptr);
+          }
         }
       }
+      ge.run(C);
+      g1.run(C);
+      p0 = p1;
     }
-    g1.run(C);
     if (!g2.outs.empty() || !exps.empty()) wait_dense();
     g2.run(C);
     // expansion into the inadmissible children, N += Q_leaf(t2) (part W_leaf(r2)^T) as two

@@ -1,25 +1,28 @@
 #!/bin/bash
-# Regenerate the round's evidence on the GPU box (run from the repo root, under gpurun):
-#   bench line, ncu launch list of the timed region, one ncu --set full capture of the dominant
-#   kernel's longest launch, trace summary, full-size c3 / c4 runs.  Outputs land in gpurun_out/;
-#   copy what is to be judged into profiles/ (tools/refresh_profiles.sh is the recipe).
+# Regenerate the round's evidence on the GPU box (run from the repo root, under gpurun): the driver's
+# default bench line (c4), the ncu launch list of its timed region (cudaProfilerStart/Stop: every
+# engine thread and stream), ncu --set full captures of the dominant kernel's largest launches, a
+# like-for-like c2 pair at n = 16,384 (GPU bench and the CPU reference arm at the same n), and the
+# full-size runs.  Outputs land in gpurun_out/$R/; copy what is judged into profiles/.
 set -u
-R=${ROUND:-r01}
-mkdir -p gpurun_out
-python bench.py --steps 10 --warmup 3 > gpurun_out/${R}_bench_c2.json 2> gpurun_out/${R}_bench_c2.err
-echo "bench rc=$?"
-# launch list of the timed region only (NVTX range "timed"), cold-cache serialised per-launch times
-ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_launches_c2.csv 2> /dev/null
-echo "launch list rc=$?"
-python tools/launch_summary.py gpurun_out/${R}_launches_c2.csv > gpurun_out/${R}_launches_c2_summary.txt
-# the dense-target assembly launch (gsum_mma_kernel<1>, the longest GEMM launch of a product)
-ncu --kernel-name-base demangled --kernel-name regex:"gsum_mma_kernel<.int.1>" --launch-skip 3 --launch-count 1 --set full --import-source on \
-    --clock-control none -o gpurun_out/${R}_gsum -f python tools/trace_config.py c2 > /dev/null 2>&1
-echo "gsum capture rc=$?"
-ncu -i gpurun_out/${R}_gsum.ncu-rep --page raw --csv > gpurun_out/${R}_gsum_raw.csv 2> /dev/null
-python tools/ncu_stalls.py gpurun_out/${R}_gsum.ncu-rep gsum_mma 30 > gpurun_out/${R}_gsum_stalls.txt 2> /dev/null
-H2G_TRACE=gpurun_out/${R}_trace_c2.json python tools/trace_config.py c2 > /dev/null 2>&1
-python tools/trace_summary.py gpurun_out/${R}_trace_c2.json > gpurun_out/${R}_trace_c2_summary.txt
-for c in c3 c4; do python tools/run_config.py $c > gpurun_out/${R}_full_$c.json 2> gpurun_out/${R}_full_$c.err; done
+R=${ROUND:-r02}
+O=gpurun_out/$R
+mkdir -p $O
+python bench.py --steps 10 --warmup 3 > $O/bench_c4.json 2> $O/bench_c4.err; echo "bench c4 rc=$?"
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/launches_c4.csv 2> /dev/null; echo "launch list rc=$?"
+python tools/launch_summary.py $O/launches_c4.csv 40 > $O/launches_c4_summary.txt
+cap() {  # kernel regex, launch skip (within tools/run_config.py c4 0 1), tag
+  ncu --kernel-name-base demangled --kernel-name "regex:$1" --launch-skip $2 --launch-count 1 --set full --import-source on \
+      --clock-control none -o $O/$3 -f python tools/run_config.py c4 0 1 > $O/$3.log 2>&1
+  ncu -i $O/$3.ncu-rep --page raw --csv > $O/$3_raw.csv 2> /dev/null
+  python tools/ncu_stalls.py $O/$3.ncu-rep "$4" 30 > $O/$3_stalls.txt 2>&1
+}
+cap "gsum_pipe_kernel<.int.1>" 0 gsum_dense gsum_pipe
+cap "gram_dd_partial_kernel" 60 gram gram_dd
+python bench.py --config c2 --steps 10 --warmup 3 > $O/bench_c2.json 2> $O/bench_c2.err; echo "bench c2 rc=$?"
+python bench.py --impl reference --config c2 --cpu-sample-n 16384 --steps 1 --warmup 0 > $O/ref_c2_16384.json 2> $O/ref_c2.err; echo "ref c2 rc=$?"
+for c in c2 c3 c4; do python tools/run_config.py $c 0 5 > $O/full_$c.json 2> $O/full_$c.err; done
+H2G_TRACE=$O/trace_c4.json python tools/trace_config.py c4 > /dev/null 2>&1
+python tools/trace_summary.py $O/trace_c4.json > $O/trace_c4_summary.txt; rm -f $O/trace_c4.json
 echo done
