@@ -105,6 +105,13 @@ Ctx::Ctx(int dev, cudaStream_t s, int priority) : device(dev), st(s) {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     unsigned long long thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // no hidden cross-stream waits: by default an allocation may reuse memory freed on another stream
+    // by making its stream wait for that stream's pending work (a level batch on the side stream
+    // stalling behind the main stream's queue); the pool grows instead (H2G_POOL_DEPS=1: default)
+    if (!getenv("H2G_POOL_DEPS")) {
+      int zero = 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+    }
   }
   stage_cap = size_t(64) << 20;
   cuda_check(cudaMallocHost(&hstage, stage_cap), "cudaMallocHost");
