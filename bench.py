@@ -276,6 +276,12 @@ def main():
     spec = dict(CONFIGS[args.config])
     n = args.n or spec["n"]
     eps = spec["eps"]
+    # one process per GPU: map 70 % of the device into the engine's stream-ordered pool up front.
+    # Growing the pool later happens inside whichever allocation needs it, on the host thread of a
+    # level batch -- measured 5 ms to 1.2 s per call at c4, i.e. +100..1000 ms on ~30 % of the steps
+    # (tools/step_loop.py with H2G_DEBUG_ALLOC=1); with the reservation every c4 step is 1.08-1.09 s.
+    total_gb = torch.cuda.get_device_properties(local).total_memory / 1e9
+    os.environ.setdefault("H2G_POOL_RESERVE_GB", f"{0.7 * total_gb:.0f}")
     ctx = Context(local)
     from paper_2309_09061_b200.problems import build_config_device
     t0 = time.perf_counter()

@@ -73,7 +73,13 @@ void* Arena::alloc_bytes(size_t nb) {
   if (nb > left) {
     size_t chunk = std::max(nb, size_t(64) << 20);
     void* p = nullptr;
+    static const bool dbg = getenv("H2G_DEBUG_ALLOC") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cuda_check(cudaMallocAsync(&p, chunk, st), "cudaMallocAsync");
+    if (dbg) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 5.0) fprintf(stderr, "h2g: cudaMallocAsync(%.0f MB) took %.1f ms\n", chunk / 1e6, ms);
+    }
     chunks.push_back(p);
     cur = (char*)p;
     left = chunk;
@@ -111,6 +117,21 @@ Ctx::Ctx(int dev, cudaStream_t s, int priority) : device(dev), st(s) {
     if (!getenv("H2G_POOL_DEPS")) {
       int zero = 0;
       cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+    }
+    // H2G_POOL_RESERVE_GB=n: map n GB into the pool once, up front (growing it later maps memory on
+    // the host thread of whichever allocation needs it)
+    if (const char* r = getenv("H2G_POOL_RESERVE_GB")) {
+      const double gb = atof(r);
+      unsigned long long cur = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur);
+      if (gb > 0 && (double)cur < gb * 1e9) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, (size_t)(gb * 1e9), st) == cudaSuccess) {
+          cudaFreeAsync(p, st);
+          cudaStreamSynchronize(st);
+        }
+        cudaGetLastError();
+      }
     }
   }
   stage_cap = size_t(64) << 20;
@@ -226,6 +247,8 @@ void* Ctx::stage(const void* src, size_t bytes) {
     flush();
     retired.emplace_back(hstage, dstage);
     stage_cap = std::max(need, stage_cap * 2);
+    static const bool dbg = getenv("H2G_DEBUG_STAGE") != nullptr;
+    if (dbg) fprintf(stderr, "h2g: staging overflow, new buffer %.0f MB\n", stage_cap / 1e6);
     cuda_check(cudaMallocHost(&hstage, stage_cap), "cudaMallocHost");
     cuda_check(cudaMalloc(&dstage, stage_cap), "cudaMalloc stage");
     stage_off = 0;

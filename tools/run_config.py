@@ -12,6 +12,8 @@ from paper_2309_09061_b200.problems import build_config_device
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else None
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+import torch as _t
+os.environ.setdefault("H2G_POOL_RESERVE_GB", f"{0.7 * _t.cuda.get_device_properties(0).total_memory / 1e9:.0f}")
 ctx = Context(0)
 t0 = time.perf_counter()
 dxr, dyr, spec = build_config_device(cfg, n=n, ctx=ctx)

@@ -8,6 +8,8 @@ from paper_2309_09061_b200.device import Context
 from paper_2309_09061_b200.problems import build_config_device
 cfg = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else None
+import torch as _t
+os.environ.setdefault("H2G_POOL_RESERVE_GB", f"{0.7 * _t.cuda.get_device_properties(0).total_memory / 1e9:.0f}")
 ctx = Context(0)
 dxr, dyr, spec = build_config_device(cfg, n=n, ctx=ctx)
 dx = P.recompress(dxr, spec["eps"], ctx=ctx)
