@@ -431,13 +431,25 @@ void GBatch::run(Ctx& C) {
   k2max = 0;
 }
 
+// H2G_GSUM_NO_WHOLE=1: every output through 64 x 64 tiles (A/B of the whole-output kernel)
+static bool whole_ok() {
+  static const bool off = getenv("H2G_GSUM_NO_WHOLE") != nullptr;
+  return !off;
+}
+
 void GBatch::prepare_tiles() {
   tiles.clear();
+  whole_tiles.clear();
   tiles.reserve(outs.size());
+  const bool w = whole && whole_ok();
   for (int i = 0; i < (int)outs.size(); ++i) {
     const GOut& o = outs[i];
     if (o.m <= 0 || o.n <= 0) continue;
     const int tm = (o.m + 63) / 64, tn = (o.n + 63) / 64;
+    if (w && tm <= 2 && tn <= 2 && (tm > 1 || tn > 1)) {
+      whole_tiles.push_back(GTile{i, 0});
+      continue;
+    }
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
   }
@@ -447,14 +459,22 @@ void GBatch::prepare_tiles() {
 void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
   HostTimer ht(C, "gbatch_run");
   if (!tiles_ready) prepare_tiles();
-  if (!tiles.empty()) {
+  if (!tiles.empty() || !whole_tiles.empty()) {
     GOut* d_o = C.push(outs);
     GTile* d_l = C.push(tiles);
+    GTile* d_w = C.push(whole_tiles);
     cudaEvent_t ev = C.prof_begin();
     C.flush();
-    cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st, tag), "gsum");
+    if (!whole_tiles.empty()) {
+      cuda_check(launch_gsum_whole(d_o, d_terms, d_w, (int)whole_tiles.size(), std::max(k2max, 64), C.st),
+                 "gsum(whole)");
+      ++C.launches;
+    }
+    if (!tiles.empty()) {
+      cuda_check(launch_gsum(d_o, d_terms, d_l, (int)tiles.size(), k2max, C.st, tag), "gsum");
+      ++C.launches;
+    }
     C.prof_end(K_GSUM, ev, flops_hint, 0.0);
-    ++C.launches;
   }
   outs.clear();
   terms.clear();
@@ -1616,7 +1636,7 @@ MatStore basis_weights(Ctx& C, Arena& ar, const Basis& W) {
 }
 
 // Top-down condensed weights Z_s (reference weights.py:60-101).
-MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling) {
+MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling, bool exact_rows) {
   const Tree& tr = h.rows();
   const int nb = h.h->bt->nb;
   std::vector<std::vector<int>> adm_of(tr.n);
@@ -1657,7 +1677,7 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
     // exactly-zero blocks are not rows of the reference's stack (weights.py:86-89): the factor's
     // row count min(M, k) -- which sets the column counts (and so the eps * max(rows, cols) floor)
     // of the SVD inputs built from these weights -- counts the nonzero blocks only
-    nrm = C.read(d_nrm, (size_t)std::max(1, nb));
+    if (exact_rows) nrm = C.read(d_nrm, (size_t)std::max(1, nb));
   }
   MatStore Z(tr.n);
   for (int lev = 0; lev <= tr.depth; ++lev) {
@@ -1678,7 +1698,7 @@ MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scal
         M += ze.r;
       }
       for (int b : adm_of[s]) {
-        if (scaling && nrm[b] == 0.0) continue;
+        if (scaling && exact_rows && nrm[b] == 0.0) continue;
         q.sl.add(Tb[b].ref(), Tb[b].r, 1.0, scaling ? d_nrm + b : nullptr);
         M += Tb[b].r;
       }

@@ -28,6 +28,7 @@ void cuda_check(cudaError_t e, const char* what);
 
 // ------------------------------------------------------------------ kernels (kernels.cu)
 cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t, int tag = 0);
+cudaError_t launch_gsum_whole(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
 cudaError_t launch_qr_chunks(const QrItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
                              cudaStream_t);
 cudaError_t launch_tsqr_merge(const MergeWork*, int nwork, size_t smem, bool rsmem, cudaStream_t);
@@ -407,7 +408,9 @@ struct GBatch {
   // launch with a device-resident term array (terms generated on the GPU); `outs` index into it
   void run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint);
   int tag = 0;               // kernel symbol (1: dense-target assembly, selectable in profilers)
+  bool whole = false;        // outputs up to 128 x 128 as one CTA each (gsum_whole_kernel: cached T / U)
   std::vector<GTile> tiles;  // prepare_tiles(): the 64x64 output tiles, built ahead (any thread)
+  std::vector<GTile> whole_tiles;  // outputs handled whole (one CTA each), when `whole`
   bool tiles_ready = false;
   void prepare_tiles();
   bool empty() const { return outs.empty(); }
@@ -596,7 +599,12 @@ void xv_compute(Ctx& C, Arena& ar, HView x, HView y, PRef P, const std::vector<i
                 std::vector<Mat>& memo);
 MatStore basis_product(Ctx& C, Arena& ar, const Basis& W, const Basis& V);
 MatStore basis_weights(Ctx& C, Arena& ar, const Basis& W);
-MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling);
+// exact_rows: leave exactly-zero blocks out of the stacks' row counts (one norm read-back); callers
+// whose truncation tolerance makes the eps * max(rows, cols) floor irrelevant (floor_free_tol) skip it
+MatStore total_weights(Ctx& C, Arena& ar, HView h, const MatStore& rw, bool scaling, bool exact_rows = true);
+// Above this tolerance the SVD floor max(rows, cols) eps sigma_1 (rows, cols <= 1e5, sigma_1 of block-
+// normalised stacks <= 1e2) stays below tol, so the exact row counts of zero-block stacks cannot matter
+constexpr double kFloorFreeTol = 1e-8;
 Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, PRef P, double tol,
                      int max_rank, bool scale, double level_decay);
 PTree product_tree(BView bx, BView by);

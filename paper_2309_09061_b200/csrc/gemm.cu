@@ -279,7 +279,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // bj0..) into one stage; `direct` operands (Ts) are not copied.
 __device__ __forceinline__ void issue_chunk(const Job& J, int ai0, int mr, int bj0, int nc, int kk, double* sA,
                                             double* sB, bool dirA, bool dirB, StageMeta* meta,
-                                            int offA, int offB, int ldT) {
+                                            int offA, int offB, int ldDA, int ldDB) {
   const int tid = threadIdx.x;
   const int kc = min(kKC, J.k - kk);
   const bool aK = J.a.cs == 1;  // A row-major (k contiguous)
@@ -322,8 +322,8 @@ __device__ __forceinline__ void issue_chunk(const Job& J, int ai0, int mr, int b
   }
   if (tid == 0) {
     StageMeta m;
-    if (dirA) { m.aI = ldT; m.aK = 1; m.skipA = offA + kk; } else { m.aI = aK ? kLdKc : 1; m.aK = aK ? 1 : kLdIc; m.skipA = -1; }
-    if (dirB) { m.bK = ldT; m.bJ = 1; m.skipB = offB + kk * ldT; } else { m.bK = bN ? kLdIc : 1; m.bJ = bN ? 1 : kLdKc; m.skipB = -1; }
+    if (dirA) { m.aI = ldDA; m.aK = 1; m.skipA = offA + kk; } else { m.aI = aK ? kLdKc : 1; m.aK = aK ? 1 : kLdIc; m.skipA = -1; }
+    if (dirB) { m.bK = ldDB; m.bJ = 1; m.skipB = offB + kk * ldDB; } else { m.bK = bN ? kLdIc : 1; m.bJ = bN ? 1 : kLdKc; m.skipB = -1; }
     m.kc4 = (kc + 3) >> 2;
     m.pad_ = 0;
     m.alpha = J.alpha;
@@ -337,7 +337,7 @@ __device__ __forceinline__ void issue_chunk(const Job& J, int ai0, int mr, int b
 template <class GetJob>
 __device__ void run_stream(Acc& acc, int njobs, GetJob getjob, int ai0, int mr, int bj0, int nc, bool dirA,
                            bool dirB, int offA, int offB, double* ring, StageMeta* metas, const double* Ts,
-                           int ldT) {
+                           int ldDA, int ldDB) {
   // chunk count
   int total = 0;
   for (int j = 0; j < njobs; ++j) total += (getjob(j).k + kKC - 1) / kKC;
@@ -354,7 +354,7 @@ __device__ void run_stream(Acc& acc, int njobs, GetJob getjob, int ai0, int mr, 
     if (c < total) {
       const int s = c % kPS;
       issue_chunk(PJ, ai0, mr, bj0, nc, pk, ring + s * 2 * kStg, ring + s * 2 * kStg + kStg, dirA, dirB, metas + s,
-                  offA, offB, ldT);
+                  offA, offB, ldDA, ldDB);
       pk += kKC;
       if (pk >= PJ.k) {
         pk = 0;
@@ -447,32 +447,32 @@ __global__ void __launch_bounds__(kThr, GSUM_PIPE_MINB) gsum_pipe_kernel(const G
             if (i < mt && j < nt) acc.v[r][c][h] += t.alpha * ld(t.a, i0 + i, j0 + j);
           }
     } else if (t.nf == 2) {
-      run_stream(acc, nrun, getjob, i0, mt, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT);
+      run_stream(acc, nrun, getjob, i0, mt, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
     } else if (t.nf == 4) {  // T (mt x ka) = sum A B, then C += T * da
       aux.zero();
-      run_stream(aux, nrun, getjob, i0, mt, 0, o.ka, false, false, 0, 0, ring, metas, Ts, ldT);
+      run_stream(aux, nrun, getjob, i0, mt, 0, o.ka, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
       acc_to_smem(aux, Ts, ldT, kT, o.ka);
       __syncthreads();
       run_stream(acc, 1, single(Job{MatRef{Ts, ldT, 1}, o.da, o.ka, 1.0}), 0, mt, j0, nt, true, false, 0, 0, ring,
-                 metas, Ts, ldT);
+                 metas, Ts, ldT, ldT);
     } else if (t.nf == 5) {  // U (kb x nt) = sum A B, then C += ab * U
       aux.zero();
-      run_stream(aux, nrun, getjob, 0, o.kb, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT);
+      run_stream(aux, nrun, getjob, 0, o.kb, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
       acc_to_smem(aux, Ts, ldT, o.kb, kT);
       __syncthreads();
       run_stream(acc, 1, single(Job{o.ab, MatRef{Ts, ldT, 1}, o.kb, 1.0}), i0, mt, 0, nt, false, true, 0, 0, ring,
-                 metas, Ts, ldT);
+                 metas, Ts, ldT, ldT);
     } else {  // nf = 3: T = alpha A[i0.., :] B (mt x k2) in Ts, 64 columns at a time, then C += T D
       for (int js = 0; js < t.k2; js += kT) {
         aux.zero();
         const int ns = min(kT, t.k2 - js);
         run_stream(aux, 1, single(Job{t.a, MatRef{t.b.p + (long long)js * t.b.cs, t.b.rs, t.b.cs}, t.k, t.alpha}),
-                   i0, mt, 0, ns, false, false, 0, 0, ring, metas, Ts, ldT);
+                   i0, mt, 0, ns, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
         acc_to_smem(aux, Ts + js, ldT, kT, ns);
       }
       __syncthreads();
       run_stream(acc, 1, single(Job{MatRef{Ts, ldT, 1}, t.d, t.k2, 1.0}), 0, mt, j0, nt, true, false, 0, 0, ring,
-                 metas, Ts, ldT);
+                 metas, Ts, ldT, ldT);
     }
     ti = te;
   }
@@ -490,12 +490,157 @@ __global__ void __launch_bounds__(kThr, GSUM_PIPE_MINB) gsum_pipe_kernel(const G
       }
 }
 
+// Whole-output variant for the coupling targets of the assembly (outputs up to 128 x 128: k~ x k~
+// couplings, k~ <= 128): ONE CTA walks the (<= 2 x 2) 64 x 64 sub-tiles of its output and keeps the
+// grouped intermediates of the first kind-a run (T = sum A S, per row strip, 64 x ka) and kind-b run
+// (U = sum S B^T, all columns, kb x n) in shared memory across the sub-tiles -- the tile kernel
+// recomputes T for every column tile and U for every row tile of the same output.
+constexpr int kLdU = 2 * kT + 4;  // cached U: kb (<= 64) x 128 columns
+
+template <int Tag>
+__global__ void __launch_bounds__(kThr, 1) gsum_whole_kernel(const GOut* __restrict__ outs,
+                                                           const GTerm* __restrict__ terms,
+                                                           const GTile* __restrict__ tiles, int k2max) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ StageMeta metas[kPS];
+  double* ring = smem;
+  double* Ts = ring + kPS * 2 * kStg;  // 64 x ldT (3-factor intermediates, not cached)
+  const int ldT = k2max + 4;
+  double* Tc = Ts + (size_t)kT * ldT;  // 64 x kLdTc: cached T of the current row strip
+  constexpr int kLdTc = kT + 4;
+  double* Uc = Tc + (size_t)kT * kLdTc;  // 64 x kLdU: cached U, all columns
+  const GOut o = outs[tiles[blockIdx.x].out];
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = warp_row0(), wc = warp_col0();
+  for (int e = threadIdx.x; e < kT * ldT; e += kThr) Ts[e] = 0.0;
+  for (int e = threadIdx.x; e < kT * kLdTc; e += kThr) Tc[e] = 0.0;
+  for (int e = threadIdx.x; e < kT * kLdU; e += kThr) Uc[e] = 0.0;
+  __syncthreads();
+  const int tm = (o.m + kT - 1) / kT, tn = (o.n + kT - 1) / kT;
+  auto single = [](Job J) { return [J](int) { return J; }; };
+  // offsets of the cached intermediates as direct operands (relative to Ts)
+  const int offTc = (int)(Tc - Ts), offUc = (int)(Uc - Ts);
+  bool u_cached = false;
+  for (int ti = 0; ti < tm; ++ti) {
+    bool t_cached = false;
+    for (int tj = 0; tj < tn; ++tj) {
+      const int i0 = ti * kT, j0 = tj * kT;
+      const int mt = min(kT, o.m - i0), nt = min(kT, o.n - j0);
+      Acc acc, aux;
+      acc.zero();
+      bool first4 = true, first5 = true;
+      int ti2 = o.t0;
+      while (ti2 < o.t1) {
+        const GTerm t = terms[ti2];
+        if (t.nf == 0) { ++ti2; continue; }
+        int te = ti2 + 1;
+        if (t.nf == 2 || t.nf == 4 || t.nf == 5)
+          while (te < o.t1 && (terms[te].nf == t.nf || terms[te].nf == 0)) ++te;
+        const int nrun = te - ti2;
+        const GTerm* run = terms + ti2;
+        auto getjob = [run](int j) {
+          const GTerm u = run[j];
+          return Job{u.a, u.b, u.nf == 0 ? 0 : u.k, u.alpha};
+        };
+        if (t.nf == 1) {
+#pragma unroll
+          for (int r = 0; r < kRT; ++r)
+#pragma unroll
+            for (int c = 0; c < kCT; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+                if (i < mt && j < nt) acc.v[r][c][h] += t.alpha * ld(t.a, i0 + i, j0 + j);
+              }
+        } else if (t.nf == 2) {
+          run_stream(acc, nrun, getjob, i0, mt, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
+        } else if (t.nf == 4) {  // T (rows of this strip x ka) = sum A B, then C += T * da
+          const bool cache = first4;
+          first4 = false;
+          if (!(cache && t_cached)) {
+            aux.zero();
+            run_stream(aux, nrun, getjob, i0, mt, 0, o.ka, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
+            acc_to_smem(aux, cache ? Tc : Ts, cache ? kLdTc : ldT, kT, o.ka);
+            __syncthreads();
+            if (cache) t_cached = true;
+          }
+          run_stream(acc, 1, single(Job{MatRef{cache ? Tc : Ts, cache ? kLdTc : ldT, 1}, o.da, o.ka, 1.0}), 0, mt,
+                     j0, nt, true, false, cache ? offTc : 0, 0, ring, metas, Ts, cache ? kLdTc : ldT, ldT);
+        } else if (t.nf == 5) {  // U (kb x all columns) = sum A B, then C += ab * U
+          const bool cache = first5;
+          first5 = false;
+          if (cache && !u_cached) {
+            for (int uj = 0; uj < tn; ++uj) {  // every column strip once, for all row strips
+              aux.zero();
+              const int ju = uj * kT, nu = min(kT, o.n - ju);
+              run_stream(aux, nrun, getjob, 0, o.kb, ju, nu, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
+              acc_to_smem(aux, Uc + ju, kLdU, o.kb, kT);
+            }
+            __syncthreads();
+            u_cached = true;
+          } else if (!cache) {
+            aux.zero();
+            run_stream(aux, nrun, getjob, 0, o.kb, j0, nt, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
+            acc_to_smem(aux, Ts, ldT, o.kb, kT);
+            __syncthreads();
+          }
+          run_stream(acc, 1, single(Job{o.ab, MatRef{cache ? Uc + j0 : Ts, cache ? kLdU : ldT, 1}, o.kb, 1.0}), i0,
+                     mt, 0, nt, false, true, 0, cache ? offUc + j0 : 0, ring, metas, Ts, ldT, cache ? kLdU : ldT);
+        } else {  // nf = 3
+          for (int js = 0; js < t.k2; js += kT) {
+            aux.zero();
+            const int ns = min(kT, t.k2 - js);
+            run_stream(aux, 1, single(Job{t.a, MatRef{t.b.p + (long long)js * t.b.cs, t.b.rs, t.b.cs}, t.k, t.alpha}),
+                       i0, mt, 0, ns, false, false, 0, 0, ring, metas, Ts, ldT, ldT);
+            acc_to_smem(aux, Ts + js, ldT, kT, ns);
+          }
+          __syncthreads();
+          run_stream(acc, 1, single(Job{MatRef{Ts, ldT, 1}, t.d, t.k2, 1.0}), 0, mt, j0, nt, true, false, 0, 0, ring,
+                     metas, Ts, ldT, ldT);
+        }
+        ti2 = te;
+      }
+#pragma unroll
+      for (int r = 0; r < kRT; ++r)
+#pragma unroll
+        for (int c = 0; c < kCT; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+            if (i < mt && j < nt) {
+              double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+              *dst = (o.beta ? *dst : 0.0) + acc.v[r][c][h];
+            }
+          }
+      __syncthreads();  // Ts / ring reuse by the next sub-tile
+    }
+  }
+}
+
+size_t gsum_whole_smem(int k2max) {
+  return sizeof(double) * ((size_t)kPS * 2 * kStg + (size_t)kT * (k2max + 4) + (size_t)kT * (kT + 4) +
+                           (size_t)kT * kLdU);
+}
+
 size_t gsum_pipe_smem(int k2max) {
   return sizeof(double) * ((size_t)kPS * 2 * kStg + (k2max > 0 ? (size_t)kT * (k2max + 4) : 0));
 }
 
 size_t gsum_mma_smem(int k2max) {
   return sizeof(double) * ((size_t)kT * kLdA + (size_t)kKC * kLdB + (k2max > 0 ? (size_t)kT * (k2max + 4) : 0));
+}
+
+cudaError_t launch_gsum_whole(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,
+                              cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute((const void*)gsum_whole_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - 1024);
+  });
+  if (ntiles == 0) return cudaSuccess;
+  gsum_whole_kernel<0><<<ntiles, kThr, gsum_whole_smem(k2max), st>>>(outs, terms, tiles, k2max);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gsum_mma(const GOut* outs, const GTerm* terms, const GTile* tiles, int ntiles, int k2max,

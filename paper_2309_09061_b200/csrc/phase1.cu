@@ -556,6 +556,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
           }
         }
     }
+    g.whole = true;  // one CTA per output up to 128 x 128, grouped intermediates cached across its tiles
     g.prepare_tiles();
     return std::make_pair(std::move(g), fl);
   });
@@ -939,7 +940,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   auto row_pass = [&](Ctx& c, Arena& out, Arena& scr) {
     ev_r[0] = mark_event(c);
     MatStore rwy = basis_weights(c, scr, *y.cb);
-    MatStore zy = total_weights(c, scr, Y, rwy, scaling);
+    MatStore zy = total_weights(c, scr, Y, rwy, scaling, tol < kFloorFreeTol);
     ev_r[1] = mark_event(c);
     Induced r = induced_rows(c, out, X, Y, zy, PRef{&P, false}, tol, max_rank, scaling, 1.0);
     ev_r[2] = mark_event(c);
@@ -948,7 +949,7 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   auto col_pass = [&](Ctx& c, Arena& out, Arena& scr) {
     ev_c[0] = mark_event(c);
     MatStore rwx = basis_weights(c, scr, *x.rb);
-    MatStore zxt = total_weights(c, scr, XT, rwx, scaling);
+    MatStore zxt = total_weights(c, scr, XT, rwx, scaling, tol < kFloorFreeTol);
     ev_c[1] = mark_event(c);
     Induced r = induced_rows(c, out, YT, XT, zxt, PRef{&P, true}, tol, max_rank, scaling, 1.0);
     ev_c[2] = mark_event(c);

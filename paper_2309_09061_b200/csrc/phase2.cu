@@ -307,7 +307,9 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
   // rows of the reference's stack (coarsening.py:237-241): their norms are read back once so that
   // the factor's row count min(M, k) -- the column count of the SVD inputs built from Z -- matches
   std::vector<double> cn_host;
-  if (scale) cn_host = C.read(d_cn, (size_t)std::max(1, pt.nb));  // coupling norms: main-stream work
+  // coupling norms (main-stream work); only needed when the SVD floor can bind (kFloorFreeTol)
+  const bool exact_rows = scale && tol < kFloorFreeTol;
+  if (exact_rows) cn_host = C.read(d_cn, (size_t)std::max(1, pt.nb));
   std::vector<int> Lp;
   for (int lev = 0; lev <= tr.depth; ++lev) {
     StageTag tag(C, "p2.Z.L" + std::to_string(lev));
@@ -330,7 +332,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       }
       for (int b : row_adm[t]) {
         // S_tr^T / ||S_tr||_2 with the norm as a device divisor
-        if (scale && cn_host[b] == 0.0) continue;
+        if (exact_rows && cn_host[b] == 0.0) continue;
         const int kc = w1.rank[pv.col(b)];
         qb.sl.add(trn(g.coup(b)), kc, 1.0, scale ? d_cn + b : nullptr);
         M += kc;
