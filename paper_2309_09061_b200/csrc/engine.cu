@@ -524,39 +524,7 @@ struct GramBatch {
   std::vector<GramWork> work;
   int mmax = 0;
   // lines of hstack(segs[s0:s1]) (hcols) or vstack (rows), m-dimensional; factor into rbuf, rows into *nr
-  // H2G_GRAM_OZ=1: partial Grams on the integer tensor cores (ozaki.cu) instead of the FP64
-  // double-double kernel (gram.cu); both feed the same pivoted Cholesky.  Experimental, off by
-  // default: measured 1.9x slower than the double-double kernel at c4 (digit extraction and the
-  // row-maximum pass are not yet overlapped with the IMMA work) and one golden rank differs (c2).
-  static bool use_oz() {
-    static const bool oz = getenv("H2G_GRAM_OZ") != nullptr;
-    return oz;
-  }
   void add(Arena& scratch, int s0, int s1, int m, long long N, int hcols, double tol, double* rbuf, int* nr) {
-    if (use_oz()) {
-      const long long cl = gram_oz_chunk_lines();
-      const int ncc = (int)std::max<long long>(1, (N + cl - 1) / cl);
-      GramItem g{};
-      g.s0 = s0;
-      g.s1 = s1;
-      g.m = m;
-      g.nslice = ncc;
-      g.N = N;
-      g.hcols = hcols;
-      g.tol = tol;
-      g.gpart = scratch.alloc((size_t)g.nslice * 2 * m * m);
-      g.rbuf = rbuf;
-      g.nr = nr;
-      const int gi = (int)items.size(), tm = gram_oz_tiles_m(m), tn = gram_oz_tiles_n(m);
-      for (int c = 0; c < ncc; ++c)
-        for (int ti = 0; ti < tm; ++ti)
-          for (int tj = 0; tj < tn; ++tj)
-            if (gram_oz_tile_needed(ti, tj))
-              work.push_back(GramWork{gi, ti, tj, c, (long long)c * cl, std::min<long long>(N, (long long)(c + 1) * cl)});
-      items.push_back(g);
-      mmax = std::max(mmax, m);
-      return;
-    }
     const int ncc = (int)std::max<long long>(1, (N + gram_cols() - 1) / gram_cols());
     GramItem g{};
     g.s0 = s0;
@@ -582,10 +550,7 @@ struct GramBatch {
     GramItem* d_it = C.push(items);
     GramWork* d_w = C.push(work);
     C.flush();
-    if (use_oz())
-      cuda_check(launch_gram_oz(d_it, d_segs, d_w, (int)work.size(), (int)items.size(), mmax, C.st), "gram(oz)");
-    else
-      cuda_check(launch_gram(d_it, d_segs, d_w, (int)work.size(), (int)items.size(), mmax, C.st), "gram");
+    cuda_check(launch_gram(d_it, d_segs, d_w, (int)work.size(), (int)items.size(), mmax, C.st), "gram");
     C.launches += 2;
   }
 };

@@ -38,13 +38,6 @@ cudaError_t launch_svd_tsqr(const SvdItem*, const Seg*, const SvdWork*, int nwor
 cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
                         int mmax, cudaStream_t st);
 size_t gram_chol_smem(int m);
-// integer tensor-core (Ozaki) partial Grams + the same Cholesky (ozaki.cu)
-cudaError_t launch_gram_oz(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
-                           int mmax, cudaStream_t st);
-int gram_oz_chunk_lines();
-bool gram_oz_tile_needed(int ti, int tj);
-int gram_oz_tiles_m(int m);
-int gram_oz_tiles_n(int m);
 cudaError_t launch_svd_finish(const SvdItem*, const Seg*, int nitems, size_t smem, bool rsmem, bool vsmem, int nmax,
                               cudaStream_t);
 cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
