@@ -163,6 +163,9 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
     if (part.on()) Lp = part.filter(tr.by_level[lev]);
     const std::vector<int>& L = part.on() ? Lp : tr.by_level[lev];
     StageTag tag(C, "p1.L" + std::to_string(lev));
+    // this level's temporaries (vhat, projected blocks, ahat, weighted stacks, SVD scratch): freed
+    // stream-ordered at the end of the level
+    Arena lvl(C.st);
     GBatch g1, g2;
     std::vector<Mat>& rf = rfb;
     for (int t : L) {
@@ -174,7 +177,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       const int kx = VX.rank[t];
       int m = 0;
       for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
-      Mat vh{sc.alloc((size_t)m * kx), m, kx};
+      Mat vh{lvl.alloc((size_t)m * kx), m, kx};
       int off = 0;
       for (int i = 0; i < tr.nkids(t); ++i) {  // vhat = vstack(bc_c E_X,c) (induced.py:177-178)
         const int c = tr.kid(t, i);
@@ -188,7 +191,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
           const int b2 = B.kid(b, i);
           if (!B.adm_leaf(b2)) continue;
           const int t2 = x.row(b2), s2 = x.col(b2);
-          Mat m2{sc.alloc((size_t)q.rank[t2] * VY.rank[s2]), q.rank[t2], VY.rank[s2]};
+          Mat m2{lvl.alloc((size_t)q.rank[t2] * VY.rank[s2]), q.rank[t2], VY.rank[s2]};
           g1.out(m2, false);
           g1.t3(R.bc[t2].ref(), x.coup(b2), P.at(s2), R.bc[t2].c, P.rows(s2));
           rf[b2] = m2;
@@ -200,7 +203,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       const int m = vx[t].r;
       for (int b : mids[t]) {
         const int s = x.col(b);
-        Mat A{sc.alloc((size_t)m * VY.rank[s]), m, VY.rank[s]};
+        Mat A{lvl.alloc((size_t)m * VY.rank[s]), m, VY.rank[s]};
         blk[b] = A;
         int off = 0;
         for (int i = 0; i < tr.nkids(t); ++i) {
@@ -236,7 +239,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
           it.out = d_nrm + b;
           nbat.items.push_back(it);
         }
-      nbat.scratch = &sc;
+      nbat.scratch = &lvl;
       nbat.run_async(C);
     }
 
@@ -253,7 +256,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       for (int b : mids[t]) {
         const Mat& Z = zy[x.col(b)];
         if (Z.r == 0 || m == 0) continue;
-        Mat w{sc.alloc((size_t)m * Z.r), m, Z.r};
+        Mat w{lvl.alloc((size_t)m * Z.r), m, Z.r};
         g3.out(w, false);
         g3.t2(blk[b].ref(), Z.tref(), Z.c);
         sv.sl.add(w.ref(), Z.r, 1.0, scale ? d_nrm + b : nullptr);  // w_i = blk_i Z_s^T / ||blk_i||
@@ -275,7 +278,7 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       sv.items.push_back(it);
     }
     g3.run(C);
-    std::vector<int> rk = sv.run(C, sc);
+    std::vector<int> rk = sv.run(C, lvl);
 
     GBatch g4;
     for (size_t li = 0; li < L.size(); ++li) {
@@ -304,6 +307,13 @@ Induced induced_rows(Ctx& C, Arena& out, HView x, HView y, const MatStore& zy, P
       }
     }
     g4.run(C);
+    for (int t : L)  // blk / rf entries of this level point into lvl
+      if (!tr.leaf(t))
+        for (int b : mids[t]) {
+          blk[b] = Mat{};
+          for (int i = 0; i < B.nkids(b); ++i) rfb[B.kid(b, i)] = Mat{};
+        }
+    mem_mark(("p1 L" + std::to_string(lev) + " ch" + std::to_string(C.channel)).c_str());
     if (part.on() && lev == part.level) {
       C.gate_enter();
       exchange_induced(C, out, part, x, y, mids, R, !x.T);  // row pass: x is X itself (not transposed)

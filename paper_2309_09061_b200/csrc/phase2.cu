@@ -356,6 +356,11 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
     const std::vector<int>& L = part.on() ? Lp : tr.by_level[lev];
     const size_t nl = L.size();
     StageTag tag(C, "p2.B.L" + std::to_string(lev));
+    // this level's temporaries (V_t, V_t Z_t^T, merged representations, admissible-leaf products,
+    // SVD scratch): freed stream-ordered when the level is done, so the pass's footprint is one
+    // level's scratch instead of the sum over levels
+    Arena lvl(C.st);
+    std::vector<int> lm_level;  // lm entries allocated from lvl (cleared with it)
     HostTimer htv(C, "p2_vz_plan");
     GBatch g1, g2;
     std::vector<Mat> V(nl), VZ(nl);
@@ -367,7 +372,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       } else {
         int m = 0;
         for (int i = 0; i < tr.nkids(t); ++i) m += q.rank[tr.kid(t, i)];
-        V[li] = Mat{sc.alloc((size_t)m * v1.rank[t]), m, v1.rank[t]};
+        V[li] = Mat{lvl.alloc((size_t)m * v1.rank[t]), m, v1.rank[t]};
         int off = 0;
         for (int i = 0; i < tr.nkids(t); ++i) {  // vhat = vstack(R_c E_c) (coarsening.py:313-314)
           const int c = tr.kid(t, i);
@@ -380,12 +385,13 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
             const int b2 = pt.kid(b, i);
             if (!pt.adm_leaf(b2) || lm[b2].p) continue;
             const int t2 = pv.row(b2), r2 = pv.col(b2);
-            lm[b2] = Mat{sc.alloc((size_t)q.rank[t2] * w1.rank[r2]), q.rank[t2], w1.rank[r2]};
+            lm[b2] = Mat{lvl.alloc((size_t)q.rank[t2] * w1.rank[r2]), q.rank[t2], w1.rank[r2]};
+            lm_level.push_back(b2);
             g1.out(lm[b2], false);
             g1.t2(S.r[t2].ref(), g.coup(b2), S.r[t2].c);
           }
       }
-      VZ[li] = Mat{sc.alloc((size_t)V[li].r * Z.r), V[li].r, Z.r};
+      VZ[li] = Mat{lvl.alloc((size_t)V[li].r * Z.r), V[li].r, Z.r};
       GBatch& gz = tr.leaf(t) ? g1 : g2;
       gz.out(VZ[li], false);
       gz.t2(V[li].ref(), Z.tref(), Z.c);
@@ -448,7 +454,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
             if (!tgt.leaf(u)) continue;
             const int c = tgt.cl[u];
             const int cols = tgt.adm[u] ? w1.rank[c] : w1.tree->size(c);
-            tgt.mat[u] = Mat{sc.alloc((size_t)rows * cols), rows, cols};
+            tgt.mat[u] = Mat{lvl.alloc((size_t)rows * cols), rows, cols};
           }
           int ro = 0;
           for (int i = 0; i < gcnt[gi]; ++i) {
@@ -473,8 +479,9 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       fprintf(stderr, "level %d: %zu merged reps, %zu nodes, %zu jobs, path pool %zu\n", lev, mblocks.size(),
               mpool.cl.size(), J.v.size(), J.pool.size());
     htm.next("p2_merge_resolve");
-    resolve_jobs(C, sc, J, w1);
+    resolve_jobs(C, lvl, J, w1);
     }
+    mem_mark(("p2 L" + std::to_string(lev) + " ch" + std::to_string(C.channel) + " reps").c_str());
 
     // scales of the flattened merged reps (coarsening.py:316-317), kept on the device
     std::vector<int> lv;
@@ -537,7 +544,8 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       it.q_out = qbuf[li].p;
       sv.items.push_back(it);
     }
-    std::vector<int> rk = sv.run(C, sc);
+    std::vector<int> rk = sv.run(C, lvl);
+    mem_mark(("p2 L" + std::to_string(lev) + " ch" + std::to_string(C.channel) + " svd").c_str());
 
     HostTimer htp(C, "p2_post");
     S.pools.emplace_back(new CT());
@@ -622,6 +630,7 @@ static CState coarse_rows(Ctx& C, Arena& out, HView g, BView coarse, double tol,
       for (int b : sub_cov[t]) all(b);
     }
     gq.run(C);
+    for (int b : lm_level) lm[b] = Mat{};
     if (part.on() && lev == part.level) {
       // every rank receives the partitioned levels' ranks, Q_t and R_t (the representations stay
       // with their rank: only its own rows' final projection reads them)
@@ -1129,6 +1138,7 @@ static std::shared_ptr<Basis> orthogonalize(Ctx& C, Arena& out, const Basis& B, 
     }
     g.run(C);
     std::vector<int> rk = sv.run(C, sc);
+    mem_mark(("p2 L" + std::to_string(lev) + " ch" + std::to_string(C.channel) + " svd").c_str());
     GBatch g2;
     for (size_t li = 0; li < L.size(); ++li) {
       const int t = L[li];

@@ -148,9 +148,11 @@ def test_partitioned_product_meets_golden_bars(world, names):
     for rank, (res, _, _) in out.items():
         for name, r in res.items():
             print(rank, name, "memory ratio", round(r["mem_ratio"], 3), r.get("bytes", ""))
-            if name == "mem:c2_full":  # n = 16,384 at P = 2 (measured 0.68: G, Z and the pass scratch
-                # halve; the inputs, the exchanged bases and the top levels are replicated)
-                assert r["mem_ratio"] <= 0.72, (rank, r)
+            if name == "mem:c2_full":  # n = 16,384 at P = 2: G, Z and the pass scratch halve; the
+                # transpose halo of G (~35 % of G on this sphere), the exchanged bases and the top levels
+                # do not.  Measured 0.72 (1.50 vs 2.07 GB) with per-level scratch arenas (0.68 = 1.79 vs
+                # 2.63 GB before them: the single-rank peak fell further than the per-rank one)
+                assert r["mem_ratio"] <= 0.75, (rank, r)
 
 
 def _nccl_worker(port, q):
