@@ -142,6 +142,10 @@ Ctx::Ctx(int dev, cudaStream_t s, int priority) : device(dev), st(s) {
 
 Ctx::~Ctx() {
   cudaStreamSynchronize(st);
+  if (mv_st) {
+    cudaStreamSynchronize(mv_st);
+    cudaStreamDestroy(mv_st);
+  }
   if (up_stream) {
     cudaStreamSynchronize(up_stream);
     cudaStreamDestroy(up_stream);
@@ -286,6 +290,15 @@ Ctx& Ctx::aux() {
   aux_->trace_out = trace_out;
   aux_->channel = 2;  // no collectives
   return *aux_;
+}
+
+cudaStream_t Ctx::mv_stream() {
+  if (!mv_st) {
+    int prio = 0;
+    cudaStreamGetPriority(st, &prio);
+    cuda_check(cudaStreamCreateWithPriority(&mv_st, cudaStreamNonBlocking, prio), "matvec stream");
+  }
+  return mv_st;
 }
 
 Ctx& Ctx::side() {

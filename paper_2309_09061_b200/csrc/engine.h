@@ -167,6 +167,7 @@ struct H2 {
   }
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
   std::vector<std::shared_ptr<const void>> keep;  // other structure this matrix points into
+  mutable std::shared_ptr<struct MvPlan> mv_plan[2];  // cached matvec launch plans (plain, transposed)
   // phase-2 block-norm batches of this matrix (product output): built on a host thread while the
   // assembly runs on the GPU, consumed by coarsen (declared last: joined before the rest goes)
   std::shared_future<std::shared_ptr<struct NormPrep>> norm_prep;
@@ -309,6 +310,8 @@ struct Ctx {
   char* up_host = nullptr;
   size_t up_cap = 0;
   std::unique_ptr<Ctx> aux_;   // low-priority stream: work ahead of the critical path (dense targets)
+  cudaStream_t mv_st = nullptr;  // matvec nearfield stream (concurrent with the transform chain)
+  cudaStream_t mv_stream();
   Ctx(int dev, cudaStream_t s, int priority = 0);
   ~Ctx();
   Ctx& side();
@@ -455,31 +458,9 @@ struct SvdBatch {
   std::vector<int> run(Ctx& C, Arena& scratch);  // sync + ranks (k1 + k2)
 };
 
-// Batched small GEMVs (matvec.cu): y (m) = (beta ? y : 0) + sum alpha * A (m x k) x (k).
-struct MvTerm {
-  MatRef a;
-  const double* x;
-  int k, pad_;
-  double alpha;
-};
-struct MvOut {
-  double* y;
-  int m, t0, t1, beta;
-};
-struct MvBatch {
-  std::vector<MvOut> outs;
-  std::vector<MvTerm> terms;
-  double bytes_a = 0.0;  // matrix bytes read (profile ledger)
-  void out(double* y, int m, bool beta) {
-    outs.push_back(MvOut{y, m, (int)terms.size(), (int)terms.size(), beta ? 1 : 0});
-  }
-  void term(MatRef a, const double* x, int k, double alpha, double elems) {
-    terms.push_back(MvTerm{a, x, k, 0, alpha});
-    outs.back().t1 = (int)terms.size();
-    bytes_a += 8.0 * elems;
-  }
-  void run(Ctx& C);
-};
+// H^2 matvec launch plan (matvec.cu): descriptors built and uploaded once per matrix and orientation,
+// replayed with the call's x, y, alpha and accumulate flag.
+struct MvPlan;
 
 using MatStore = std::vector<Mat>;
 struct PRef {  // basis product view (transposed for the column pass)

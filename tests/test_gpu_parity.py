@@ -224,6 +224,28 @@ def test_gpu_matvec_matches_host(name):
         assert abs(gv @ u - v @ gtu) <= 1e-12 * np.linalg.norm(gv) * np.linalg.norm(u)
 
 
+@pytest.mark.parametrize("name", ["c1"] + RANDOM_CASES)
+def test_gpu_matvec_on_reference_z(name):
+    """The GPU matvec / adjoint (csrc/matvec.cu) applied to the reference's OWN product Z (stored
+    packed in the fixture) reproduces the reference's own h2_matvec / h2_matvec_adjoint outputs
+    (h2.py:224-267, recorded as probe.zv / probe.ztv by make_golden.py:198-215): the same matrix, so
+    only the summation order differs (<= 1e-13)."""
+    P = _P()
+    import torch
+    from paper_2309_09061_b200.packed import unpack_h2
+    d = load(name)
+    if "z/bt.row" not in d:
+        pytest.skip("fixture without the reference Z")
+    x = unpack_h2(d, "x/") if "x/bt.row" in d else None
+    zr = unpack_h2(d, "z/", rows=x.block_tree.rows if x is not None else None,
+                   cols=x.block_tree.cols if x is not None else None)
+    dz = P.DeviceH2.upload(zr)
+    for i, v in enumerate(d["probe.v"]):
+        vt = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        assert rel(dz.matvec(vt).cpu().numpy(), d["probe.zv"][i]) <= 1e-13
+        assert rel(dz.matvec(vt, trans=True).cpu().numpy(), d["probe.ztv"][i]) <= 1e-13
+
+
 @pytest.mark.parametrize("name", RANDOM_CASES + CONFIG_CASES)
 def test_gpu_error_estimate_matches_reference(name):
     """GPU power-iteration |XY - Z|_2 / |XY|_2 (bench.py:147-174) against the reference's own value."""
