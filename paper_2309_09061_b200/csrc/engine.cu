@@ -275,21 +275,24 @@ void Ctx::flush() {
   }
 }
 
-Ctx& Ctx::aux() {
-  if (!aux_) {
+Ctx& Ctx::aux(bool urgent) {
+  std::unique_ptr<Ctx>& a = urgent ? aux_hi_ : aux_;
+  if (!a) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    aux_.reset(new Ctx(device, nullptr, least));
+    int prio = least;
+    if (urgent) cudaStreamGetPriority(st, &prio);  // as urgent as the main stream
+    a.reset(new Ctx(device, nullptr, prio));
   }
-  aux_->timing = timing;
-  aux_->prof = prof;
-  aux_->trace = trace;
-  aux_->trace_tid = 2;
-  aux_->trace_base = trace_base;
-  aux_->trace_host0 = trace_host0;
-  aux_->trace_out = trace_out;
-  aux_->channel = 2;  // no collectives
-  return *aux_;
+  a->timing = timing;
+  a->prof = prof;
+  a->trace = trace;
+  a->trace_tid = urgent ? 3 : 2;
+  a->trace_base = trace_base;
+  a->trace_host0 = trace_host0;
+  a->trace_out = trace_out;
+  a->channel = 2;  // no collectives
+  return *a;
 }
 
 cudaStream_t Ctx::mv_stream() {
@@ -765,7 +768,7 @@ void NormBatch::run_async(Ctx& C) {
   size_t smem = 0, smem_g = 0;
   // small: single segment, both sides <= 64 / 128 (warp Lanczos); big: CTA Gram in shared memory;
   // huge: CTA Gram in global scratch
-  std::vector<NormItem> big, small, huge, mid;  // mid: single segment up to 128 x 128 (CTA Lanczos)
+  std::vector<NormItem> big, small, huge, mid, lz;  // mid / lz: single segment up to 128 x 128 (CTA Lanczos)
   size_t smem_mid = 0;
   std::unique_ptr<Arena> local;
   for (auto& it : items) {
@@ -776,6 +779,13 @@ void NormBatch::run_async(Ctx& C) {
       continue;
     }
     if (it.s1 - it.s0 == 1 && it.m <= 128 && it.N <= 128) {
+      // large ones (the 128 x 128 nearfield blocks) keep A in registers (norm_lz_kernel, one CTA per
+      // SM: 1.9x on them); smaller ones run several shared-memory CTAs per SM (norm_cta_kernel)
+      static const bool cta_all = getenv("H2G_NORM_CTA") != nullptr;  // A/B: shared-memory kernel only
+      if (!cta_all && it.m * it.N > 96 * 96) {
+        lz.push_back(it);
+        continue;
+      }
       smem_mid = std::max(smem_mid, norm_cta_smem(it.m, (int)it.N));
       mid.push_back(it);
       continue;
@@ -796,10 +806,10 @@ void NormBatch::run_async(Ctx& C) {
     smem_g = std::max(smem_g, norm_smem(it.m, it.N, false));
     huge.push_back(it);
   }
-  if (!big.empty() || !small.empty() || !huge.empty() || !mid.empty()) {
+  if (!big.empty() || !small.empty() || !huge.empty() || !mid.empty() || !lz.empty()) {
     double fl = 0, by = 0;
     if (C.prof)
-      for (auto* v : {&big, &small, &huge, &mid})
+      for (auto* v : {&big, &small, &huge, &mid, &lz})
         for (auto& it : *v) {  // Gram on the short side + tridiagonalisation (reference's work)
           const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
           fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
@@ -829,6 +839,12 @@ void NormBatch::run_async(Ctx& C) {
       NormItem* d_mid = C.push(mid);
       C.flush();
       cuda_check(launch_norm_cta(d_mid, d_s, (int)mid.size(), smem_mid, C.st), "norm_cta");
+      ++C.launches;
+    }
+    if (!lz.empty()) {
+      NormItem* d_lz = C.push(lz);
+      C.flush();
+      cuda_check(launch_norm_lz(d_lz, d_s, (int)lz.size(), C.st), "norm_lz");
       ++C.launches;
     }
     C.prof_end(K_NORM, ev, fl, by);

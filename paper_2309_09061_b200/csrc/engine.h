@@ -44,6 +44,7 @@ cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cu
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
 cudaError_t launch_norm_cta(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t);
+cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
 size_t norm_cta_smem(int m, int N);
 cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t);
 cudaError_t launch_tile_absorb(const TileItem*, const Seg*, const TileWork*, int nwork, int nmax, cudaStream_t);
@@ -310,12 +311,13 @@ struct Ctx {
   char* up_host = nullptr;
   size_t up_cap = 0;
   std::unique_ptr<Ctx> aux_;   // low-priority stream: work ahead of the critical path (dense targets)
+  std::unique_ptr<Ctx> aux_hi_;  // normal-priority auxiliary stream (phase-2 nearfield norms)
   cudaStream_t mv_st = nullptr;  // matvec nearfield stream (concurrent with the transform chain)
   cudaStream_t mv_stream();
   Ctx(int dev, cudaStream_t s, int priority = 0);
   ~Ctx();
   Ctx& side();
-  Ctx& aux();
+  Ctx& aux(bool urgent = false);  // urgent: main-stream priority instead of the lowest
   void join_side(Ctx& S);  // main stream waits for the side stream's queued work
   void* stage(const void* src, size_t bytes);  // returns device pointer (copied at the next flush())
   void flush();  // enqueue the host->device copy of everything staged since the last flush

@@ -1199,6 +1199,7 @@ __device__ double sturm_lambda_max(const double* d, const double* e, int g, doub
       } else {
         nlo = lo + (hi - lo) * 32.0 / 33.0;
       }
+      if (nlo == lo && nhi == hi) break;  // a few ulps wide: no further progress possible
       lo = nlo;
       hi = nhi;
     }
@@ -1410,6 +1411,9 @@ __device__ double warp_lambda_max(const double* d, const double* e, int g) {
     if (f1) first = min(first, 2 * (__ffs(f1) - 1) + 2);
     const double nhi = first < 65 ? lo + w * first : hi;
     const double nlo = first < 65 ? lo + w * (first - 1) : lo + w * 64.0;
+    // a bracket a few ulps wide cannot shrink further (its points round onto its ends): stop there
+    // instead of spinning through the remaining rounds
+    if (nlo == lo && nhi == hi) break;
     lo = nlo;
     hi = nhi;
   }
@@ -1715,7 +1719,7 @@ __global__ void __launch_bounds__(kNCThreads) norm_cta_kernel(const NormItem* __
       break;
     }
     if (tid == 0) be[k] = b;
-    if ((k & 1) == 1 && k >= 5) {  // top Ritz value settled to 1e-14 relative: stop
+    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
       __syncthreads();
       if (warp == 0) {
         const double th = warp_lambda_max(al, be, k + 1);
@@ -1752,6 +1756,165 @@ cudaError_t launch_norm_cta(const NormItem* items, const Seg* segs, int nitems, 
   init_attributes();
   if (nitems == 0) return cudaSuccess;
   norm_cta_kernel<<<nitems, kNCThreads, smem, st>>>(items, segs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// norm_lz_kernel: sigma_1 of a single-segment matrix with m, N <= 128 (the product's nearfield blocks
+// and k~ x k~ couplings, phase 2's block norms), replacing norm_cta_kernel for them.  The matrix lives
+// in REGISTERS: 512 threads, thread (rg, cg) holds A[rg + 32p][cg + 16q] (p < 4, q < 8; lanes 0-15 of
+// a warp cover 16 consecutive columns, so every load instruction reads full lines), so the Lanczos
+// matvecs u = A v, w = A^T u never touch shared memory for A (the shared-memory version moved
+// 2 x 128 KB per iteration through 128 B/clk and held one CTA per SM for its A).  u is reduced over
+// the 16 column lanes by shuffles, w over the 32 row groups by one shuffle step and a 16-way
+// shared-memory sum.  Lanczos on A^T A with the same start vector, early exit and exact-zero rule as
+// norm_cta_kernel; the top Ritz value is re-evaluated every 2 steps from step 7.
+// ---------------------------------------------------------------------------------------------
+static constexpr int kLzThreads = 512;
+
+__global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* __restrict__ items,
+                                                                const Seg* __restrict__ segs) {
+  __shared__ double part[16][kNC];   // w partials per warp
+  __shared__ double vs[kNC];         // current Lanczos vector
+  __shared__ double red[2][4];
+  __shared__ double al[kNC], be[kNC];
+  __shared__ double amax_s[16];
+  __shared__ double lam_s;
+  __shared__ int stop_s;
+  const NormItem it = items[blockIdx.x];
+  const Seg sg = segs[it.s0];
+  const int m = it.m, N = (int)it.N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cg = lane & 15, rg = 2 * warp + (lane >> 4);
+  const double ssc = seg_scale(sg);
+  double a[4][8];
+  double amax = 0.0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = rg + 32 * p, j = cg + 16 * q;
+      const double x = (i < m && j < N) ? ssc * __ldg(sg.a.p + (long long)i * sg.a.rs + (long long)j * sg.a.cs) : 0.0;
+      a[p][q] = x;
+      amax = fmax(amax, fabs(x));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) amax_s[warp] = amax;
+  // deterministic pseudo-random positive start vector (as norm_cta_kernel), length N
+  double vt = 0.0;
+  if (tid < N) {
+    unsigned x = 2654435761u * (tid + 1) ^ (tid < 32 ? 0x9e3779b9u : 0x85ebca6bu);
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    vt = 0.5 + (double)(x & 0xffff) / 65536.0;
+  }
+  auto sum4 = [&](double x, int slot) -> double {  // sum over threads 0..127 (warps 0-3); all call
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (warp < 4 && lane == 0) red[slot][warp] = x;
+    __syncthreads();
+    return (red[slot][0] + red[slot][1]) + (red[slot][2] + red[slot][3]);
+  };
+  {
+    const double nv = sqrt(sum4(tid < N ? vt * vt : 0.0, 0));
+    double mx = 0.0;
+    for (int w = 0; w < 16; ++w) mx = fmax(mx, amax_s[w]);
+    if (mx == 0.0) {
+      if (tid == 0) *it.out = 0.0;
+      return;
+    }
+    vt = tid < N ? vt / nv : 0.0;
+    if (tid < kNC) vs[tid] = vt;  // zero past N: the matvec reads all 128 (0 * uninitialised may be NaN)
+  }
+  __syncthreads();
+  const int g = min(m, N);
+  double vprev = 0.0, bprev = 0.0, theta = 0.0, done = -1.0;
+  int k = 0;
+  for (; k < g; ++k) {
+    // u = A v over this thread's 4 rows, reduced over the 16 column lanes
+    double vq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) vq[q] = vs[cg + 16 * q];
+    double u[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        s0 = fma(a[p][q], vq[q], s0);
+        s1 = fma(a[p][q + 1], vq[q + 1], s1);
+      }
+      u[p] = s0 + s1;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) u[p] += __shfl_xor_sync(0xffffffffu, u[p], o);
+    // w = A^T u over this thread's 8 columns, reduced over the two row groups of the warp, then
+    // over the 16 warps in shared memory (fixed order)
+    double w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) s = fma(a[p][q], u[p], s);
+      w[q] = s + __shfl_xor_sync(0xffffffffu, s, 16);
+    }
+    if (lane < 16)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) part[warp][cg + 16 * q] = w[q];
+    __syncthreads();
+    double wt = 0.0;
+    if (tid < N) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 16; ww += 2) {
+        s0 += part[ww][tid];
+        s1 += part[ww + 1][tid];
+      }
+      wt = s0 + s1;
+    }
+    const double alpha = sum4(wt * vt, 0);
+    if (tid < N) wt -= alpha * vt + bprev * vprev;
+    const double b = sqrt(sum4(tid < N ? wt * wt : 0.0, 1));
+    if (tid == 0) al[k] = alpha;
+    if (k + 1 == g || b <= 1e-15 * (fabs(alpha) + bprev)) {
+      ++k;
+      break;
+    }
+    if (tid == 0) be[k] = b;
+    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
+      __syncthreads();
+      if (warp == 0) {
+        const double th = warp_lambda_max(al, be, k + 1);
+        if (lane == 0) {
+          lam_s = th;
+          stop_s = th - theta <= 1e-14 * th;
+        }
+      }
+      __syncthreads();
+      if (stop_s) {
+        done = lam_s;
+        break;
+      }
+      theta = lam_s;
+    }
+    vprev = vt;
+    bprev = b;
+    vt = tid < N ? wt / b : 0.0;
+    if (tid < kNC) vs[tid] = vt;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double lam = done >= 0.0 ? done : warp_lambda_max(al, be, k);
+    if (lane == 0) *it.out = sqrt(fmax(lam, 0.0));
+  }
+}
+
+cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, cudaStream_t st) {
+  if (nitems == 0) return cudaSuccess;
+  norm_lz_kernel<<<nitems, kLzThreads, 0, st>>>(items, segs);
   return cudaGetLastError();
 }
 

@@ -1001,7 +1001,9 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   double* d_cn = sc.alloc(std::max(1, g.bt->nb));
   if (scale) {
     StageTag tag(C, "p2.norms");
-    if (!serial_passes()) all_norms(C, sc, g, d_cn, d_nn, &C.aux(), &nn_ready);
+    // the nearfield norms gate the leaf-level SVDs: on a normal-priority auxiliary stream (the
+    // low-priority one was starved by the Z levels and made the leaf SVDs wait ~26 ms at c4)
+    if (!serial_passes()) all_norms(C, sc, g, d_cn, d_nn, &C.aux(true), &nn_ready);
     else all_norms(C, sc, g, d_cn, d_nn);
   }
   const cudaEvent_t ev_norms = mark_event(C);
@@ -1075,7 +1077,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
     Z->owned.push_back(pf.arena);
   }
   Z->owned.push_back(ar2);
-  if (nn_ready) C.join_side(C.aux());  // counters / profile of the auxiliary stream's norms
+  if (nn_ready) C.join_side(C.aux(true));  // counters / profile of the auxiliary stream's norms
   Z->own_rows = g.own_rows;
   Z->own_cols = g.own_cols;
   if (C.timing) {

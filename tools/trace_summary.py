@@ -53,5 +53,5 @@ for e in sub:
     key = (e.get("args", {}).get("tag", ""), e["tid"])
     if key in tags: tags[key][5][e["name"]] = tags[key][5].get(e["name"], 0) + e["dur"]
 for (tag, tid), t in sorted(tags.items(), key=lambda kv: kv[1][2]):
-    print(f"  {tag:14s} s{tid}  n={t[0]:3d}  dev {t[1]/1e3:6.2f}  span {(t[3]-t[2])/1e3:6.2f}  {t[4]:7.3f} GF  "
+    print(f"  {tag:14s} s{tid}  n={t[0]:3d}  [{t[2]/1e3:7.1f} .. {t[3]/1e3:7.1f}]  dev {t[1]/1e3:6.2f}  span {(t[3]-t[2])/1e3:6.2f}  {t[4]:7.3f} GF  "
           + " ".join(f"{k}:{v/1e3:.2f}" for k, v in sorted(t[5].items(), key=lambda kv: -kv[1])))
