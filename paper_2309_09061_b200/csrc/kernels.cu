@@ -1152,8 +1152,8 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
 }
 
 // ---------------------------------------------------------------------------------------------
-// norm_kernel: sigma_1 of hstack(segs) (m x N).  Gram on the row side (m <= N),
-// else on the column side; tridiagonalise; Sturm multisection for lambda_max.
+// norm_kernel: sigma_1 of hstack(segs) (m x N).  Gram on the row side (m <= N), else on the column
+// side; Lanczos on the Gram with Sturm multisection on its tridiagonal for lambda_max.
 // ---------------------------------------------------------------------------------------------
 
 __device__ double sturm_lambda_max(const double* d, const double* e, int g, double* red) {
@@ -1210,6 +1210,8 @@ __device__ double sturm_lambda_max(const double* d, const double* e, int g, doub
   __syncthreads();
   return r;
 }
+
+__device__ double warp_lambda_max(const double* d, const double* e, int g);
 
 __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restrict__ items,
                                                         const Seg* __restrict__ segs) {
@@ -1278,65 +1280,87 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
     if (j < i) G[q] = G[j * g + i];
   }
   __syncthreads();
-  // Householder tridiagonalisation (lower), trailing block updated in place
-  for (int j = 0; j + 2 < g; ++j) {
-    double part = 0.0;
-    for (int i = j + 2 + threadIdx.x; i < g; i += blockDim.x) part += G[i * g + j] * G[i * g + j];
-    part = warp_sum(part);
-    if (lane == 0) red[warp] = part;
+  // Lanczos on the symmetric Gram (sigma_1^2 = lambda_max(G)) with the early exit of the Lanczos
+  // kernels -- a few block-wide G v products instead of g Householder steps of five barriers each
+  // (the tridiagonalisation was the bulk of this kernel on phase 2's merged representations)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* al = d;      // Lanczos diagonal (g)
+  double* be = e;      // off-diagonal (g)
+  double* q = p + g;   // previous Lanczos vector (g); p holds w
+  auto block_sum = [&](double x) -> double {
+    x = warp_sum(x);
+    __syncthreads();
+    if (lane == 0) red[warp] = x;
     __syncthreads();
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += red[w];
-    const double alpha = G[(j + 1) * g + j];
-    __syncthreads();
-    if (s == 0.0) {
-      if (threadIdx.x == 0) { e[j] = alpha; d[j] = G[j * g + j]; }
-      __syncthreads();
-      continue;
-    }
-    const double nrm = sqrt(alpha * alpha + s);
-    const double beta = alpha >= 0.0 ? -nrm : nrm;
-    const double tau = (beta - alpha) / beta;
-    const double scale = 1.0 / (alpha - beta);
-    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) v[i] = (i == j + 1) ? 1.0 : G[i * g + j] * scale;
-    __syncthreads();
-    // p = tau * G' v
-    for (int i = j + 1 + warp; i < g; i += nw) {
-      double acc = 0.0;
-      for (int c = j + 1 + lane; c < g; c += 32) acc = fma(G[i * g + c], v[c], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) p[i] = tau * acc;
-    }
-    __syncthreads();
-    double pv = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) pv += p[i] * v[i];
-    pv = warp_sum(pv);
-    if (lane == 0) red[warp] = pv;
-    __syncthreads();
-    double kk = 0.0;
-    for (int w = 0; w < nw; ++w) kk += red[w];
-    kk *= 0.5 * tau;
-    __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < g; i += blockDim.x) p[i] -= kk * v[i];  // w
-    __syncthreads();
-    const int t = g - j - 1;
-    for (int q = threadIdx.x; q < t * t; q += blockDim.x) {
-      const int i = j + 1 + q / t, c = j + 1 + q % t;
-      G[i * g + c] -= v[i] * p[c] + p[i] * v[c];
-    }
-    if (threadIdx.x == 0) { e[j] = beta; d[j] = G[j * g + j]; }
-    __syncthreads();
+    return s;
+  };
+  double part = 0.0;
+  for (int i = tid; i < g; i += nt) {
+    unsigned x = 2654435761u * (i + 1) ^ (i < 32 ? 0x9e3779b9u : 0x85ebca6bu);
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    v[i] = 0.5 + (double)(x & 0xffff) / 65536.0;
+    q[i] = 0.0;
+    part += v[i] * v[i];
   }
-  if (threadIdx.x == 0) {
-    if (g >= 2) {
-      d[g - 2] = G[(g - 2) * g + (g - 2)];
-      e[g - 2] = G[(g - 1) * g + (g - 2)];
+  const double nv = sqrt(block_sum(part));
+  for (int i = tid; i < g; i += nt) v[i] /= nv;
+  __syncthreads();
+  double bprev = 0.0, theta = 0.0, done = -1.0;
+  int k = 0;
+  for (; k < g; ++k) {
+    double pa = 0.0;
+    for (int i = tid; i < g; i += nt) {  // w = G v: column i of the symmetric G (conflict-free)
+      double s0 = 0.0, s1 = 0.0;
+      int j = 0;
+      for (; j + 1 < g; j += 2) {
+        s0 = fma(G[(long long)j * g + i], v[j], s0);
+        s1 = fma(G[(long long)(j + 1) * g + i], v[j + 1], s1);
+      }
+      if (j < g) s0 = fma(G[(long long)j * g + i], v[j], s0);
+      p[i] = s0 + s1;
+      pa += p[i] * v[i];
     }
-    d[g - 1] = G[(g - 1) * g + (g - 1)];
+    const double a = block_sum(pa);
+    double pb = 0.0;
+    for (int i = tid; i < g; i += nt) {
+      p[i] -= a * v[i] + bprev * q[i];
+      pb += p[i] * p[i];
+    }
+    const double bb = sqrt(block_sum(pb));
+    if (tid == 0) al[k] = a;
+    if (k + 1 == g || bb <= 1e-15 * (fabs(a) + bprev)) {
+      ++k;
+      break;
+    }
+    if (tid == 0) be[k] = bb;
+    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
+      __syncthreads();
+      if (warp == 0) {
+        const double th = warp_lambda_max(al, be, k + 1);
+        if (lane == 0) red[nw] = th;
+      }
+      __syncthreads();
+      const double th = red[nw];
+      if (th - theta <= 1e-14 * th) {
+        done = th;
+        break;
+      }
+      theta = th;
+    }
+    for (int i = tid; i < g; i += nt) {
+      q[i] = v[i];
+      v[i] = p[i] / bb;
+    }
+    bprev = bb;
+    __syncthreads();
   }
   __syncthreads();
-  const double lam = sturm_lambda_max(d, e, g, red);
-  if (threadIdx.x == 0) *it.out = sqrt(fmax(lam, 0.0));
+  if (warp == 0) {
+    const double lam = done >= 0.0 ? done : warp_lambda_max(al, be, k);
+    if (lane == 0) *it.out = sqrt(fmax(lam, 0.0));
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2115,7 +2139,7 @@ size_t norm_smem(int m, long long N, bool gram_in_smem) {
   const bool rowside = m <= N;  // Gram on the smaller side
   const int g = rowside ? m : (int)N;
   const int w = rowside ? m : (int)N;
-  return sizeof(double) * ((gram_in_smem ? (size_t)g * g : 0) + (size_t)kPanel * w + 4 * (size_t)g);
+  return sizeof(double) * ((gram_in_smem ? (size_t)g * g : 0) + (size_t)kPanel * w + 5 * (size_t)g);
 }
 
 cudaError_t launch_norm(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t st) {
