@@ -768,7 +768,7 @@ void NormBatch::run_async(Ctx& C) {
   size_t smem = 0, smem_g = 0;
   // small: single segment, both sides <= 64 / 128 (warp Lanczos); big: CTA Gram in shared memory;
   // huge: CTA Gram in global scratch
-  std::vector<NormItem> big, small, huge, mid, lz;  // mid / lz: single segment up to 128 x 128 (CTA Lanczos)
+  std::vector<NormItem> big, small, huge, mid, lz, lz64, lz96;  // mid / lz*: single segment up to 128 x 128
   size_t smem_mid = 0;
   std::unique_ptr<Arena> local;
   for (auto& it : items) {
@@ -782,8 +782,8 @@ void NormBatch::run_async(Ctx& C) {
       // large ones (the 128 x 128 nearfield blocks) keep A in registers (norm_lz_kernel, one CTA per
       // SM: 1.9x on them); smaller ones run several shared-memory CTAs per SM (norm_cta_kernel)
       static const bool cta_all = getenv("H2G_NORM_CTA") != nullptr;  // A/B: shared-memory kernel only
-      if (!cta_all && it.m * it.N > 96 * 96) {
-        lz.push_back(it);
+      if (!cta_all) {
+        (it.m <= 64 && it.N <= 64 ? lz64 : (it.m <= 96 && it.N <= 96 ? lz96 : lz)).push_back(it);
         continue;
       }
       smem_mid = std::max(smem_mid, norm_cta_smem(it.m, (int)it.N));
@@ -806,10 +806,10 @@ void NormBatch::run_async(Ctx& C) {
     smem_g = std::max(smem_g, norm_smem(it.m, it.N, false));
     huge.push_back(it);
   }
-  if (!big.empty() || !small.empty() || !huge.empty() || !mid.empty() || !lz.empty()) {
+  if (!big.empty() || !small.empty() || !huge.empty() || !mid.empty() || !lz.empty() || !lz64.empty() || !lz96.empty()) {
     double fl = 0, by = 0;
     if (C.prof)
-      for (auto* v : {&big, &small, &huge, &mid, &lz})
+      for (auto* v : {&big, &small, &huge, &mid, &lz, &lz64, &lz96})
         for (auto& it : *v) {  // Gram on the short side + tridiagonalisation (reference's work)
           const double mn = std::min<double>(it.m, (double)it.N), mx = std::max<double>(it.m, (double)it.N);
           fl += 2 * mn * mn * mx + 4.0 / 3 * mn * mn * mn;
@@ -841,10 +841,12 @@ void NormBatch::run_async(Ctx& C) {
       cuda_check(launch_norm_cta(d_mid, d_s, (int)mid.size(), smem_mid, C.st), "norm_cta");
       ++C.launches;
     }
-    if (!lz.empty()) {
-      NormItem* d_lz = C.push(lz);
+    for (auto* v : {&lz64, &lz96, &lz}) {
+      if (v->empty()) continue;
+      NormItem* d_lz = C.push(*v);
       C.flush();
-      cuda_check(launch_norm_lz(d_lz, d_s, (int)lz.size(), C.st), "norm_lz");
+      const int cap = v == &lz64 ? 64 : (v == &lz96 ? 96 : 128);
+      cuda_check(launch_norm_lz(d_lz, d_s, (int)v->size(), cap, cap, C.st), "norm_lz");
       ++C.launches;
     }
     C.prof_end(K_NORM, ev, fl, by);

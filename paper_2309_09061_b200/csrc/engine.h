@@ -44,7 +44,7 @@ cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cu
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
 cudaError_t launch_norm_cta(const NormItem* items, const Seg* segs, int nitems, size_t smem, cudaStream_t);
-cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
+cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, int mmax, int nmax, cudaStream_t);
 size_t norm_cta_smem(int m, int N);
 cudaError_t launch_asm_expand(const AsmTables& T, int ntrip, GTerm* terms, cudaStream_t);
 cudaError_t launch_tile_absorb(const TileItem*, const Seg*, const TileWork*, int nwork, int nmax, cudaStream_t);

@@ -1335,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const NormItem* __restri
       break;
     }
     if (tid == 0) be[k] = bb;
-    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
+    if ((k & 1) == 1 && k >= 5) {  // top Ritz value settled to 1e-14 relative: stop
       __syncthreads();
       if (warp == 0) {
         const double th = warp_lambda_max(al, be, k + 1);
@@ -1743,7 +1743,7 @@ __global__ void __launch_bounds__(kNCThreads) norm_cta_kernel(const NormItem* __
       break;
     }
     if (tid == 0) be[k] = b;
-    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
+    if ((k & 1) == 1 && k >= 5) {  // top Ritz value settled to 1e-14 relative: stop
       __syncthreads();
       if (warp == 0) {
         const double th = warp_lambda_max(al, be, k + 1);
@@ -1792,17 +1792,19 @@ cudaError_t launch_norm_cta(const NormItem* items, const Seg* segs, int nitems, 
 // 2 x 128 KB per iteration through 128 B/clk and held one CTA per SM for its A).  u is reduced over
 // the 16 column lanes by shuffles, w over the 32 row groups by one shuffle step and a 16-way
 // shared-memory sum.  Lanczos on A^T A with the same start vector, early exit and exact-zero rule as
-// norm_cta_kernel; the top Ritz value is re-evaluated every 2 steps from step 7.
+// norm_cta_kernel; the top Ritz value is re-evaluated every 2 steps from step 5.
 // ---------------------------------------------------------------------------------------------
-static constexpr int kLzThreads = 512;
 
-__global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* __restrict__ items,
-                                                                const Seg* __restrict__ segs) {
-  __shared__ double part[16][kNC];   // w partials per warp
-  __shared__ double vs[kNC];         // current Lanczos vector
+// NW warps (2 NW row groups) x P rows x Q column groups of 16: up to 2 NW P rows and 16 Q columns
+template <int NW, int P, int Q>
+__global__ void __launch_bounds__(32 * NW, NW >= 16 ? 1 : (NW >= 12 ? 2 : 3))
+    norm_lz_kernel(const NormItem* __restrict__ items, const Seg* __restrict__ segs) {
+  constexpr int RG = 2 * NW, NCOL = 16 * Q;
+  __shared__ double part[NW][NCOL];  // w partials per warp
+  __shared__ double vs[NCOL];        // current Lanczos vector
   __shared__ double red[2][4];
   __shared__ double al[kNC], be[kNC];
-  __shared__ double amax_s[16];
+  __shared__ double amax_s[NW];
   __shared__ double lam_s;
   __shared__ int stop_s;
   const NormItem it = items[blockIdx.x];
@@ -1811,13 +1813,13 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cg = lane & 15, rg = 2 * warp + (lane >> 4);
   const double ssc = seg_scale(sg);
-  double a[4][8];
+  double a[P][Q];
   double amax = 0.0;
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
+  for (int p = 0; p < P; ++p)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int i = rg + 32 * p, j = cg + 16 * q;
+    for (int q = 0; q < Q; ++q) {
+      const int i = rg + RG * p, j = cg + 16 * q;
       const double x = (i < m && j < N) ? ssc * __ldg(sg.a.p + (long long)i * sg.a.rs + (long long)j * sg.a.cs) : 0.0;
       a[p][q] = x;
       amax = fmax(amax, fabs(x));
@@ -1842,13 +1844,13 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
   {
     const double nv = sqrt(sum4(tid < N ? vt * vt : 0.0, 0));
     double mx = 0.0;
-    for (int w = 0; w < 16; ++w) mx = fmax(mx, amax_s[w]);
+    for (int w = 0; w < NW; ++w) mx = fmax(mx, amax_s[w]);
     if (mx == 0.0) {
       if (tid == 0) *it.out = 0.0;
       return;
     }
     vt = tid < N ? vt / nv : 0.0;
-    if (tid < kNC) vs[tid] = vt;  // zero past N: the matvec reads all 128 (0 * uninitialised may be NaN)
+    if (tid < NCOL) vs[tid] = vt;  // zero past N: the matvec reads all columns (0 * uninitialised may be NaN)
   }
   __syncthreads();
   const int g = min(m, N);
@@ -1856,43 +1858,43 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
   int k = 0;
   for (; k < g; ++k) {
     // u = A v over this thread's 4 rows, reduced over the 16 column lanes
-    double vq[8];
+    double vq[Q];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) vq[q] = vs[cg + 16 * q];
-    double u[4];
+    for (int q = 0; q < Q; ++q) vq[q] = vs[cg + 16 * q];
+    double u[P];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < P; ++p) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; q += 2) {
+      for (int q = 0; q < Q; q += 2) {
         s0 = fma(a[p][q], vq[q], s0);
-        s1 = fma(a[p][q + 1], vq[q + 1], s1);
+        if (q + 1 < Q) s1 = fma(a[p][q + 1], vq[q + 1], s1);
       }
       u[p] = s0 + s1;
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) u[p] += __shfl_xor_sync(0xffffffffu, u[p], o);
+      for (int p = 0; p < P; ++p) u[p] += __shfl_xor_sync(0xffffffffu, u[p], o);
     // w = A^T u over this thread's 8 columns, reduced over the two row groups of the warp, then
     // over the 16 warps in shared memory (fixed order)
-    double w[8];
+    double w[Q];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < Q; ++q) {
       double s = 0.0;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) s = fma(a[p][q], u[p], s);
+      for (int p = 0; p < P; ++p) s = fma(a[p][q], u[p], s);
       w[q] = s + __shfl_xor_sync(0xffffffffu, s, 16);
     }
     if (lane < 16)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) part[warp][cg + 16 * q] = w[q];
+      for (int q = 0; q < Q; ++q) part[warp][cg + 16 * q] = w[q];
     __syncthreads();
     double wt = 0.0;
     if (tid < N) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < 16; ww += 2) {
+      for (int ww = 0; ww < NW; ww += 2) {
         s0 += part[ww][tid];
         s1 += part[ww + 1][tid];
       }
@@ -1907,7 +1909,7 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
       break;
     }
     if (tid == 0) be[k] = b;
-    if ((k & 1) == 1 && k >= 7) {  // top Ritz value settled to 1e-14 relative: stop
+    if ((k & 1) == 1 && k >= 5) {  // top Ritz value settled to 1e-14 relative: stop
       __syncthreads();
       if (warp == 0) {
         const double th = warp_lambda_max(al, be, k + 1);
@@ -1926,7 +1928,7 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
     vprev = vt;
     bprev = b;
     vt = tid < N ? wt / b : 0.0;
-    if (tid < kNC) vs[tid] = vt;
+    if (tid < NCOL) vs[tid] = vt;
     __syncthreads();
   }
   __syncthreads();
@@ -1936,9 +1938,11 @@ __global__ void __launch_bounds__(kLzThreads, 1) norm_lz_kernel(const NormItem* 
   }
 }
 
-cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, cudaStream_t st) {
+cudaError_t launch_norm_lz(const NormItem* items, const Seg* segs, int nitems, int mmax, int nmax, cudaStream_t st) {
   if (nitems == 0) return cudaSuccess;
-  norm_lz_kernel<<<nitems, kLzThreads, 0, st>>>(items, segs);
+  if (mmax <= 64 && nmax <= 64) norm_lz_kernel<8, 4, 4><<<nitems, 256, 0, st>>>(items, segs);
+  else if (mmax <= 96 && nmax <= 96) norm_lz_kernel<12, 4, 6><<<nitems, 384, 0, st>>>(items, segs);
+  else norm_lz_kernel<16, 4, 8><<<nitems, 512, 0, st>>>(items, segs);
   return cudaGetLastError();
 }
 
