@@ -76,6 +76,9 @@ int h2g_ctx_host_times(h2g_ctx* ctx, char* buf, int len, int reset);
    (0 gsum, 1 qr_r, 2 svd, 3 norm, 4 gather, 5 mv); out24 = per class {launches, ms, algorithmic flops,
    bytes} */
 int h2g_ctx_set_profile(h2g_ctx* ctx, int on);
+/* serial mode (process-wide): the row and column passes and the auxiliary launches of a product run
+   one after the other on the main stream, so profile-mode events time each launch by itself */
+int h2g_set_serial(int on);
 int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* out24, int reset);
 /* timeline: trace_begin turns on per-launch events; trace_dump writes a chrome://tracing JSON */
 int h2g_ctx_trace_begin(h2g_ctx* ctx);

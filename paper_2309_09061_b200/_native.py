@@ -40,6 +40,7 @@ SIGNATURES = {
     "h2g_ctx_synchronize": (C.c_int, [P]),
     "h2g_ctx_host_times": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int]),
     "h2g_ctx_set_profile": (C.c_int, [P, C.c_int]),
+    "h2g_set_serial": (C.c_int, [C.c_int]),
     "h2g_ctx_kernel_stats": (C.c_int, [P, F64P, C.c_int]),
     "h2g_ctx_trace_begin": (C.c_int, [P]),
     "h2g_ctx_trace_dump": (C.c_int, [P, C.c_char_p]),

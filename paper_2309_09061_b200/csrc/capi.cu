@@ -108,6 +108,11 @@ int h2g_ctx_set_profile(h2g_ctx* ctx, int on) {
   return 0;
 }
 
+int h2g_set_serial(int on) {
+  g_serial.store(on != 0);
+  return 0;
+}
+
 int h2g_ctx_kernel_stats(h2g_ctx* ctx, double* o, int reset) {
   return guarded([&] {
     ctx->c.sync();

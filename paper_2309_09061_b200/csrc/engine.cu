@@ -25,6 +25,8 @@ void cuda_check(cudaError_t e, const char* what) {
 
 // ============================================================================ infrastructure
 
+std::atomic<bool> g_serial{false};  // h2g_set_serial (engine.h serial_passes)
+
 // Process-wide payload of the arenas (bytes handed out, not the chunks behind them): the memory a
 // product actually needs, independent of the 64 MB chunk granularity (h2g_ctx_mem).
 std::atomic<long long> g_arena_payload{0}, g_arena_payload_high{0};

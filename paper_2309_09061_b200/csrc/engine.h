@@ -372,10 +372,12 @@ struct HostTimer {
   }
 };
 
-// H2G_SERIAL=1: run the row and column passes one after the other on the main stream (profiling).
+// H2G_SERIAL=1 (or h2g_set_serial): run the row and column passes one after the other on the main
+// stream (profiling).  Read at the start of each pass structure decision; toggle between products only.
+extern std::atomic<bool> g_serial;
 inline bool serial_passes() {
-  static const bool on = getenv("H2G_SERIAL") != nullptr;
-  return on;
+  static const bool env = getenv("H2G_SERIAL") != nullptr;
+  return env || g_serial.load();
 }
 
 // Labels the launches issued in its scope (trace mode only).

@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.h"
@@ -720,7 +723,15 @@ void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool a
     if (!std::equal(f, f + 6, slot->f) || fn[0] != slot->fn[0] || fn[1] != slot->fn[1] || dist != slot->fdist)
       slot.reset();
   }
-  if (!slot) slot = build_plan(C, g);
+  if (!slot) {
+    static const bool dbg = getenv("H2G_DEBUG_MV") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    slot = build_plan(C, g);
+    if (dbg)
+      fprintf(stderr, "h2g: matvec plan (%s) built in %.2f ms, %zu launches\n", g.T ? "adjoint" : "plain",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+              slot->launches.size());
+  }
   replay(C, *slot, MvCall{x, y, alpha, accumulate ? 1 : 0});
 }
 

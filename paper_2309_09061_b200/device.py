@@ -82,6 +82,11 @@ class Context:
     def set_profile(self, on: bool):
         N.check(self.lib.h2g_ctx_set_profile(self.h, 1 if on else 0))
 
+    def set_serial(self, on: bool):
+        """Process-wide serial mode (h2g_set_serial): a product's passes and auxiliary launches run one
+        after the other on the main stream, so profile-mode events time every launch by itself."""
+        N.check(self.lib.h2g_set_serial(1 if on else 0))
+
     def kernel_stats(self, reset: bool = True) -> dict:
         out = np.zeros(4 * len(self.KCLASSES))
         N.check(self.lib.h2g_ctx_kernel_stats(self.h, out.ctypes.data_as(N.F64P), 1 if reset else 0))
