@@ -978,14 +978,22 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   if (sm_prep > kSmemLimit) throw StructureErr("svd: protected basis too large for shared memory");
   std::vector<SvdWork> work;
   std::vector<std::tuple<double*, int, int>> parts;
-  // the finish stage keeps R in shared memory when it fits (first choice), V beside it when that fits too
-  bool fin_vsmem = true;
+  // the finish stage keeps R in shared memory when it fits (first choice), V beside it when that fits too;
+  // else R alone at its unpadded stride ("tight": the top-level row clusters of c4, n up to ~168)
+  bool fin_tight = false;
+  if (!fin_rsmem) {
+    fin_tight = true;
+    for (const SvdItem& it : live)
+      if (svd_finish_smem(it.m, it.kx, true, false, true) > kSmemLimit) fin_tight = false;
+    if (fin_tight) fin_rsmem = true;
+  }
+  bool fin_vsmem = !fin_tight;
   for (const SvdItem& it : live)
-    if (svd_finish_smem(it.m, it.kx, fin_rsmem, true) > kSmemLimit) fin_vsmem = false;
+    if (!fin_tight && svd_finish_smem(it.m, it.kx, fin_rsmem, true) > kSmemLimit) fin_vsmem = false;
   for (size_t i = 0; i < live.size(); ++i) {
     const SvdItem& it = live[i];
     const int n = it.m - std::min(it.m, it.kx);
-    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem, fin_vsmem));
+    sm_fin = std::max(sm_fin, svd_finish_smem(it.m, it.kx, fin_rsmem, fin_vsmem, fin_tight));
     if (sm_fin > kSmemLimit) throw StructureErr("svd: item too large for shared memory");
     if (it.pre_nr || tile_path(n)) continue;
     sm_tsqr = std::max(sm_tsqr, svd_tsqr_smem(it.m, it.kx, rsmem));
@@ -1043,7 +1051,7 @@ std::vector<int> SvdBatch::run(Ctx& C, Arena& scratch) {
   int fin_nmax = 0;
   for (auto& it : live) fin_nmax = std::max(fin_nmax, it.m - std::min(it.m, it.kx));
   C.flush();
-  cuda_check(launch_svd_finish(d_items, d_s, (int)live.size(), sm_fin, fin_rsmem, fin_vsmem, fin_nmax, C.st),
+  cuda_check(launch_svd_finish(d_items, d_s, (int)live.size(), sm_fin, fin_rsmem, fin_vsmem, fin_nmax, C.st, fin_tight),
              "svd_finish");
   C.sub_end(S_SVD_FIN, sf);
   ++C.launches;

@@ -39,7 +39,7 @@ cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* 
                         int mmax, cudaStream_t st);
 size_t gram_chol_smem(int m);
 cudaError_t launch_svd_finish(const SvdItem*, const Seg*, int nitems, size_t smem, bool rsmem, bool vsmem, int nmax,
-                              cudaStream_t);
+                              cudaStream_t, bool tight = false);
 cudaError_t launch_norm(const NormItem*, const Seg*, int nitems, size_t smem, cudaStream_t);
 cudaError_t launch_gather(const long long* items, int nitems, cudaStream_t);
 cudaError_t launch_norm_warp(const NormItem* items, const Seg* segs, int nitems, cudaStream_t);
@@ -54,7 +54,7 @@ size_t svd_prep_smem(int m, int kx, bool with_q = true);
 size_t qr_smem(int n, bool rsmem);
 size_t svd_tsqr_smem(int m, int kx, bool rsmem);
 size_t merge_smem(int n, bool rsmem);
-size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem = true);
+size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem = true, bool tight = false);
 size_t norm_smem(int m, long long N, bool gram_in_smem = true);
 
 // ------------------------------------------------------------------ structure

@@ -939,18 +939,37 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
     }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ldv = kx | 1;
+  // vsm bit 1: "tight" layout -- R at the unpadded stride n (rounded up to even) and the QRCP work
+  // vectors in global memory (the R input buffer, free once R is in shared memory), for n up to
+  // ~168 where the padded layout misses the 227 KB by a few KB (the top-level clusters of c4's
+  // row pass: shared memory instead of the global-memory fallback, ~3.5x on those launches)
+  const bool tight = RS && (vsm & 2);
+  vsm &= 1;
   double* sig = smem;                        // n
   int* ord = (int*)(sig + n);                // n ints
-  double* cn = sig + n + (n / 2 + 1);        // QRCP column norms (n), reference norms (n), reflector (n)
-  double* cn0 = cn + n;
-  double* vh = cn0 + n;
-  int* perm = (int*)(vh + n);                // n ints
-  int* iperm = perm + n;                     // n ints
-  // R in shared memory: 16-byte aligned rows of stride ld = fin_ld(n) (padding columns zero), so the
-  // octet Jacobi moves double2 and the QRCP trailing update's 4 x 4 (rows x columns) half-warp
-  // accesses fall in distinct banks; in global memory (the merge output) the stride stays n
-  const int ld = RS ? fin_ld(n) : n;
-  double* R = RS ? smem + (((int)(vh + 2 * n + 1 - smem) + 1) & ~1) : it.rbuf;
+  double *cn, *cn0, *vh, *R;
+  int *perm, *iperm;
+  int ld;
+  if (tight) {
+    perm = (int*)(sig + n + (n / 2 + 1));    // n ints
+    iperm = perm + n;                        // n ints
+    ld = n + (n & 1);
+    R = smem + ((n + (n / 2 + 1) + n + 1) & ~1);
+    cn = it.rbuf;                            // QRCP column norms, reference norms, reflector
+    cn0 = cn + n;
+    vh = cn0 + n;
+  } else {
+    cn = sig + n + (n / 2 + 1);              // QRCP column norms (n), reference norms (n), reflector (n)
+    cn0 = cn + n;
+    vh = cn0 + n;
+    perm = (int*)(vh + n);                   // n ints
+    iperm = perm + n;                        // n ints
+    // R in shared memory: 16-byte aligned rows of stride ld = fin_ld(n) (padding columns zero), so
+    // the octet Jacobi moves double2 and the QRCP trailing update's 4 x 4 (rows x columns) half-warp
+    // accesses fall in distinct banks; in global memory (the merge output) the stride stays n
+    ld = RS ? fin_ld(n) : n;
+    R = RS ? smem + (((int)(vh + 2 * n + 1 - smem) + 1) & ~1) : it.rbuf;
+  }
   // V (m x ldv, reflectors of the protected basis) and tv (kx + 1): staged in shared memory after
   // the rest when they fit (vsm), else read where the tsqr stage left them
   double* V = vsm ? (RS ? R + (long long)n * ld : vh + n + n + 1) : it.vws;
@@ -2104,9 +2123,11 @@ size_t merge_smem(int n, bool rsmem) {
   return sizeof(double) * ((size_t)kPanel * (n | 1) + 68 + (rsmem ? (size_t)n * n : 0));
 }
 
-size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem) {
+size_t svd_finish_smem(int m, int kx, bool rsmem, bool vsmem, bool tight) {
   const int k1 = m < kx ? m : kx;
   const int n = m - k1;
+  if (tight)  // sig, ord, perm, iperm and R at stride n (even); no V
+    return sizeof(double) * ((((size_t)n + (n / 2 + 1) + n + 1) & ~size_t(1)) + (size_t)n * (n + (n & 1)));
   return sizeof(double) * ((vsmem ? (size_t)m * (kx | 1) + kx + 1 : 0) + n + (n / 2 + 1) + 4 * (size_t)n + 2 +
                            (rsmem ? (size_t)n * fin_ld(n) : 0));
 }
@@ -2120,10 +2141,10 @@ cudaError_t launch_svd_tsqr(const SvdItem* items, const Seg* segs, const SvdWork
 }
 
 cudaError_t launch_svd_finish(const SvdItem* items, const Seg* segs, int nitems, size_t smem, bool rsmem, bool vsmem,
-                              int nmax, cudaStream_t st) {
+                              int nmax, cudaStream_t st, bool tight) {
   init_attributes();
   if (nitems == 0) return cudaSuccess;
-  const int v = vsmem ? 1 : 0;
+  const int v = (vsmem && !tight ? 1 : 0) | (tight && rsmem ? 2 : 0);
   const long long sd = (long long)(smem / sizeof(double));
   if (rsmem) {
     if (nmax <= 64) svd_finish_kernel<8, true><<<nitems, NT, smem, st>>>(items, segs, v, sd);

@@ -736,6 +736,19 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   static const bool exp3 = getenv("H2G_EXPAND_3F") != nullptr;  // previous one-launch form (A/B)
   static const bool push3 = getenv("H2G_PUSH_3F") != nullptr;  // previous 3-factor pushes (A/B)
   constexpr size_t kPushBudget = size_t(1) << 27;  // doubles (1 GiB) of E_t2 S intermediates per chunk
+  // The expansions into the dense targets write nothing a later push-down level reads: they run on
+  // the normal-priority auxiliary stream, overlapping the next levels' coupling pushes and phase 2's
+  // coupling norms and Z levels (which read couplings only).  Phase 2's nearfield readers follow
+  // them on that stream (nearfield norms) or wait for G->near_ready.  Partitioned products exchange
+  // G's blocks right after the push-down and keep them on the main stream.
+  static const bool sync_exp = getenv("H2G_SYNC_EXPAND") != nullptr;  // A/B: expansions on the main stream
+  Ctx* Ep = (!serial_passes() && !part.on() && !exp3 && !sync_exp) ? &C.aux(true) : nullptr;
+  std::shared_ptr<Arena> pa;  // the expansions' k~ x k~ parts (read on Ep, freed after it)
+  if (Ep) {
+    pa = std::make_shared<Arena>(C.st);
+    Ep->tag = "p1.expand";
+  }
+  bool dense_wait_ep = early;
   for (int lev = 0; lev < B.depth; ++lev) {
     GBatch g1, g2;
     std::vector<Expansion> exps;
@@ -787,7 +800,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
           }
           const bool push_e = push3 && t2 != t;
           if (B.near_leaf(ch)) {
-            Mat part{sc.alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
+            Mat part{(Ep ? *pa : sc).alloc((size_t)Q.rank[t2] * W.rank[r2]), Q.rank[t2], W.rank[r2]};
             g1.out(part, false);
             emit_push(g1, push_e ? &E : nullptr, src, r2 != r ? &F : nullptr);
             if (exp3) {
@@ -806,8 +819,20 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
       g1.run(C);
       p0 = p1;
     }
-    if (!g2.outs.empty() || !exps.empty()) wait_dense();
+    if (!g2.outs.empty() || (!exps.empty() && !Ep)) wait_dense();
     g2.run(C);
+    Ctx& XC = Ep ? *Ep : C;  // stream of this level's expansions
+    if (Ep && !exps.empty()) {
+      if (dense_wait_ep) {  // the dense targets first
+        cuda_check(cudaStreamWaitEvent(Ep->st, pt.early.done, 0), "wait dense targets");
+        dense_wait_ep = false;
+      }
+      cudaEvent_t e;  // this level's parts are written on the main stream
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(e, C.st), "event");
+      cuda_check(cudaStreamWaitEvent(Ep->st, e, 0), "wait parts");
+      cudaEventDestroy(e);
+    }
     // expansion into the inadmissible children, N += Q_leaf(t2) (part W_leaf(r2)^T) as two
     // 2-factor launches: T = Q_leaf part once per target (a 3-factor term recomputes it for every
     // 64-column tile of the target and pads its middle dimension to 64), then N += T W_leaf^T.
@@ -821,7 +846,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
         if (e1 > e0 && need + sz > kExpBudget) break;
         need += sz;
       }
-      Arena ta(C.st);
+      Arena ta(XC.st);
       GBatch ga, gb;
       for (size_t e = e0; e < e1; ++e) {
         const int ch = exps[e].ch;
@@ -832,15 +857,34 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
         gb.out(Mat{G->near[ch], rows.size(t2), cols.size(r2)}, true);
         gb.t2(Tm.ref(), W.leafm(r2).tref(), W.rank[r2]);
       }
-      ga.run(C);
-      gb.run(C);
+      ga.run(XC);
+      gb.run(XC);
       e0 = e1;
     }
   }
-  wait_dense();
-  if (pt.dev.block) {  // after the main stream has waited for the dense targets' expansion
-    cudaFreeAsync(pt.dev.block, C.st);
+  if (Ep && dense_wait_ep) {  // no expansion at all: the event below must still cover the dense targets
+    cuda_check(cudaStreamWaitEvent(Ep->st, pt.early.done, 0), "wait dense targets");
+    dense_wait_ep = false;
+  }
+  if (!Ep) wait_dense();
+  if (Ep) {
+    Ep->tag.clear();
+    // the parts are freed on the expansion stream once it has consumed them
+    pa->cross_stream = true;
+    pa->free_st = Ep->st;
+    pa->after = {C.st};
+    pa.reset();
+    // G's nearfield is complete at this event (dense targets and expansions): readers wait for it
+    cuda_check(cudaEventCreateWithFlags(&G->near_ready, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(G->near_ready, Ep->st), "event");
+  }
+  if (pt.dev.block) {  // after the stream that frees them has waited for the dense targets' expansion
+    cudaFreeAsync(pt.dev.block, Ep ? Ep->st : C.st);
     pt.dev.block = nullptr;
+  }
+  if (Ep && pt.early.done) {  // Ep waited for it above
+    cudaEventDestroy(pt.early.done);
+    pt.early.done = nullptr;
   }
   if (part.on()) {
     // G stays distributed by block rows: each rank keeps the blocks of its own rows (and the
@@ -1027,7 +1071,18 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   StageTag taga(C, "p1.asm");
   auto G = assemble(C, X, Y, qr, qc, PRef{&P, false}, pt, have_rf ? &rf : nullptr);
   mem_mark("p1 assembled");
-  if (A) C.join_side(*A);  // counters / profile of the auxiliary stream's work
+  if (A) {
+    if (G->near_ready && !C.prof) {
+      // the push-down expansions (normal-priority auxiliary stream) waited for the dense targets
+      // and G->near_ready completes both: the main stream goes on with phase 2 instead of waiting
+      // here for the low-priority stream; its arena is freed after that stream's queued work
+      C.launches += A->launches;
+      A->launches = 0;
+      if (pt.early.near) pt.early.near->after.push_back(A->st);
+    } else {
+      C.join_side(*A);  // counters / profile of the auxiliary stream's work
+    }
+  }
   record(C, e4);
   G->owned.push_back(keep);
   G->owned.push_back(keep2);

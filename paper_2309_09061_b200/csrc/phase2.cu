@@ -877,6 +877,7 @@ static void all_norms(Ctx& C, Arena& sc, const H2& g, double* d_cn, double* d_nn
     cuda_check(cudaEventRecord(e, C.st), "event");  // G final, d_nn zero-filled
     cuda_check(cudaStreamWaitEvent(A->st, e, 0), "wait");
     cudaEventDestroy(e);
+    if (g.near_ready) cuda_check(cudaStreamWaitEvent(A->st, g.near_ready, 0), "wait nearfield");
     nbn.run_async(*A);
     A->flush();
     cuda_check(cudaEventCreateWithFlags(nn_ready, cudaEventDisableTiming), "event");
@@ -938,24 +939,21 @@ static NearPrefetch prefetch_near(Ctx& C, const H2& g, const Blocks& cbk, double
   P.arena = std::make_shared<Arena>(C.up_stream);
   double* stage = P.arena->alloc(off);
   for (size_t i = 2; i < items.size(); i += 3) items[i] = (long long)(stage + items[i]);
-  long long* di = C.push(items);
-  C.flush();
+  // the gather's descriptors live in the prefetch arena (copied on the copy stream, from pageable
+  // memory: the call returns once the host vector has been read), not in C's staging buffer that the
+  // next host sync recycles -- so the main stream never has to wait for the copy stream
+  long long* di = (long long*)P.arena->alloc_bytes(items.size() * sizeof(long long));
+  cuda_check(cudaMemcpyAsync(di, items.data(), items.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                             C.up_stream),
+             "prefetch descriptors");
   cudaEvent_t e;
   cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-  cuda_check(cudaEventRecord(e, C.st), "event");  // G complete and the item list copied
+  cuda_check(cudaEventRecord(e, C.st), "event");  // G's blocks complete on the main stream
   cuda_check(cudaStreamWaitEvent(C.up_stream, e, 0), "wait");
   cudaEventDestroy(e);
+  if (g.near_ready) cuda_check(cudaStreamWaitEvent(C.up_stream, g.near_ready, 0), "wait nearfield");
   cuda_check(launch_gather(di, (int)npf, C.up_stream), "gather(prefetch)");
   ++C.launches;
-  {  // the gather reads its descriptors from C's staging buffer, which C.sync() recycles: order the
-     // main stream after the gather so that no later host sync can hand the buffer out while the
-     // copy stream has not yet consumed it (the D2H copies below stay asynchronous)
-    cudaEvent_t g;
-    cuda_check(cudaEventCreateWithFlags(&g, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventRecord(g, C.up_stream), "event");
-    cuda_check(cudaStreamWaitEvent(C.st, g, 0), "wait");
-    cudaEventDestroy(g);
-  }
   for (int b = 0; b < cbk.nb;) {  // one copy per run of consecutive prefetched blocks
     if (!P.mask[b]) { ++b; continue; }
     const long long lo = zoff[b];
@@ -982,7 +980,11 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   if (C.timing) { e0 = C.event(); cudaEventRecord(e0, C.st); }
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   HostTimer htpre(C, "p2_pre");
-  wait_near(C, g);
+  // g's nearfield may still be in flight on the auxiliary stream (multiply's push-down expansions):
+  // with block scaling its readers -- the nearfield norms on that stream, the leaf SVDs behind
+  // nn_ready, the prefetch copy -- are ordered after it, so the main stream starts on the couplings
+  const bool near_async = scale && !serial_passes() && g.near_ready;
+  if (!near_async) wait_near(C, g);
   NearPrefetch pf;
   if (near_host && g.near_owner) pf = prefetch_near(C, g, *coarse, near_host, near_cap);
   htpre.stop();
