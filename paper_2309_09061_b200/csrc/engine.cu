@@ -539,7 +539,7 @@ static bool gram_path(int kx, int n, long long N) {
 // Items of one double-double Gram launch pair (gram.cu), shared by the SVD and QR batches.
 struct GramBatch {
   std::vector<GramItem> items;
-  std::vector<GramWork> work;
+  std::vector<GramWork> work, wflat;  // tiled / flat (m <= kGramFlatMax) work units
   int mmax = 0;
   // lines of hstack(segs[s0:s1]) (hcols) or vstack (rows), m-dimensional; factor into rbuf, rows into *nr
   void add(Arena& scratch, int s0, int s1, int m, long long N, int hcols, double tol, double* rbuf, int* nr) {
@@ -548,7 +548,9 @@ struct GramBatch {
     g.s0 = s0;
     g.s1 = s1;
     g.m = m;
-    g.nslice = ncc * gram_reps(m);  // partial slices summed by the Cholesky CTA
+    static const bool tiled = getenv("H2G_GRAM_TILED") != nullptr;  // A/B: 64 x 64 tiles for every m
+    const bool flat = m > 64 && m <= kGramFlatMax && !tiled;
+    g.nslice = flat ? ncc : ncc * gram_reps(m);  // partial slices summed by the Cholesky CTA
     g.N = N;
     g.hcols = hcols;
     g.tol = tol;
@@ -556,20 +558,37 @@ struct GramBatch {
     g.rbuf = rbuf;
     g.nr = nr;
     const int gi = (int)items.size(), nt = (m + 63) / 64;
-    for (int c = 0; c < ncc; ++c)
-      for (int ti = 0; ti < nt; ++ti)
-        for (int tj = ti; tj < nt; ++tj)
-          work.push_back(GramWork{gi, ti, tj, c, (long long)c * gram_cols(), std::min<long long>(N, (long long)(c + 1) * gram_cols())});
+    if (flat) {
+      // 64 < m <= 128: the upper triangle's 4 x 4 blocks dealt out evenly in contiguous runs, one
+      // block per thread over all of a panel's lines (64 x 64 tiles left most of the second tile
+      // row idle for m ~ 66-97: 20-40 % of the threads busy; splitting lines over replicas costs
+      // more staging per product than it gains, measured)
+      const int nb = (m + 3) / 4, nblk = nb * (nb + 1) / 2;
+      const int best_r = 1;
+      const int ncta = (nblk + kGramFlatThreads - 1) / kGramFlatThreads;
+      const int bpc = (nblk + ncta - 1) / ncta;
+      for (int c = 0; c < ncc; ++c)
+        for (int b0 = 0; b0 < nblk; b0 += bpc)
+          wflat.push_back(GramWork{gi, b0, std::min(bpc, nblk - b0) | (best_r << 16), c, (long long)c * gram_cols(),
+                                   std::min<long long>(N, (long long)(c + 1) * gram_cols())});
+    } else {
+      for (int c = 0; c < ncc; ++c)
+        for (int ti = 0; ti < nt; ++ti)
+          for (int tj = ti; tj < nt; ++tj)
+            work.push_back(GramWork{gi, ti, tj, c, (long long)c * gram_cols(), std::min<long long>(N, (long long)(c + 1) * gram_cols())});
+    }
     items.push_back(g);
     mmax = std::max(mmax, m);
   }
   void launch(Ctx& C, const Seg* d_segs) {
     if (items.empty()) return;
     GramItem* d_it = C.push(items);
-    GramWork* d_w = C.push(work);
+    const int nflat = (int)wflat.size();
+    wflat.insert(wflat.end(), work.begin(), work.end());
+    GramWork* d_w = C.push(wflat);
     C.flush();
-    cuda_check(launch_gram(d_it, d_segs, d_w, (int)work.size(), (int)items.size(), mmax, C.st), "gram");
-    C.launches += 2;
+    cuda_check(launch_gram(d_it, d_segs, d_w, (int)wflat.size(), nflat, (int)items.size(), mmax, C.st), "gram");
+    C.launches += 1 + (nflat > 0 && nflat < (int)wflat.size() ? 2 : 1);
   }
 };
 

@@ -35,8 +35,8 @@ cudaError_t launch_tsqr_merge(const MergeWork*, int nwork, size_t smem, bool rsm
 cudaError_t launch_qr_out(const QrItem*, int nitems, cudaStream_t);
 cudaError_t launch_svd_tsqr(const SvdItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
                             cudaStream_t);
-cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
-                        int mmax, cudaStream_t st);
+cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nflat,
+                        int nitems, int mmax, cudaStream_t st);
 size_t gram_chol_smem(int m);
 cudaError_t launch_svd_finish(const SvdItem*, const Seg*, int nitems, size_t smem, bool rsmem, bool vsmem, int nmax,
                               cudaStream_t, bool tight = false);

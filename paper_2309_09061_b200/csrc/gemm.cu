@@ -10,8 +10,11 @@
 #include <cstdlib>
 #include <mutex>
 
+#ifndef GSUM_WARPS  // warps per 64 x 64 output tile: 8 (16 x 32 each) or 4 (32 x 32 each)
+#define GSUM_WARPS 8
+#endif
 #ifndef GSUM_PIPE_MINB
-#define GSUM_PIPE_MINB 2
+#define GSUM_PIPE_MINB (GSUM_WARPS == 4 ? 3 : 2)
 #endif
 
 #include "h2g_types.h"
@@ -24,7 +27,7 @@ constexpr int kT = 64;            // output tile
 constexpr int kKC = 16;           // k chunk
 constexpr int kLdA = kKC + 4;     // As[64][20]
 constexpr int kLdB = kT + 8;      // Bs[16][72]
-constexpr int kThr = 256;         // 8 warps, each a 16 x 32 quadrant (2 x 4 DMMA tiles)
+constexpr int kThr = 32 * GSUM_WARPS;  // 8 warps of 16 x 32 (2 x 4 DMMA tiles) or 4 of 32 x 32 (4 x 4)
 constexpr int kPerA = kT * kKC / kThr;  // 4 elements per thread per chunk
 constexpr int kPerB = kKC * kT / kThr;  // 4
 
@@ -38,7 +41,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-constexpr int kRT = 2, kCT = 4;  // DMMA tiles per warp (rows x cols)
+constexpr int kRT = GSUM_WARPS == 4 ? 4 : 2, kCT = 4;  // DMMA tiles per warp (rows x cols)
 
 struct Acc {
   double v[kRT][kCT][2];
@@ -50,7 +53,7 @@ struct Acc {
   }
 };
 
-__device__ __forceinline__ int warp_row0() { return (threadIdx.x >> 6) * 16; }
+__device__ __forceinline__ int warp_row0() { return (threadIdx.x >> 6) * 8 * kRT; }
 __device__ __forceinline__ int warp_col0() { return ((threadIdx.x >> 5) & 1) * 32; }
 
 // chunk loads: A rows i0..i0+63 (only < mt valid), k cols kk..kk+15 (only < kc); B likewise

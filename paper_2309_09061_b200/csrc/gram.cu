@@ -34,6 +34,7 @@ namespace {
 constexpr int kGT = 64;    // Gram tile
 constexpr int kGP = 32;    // panel columns
 constexpr int kGThr = 256;
+static_assert(kGramFlatThreads <= kGThr && kGramFlatThreads % 32 == 0, "flat Gram CTA size");
 constexpr int kGSeg = 64;  // staged segment descriptors per Gram CTA
 constexpr int kCThr = 512;
 constexpr double kEpsG = 2.220446049250313e-16;
@@ -121,7 +122,9 @@ __device__ __forceinline__ void g_cp_async8(double* dst, const double* src, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
 }
 
-__global__ void __launch_bounds__(kGThr, 2) gram_dd_partial_kernel(const GramItem* __restrict__ items,
+// FLAT: the 64 < m <= 128 block-list work units (own instantiation: separate registers), NT threads
+template <bool FLAT, int NT = FLAT ? kGramFlatThreads : kGThr>
+__global__ void __launch_bounds__(NT, 2) gram_dd_partial_kernel(const GramItem* __restrict__ items,
                                                                    const Seg* __restrict__ segs,
                                                                    const GramWork* __restrict__ work) {
   extern __shared__ __align__(16) double gring[];  // kGStages x {Pa, Pb} x [kGP][kGLd]
@@ -133,8 +136,154 @@ __global__ void __launch_bounds__(kGThr, 2) gram_dd_partial_kernel(const GramIte
   const GramWork w = work[blockIdx.x];
   const GramItem it = items[w.item];
   const int m = it.m;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = NT / 32;
+  double hi[16], lo[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0.0;
+  if (tid == 0) {
+    const int a = gfind_seg(segs, it.s0, it.s1, w.c0);
+    const int b = gfind_seg(segs, it.s0, it.s1, w.c1 - 1);
+    s_first = a;
+    s_n = b - a + 1;
+  }
+  __syncthreads();
+  const int sfirst = s_first, ns = s_n;
+  const bool staged = ns <= kGSeg;
+  if (staged)
+    for (int q = tid; q < ns; q += NT) {
+      const Seg sg = segs[sfirst + q];
+      s_off[q] = sg.off;
+      s_p[q] = sg.a.p;
+      s_rs[q] = it.hcols ? sg.a.rs : sg.a.cs;  // element stride along a line
+      s_cs[q] = it.hcols ? sg.a.cs : sg.a.rs;  // line stride
+      s_sc[q] = gseg_scale(sg);
+    }
+  __syncthreads();
+  const long long npan = (w.c1 - w.c0 + kGP - 1) / kGP;
+  // segment of line c: its column pointer, element stride and scale
+  auto line = [&](long long c, const double*& col, long long& rs, double& sc) {
+    if (staged) {
+      int lo2 = 0, hi2 = ns - 1;
+      while (lo2 < hi2) {
+        const int mid = (lo2 + hi2 + 1) >> 1;
+        if (s_off[mid] <= c) lo2 = mid; else hi2 = mid - 1;
+      }
+      col = s_p[lo2] + (c - s_off[lo2]) * s_cs[lo2];
+      rs = s_rs[lo2];
+      sc = s_sc[lo2];
+    } else {
+      const Seg sg = segs[gfind_seg(segs, it.s0, it.s1, c)];
+      col = sg.a.p + (c - sg.off) * (it.hcols ? sg.a.cs : sg.a.rs);
+      rs = it.hcols ? sg.a.rs : sg.a.cs;
+      sc = gseg_scale(sg);
+    }
+  };
+  const double* dummy = segs[it.s0].a.p;
+  if (FLAT) {
+    // ---- flat path (m <= 128): this CTA owns the 4 x 4 blocks b0 .. b0 + nbw - 1 of the upper
+    // triangle (row-major order), `reps` threads per block splitting each panel's lines; every
+    // panel stages all m rows (zero-padded to a multiple of 4), the replicas are summed in shared
+    // memory at the end (one partial slice per column chunk)
+    const int reps = w.tj >> 16, nbw = w.tj & 0xffff, b0 = w.ti;
+    const int nb = (m + 3) / 4, mp = 4 * nb, ldf = mp + 2;
+    const int bpc = reps > 1 ? NT / reps : NT;
+    const int lb = tid % bpc, rep = tid / bpc;
+    const bool act = lb < nbw;
+    int bi = 0, bj = 0;
+    {
+      int rem = b0 + (act ? lb : 0);
+      while (bi < nb && rem >= nb - bi) { rem -= nb - bi; ++bi; }
+      bj = bi + rem;
+    }
+    auto stage_f = [&](int s) { return gring + (size_t)s * kGP * ldf; };
+    double scf0 = 0.0, scf1 = 0.0, scf2 = 0.0;
+    auto issue_f = [&](long long p) {
+      if (p < npan) {
+        const int s = (int)(p % kGStages);
+        const long long c = w.c0 + p * kGP + lane;
+        const double* col = nullptr;
+        long long rs = 0;
+        double sc = 0.0;
+        if (c < w.c1) line(c, col, rs, sc);
+        if (s == 0) scf0 = sc; else if (s == 1) scf1 = sc; else scf2 = sc;
+        double* P = stage_f(s);
+        for (int r = warp; r < mp; r += nw) {
+          const bool v = col && r < m;
+          g_cp_async8(&P[lane * ldf + r], v ? col + (long long)r * rs : dummy, v);
+        }
+      }
+      asm volatile("cp.async.commit_group;");
+    };
+#pragma unroll
+    for (int p = 0; p < kGStages - 1; ++p) issue_f(p);
+    for (long long p = 0; p < npan; ++p) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(kGStages - 2));
+      {
+        const int s = (int)(p % kGStages);
+        const double sc = s == 0 ? scf0 : (s == 1 ? scf1 : scf2);
+        double* P = stage_f(s);
+        for (int r = warp; r < mp; r += nw) P[lane * ldf + r] *= sc;
+      }
+      __syncthreads();
+      issue_f(p + kGStages - 1);
+      if (act) {
+        const double* P = stage_f((int)(p % kGStages));
+#pragma unroll 2
+        for (int q0 = rep; q0 < kGP; q0 += reps) {
+          const double2 a01 = *reinterpret_cast<const double2*>(&P[q0 * ldf + 4 * bi]);
+          const double2 a23 = *reinterpret_cast<const double2*>(&P[q0 * ldf + 4 * bi + 2]);
+          const double2 b01 = *reinterpret_cast<const double2*>(&P[q0 * ldf + 4 * bj]);
+          const double2 b23 = *reinterpret_cast<const double2*>(&P[q0 * ldf + 4 * bj + 2]);
+          const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+          const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int q = 4 * u + v;
+              const double pr = a[u] * b[v];
+              const double pe = fma(a[u], b[v], -pr);
+              double s2, e;
+              two_sum(hi[q], pr, s2, e);
+              hi[q] = s2;
+              lo[q] += e + pe;
+            }
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;");
+    __syncthreads();  // the ring is free: replicas' partial sums go there
+    double* rb = gring;
+    if (act && rep > 0)
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        rb[(size_t)tid * 32 + q] = hi[q];
+        rb[(size_t)tid * 32 + 16 + q] = lo[q];
+      }
+    __syncthreads();
+    if (!act || rep > 0) return;
+    double* gh = it.gpart + (size_t)w.chunk * 2 * m * m;
+    double* gl = gh + (size_t)m * m;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int q = 4 * u + v;
+        dd acc = fast_two_sum(hi[q], lo[q]);
+        for (int r2 = 1; r2 < reps; ++r2) {  // fixed order: the result does not depend on scheduling
+          const size_t o = (size_t)(r2 * bpc + lb) * 32;
+          acc = dd_add(acc, dd{rb[o + q], rb[o + 16 + q]});
+        }
+        const int i = 4 * bi + u, j = 4 * bj + v;
+        if (i < m && j < m && i <= j) {
+          gh[(size_t)i * m + j] = acc.hi;
+          gl[(size_t)i * m + j] = acc.lo;
+        }
+      }
+    return;
+  }
+  // ---- tiled path: one 64 x 64 tile (ti, tj) of G's upper triangle
   const int ia = w.ti * kGT, jb = w.tj * kGT;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kGThr / 32;
   const bool diag = w.ti == w.tj;
   const int nbi = (min(kGT, m - ia) + 3) / 4, nbj = (min(kGT, m - jb) + 3) / 4;
   const int nblk = diag ? nbi * (nbi + 1) / 2 : nbi * nbj;
@@ -150,29 +299,6 @@ __global__ void __launch_bounds__(kGThr, 2) gram_dd_partial_kernel(const GramIte
     bi = blk / nbj;
     bj = blk % nbj;
   }
-  double hi[16], lo[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) hi[q] = lo[q] = 0.0;
-  if (tid == 0) {
-    const int a = gfind_seg(segs, it.s0, it.s1, w.c0);
-    const int b = gfind_seg(segs, it.s0, it.s1, w.c1 - 1);
-    s_first = a;
-    s_n = b - a + 1;
-  }
-  __syncthreads();
-  const int sfirst = s_first, ns = s_n;
-  const bool staged = ns <= kGSeg;
-  if (staged)
-    for (int q = tid; q < ns; q += kGThr) {
-      const Seg sg = segs[sfirst + q];
-      s_off[q] = sg.off;
-      s_p[q] = sg.a.p;
-      s_rs[q] = it.hcols ? sg.a.rs : sg.a.cs;  // element stride along a line
-      s_cs[q] = it.hcols ? sg.a.cs : sg.a.rs;  // line stride
-      s_sc[q] = gseg_scale(sg);
-    }
-  __syncthreads();
-  const long long npan = (w.c1 - w.c0 + kGP - 1) / kGP;
   // this thread's copies: column `lane` of the panel, rows warp, warp + nw, ...
   auto stage_a = [&](int s) { return gring + (size_t)s * 2 * kGP * kGLd; };
   auto stage_b = [&](int s) { return gring + (size_t)s * 2 * kGP * kGLd + kGP * kGLd; };
@@ -205,7 +331,6 @@ __global__ void __launch_bounds__(kGThr, 2) gram_dd_partial_kernel(const GramIte
       if (s == 0) sc0 = sc; else if (s == 1) sc1 = sc; else sc2 = sc;
       double* Pa = stage_a(s);
       double* Pb = stage_b(s);
-      const double* dummy = segs[it.s0].a.p;
       for (int r = warp; r < kGT; r += nw) {
         const int ra = ia + r, rb = jb + r;
         const bool va = col && ra < m;
@@ -444,18 +569,21 @@ size_t gram_chol_smem(int m) {
 
 cudaError_t launch_gram_chol(const GramItem* items, int nitems, int mmax, cudaStream_t st);
 
-cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nitems,
-                        int mmax, cudaStream_t st) {
+cudaError_t launch_gram(const GramItem* items, const Seg* segs, const GramWork* work, int nwork, int nflat,
+                        int nitems, int mmax, cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, (const void*)gram_chol_kernel);
     cudaFuncSetAttribute((const void*)gram_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024 - (int)fa.sharedSizeBytes);
-    cudaFuncSetAttribute((const void*)gram_dd_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gram_partial_smem());
+    for (const void* fn : {(const void*)gram_dd_partial_kernel<true>, (const void*)gram_dd_partial_kernel<false>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_partial_smem());
   });
-  if (nwork > 0) gram_dd_partial_kernel<<<nwork, kGThr, gram_partial_smem(), st>>>(items, segs, work);
+  // work units: the flat ones (m <= 128) first, then the tiled ones
+  if (nflat > 0) gram_dd_partial_kernel<true><<<nflat, kGramFlatThreads, gram_partial_smem(), st>>>(items, segs, work);
+  if (nwork > nflat)
+    gram_dd_partial_kernel<false><<<nwork - nflat, kGThr, gram_partial_smem(), st>>>(items, segs, work + nflat);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nitems == 0) return e;
   return launch_gram_chol(items, nitems, mmax, st);

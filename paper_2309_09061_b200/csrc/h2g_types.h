@@ -120,7 +120,10 @@ struct GramItem {
   int* nr;                // rows of the factor
 };
 
-// One CTA of the double-double Gram (gram.cu): columns [c0, c1) of item `item`, G tile (ti, tj).
+// One CTA of the double-double Gram (gram.cu): columns [c0, c1) of item `item`, G tile (ti, tj); for
+// m <= kGramFlatMax, ti = first 4 x 4 block (row-major upper triangle) and tj = blocks | reps << 16.
+constexpr int kGramFlatMax = 128;
+constexpr int kGramFlatThreads = 192;  // CTA size of the flat path (528 blocks of m = 128: 3 x 176)
 struct GramWork {
   int item, ti, tj, chunk;
   long long c0, c1;
