@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
   double* Gh = gsm;
   double* Gl = Gh + np;
   int* roff = reinterpret_cast<int*>(Gl + np);  // packed offset of (i, i)
-  unsigned char* done = reinterpret_cast<unsigned char*>(roff + m);
+  int* act = roff + m;                      // two sorted lists of the not-yet-pivoted indices (m each)
+  unsigned char* done = reinterpret_cast<unsigned char*>(act + 2 * m);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5, nt = blockDim.x;
   double* R = it.rbuf;  // m x m, row-major
   for (int i = tid; i < m; i += blockDim.x) roff[i] = (int)pidx(i, i, m);
@@ -441,7 +442,10 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
       Gh[e] = acc.hi;
       Gl[e] = acc.lo;
     }
-  for (int c = tid; c < m; c += nt) done[c] = 0;
+  for (int c = tid; c < m; c += nt) {
+    done[c] = 0;
+    act[c] = c;
+  }
   __syncthreads();
   // argmax partials of the diagonal (buffer 0)
   {
@@ -496,14 +500,25 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
         R[(size_t)j * m + c] = v;
       }
     }
-    // Schur complement of the remaining rows / columns; diagonal argmax partials for step j + 1
+    // Schur complement of the remaining rows / columns over the compact sorted list of the indices
+    // not pivoted yet (r = m - j of them, p among them): (m - j)^2 / 2 entries per step instead of a
+    // sweep over all m^2 / 2 behind per-entry `done` tests; the list without p (still sorted) is
+    // written for step j + 1.  Diagonal argmax partials for step j + 1 as the diagonal is updated.
+    const int r = m - j;
+    const int* ac = act + (j & 1) * m;
+    int* an = act + ((j + 1) & 1) * m;
+    for (int t = tid; t < r; t += nt) {
+      const int a = ac[t];
+      if (a != p) an[a < p ? t : t - 1] = a;
+    }
     double cbest = -1.0;
     int cbi = m;
     // two rows per warp iteration: their double-double chains are independent and interleave
-    for (int a0 = warp; a0 < m; a0 += 2 * nw) {
-      const int a1 = a0 + nw;
-      const bool v0 = a0 != p && !done[a0];
-      const bool v1 = a1 < m && a1 != p && !done[a1];
+    for (int i0 = warp; i0 < r; i0 += 2 * nw) {
+      const int i1 = i0 + nw;
+      const int a0 = ac[i0], a1 = i1 < r ? ac[i1] : m;
+      const bool v0 = a0 != p;
+      const bool v1 = i1 < r && a1 != p;
       dd g0{0.0, 0.0}, g1{0.0, 0.0};
       if (v0) {
         const long long e = a0 < p ? PX(a0, p) : PX(p, a0);
@@ -514,10 +529,11 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
         g1 = dd_mul(dd{Gh[e], Gl[e]}, inv);
       }
       if (!v0 && !v1) continue;
-      for (int k = lane; a0 + k < m; k += 32) {
-        const int b0 = a0 + k, b1 = a1 + k;
-        const bool w0 = v0 && b0 != p && !done[b0];
-        const bool w1 = v1 && b1 < m && b1 != p && !done[b1];
+      for (int k = lane; i0 + k < r; k += 32) {
+        const int b0 = ac[i0 + k];
+        const int b1 = i1 + k < r ? ac[i1 + k] : m;
+        const bool w0 = v0 && b0 != p;
+        const bool w1 = v1 && i1 + k < r && b1 != p;
         dd x0{0.0, 0.0}, y0{0.0, 0.0}, x1{0.0, 0.0}, y1{0.0, 0.0};
         long long e0 = 0, e1 = 0;
         if (w0) {
@@ -564,7 +580,7 @@ __global__ void __launch_bounds__(kCThr, 1) gram_chol_kernel(const GramItem* __r
 
 size_t gram_chol_smem(int m) {
   const size_t np = (size_t)m * (m + 1) / 2;
-  return sizeof(double) * 2 * np + sizeof(int) * (size_t)m + (size_t)m + 16;
+  return sizeof(double) * 2 * np + sizeof(int) * 3 * (size_t)m + (size_t)m + 16;
 }
 
 cudaError_t launch_gram_chol(const GramItem* items, int nitems, int mmax, cudaStream_t st);
