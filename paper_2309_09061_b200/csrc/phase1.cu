@@ -953,6 +953,11 @@ std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int m
   Ctx* A = nullptr;
   if (ahead) {
     A = &C.aux();
+    // recycle its staging buffer (and free any retired one): the previous product's dense launch is
+    // long finished (its coarsen joined the expansion stream, which waited for it), so this does not
+    // wait in practice -- without it the buffer's offset only grew and every few products an
+    // overflow reallocated it (pinned cudaMallocHost + cudaMalloc: +100-300 ms steps)
+    A->sync();
     cuda_check(cudaEventCreateWithFlags(&p_ready, cudaEventDisableTiming), "event");
     cuda_check(cudaEventRecord(p_ready, C.st), "event");
   }
