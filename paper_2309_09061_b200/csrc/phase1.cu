@@ -745,6 +745,7 @@ std::shared_ptr<H2> assemble(Ctx& C, HView x, HView y, Induced& qr, Induced& qc,
   Ctx* Ep = (!serial_passes() && !part.on() && !exp3 && !sync_exp) ? &C.aux(true) : nullptr;
   std::shared_ptr<Arena> pa;  // the expansions' k~ x k~ parts (read on Ep, freed after it)
   if (Ep) {
+    Ep->sync();  // recycle its staging (a product without coarsen never joins it)
     pa = std::make_shared<Arena>(C.st);
     Ep->tag = "p1.expand";
   }
