@@ -922,7 +922,7 @@ static constexpr int NT = 512;
 // RS: R in shared memory (compile-time, so every access to it is an LDS/STS rather than a generic
 // load), else R is worked on in place in global memory (items too large for shared memory).
 template <int NPLO, bool RS>
-__global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
+__global__ void __launch_bounds__(NT, (NPLO >= 16 || NPLO == 0) ? 1 : 2) svd_finish_kernel(const SvdItem* __restrict__ items,
                                                                              const Seg* __restrict__ segs,
                                                                              int vsm, long long smem_doubles) {
   extern __shared__ __align__(16) double smem[];
@@ -1005,6 +1005,8 @@ __global__ void __launch_bounds__(NT, NPLO >= 16 ? 1 : 2) svd_finish_kernel(cons
     tk[2] = clock64();
     const int sw = (NPLO > 0 && n <= 8 * NPLO)
                        ? jacobi_rows_oct<(NPLO > 0 ? NPLO : 2), RS>(R, nr, n, ld, flag, jred)
+                       : (NPLO == 0 && n <= 256)
+                       ? jacobi_rows<(NPLO == 0 ? 16 : 1)>(R, nr, n, ld, flag, jred)  // rows cached in registers
                        : jacobi_rows<0>(R, nr, n, ld, flag, jred);
     tk[3] = clock64();
     if (it.sweeps_out && threadIdx.x == 0) {
