@@ -356,11 +356,15 @@ def test_block_relative_error_per_coarse_leaf():
 
 
 @pytest.mark.parametrize("env", [{"H2G_NO_GRAM": "1", "H2G_NO_GRAM_QR": "1"},  # Householder TSQR everywhere
-                                 {"H2G_GRAM_PROT": "1"}])                        # Gram for protected SVDs too
+                                 {"H2G_GRAM_PROT": "1"},                         # Gram for protected SVDs too
+                                 {"H2G_GRAM_TILED": "1", "H2G_NORM_CTA": "1"},   # 64x64 Gram tiles, smem Lanczos
+                                 {"H2G_SYNC_EXPAND": "1", "H2G_SERIAL": "1"}])   # expansions / passes in line
 def test_alternative_factorisation_paths(env):
     """The factorisation paths selected by environment switches (read once per process) keep every
     golden gate: the Householder TSQR + QRCP path that the double-double Gram path replaced by
-    default, and the opt-in Gram path for the protected-basis SVDs of phase 1."""
+    default, the opt-in Gram path for the protected-basis SVDs of phase 1, the 64 x 64-tile Gram
+    decomposition and shared-memory Lanczos norms the block-list Gram and register-tile norms
+    replaced, and the push-down expansions / row and column passes on the main stream."""
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
