@@ -407,20 +407,75 @@ void GBatch::t3(MatRef a, MatRef b, MatRef d, int k, int k2, double al) {
   outs.back().t1 = (int)terms.size();
 }
 
+
+// H2G_DEBUG_GSUM=1: per launch, how full its 64 x 64 tiles are (live 16 x 32 warp quadrants of 8)
+static void gsum_tile_stats(const char* tag, const std::vector<GOut>& outs, const std::vector<GTile>& tiles,
+                            const std::vector<GTerm>* terms) {
+  static const bool dbg = getenv("H2G_DEBUG_GSUM") != nullptr;
+  if (!dbg || tiles.size() < 500) return;
+  double live = 0, full = 0, cells = 0, ksum = 0, kcnt = 0;
+  long long hist[9] = {0};
+  for (const GTile& t : tiles) {
+    const GOut& o = outs[t.out];
+    const int i0 = (t.tij & 0xffff) * 64, j0 = (t.tij >> 16) * 64;
+    const int mt = std::min(64, o.m - i0), nt = std::min(64, o.n - j0);
+    const int lw = ((mt + 15) / 16) * ((nt + 31) / 32);
+    live += lw;
+    ++hist[lw];
+    full += (mt == 64 && nt == 64);
+    cells += (double)mt * nt;
+    if (terms)
+      for (int i = o.t0; i < o.t1; ++i) {
+        const GTerm& u = (*terms)[i];
+        if (u.nf >= 2) { ksum += u.k; ++kcnt; }
+      }
+  }
+  const double n = (double)tiles.size();
+  fprintf(stderr, "gsum[%s] tiles %zu outs %zu: full %.2f, live warps %.2f/8, cell fill %.2f, mean k %.1f (%.1f terms/tile), live hist",
+          tag ? tag : "", tiles.size(), outs.size(), full / n, live / n, cells / (4096.0 * n), ksum / std::max(1.0, kcnt), kcnt / n);
+  for (int i = 1; i <= 8; ++i) fprintf(stderr, " %lld", hist[i]);
+  fprintf(stderr, "\n");
+}
+
 void GBatch::run(Ctx& C) {
   HostTimer ht(C, "gbatch_run");
   std::vector<GTile> tiles;
+  // batches of plain sums and 2-factor products (no grouped / 3-factor terms) take the lean kernel:
+  // 4-warp CTAs in the arrangement (32 x 64, 64 x 32, 16 x 128) that covers each output with the
+  // fewest CTAs (H2G_GSUM_NO_LEAN=1: 64 x 64 tiles, for A/B)
+  static const bool no_lean = getenv("H2G_GSUM_NO_LEAN") != nullptr;
+  bool lean = !no_lean && tag == 0;
+  if (lean)
+    for (const GTerm& t : terms)
+      if (t.nf > 2) { lean = false; break; }
+  if (lean)
+    for (const GOut& o : outs)
+      if (o.ka || o.kb) { lean = false; break; }
+  std::vector<GLTile> ltiles;
+  bool wide = false;
   for (int i = 0; i < (int)outs.size(); ++i) {
     const GOut& o = outs[i];
     if (o.m <= 0 || o.n <= 0) continue;
+    if (lean) {
+      auto cd = [](int a, int b) { return (a + b - 1) / b; };
+      const int n0 = cd(o.m, 32) * cd(o.n, 64), n1 = cd(o.m, 64) * cd(o.n, 32), n2 = cd(o.m, 16) * cd(o.n, 128);
+      const int lay = (n2 < n0 && n2 < n1) ? 2 : (n1 < n0 ? 1 : 0);
+      const int TM = lay == 0 ? 32 : (lay == 1 ? 64 : 16), TN = lay == 0 ? 64 : (lay == 1 ? 32 : 128);
+      wide |= lay == 2;
+      for (int a = 0; a < o.m; a += TM)
+        for (int b = 0; b < o.n; b += TN) ltiles.push_back(GLTile{i, a, b, lay});
+      continue;
+    }
     const int tm = (o.m + 63) / 64, tn = (o.n + 63) / 64;
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
   }
-  if (tiles.empty()) return;
+  if (tiles.empty() && ltiles.empty()) return;
+  gsum_tile_stats(C.tag.c_str(), outs, tiles, &terms);
   GOut* d_o = C.push(outs);
   GTerm* d_t = C.push(terms);
   GTile* d_l = C.push(tiles);
+  GLTile* d_ll = C.push(ltiles);
   double fl = 0, by = 0;
   if (C.prof) {  // algorithmic work: each product once at its own shape
     for (const GOut& o : outs) {
@@ -439,7 +494,8 @@ void GBatch::run(Ctx& C) {
   }
   cudaEvent_t ev = C.prof_begin();
   C.flush();
-  cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+  if (lean) cuda_check(launch_gsum_lean(d_o, d_t, d_ll, (int)ltiles.size(), wide, C.st), "gsum(lean)");
+  else cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
   C.prof_end(K_GSUM, ev, fl, by);
   ++C.launches;
   outs.clear();
@@ -478,6 +534,7 @@ void GBatch::run_device_terms(Ctx& C, const GTerm* d_terms, double flops_hint) {
   HostTimer ht(C, "gbatch_run");
   if (!tiles_ready) prepare_tiles();
   if (!tiles.empty() || !whole_tiles.empty()) {
+    gsum_tile_stats(C.tag.c_str(), outs, tiles, nullptr);
     GOut* d_o = C.push(outs);
     GTile* d_l = C.push(tiles);
     GTile* d_w = C.push(whole_tiles);

@@ -44,6 +44,14 @@ struct GTile {
   int tij;  // ti | (tj << 16)
 };
 
+// One tile of a GOut for the lean 2-factor kernel (gemm_lean.cu): origin and warp arrangement
+// (lay 0: 2 x 2 warps = 32 x 64, 1: 4 x 1 = 64 x 32, 2: 1 x 4 = 16 x 128; a warp owns 16 x 32).
+struct GLTile {
+  int out;
+  int i0, j0;
+  int lay;
+};
+
 // Segment of a stacked operand.  hstack: a is (m x w); vstack: a is (w x n).  Scaled by `scale`.
 struct Seg {
   MatRef a;
