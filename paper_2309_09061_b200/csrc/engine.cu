@@ -451,11 +451,22 @@ void GBatch::run(Ctx& C) {
   if (lean)
     for (const GOut& o : outs)
       if (o.ka || o.kb) { lean = false; break; }
-  std::vector<GLTile> ltiles;
+  std::vector<GLTile> ltiles, stiles;
   bool wide = false;
+  static const bool no_sum = getenv("H2G_GSUM_NO_SUM") != nullptr;  // A/B: sums through the GEMM kernels
+  const int sum_chunk = gsum_sum_chunk();
   for (int i = 0; i < (int)outs.size(); ++i) {
     const GOut& o = outs[i];
     if (o.m <= 0 || o.n <= 0) continue;
+    if (!no_sum && !o.ka && !o.kb) {  // plain sums / copies: the elementwise kernel
+      bool sum_only = true;
+      for (int t = o.t0; t < o.t1 && sum_only; ++t) sum_only = terms[t].nf <= 1;
+      if (sum_only) {
+        const long long tot = (long long)o.m * o.n;
+        for (long long a = 0; a * sum_chunk < tot; ++a) stiles.push_back(GLTile{i, (int)a, 0, 0});
+        continue;
+      }
+    }
     if (lean) {
       auto cd = [](int a, int b) { return (a + b - 1) / b; };
       const int n0 = cd(o.m, 32) * cd(o.n, 64), n1 = cd(o.m, 64) * cd(o.n, 32), n2 = cd(o.m, 16) * cd(o.n, 128);
@@ -470,12 +481,13 @@ void GBatch::run(Ctx& C) {
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
   }
-  if (tiles.empty() && ltiles.empty()) return;
+  if (tiles.empty() && ltiles.empty() && stiles.empty()) return;
   gsum_tile_stats(C.tag.c_str(), outs, tiles, &terms);
   GOut* d_o = C.push(outs);
   GTerm* d_t = C.push(terms);
   GTile* d_l = C.push(tiles);
   GLTile* d_ll = C.push(ltiles);
+  GLTile* d_sl = C.push(stiles);
   double fl = 0, by = 0;
   if (C.prof) {  // algorithmic work: each product once at its own shape
     for (const GOut& o : outs) {
@@ -494,10 +506,18 @@ void GBatch::run(Ctx& C) {
   }
   cudaEvent_t ev = C.prof_begin();
   C.flush();
-  if (lean) cuda_check(launch_gsum_lean(d_o, d_t, d_ll, (int)ltiles.size(), wide, C.st), "gsum(lean)");
-  else cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+  if (!stiles.empty()) {
+    cuda_check(launch_gsum_sum(d_o, d_t, d_sl, (int)stiles.size(), C.st), "gsum(sum)");
+    ++C.launches;
+  }
+  if (!ltiles.empty()) {
+    cuda_check(launch_gsum_lean(d_o, d_t, d_ll, (int)ltiles.size(), wide, C.st), "gsum(lean)");
+    ++C.launches;
+  } else if (!tiles.empty()) {
+    cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
+    ++C.launches;
+  }
   C.prof_end(K_GSUM, ev, fl, by);
-  ++C.launches;
   outs.clear();
   terms.clear();
   tiles.clear();

@@ -29,6 +29,8 @@ void cuda_check(cudaError_t e, const char* what);
 // ------------------------------------------------------------------ kernels (kernels.cu)
 cudaError_t launch_gsum(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t, int tag = 0);
 cudaError_t launch_gsum_lean(const GOut*, const GTerm*, const GLTile*, int ntiles, bool wide, cudaStream_t);
+cudaError_t launch_gsum_sum(const GOut*, const GTerm*, const GLTile*, int ntiles, cudaStream_t);
+int gsum_sum_chunk();
 cudaError_t launch_gsum_whole(const GOut*, const GTerm*, const GTile*, int ntiles, int k2max, cudaStream_t);
 cudaError_t launch_qr_chunks(const QrItem*, const Seg*, const SvdWork*, int nwork, size_t smem, bool rsmem,
                              cudaStream_t);

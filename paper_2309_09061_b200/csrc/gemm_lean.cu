@@ -214,6 +214,56 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
   }
 }
 
+
+// Outputs that are plain sums (every term nf <= 1: the gathers of phase 2's column-tree representatives
+// and of the basis stacks are one-term copies) need no tensor work: one CTA per 1024 consecutive
+// elements of the row-major output, 8 per thread with consecutive lanes on consecutive columns, the
+// term loop outermost so that a term's 8 loads are in flight together.  The lean / tile kernels spend
+// four dependent global round trips per CTA on such an output at 12-16 warps per SM.
+// Same expression per element as the GEMM kernels' nf = 1 path (bitwise equal).
+constexpr int kSumThr = 128, kSumPer = 8;
+
+__global__ void __launch_bounds__(kSumThr, 8) gsum_sum_kernel(const GOut* __restrict__ outs,
+                                                          const GTerm* __restrict__ terms,
+                                                          const GLTile* __restrict__ tiles) {
+  const GLTile tl = tiles[blockIdx.x];
+  const GOut o = outs[tl.out];
+  const long long total = (long long)o.m * o.n;
+  const long long e0 = (long long)tl.i0 * (kSumThr * kSumPer) + threadIdx.x;
+  int ii[kSumPer], jj[kSumPer];
+  double acc[kSumPer];
+#pragma unroll
+  for (int q = 0; q < kSumPer; ++q) {
+    const long long e = e0 + (long long)q * kSumThr;
+    const bool v = e < total;
+    ii[q] = v ? (int)(e / o.n) : -1;
+    jj[q] = v ? (int)(e - (long long)ii[q] * o.n) : 0;
+    acc[q] = 0.0;
+  }
+  for (int ti = o.t0; ti < o.t1; ++ti) {
+    if (terms[ti].nf != 1) continue;
+    const MatRef a = terms[ti].a;
+    const double al = terms[ti].alpha;
+#pragma unroll
+    for (int q = 0; q < kSumPer; ++q)
+      if (ii[q] >= 0) acc[q] += al * a.p[(long long)ii[q] * a.rs + (long long)jj[q] * a.cs];
+  }
+#pragma unroll
+  for (int q = 0; q < kSumPer; ++q)
+    if (ii[q] >= 0) {
+      double* dst = o.c + (long long)ii[q] * o.ldc + jj[q];
+      *dst = (o.beta ? *dst : 0.0) + acc[q];
+    }
+}
+
+cudaError_t launch_gsum_sum(const GOut* outs, const GTerm* terms, const GLTile* tiles, int ntiles, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  gsum_sum_kernel<<<ntiles, kSumThr, 0, st>>>(outs, terms, tiles);
+  return cudaGetLastError();
+}
+
+int gsum_sum_chunk() { return kSumThr * kSumPer; }
+
 // `wide`: the batch holds 1 x 4 tiles (16 x 128: the larger stage)
 cudaError_t launch_gsum_lean(const GOut* outs, const GTerm* terms, const GLTile* tiles, int ntiles, bool wide,
                              cudaStream_t st) {
