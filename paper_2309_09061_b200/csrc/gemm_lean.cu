@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
   const GLTile tl = tiles[blockIdx.x];
   const GOut o = outs[tl.out];
   const int WC = tl.lay == 0 ? 2 : (tl.lay == 1 ? 1 : 4);  // warp columns
-  const int TM = 16 * (kW / WC), TN = 32 * WC;
+  const int lgTM = tl.lay == 0 ? 5 : (tl.lay == 1 ? 6 : 4), lgTN = tl.lay == 0 ? 6 : (tl.lay == 1 ? 5 : 7);
+  const int TM = 1 << lgTM, TN = 1 << lgTN;
   const int szA = TM * kLdK, stg = (TM + TN) * kLdK;  // doubles per stage (A | B), either layout fits
   const int ldAk = TM + 4, ldBk = TN + 4;              // [k][line] strides
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -101,32 +102,34 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
           double* sA = ring + (c % kPS) * stg;
           double* sB = sA + szA;
           const int kc = min(kKC, Pk - pk);
-          if (PA.cs == 1) {  // k contiguous: [i][k]
-            for (int e = tid; e < TM * kKC; e += kThr) {
-              const int i = e / kKC, l = e % kKC;
-              const bool v = i < mt && l < kc;
-              cp_async8(sA + i * kLdK + l, v ? PA.p + (long long)(i0 + i) * PA.rs + (pk + l) : PA.p, v);
-            }
-          } else {  // [k][i]
-            for (int e = tid; e < TM * kKC; e += kThr) {
-              const int l = e / TM, i = e % TM;
-              const bool v = i < mt && l < kc;
-              cp_async8(sA + l * ldAk + i,
-                        v ? PA.p + (long long)(i0 + i) * PA.rs + (long long)(pk + l) * PA.cs : PA.p, v);
+          // each thread copies a fixed fast-dimension line, stepping over the slow dimension
+          // (no per-element index arithmetic: the tile extents are powers of two)
+          {
+            const bool aK = PA.cs == 1;  // k contiguous: [i][k], else [k][i]
+            const int lg = aK ? 4 : lgTM;
+            const int f = tid & ((1 << lg) - 1), step = kThr >> lg, S = aK ? TM : kKC;
+            const bool fv = f < (aK ? kc : mt);
+            const int lim = aK ? mt : kc, dS = aK ? kLdK : ldAk;
+            const long long gS = aK ? (long long)PA.rs : (long long)PA.cs;
+            const double* src = aK ? PA.p + (long long)i0 * PA.rs + (pk + f)
+                                   : PA.p + (long long)(i0 + f) * PA.rs + (long long)pk * PA.cs;
+            for (int q = tid >> lg; q < S; q += step) {
+              const bool v = fv && q < lim;
+              cp_async8(sA + q * dS + f, v ? src + q * gS : PA.p, v);
             }
           }
-          if (PB.cs == 1) {  // j contiguous: [k][j]
-            for (int e = tid; e < TN * kKC; e += kThr) {
-              const int l = e / TN, j = e % TN;
-              const bool v = j < nt && l < kc;
-              cp_async8(sB + l * ldBk + j, v ? PB.p + (long long)(pk + l) * PB.rs + (j0 + j) : PB.p, v);
-            }
-          } else {  // [j][k]
-            for (int e = tid; e < TN * kKC; e += kThr) {
-              const int j = e / kKC, l = e % kKC;
-              const bool v = j < nt && l < kc;
-              cp_async8(sB + j * kLdK + l,
-                        v ? PB.p + (long long)(pk + l) * PB.rs + (long long)(j0 + j) * PB.cs : PB.p, v);
+          {
+            const bool bN = PB.cs == 1;  // j contiguous: [k][j], else [j][k]
+            const int lg = bN ? lgTN : 4;
+            const int f = tid & ((1 << lg) - 1), step = kThr >> lg, S = bN ? kKC : TN;
+            const bool fv = f < (bN ? nt : kc);
+            const int lim = bN ? kc : nt, dS = bN ? ldBk : kLdK;
+            const long long gS = bN ? (long long)PB.rs : (long long)PB.cs;
+            const double* src = bN ? PB.p + (long long)pk * PB.rs + (j0 + f)
+                                   : PB.p + (long long)(pk + f) * PB.rs + (long long)j0 * PB.cs;
+            for (int q = tid >> lg; q < S; q += step) {
+              const bool v = fv && q < lim;
+              cp_async8(sB + q * dS + f, v ? src + q * gS : PB.p, v);
             }
           }
           pk += kKC;
