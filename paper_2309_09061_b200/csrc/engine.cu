@@ -470,7 +470,9 @@ void GBatch::run(Ctx& C) {
     if (lean) {
       auto cd = [](int a, int b) { return (a + b - 1) / b; };
       const int n0 = cd(o.m, 32) * cd(o.n, 64), n1 = cd(o.m, 64) * cd(o.n, 32), n2 = cd(o.m, 16) * cd(o.n, 128);
-      const int lay = (n2 < n0 && n2 < n1) ? 2 : (n1 < n0 ? 1 : 0);
+      // the 16 x 128 arrangement needs the larger stage (3 CTAs per SM instead of 4 for the whole
+      // launch): only where it halves the CTA count
+      const int lay = (2 * n2 <= n0 && 2 * n2 <= n1) ? 2 : (n1 < n0 ? 1 : 0);
       const int TM = lay == 0 ? 32 : (lay == 1 ? 64 : 16), TN = lay == 0 ? 64 : (lay == 1 ? 32 : 128);
       wide |= lay == 2;
       for (int a = 0; a < o.m; a += TM)
@@ -482,6 +484,27 @@ void GBatch::run(Ctx& C) {
       for (int b = 0; b < tn; ++b) tiles.push_back(GTile{i, a | (b << 16)});
   }
   if (tiles.empty() && ltiles.empty() && stiles.empty()) return;
+  {
+    static const bool dbg = getenv("H2G_DEBUG_GSUM") != nullptr;
+    if (dbg && ltiles.size() >= 500) {
+      long long n1 = 0, n2 = 0, no = 0, k2 = 0, cells = 0;
+      std::vector<char> seen(outs.size(), 0);
+      for (const GLTile& t : ltiles) {
+        if (seen[t.out]) continue;
+        seen[t.out] = 1;
+        const GOut& o = outs[t.out];
+        ++no;
+        cells += (long long)o.m * o.n;
+        for (int i = o.t0; i < o.t1; ++i) {
+          if (terms[i].nf == 1) ++n1;
+          else if (terms[i].nf == 2) { ++n2; k2 += terms[i].k; }
+        }
+      }
+      fprintf(stderr, "gsum-lean[%s] tiles %zu (sum tiles %zu) outs %lld: mean m*n %.0f, nf1 terms/out %.2f, nf2 terms/out %.2f, mean k %.1f, wide %d\n",
+              C.tag.c_str(), ltiles.size(), stiles.size(), no, (double)cells / std::max(1LL, no), (double)n1 / std::max(1LL, no),
+              (double)n2 / std::max(1LL, no), (double)k2 / std::max(1LL, n2), (int)wide);
+    }
+  }
   gsum_tile_stats(C.tag.c_str(), outs, tiles, &terms);
   GOut* d_o = C.push(outs);
   GTerm* d_t = C.push(terms);

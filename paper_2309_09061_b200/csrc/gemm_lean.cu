@@ -64,6 +64,20 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
 
+  // accumulating outputs (beta): the epilogue's read of C was the kernel's largest stall (28 % of the
+  // warp samples on the DADDs behind those loads, push-down launch, ncu) -- request the lines now
+  if (o.beta && live) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4;
+        if (i < mt && j < nt) {
+          const double* q = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+        }
+      }
+  }
   int ti = o.t0;
   while (ti < o.t1) {
     const int nf0 = terms[ti].nf;
