@@ -273,17 +273,13 @@ static int upload_impl(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, c
     if (coup_len > 0)
       cuda_check(cudaMemcpyAsync(dc, coup_data, coup_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
     if (near_len > 0) {
-      if (async_near) {  // the nearfield streams in on the copy stream while the product starts
-        if (!C.up_stream) cuda_check(cudaStreamCreateWithFlags(&C.up_stream, cudaStreamNonBlocking), "stream");
-        cudaEvent_t alloc_done;
-        cuda_check(cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventRecord(alloc_done, C.st), "event");
-        cuda_check(cudaStreamWaitEvent(C.up_stream, alloc_done, 0), "wait");
-        cudaEventDestroy(alloc_done);
-        cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.up_stream),
-                   "upload");
-        cuda_check(cudaEventCreateWithFlags(&h->near_ready, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventRecord(h->near_ready, C.up_stream), "event");
+      if (async_near) {  // the nearfield streams in on the copy stream while the product starts;
+                         // the copy is issued at the matrix's first use (H2::start_near)
+        cuda_check(cudaEventCreateWithFlags(&h->near_alloc, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(h->near_alloc, C.st), "event");
+        h->near_src = near_data;
+        h->near_dst = dn;
+        h->near_bytes = (size_t)near_len * sizeof(double);
       } else {
         cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
       }
@@ -510,6 +506,8 @@ int h2g_matvec(h2g_ctx* ctx, h2g_h2* g, int trans, const double* x, double* y, d
 
 int h2g_multiply(h2g_ctx* ctx, h2g_h2* x, h2g_h2* y, double tol, int max_rank, int scaling, h2g_h2** g) {
   return guarded([&] {
+    x->h->start_near(ctx->c);
+    y->h->start_near(ctx->c);
     need_whole(ctx->c, *x->h);
     need_whole(ctx->c, *y->h);
     auto G = multiply(ctx->c, *x->h, *y->h, tol, max_rank, scaling != 0);

@@ -388,6 +388,16 @@ cudaEvent_t Ctx::event() {
   return e;
 }
 
+void H2::start_near(Ctx& C) const {
+  if (!near_src) return;
+  if (!C.up_stream) cuda_check(cudaStreamCreateWithFlags(&C.up_stream, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamWaitEvent(C.up_stream, near_alloc, 0), "wait");
+  cuda_check(cudaMemcpyAsync(near_dst, near_src, near_bytes, cudaMemcpyHostToDevice, C.up_stream), "upload");
+  cuda_check(cudaEventCreateWithFlags(&near_ready, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(near_ready, C.up_stream), "event");
+  near_src = nullptr;
+}
+
 void GBatch::t1(MatRef a, double al) {
   terms.push_back(GTerm{a, MatRef{nullptr, 0, 0}, MatRef{nullptr, 0, 0}, 0, 0, 1, 0, al});
   outs.back().t1 = (int)terms.size();

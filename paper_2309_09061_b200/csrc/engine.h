@@ -149,6 +149,8 @@ struct Basis {  // leaf (size x k, ld k); xfer (k_c x k_parent, ld k_parent)
   Mat xferm(int c) const { return Mat{xfer[c], rank[c], rank[tree->parent[c]]}; }
 };
 
+struct Ctx;
+
 struct H2 {
   std::shared_ptr<const Blocks> bt;
   // partitioned product (multi-GPU): this rank holds the leaf blocks of its own block rows (plus the
@@ -159,7 +161,16 @@ struct H2 {
   std::vector<double*> coup, near;
   std::vector<ArenaPtr> owned;
   ArenaPtr near_owner;  // arena holding the nearfield blocks (shared by a coarsened result)
-  cudaEvent_t near_ready = nullptr;  // asynchronous upload: the nearfield copy completes at this event
+  // asynchronous upload: the nearfield copy completes at this event.  The copy itself is deferred
+  // (start_near) until the matrix is first used, so that the small arrays (bases, couplings) of a
+  // second operand uploaded right after do not queue behind 3 GB of nearfield on the copy engine:
+  // multiply starts both operands' copies after all the small ones.
+  mutable cudaEvent_t near_ready = nullptr;
+  mutable const double* near_src = nullptr;  // pending host source (pinned or pageable), null once started
+  mutable double* near_dst = nullptr;
+  mutable size_t near_bytes = 0;
+  mutable cudaEvent_t near_alloc = nullptr;  // the device allocation is stream-ordered: the copy follows it
+  void start_near(Ctx& C) const;
   // nearfield prefetch to the host (coarsen with a host buffer): blocks already copied, the target
   // buffer and the event that completes the copy
   std::vector<char> near_on_host;
@@ -167,6 +178,7 @@ struct H2 {
   cudaEvent_t near_host_ready = nullptr;
   ~H2() {
     if (near_ready) cudaEventDestroy(near_ready);
+    if (near_alloc) cudaEventDestroy(near_alloc);
     if (near_host_ready) cudaEventDestroy(near_host_ready);
   }
   std::shared_ptr<Tree> own_rows, own_cols;  // trees owned by this matrix (when built here)
@@ -601,6 +613,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
 void h2_matvec(Ctx& C, HView g, const double* x, double* y, double alpha, bool accumulate);
 // make the context's stream wait for an asynchronously uploaded nearfield (no-op otherwise)
 inline void wait_near(Ctx& C, const H2& h) {
+  h.start_near(C);
   if (h.near_ready) cuda_check(cudaStreamWaitEvent(C.st, h.near_ready, 0), "wait nearfield upload");
 }
 std::shared_ptr<H2> build_kernel_h2(Ctx& C, std::shared_ptr<const Blocks> bt, int kind, int dim,

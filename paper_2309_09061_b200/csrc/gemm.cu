@@ -433,6 +433,18 @@ __global__ void __launch_bounds__(kThr, GSUM_PIPE_MINB) gsum_pipe_kernel(const G
   const int wr = warp_row0(), wc = warp_col0();
   if (k2max > 0)  // intermediates are read in place: keep their unwritten padding finite
     for (int e = threadIdx.x; e < kT * ldT; e += kThr) Ts[e] = 0.0;
+  if (o.beta) {  // accumulating output: request C's lines now, the epilogue reads them (see gemm_lean.cu)
+#pragma unroll
+    for (int r = 0; r < kRT; ++r)
+#pragma unroll
+      for (int c = 0; c < kCT; ++c) {
+        const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4;
+        if (i < mt && j < nt) {
+          const double* q = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+        }
+      }
+  }
   Acc acc, aux;
   acc.zero();
   auto single = [](Job J) { return [J](int) { return J; }; };

@@ -937,6 +937,8 @@ static float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 // Phase-1 driver (reference induced.py:358-372).
 std::shared_ptr<H2> multiply(Ctx& C, const H2& x, const H2& y, double tol, int max_rank, bool scaling) {
+  x.start_near(C);  // deferred nearfield uploads: both operands' small arrays are queued by now
+  y.start_near(C);
   if (!x.bt->cols->same(*y.bt->rows)) throw InvalidInput("x and y do not share the middle cluster tree");
   if (tol < 0) throw InvalidInput("tolerance must be >= 0");
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr, e4 = nullptr;

@@ -983,6 +983,7 @@ std::shared_ptr<H2> coarsen(Ctx& C, const H2& g, std::shared_ptr<const Blocks> c
   // g's nearfield may still be in flight on the auxiliary stream (multiply's push-down expansions):
   // with block scaling its readers -- the nearfield norms on that stream, the leaf SVDs behind
   // nn_ready, the prefetch copy -- are ordered after it, so the main stream starts on the couplings
+  g.start_near(C);  // a deferred upload (an uploaded matrix coarsened directly)
   const bool near_async = scale && !serial_passes() && g.near_ready;
   if (!near_async) wait_near(C, g);
   NearPrefetch pf;
@@ -1170,6 +1171,7 @@ static std::shared_ptr<Basis> orthogonalize(Ctx& C, Arena& out, const Basis& B, 
 
 // Input preparation: orthogonalise, then coarsen onto the own block tree (coarsening.py:425-445).
 std::shared_ptr<H2> recompress(Ctx& C, const H2& g, double tol, int max_rank) {
+  g.start_near(C);
   auto ar = std::make_shared<Arena>(C.st);
   MatStore rr, rc;
   auto qr = orthogonalize(C, *ar, *g.rb, rr);

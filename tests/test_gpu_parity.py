@@ -201,6 +201,32 @@ def test_packed_host_buffer_path():
     assert np.array_equal(z4["near_data"], zp["near_data"])
 
 
+def test_deferred_nearfield_upload_first_uses():
+    """An asynchronous upload defers the nearfield copy to the matrix's first use (H2::start_near): every
+    first use -- matvec, download, coarsen, recompress, multiply -- must see the complete matrix."""
+    P = _P()
+    import torch
+    from paper_2309_09061_b200.packed import pack_h2
+    d = load("rand_s0_tol1e-3")
+    x, y, eps = _inputs(d)
+    xp = pack_h2(x)
+    xp.update({k: torch.from_numpy(v).pin_memory().numpy() for k, v in xp.items() if k.endswith("data")})
+    ref = P.DeviceH2.upload_packed(xp, x.block_tree)
+    v = np.random.default_rng(11).standard_normal(x.shape[1])
+    want = ref.matvec(v)
+    up = lambda: P.DeviceH2.upload_packed(xp, x.block_tree, asynchronous=True)
+    assert torch.equal(up().matvec(v), want)
+    got = up().download_packed()
+    for k, a in ref.download_packed().items():
+        assert np.array_equal(got[k], a), k
+    zr = P.coarsen(ref, x.block_tree, eps)
+    assert torch.equal(P.coarsen(up(), x.block_tree, eps).matvec(v), zr.matvec(v))
+    assert torch.equal(P.recompress(up(), eps).matvec(v), P.recompress(ref, eps).matvec(v))
+    a, b = up(), up()
+    g = P.multiply(a, b, eps)
+    assert torch.equal(g.matvec(v), P.multiply(ref, ref, eps).matvec(v))
+
+
 @pytest.mark.parametrize("name", ["rand_s0_tol1e-3", "c1"])
 def test_gpu_matvec_matches_host(name):
     """GPU h2_matvec / adjoint (h2.py:224-267) against the host restatement on Z and X."""
