@@ -216,6 +216,10 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
     ti = te;
   }
   if (live) {
+    // accumulating outputs: read all 16 entries of C first, then add and store.  In a single loop the
+    // compiler must keep each store ahead of the next load (C is not restrict-qualified), which
+    // serialises 16 L2 round trips: 40 % of the warp samples of an expansion launch sat on these adds.
+    double cv[2][4][2];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -223,10 +227,16 @@ __global__ void __launch_bounds__(kThr, 4) gsum_lean_kernel(const GOut* __restri
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
-          if (i < mt && j < nt) {
-            double* dst = o.c + (long long)(i0 + i) * o.ldc + (j0 + j);
-            *dst = (o.beta ? *dst : 0.0) + acc[r][c][h];
-          }
+          cv[r][c][h] = (o.beta && i < mt && j < nt) ? o.c[(long long)(i0 + i) * o.ldc + (j0 + j)] : 0.0;
+        }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = wr + r * 8 + g, j = wc + c * 8 + 2 * t4 + h;
+          if (i < mt && j < nt) o.c[(long long)(i0 + i) * o.ldc + (j0 + j)] = cv[r][c][h] + acc[r][c][h];
         }
   }
 }
@@ -265,12 +275,12 @@ __global__ void __launch_bounds__(kSumThr, 8) gsum_sum_kernel(const GOut* __rest
     for (int q = 0; q < kSumPer; ++q)
       if (ii[q] >= 0) acc[q] += al * a.p[(long long)ii[q] * a.rs + (long long)jj[q] * a.cs];
   }
+  double cv[kSumPer];  // all reads of C before the first store (see gsum_lean_kernel's epilogue)
+#pragma unroll
+  for (int q = 0; q < kSumPer; ++q) cv[q] = (o.beta && ii[q] >= 0) ? o.c[(long long)ii[q] * o.ldc + jj[q]] : 0.0;
 #pragma unroll
   for (int q = 0; q < kSumPer; ++q)
-    if (ii[q] >= 0) {
-      double* dst = o.c + (long long)ii[q] * o.ldc + jj[q];
-      *dst = (o.beta ? *dst : 0.0) + acc[q];
-    }
+    if (ii[q] >= 0) o.c[(long long)ii[q] * o.ldc + jj[q]] = cv[q] + acc[q];
 }
 
 cudaError_t launch_gsum_sum(const GOut* outs, const GTerm* terms, const GLTile* tiles, int ntiles, cudaStream_t st) {
