@@ -426,6 +426,12 @@ __global__ void __launch_bounds__(kThr, GSUM_PIPE_MINB) gsum_pipe_kernel(const G
   const int ldT = k2max + 4;
   const GTile tl = tiles[blockIdx.x];
   const GOut o = outs[tl.out];
+  // the output's term descriptors are read one dependent load at a time (13 % of gsum_whole's warp
+  // samples waited on them): request their lines up front
+  for (const char* q = (const char*)(terms + o.t0) + threadIdx.x * 128; q < (const char*)(terms + o.t1);
+       q += kThr * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+
   const int i0 = (tl.tij & 0xffff) * kT, j0 = (tl.tij >> 16) * kT;
   const int mt = min(kT, o.m - i0), nt = min(kT, o.n - j0);
   const int lane = threadIdx.x & 31;
@@ -536,6 +542,11 @@ __global__ void __launch_bounds__(kThr, 1) gsum_whole_kernel(const GOut* __restr
   constexpr int kLdTc = kT + 4;
   double* Uc = Tc + (size_t)kT * kLdTc;  // 64 x kLdU: cached U, all columns
   const GOut o = outs[tiles[blockIdx.x].out];
+  // the output's term descriptors are read one dependent load at a time (13 % of gsum_whole's warp
+  // samples waited on them): request their lines up front
+  for (const char* q = (const char*)(terms + o.t0) + threadIdx.x * 128; q < (const char*)(terms + o.t1);
+       q += kThr * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int wr = warp_row0(), wc = warp_col0();
