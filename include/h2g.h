@@ -109,8 +109,11 @@ int h2g_h2_upload(h2g_ctx* ctx, h2g_blocks* bt,
                   const long long* near_off, const double* near_data, long long near_len, h2g_h2** out);
 /* same, but the nearfield array is copied asynchronously on the context's copy stream: the call
    returns once bases and couplings are enqueued; kernels that read the nearfield wait for it on
-   the device. near_data must stay valid until the next synchronising call on the context
-   (h2g_h2_download, h2g_ctx_synchronize). */
+   the device. The nearfield copy itself is issued at the matrix's first use (so that a second
+   operand's bases and couplings are not queued behind it) or by h2g_ctx_synchronize, whichever comes
+   first. near_data must stay valid until h2g_ctx_synchronize returns (it starts a pending copy and
+   drains the copy stream), or until a synchronising call that follows a use of the matrix
+   (h2g_h2_download of a result computed from it). */
 int h2g_h2_upload_async(h2g_ctx* ctx, h2g_blocks* bt,
                         const long long* rb_rank, const long long* rb_leaf_off, const long long* rb_xfer_off,
                         const double* rb_data, long long rb_len,

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/h2g.h): handles, upload / download in the packed layout, status codes.
 #include <malloc.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -180,7 +181,16 @@ int h2g_ctx_trace_dump(h2g_ctx* ctx, const char* path) {
 }
 
 int h2g_ctx_synchronize(h2g_ctx* ctx) {
-  return guarded([&] { ctx->c.sync(); });
+  return guarded([&] {
+    // asynchronous uploads: the caller may release near_data after this call, so deferred nearfield
+    // copies start now and the copy stream is drained too
+    Ctx& C = ctx->c;
+    for (auto& w : C.deferred_near)
+      if (auto h = w.lock()) h->start_near(C);
+    C.deferred_near.clear();
+    if (C.up_stream) cuda_check(cudaStreamSynchronize(C.up_stream), "cudaStreamSynchronize");
+    C.sync();
+  });
 }
 
 int h2g_tree_create(h2g_ctx*, int n, const long long* start, const long long* stop, const long long* cptr,
@@ -280,6 +290,14 @@ static int upload_impl(h2g_ctx* ctx, h2g_blocks* bt, const long long* rb_rank, c
         h->near_src = near_data;
         h->near_dst = dn;
         h->near_bytes = (size_t)near_len * sizeof(double);
+        if (C.deferred_near.size() >= 64)  // drop matrices already destroyed or started
+          C.deferred_near.erase(std::remove_if(C.deferred_near.begin(), C.deferred_near.end(),
+                                               [](const std::weak_ptr<H2>& w) {
+                                                 auto p = w.lock();
+                                                 return !p || !p->near_src;
+                                               }),
+                                C.deferred_near.end());
+        C.deferred_near.push_back(h);
       } else {
         cuda_check(cudaMemcpyAsync(dn, near_data, near_len * sizeof(double), cudaMemcpyHostToDevice, C.st), "upload");
       }

@@ -323,6 +323,7 @@ struct Ctx {
   int channel = 0;  // communicator of this context's host thread (side context: 1)
   std::unique_ptr<Ctx> side_;  // second stream + staging for the concurrent column passes
   cudaStream_t up_stream = nullptr;  // structure uploads from the planner thread
+  std::vector<std::weak_ptr<H2>> deferred_near;  // asynchronous uploads whose nearfield copy has not started
   char* up_host = nullptr;
   size_t up_cap = 0;
   std::unique_ptr<Ctx> aux_;   // low-priority stream: work ahead of the critical path (dense targets)

@@ -225,6 +225,15 @@ def test_deferred_nearfield_upload_first_uses():
     a, b = up(), up()
     g = P.multiply(a, b, eps)
     assert torch.equal(g.matvec(v), P.multiply(ref, ref, eps).matvec(v))
+    # the host array may be released after a synchronising call even if the matrix was not used yet
+    # (include/h2g.h): the deferred copy starts, and the copy stream drains, inside ctx.synchronize()
+    near = xp["near_data"]
+    xq = dict(xp)
+    xq["near_data"] = torch.from_numpy(near.copy()).pin_memory().numpy()
+    late = P.DeviceH2.upload_packed(xq, x.block_tree, asynchronous=True)
+    late.ctx.synchronize()
+    xq["near_data"][:] = np.nan  # stands for freed memory
+    assert torch.equal(late.matvec(v), want)
 
 
 @pytest.mark.parametrize("name", ["rand_s0_tol1e-3", "c1"])
