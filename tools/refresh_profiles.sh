@@ -20,6 +20,7 @@ cap() {  # kernel regex, launch skip (within tools/run_config.py c4 0 1), tag
 }
 cap "gsum_pipe_kernel<.int.1>" 0 gsum_dense gsum_pipe
 cap "gram_dd_partial_kernel" 60 gram gram_dd
+bash tools/gpu_r02_lean2.sh > /dev/null 2>&1; cp gpurun_out/lean2/lean_stalls.txt $O/lean_stalls.txt  # longest gsum_lean_kernel launch of a serialized product
 python bench.py --config c2 --steps 10 --warmup 3 > $O/bench_c2.json 2> $O/bench_c2.err; echo "bench c2 rc=$?"
 python bench.py --impl reference --config c2 --cpu-sample-n 16384 --steps 1 --warmup 0 > $O/ref_c2_16384.json 2> $O/ref_c2.err; echo "ref c2 rc=$?"
 for c in c2 c3 c4; do python tools/run_config.py $c 0 5 > $O/full_$c.json 2> $O/full_$c.err; done
