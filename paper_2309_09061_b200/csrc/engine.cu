@@ -450,17 +450,11 @@ static void gsum_tile_stats(const char* tag, const std::vector<GOut>& outs, cons
 void GBatch::run(Ctx& C) {
   HostTimer ht(C, "gbatch_run");
   std::vector<GTile> tiles;
-  // batches of plain sums and 2-factor products (no grouped / 3-factor terms) take the lean kernel:
+  // outputs whose terms are plain sums and 2-factor products (no grouped / 3-factor terms) take the lean kernel:
   // 4-warp CTAs in the arrangement (32 x 64, 64 x 32, 16 x 128) that covers each output with the
   // fewest CTAs (H2G_GSUM_NO_LEAN=1: 64 x 64 tiles, for A/B)
   static const bool no_lean = getenv("H2G_GSUM_NO_LEAN") != nullptr;
-  bool lean = !no_lean && tag == 0;
-  if (lean)
-    for (const GTerm& t : terms)
-      if (t.nf > 2) { lean = false; break; }
-  if (lean)
-    for (const GOut& o : outs)
-      if (o.ka || o.kb) { lean = false; break; }
+  const bool lean_ok = !no_lean && tag == 0;  // decided per output: a batch may mix both kinds
   std::vector<GLTile> ltiles, stiles;
   bool wide = false;
   static const bool no_sum = getenv("H2G_GSUM_NO_SUM") != nullptr;  // A/B: sums through the GEMM kernels
@@ -477,6 +471,8 @@ void GBatch::run(Ctx& C) {
         continue;
       }
     }
+    bool lean = lean_ok && !o.ka && !o.kb;
+    for (int t = o.t0; t < o.t1 && lean; ++t) lean = terms[t].nf <= 2;
     if (lean) {
       auto cd = [](int a, int b) { return (a + b - 1) / b; };
       const int n0 = cd(o.m, 32) * cd(o.n, 64), n1 = cd(o.m, 64) * cd(o.n, 32), n2 = cd(o.m, 16) * cd(o.n, 128);
@@ -546,7 +542,8 @@ void GBatch::run(Ctx& C) {
   if (!ltiles.empty()) {
     cuda_check(launch_gsum_lean(d_o, d_t, d_ll, (int)ltiles.size(), wide, C.st), "gsum(lean)");
     ++C.launches;
-  } else if (!tiles.empty()) {
+  }
+  if (!tiles.empty()) {
     cuda_check(launch_gsum(d_o, d_t, d_l, (int)tiles.size(), k2max, C.st), "gsum");
     ++C.launches;
   }
